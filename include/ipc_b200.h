@@ -1,0 +1,139 @@
+/* C-ABI of the B200 IPC time-step library (libipc_b200.so).
+ *
+ * Drop-in boundary for the reference package's per-step path
+ * (reference: /root/reference/pkg/src/srsim). The reference is pure Python,
+ * so there is no foreign interface to re-bind; each entry point below
+ * replaces the named reference function and is bound from Python with
+ * ctypes (paper_2311_05945_b200/_native.py).
+ *
+ * Plain pointers and sizes only. Unless stated otherwise pointers are HOST
+ * pointers; the library owns all device memory. Every call returns 0 on
+ * success and a negative code on failure (message: ipc_last_error()).
+ */
+#ifndef IPC_B200_H
+#define IPC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ipc_world ipc_world;
+
+/* Packed description of a batch of independent scenes ("environments").
+ * Mirrors the reference scene data (scene.py:23 build_collision,
+ * bodies.py GlobalState/SoftBody/AffineBody, constraints.py
+ * KinematicConstraint) flattened over environments; per-environment ranges
+ * are prefix arrays of length n_env + 1. All element indices are global. */
+typedef struct {
+  int32_t n_env, n_dof, n_vert, n_aff, n_tet, n_slot, n_tri, n_edge, n_cbody, n_cons;
+  const int32_t *env_dof, *env_vert, *env_aff, *env_tet, *env_slot, *env_tri, *env_edge,
+      *env_cbody, *env_cons;
+  const uint8_t *env_pairs;      /* Scene.tables.needs_pair_search() */
+  const uint8_t *env_has_ground; /* Scene.ground_y is not None */
+  const double *env_ground_y, *env_gravity /* 3 per env */, *env_dhat, *env_kappa, *env_kappa0,
+      *env_mu, *env_eps_v;
+  const int32_t *vert_dof; /* DoF index of each soft vertex's x coordinate */
+  const double *vert_mass;
+  const int32_t *aff_dof;  /* first DoF of each affine body */
+  const double *aff_M /* 144 */, *aff_acc /* 12: M_b^-1 f_gravity */, *aff_ortho /* stiffness*volume */;
+  const int32_t *tet_dof;  /* 4 per tet: DoF index of each corner */
+  const double *tet_Dminv /* 9 */, *tet_vol, *tet_mu, *tet_lam;
+  const uint8_t *tet_model; /* 0 NeoHookean, 1 StVK, 2 FixedCorotated */
+  const uint8_t *slot_aff;  /* contact slot kind: 1 = rides an affine body */
+  const int32_t *slot_dof;  /* soft: DoF index; affine: body's first DoF */
+  const double *slot_rest;  /* 3 per slot: rest position (affine lever arm) */
+  const int32_t *slot_cbody;
+  const int32_t *tri_v /* 3 */, *tri_cbody, *edge_v /* 2 */, *edge_cbody;
+  const double *edge_len2;
+  const uint8_t *cbody_rigid, *cbody_kin;
+  const uint64_t *cbody_excl; /* bit j: excluded against env-local collision body j */
+  const int32_t *cons_aff;    /* affine body index of each kinematic constraint */
+  const double *cons_kappa0, *cons_mass;
+  const double *x0, *v0; /* initial DoF state, n_dof each */
+} ipc_world_desc;
+
+/* ref solver.py:56 SolverConfig */
+typedef struct {
+  double h, newton_tol;
+  int32_t max_newton_iters, max_line_search_halvings;
+  double ccd_conservative_factor;
+  int32_t friction_fixed_point_iters, al_max_outer;
+} ipc_step_config;
+
+/* ref solver.py:75 StepReport (per environment) */
+typedef struct {
+  int32_t newton_iters, ccd_invocations, converged, line_search_failed, al_outer, error;
+  double final_grad_norm, min_dist_before, min_dist_after, kappa;
+} ipc_step_report;
+
+const char *ipc_last_error(void);
+int ipc_device_count(void);
+
+/* Upload a batch (replaces ref scene.py:143 make_scene's per-scene setup). */
+int ipc_world_create(const ipc_world_desc *desc, ipc_world **out);
+int ipc_world_destroy(ipc_world *w);
+
+/* One implicit step of every environment (replaces ref solver.py:360 step).
+ * cons_targets: 12 doubles per kinematic constraint (the bodies' target_q),
+ * or NULL to keep the previous targets. reports: n_env entries or NULL. */
+int ipc_world_step(ipc_world *w, const ipc_step_config *cfg, const double *cons_targets,
+                   ipc_step_report *reports);
+
+/* State transfer, host buffers (replaces GlobalState.gather/scatter). */
+int ipc_world_get_state(ipc_world *w, double *x, double *v);
+int ipc_world_set_state(ipc_world *w, const double *x, const double *v);
+/* Device pointers of the resident state (n_dof doubles each). */
+int ipc_world_state_device(ipc_world *w, double **x, double **v);
+int ipc_world_get_kappa(ipc_world *w, double *kappa);
+int ipc_world_set_kappa(ipc_world *w, const double *kappa);
+/* Kinematic multipliers / penalties after the last step (12 + 1 per constraint). */
+int ipc_world_get_constraints(ipc_world *w, double *lam, double *kappa);
+
+/* World-frame contact force (N) on every slot at the current state
+ * (replaces ref robot/sensing.py:30 slot_contact_forces). out: 3*n_slot. */
+int ipc_world_slot_forces(ipc_world *w, double h, double *out);
+
+/* Discrete candidates at the current state (ref broadphase.py:169), for
+ * parity checks. which: 0 PT, 1 EE, 2 ground. Writes up to cap pairs
+ * (2 ints each; ground: 1 int) of env `env`, returns the count via *n. */
+int ipc_world_candidates(ipc_world *w, int env, int which, int32_t *out, int64_t cap, int64_t *n);
+
+/* Per-env minimum contact distance at the current state, inf when no
+ * candidate (ref contact.py:595 ContactStats.min_dist). out: n_env. */
+int ipc_world_min_distance(ipc_world *w, double *out);
+
+/* Per-env minimum distance between two groups of collision bodies over
+ * candidates within dhat (ref robot/proximity.py:245 min_group_distance);
+ * group_a/group_b: n_env bitmasks over env-local collision body ids.
+ * out: n_env (inf when no candidate pair joins the groups). */
+int ipc_world_group_distance(ipc_world *w, const uint64_t *group_a, const uint64_t *group_b,
+                             double *out);
+/* Per-env lowest slot height above the ground over a group of collision
+ * bodies (ref robot/proximity.py:286 min_ground_distance). */
+int ipc_world_ground_distance(ipc_world *w, const uint64_t *group, double *out);
+/* Per-env summed contact force (N, world frame) on groups of collision
+ * bodies: groups = n_env*n_groups bitmasks, out = n_env*n_groups*3
+ * (ref robot/sensing.py:52 body_contact_force / :61 finger_forces). */
+int ipc_world_group_forces(ipc_world *w, double h, const uint64_t *groups, int n_groups,
+                           double *out);
+
+/* Kernel-level entry points used by the parity tests (host buffers).
+ * ipc_dist2_derivs: n stencils (12 doubles each) -> region, s, grad 12, hess 144
+ *   (replaces ref geometry/distance.py:38/:125 + distgrad.py:300). kind 0 PT, 1 EE. */
+int ipc_dist2_derivs(int kind, int64_t n, const double *stencils, int32_t *region, double *s,
+                     double *grad, double *hess);
+/* ref geometry/ccd.py:395 pair_ccd */
+int ipc_ccd_pairs(int kind, int64_t n, const double *px, const double *pdx, double conservative,
+                  double *alpha);
+/* ref energy/spd.py:6 spd_project, dim in {6, 9, 12} */
+int ipc_psd_project(int dim, int64_t n, double *mats);
+/* ref energy/elastic.py:173-167: psi, PK1 (9), F-space Hessian (81) */
+int ipc_elastic_eval(int model, int64_t n, const double *F, double mu, double lam, double *psi,
+                     double *P, double *H9);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IPC_B200_H */

@@ -1,0 +1,1020 @@
+// Host engine of libipc_b200.so: owns the device-resident world and drives
+// the per-step kernel sequence (ref solver.py:360 step / :295 _newton_solve).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ipc_b200.h"
+#include "solve.cuh"
+
+using namespace ipc;
+
+static thread_local std::string g_err;
+
+static int set_err(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return -1;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      throw std::runtime_error(std::string(#call) + ": " + cudaGetErrorString(e_));  \
+  } while (0)
+
+#define GUARD(...)                                    \
+  try {                                                \
+    __VA_ARGS__;                                       \
+    return 0;                                          \
+  } catch (const std::exception& ex) {                 \
+    return set_err("%s", ex.what());                   \
+  }
+
+static inline int nblk(long long n, int t) { return (int)std::max<long long>(1, (n + t - 1) / t); }
+
+namespace ipc {
+__global__ void k_mark_unconverged(int n_env, EnvState S) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n_env && S.newton_active[e]) {
+    S.converged[e] = 0;
+    S.newton_active[e] = 0;
+  }
+}
+__global__ void k_step_begin(int n_env, EnvState S) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_env) return;
+  S.newton_iters[e] = 0; S.ccd_calls[e] = 0; S.al_outer[e] = 0; S.ls_failed[e] = 0;
+  S.converged[e] = 1; S.err[e] = 0; S.min_s_before[e] = INFINITY; S.gnorm[e] = 0.0;
+}
+// intersection check of the incoming state: any candidate value is inf
+__global__ void k_start_check(World W, EnvState S, Cands C, const double* ptv, const double* eev,
+                              const double* gv, int* ok) {
+  int e = blockIdx.x;
+  int bad = 0;
+  for (int k = threadIdx.x; k < C.n_pt[e]; k += blockDim.x) bad |= isinf(ptv[C.pt_off[e] + k]);
+  for (int k = threadIdx.x; k < C.n_ee[e]; k += blockDim.x) bad |= isinf(eev[C.ee_off[e] + k]);
+  for (int k = threadIdx.x; k < C.n_gnd[e]; k += blockDim.x) bad |= isinf(gv[C.gnd_off[e] + k]);
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    ok[e] = !bad;
+    S.err[e] = bad;
+  }
+}
+__global__ void k_copy_int(int n, const int* a, int* b) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = a[i];
+}
+__global__ void k_and_not(int n, int* a, const int* b) {  // a &= !b
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && b[i]) a[i] = 0;
+}
+// slot forces: -∂B/∂x_slot / h², each slot gathers its own contributions
+// in candidate order (deterministic)
+__global__ void k_slot_forces(World W, Cands C, const double* pt_g, const unsigned char* pt_act,
+                              const double* ee_g, const unsigned char* ee_act, const double* gnd_gy,
+                              double h, double* out) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= W.n_slot) return;
+  int e = W.slot_env[s];
+  double f[3] = {0, 0, 0};
+  for (int kind = 0; kind < 2; ++kind) {
+    int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
+    long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
+    const unsigned char* act = kind == 0 ? pt_act : ee_act;
+    const double* g = kind == 0 ? pt_g : ee_g;
+    for (int k = 0; k < n; ++k) {
+      long long q = off + k;
+      if (!act[q]) continue;
+      int2 pr = kind == 0 ? C.pt[q] : C.ee[q];
+      int sl[4];
+      if (kind == 0) {
+        int3 tv = W.tri_v[pr.y];
+        sl[0] = pr.x; sl[1] = tv.x; sl[2] = tv.y; sl[3] = tv.z;
+      } else {
+        int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
+        sl[0] = a.x; sl[1] = a.y; sl[2] = b.x; sl[3] = b.y;
+      }
+      for (int a = 0; a < 4; ++a)
+        if (sl[a] == s)
+          for (int c = 0; c < 3; ++c) f[c] += g[12 * q + 3 * a + c];
+    }
+  }
+  for (int k = 0; k < C.n_gnd[e]; ++k)
+    if (C.gnd[C.gnd_off[e] + k] == s) f[1] += gnd_gy[C.gnd_off[e] + k];
+  double ih = 1.0 / (h * h);
+  for (int c = 0; c < 3; ++c) out[3 * s + c] = -f[c] * ih;
+}
+__global__ void k_group_forces(World W, const double* slot_f, const unsigned long long* groups, int ng,
+                               double* out) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= W.n_env * ng) return;
+  int e = q / ng;
+  unsigned long long m = groups[q];
+  int cb0 = W.env_cbody[e];
+  double f[3] = {0, 0, 0};
+  for (int s = W.env_slot[e]; s < W.env_slot[e + 1]; ++s)
+    if ((m >> (W.slot_cbody[s] - cb0)) & 1ull)
+      for (int c = 0; c < 3; ++c) f[c] += slot_f[3 * s + c];
+  for (int c = 0; c < 3; ++c) out[3 * q + c] = f[c];
+}
+__global__ void k_group_distance(World W, Cands C, const double* xw, const unsigned long long* ga,
+                                 const unsigned long long* gb, double* out) {
+  int e = blockIdx.x;
+  __shared__ double sh[8];
+  int cb0 = W.env_cbody[e];
+  unsigned long long A = ga[e], B = gb[e];
+  double best = INFINITY;
+  for (int k = threadIdx.x; k < C.n_pt[e]; k += blockDim.x) {
+    int2 pr = C.pt[C.pt_off[e] + k];
+    int bv = W.slot_cbody[pr.x] - cb0, bt = W.tri_cbody[pr.y] - cb0;
+    bool in = (((A >> bv) & 1) && ((B >> bt) & 1)) || (((B >> bv) & 1) && ((A >> bt) & 1));
+    if (!in) continue;
+    int3 tv = W.tri_v[pr.y];
+    V3 p = ld3(xw + 3 * pr.x), t0 = ld3(xw + 3 * tv.x), t1 = ld3(xw + 3 * tv.y), t2 = ld3(xw + 3 * tv.z);
+    best = fmin(best, pt_dist2(pt_region(p, t0, t1, t2), p, t0, t1, t2));
+  }
+  for (int k = threadIdx.x; k < C.n_ee[e]; k += blockDim.x) {
+    int2 pr = C.ee[C.ee_off[e] + k];
+    int b1 = W.edge_cbody[pr.x] - cb0, b2 = W.edge_cbody[pr.y] - cb0;
+    bool in = (((A >> b1) & 1) && ((B >> b2) & 1)) || (((B >> b1) & 1) && ((A >> b2) & 1));
+    if (!in) continue;
+    int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
+    V3 a0 = ld3(xw + 3 * a.x), a1 = ld3(xw + 3 * a.y), b0 = ld3(xw + 3 * b.x), b1v = ld3(xw + 3 * b.y);
+    best = fmin(best, ee_dist2(ee_region(a0, a1, b0, b1v, nullptr), a0, a1, b0, b1v));
+  }
+  // min-reduce (exact, order independent)
+  for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_down_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmin(r, sh[w]);
+    out[e] = isinf(r) ? INFINITY : sqrt(r);
+  }
+}
+__global__ void k_ground_distance(World W, const double* xw, const unsigned long long* g, double* out) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= W.n_env) return;
+  if (!W.env_has_ground[e]) {
+    out[e] = INFINITY;
+    return;
+  }
+  int cb0 = W.env_cbody[e];
+  double lo = INFINITY;
+  for (int s = W.env_slot[e]; s < W.env_slot[e + 1]; ++s)
+    if ((g[e] >> (W.slot_cbody[s] - cb0)) & 1ull) lo = fmin(lo, xw[3 * s + 1]);
+  out[e] = isinf(lo) ? INFINITY : lo - W.env_ground_y[e];
+}
+}  // namespace ipc
+
+
+struct Pool {
+  std::vector<void*> ptrs;
+  template <typename T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    CK(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  template <typename T>
+  T* upload(const T* host, size_t n) {
+    T* d = alloc<T>(n);
+    if (host && n) CK(cudaMemcpy(d, host, n * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  }
+  void free_one(void* p) {
+    auto it = std::find(ptrs.begin(), ptrs.end(), p);
+    if (it != ptrs.end()) {
+      cudaFree(p);
+      ptrs.erase(it);
+    }
+  }
+  ~Pool() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+// candidate storage with per-env capacities
+struct CandStore {
+  Cands c{};
+  std::vector<long long> pt_cap, ee_cap;  // per env
+  long long* d_pt_off = nullptr;
+  long long* d_ee_off = nullptr;
+  long long pt_total = 0, ee_total = 0;
+  int max_pt_cap = 0, max_ee_cap = 0;
+};
+
+// element output buffers sized to a candidate store
+struct PairBufs {
+  double *pt_val = nullptr, *ee_val = nullptr, *gnd_val = nullptr;
+  double *pt_g = nullptr, *pt_h = nullptr, *ee_g = nullptr, *ee_h = nullptr;
+  unsigned char *pt_act = nullptr, *ee_act = nullptr;
+  double *gnd_gy = nullptr, *gnd_hyy = nullptr;
+};
+
+struct ipc_world {
+  Pool pool;
+  World W{};
+  EnvState S{};
+  int n_env = 0;
+  std::vector<int> h_env_slot, h_env_dof, h_env_tri, h_env_edge, h_env_cbody;
+  int max_env_dof = 0;
+  CandStore dcd, sweep;
+  PairBufs pb_dcd, pb_sweep;
+  Lags L{};
+  long long* d_lag_off = nullptr;
+  Derivs D{};
+  double *body_val = nullptr, *tet_val = nullptr, *fr_val = nullptr, *frg_val = nullptr;
+  double *xlo = nullptr, *xhi = nullptr, *xwt = nullptr;
+  double *env_alpha = nullptr;
+  int *ok = nullptr, *al_flag = nullptr, *accepted = nullptr, *ls_count = nullptr, *d_count = nullptr;
+  int* h_count = nullptr;  // pinned
+  double* slot_force = nullptr;
+  double* d_targets = nullptr;
+  bool lags_stale = false;
+  std::vector<double> h_targets;
+  bool targets_set = false;
+  cudaStream_t st = 0;
+
+  ~ipc_world() {
+    if (h_count) cudaFreeHost(h_count);
+  }
+
+  int count(const int* flag) {
+    k_count<<<1, 256, 0, st>>>(n_env, flag, d_count);
+    CK(cudaMemcpyAsync(h_count, d_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return *h_count;
+  }
+
+  void alloc_cands(CandStore& cs, const std::vector<long long>& ptc, const std::vector<long long>& eec) {
+    cs.pt_cap = ptc;
+    cs.ee_cap = eec;
+    std::vector<long long> po(n_env + 1, 0), eo(n_env + 1, 0);
+    cs.max_pt_cap = cs.max_ee_cap = 0;
+    for (int e = 0; e < n_env; ++e) {
+      po[e + 1] = po[e] + ptc[e];
+      eo[e + 1] = eo[e] + eec[e];
+      cs.max_pt_cap = std::max<long long>(cs.max_pt_cap, ptc[e]);
+      cs.max_ee_cap = std::max<long long>(cs.max_ee_cap, eec[e]);
+    }
+    cs.pt_total = po[n_env];
+    cs.ee_total = eo[n_env];
+    if (cs.d_pt_off) { pool.free_one(cs.d_pt_off); pool.free_one(cs.d_ee_off); pool.free_one(cs.c.pt); pool.free_one(cs.c.ee); }
+    cs.d_pt_off = pool.upload(po.data(), po.size());
+    cs.d_ee_off = pool.upload(eo.data(), eo.size());
+    cs.c.pt = pool.alloc<int2>(cs.pt_total);
+    cs.c.ee = pool.alloc<int2>(cs.ee_total);
+    cs.c.pt_off = cs.d_pt_off;
+    cs.c.ee_off = cs.d_ee_off;
+    if (!cs.c.gnd) {
+      cs.c.gnd = pool.alloc<int>(W.n_slot);
+      cs.c.n_pt = pool.alloc<int>(n_env);
+      cs.c.n_ee = pool.alloc<int>(n_env);
+      cs.c.n_gnd = pool.alloc<int>(n_env);
+      cs.c.gnd_off = W.env_slot;
+      cs.c.overflow = pool.alloc<int>(1);
+    }
+  }
+
+  void alloc_pairbufs(PairBufs& b, const CandStore& cs, bool derivs) {
+    for (void* p : {(void*)b.pt_val, (void*)b.ee_val, (void*)b.pt_g, (void*)b.pt_h, (void*)b.ee_g,
+                    (void*)b.ee_h, (void*)b.pt_act, (void*)b.ee_act})
+      if (p) pool.free_one(p);
+    b.pt_val = pool.alloc<double>(cs.pt_total);
+    b.ee_val = pool.alloc<double>(cs.ee_total);
+    if (!b.gnd_val) b.gnd_val = pool.alloc<double>(W.n_slot);
+    if (derivs) {
+      b.pt_g = pool.alloc<double>(12 * cs.pt_total);
+      b.pt_h = pool.alloc<double>(PK * cs.pt_total);
+      b.ee_g = pool.alloc<double>(12 * cs.ee_total);
+      b.ee_h = pool.alloc<double>(PK * cs.ee_total);
+      b.pt_act = pool.alloc<unsigned char>(cs.pt_total);
+      b.ee_act = pool.alloc<unsigned char>(cs.ee_total);
+      if (!b.gnd_gy) {
+        b.gnd_gy = pool.alloc<double>(W.n_slot);
+        b.gnd_hyy = pool.alloc<double>(W.n_slot);
+      }
+    } else {
+      b.pt_g = b.pt_h = b.ee_g = b.ee_h = nullptr;
+      b.pt_act = b.ee_act = nullptr;
+    }
+  }
+
+  void alloc_lags() {
+    std::vector<long long> lo(n_env + 1, 0);
+    for (int e = 0; e < n_env; ++e) lo[e + 1] = lo[e] + dcd.pt_cap[e] + dcd.ee_cap[e];
+    long long tot = lo[n_env];
+    for (void* p : {(void*)d_lag_off, (void*)L.slots, (void*)L.gamma, (void*)L.tangent, (void*)L.lam,
+                    (void*)fr_val, (void*)D.fr_g, (void*)D.fr_h})
+      if (p) pool.free_one(p);
+    d_lag_off = pool.upload(lo.data(), lo.size());
+    L.off = d_lag_off;
+    L.slots = pool.alloc<int4>(tot);
+    L.gamma = pool.alloc<double>(4 * tot);
+    L.tangent = pool.alloc<double>(6 * tot);
+    L.lam = pool.alloc<double>(tot);
+    if (!L.n) {
+      L.n = pool.alloc<int>(n_env);
+      L.g_slot = pool.alloc<int>(W.n_slot);
+      L.g_lam = pool.alloc<double>(W.n_slot);
+      L.g_n = pool.alloc<int>(n_env);
+      frg_val = pool.alloc<double>(W.n_slot);
+      D.frg_g = pool.alloc<double>(3 * W.n_slot);
+      D.frg_h = pool.alloc<double>(9 * W.n_slot);
+    }
+    fr_val = pool.alloc<double>(tot);
+    D.fr_g = pool.alloc<double>(12 * tot);
+    D.fr_h = pool.alloc<double>(PK * tot);
+  }
+
+  // run broad phase; grow capacities and retry on overflow
+  void broad(CandStore& cs, PairBufs& pb, bool derivs, const double* lo, const double* hi,
+             const int* env_mask) {
+    for (int attempt = 0; attempt < 8; ++attempt) {
+      CK(cudaMemsetAsync(cs.c.overflow, 0, sizeof(int), st));
+      for (int kind = 0; kind < 3; ++kind) k_broad<<<n_env, BP_THREADS, 0, st>>>(W, lo, hi, cs.c, kind, env_mask);
+      CK(cudaGetLastError());
+      int ov = 0;
+      CK(cudaMemcpyAsync(h_count, cs.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      ov = *h_count;
+      if (!ov) return;
+      // grow: read counts are clipped, so grow every env capacity 4x
+      std::vector<long long> ptc = cs.pt_cap, eec = cs.ee_cap;
+      for (int e = 0; e < n_env; ++e) {
+        long long nv = h_env_slot[e + 1] - h_env_slot[e], nt = h_env_tri[e + 1] - h_env_tri[e];
+        long long ne = h_env_edge[e + 1] - h_env_edge[e];
+        ptc[e] = std::min(nv * nt, 4 * ptc[e]);
+        eec[e] = std::min(ne * ne, 4 * eec[e]);
+      }
+      alloc_cands(cs, ptc, eec);
+      alloc_pairbufs(pb, cs, derivs);
+      if (&cs == &dcd) lags_stale = true;
+    }
+    throw std::runtime_error("broad phase capacity overflow persists");
+  }
+
+  void world_pos(const double* x, double* xw) {
+    k_world<<<nblk(W.n_slot, 256), 256, 0, st>>>(W, x, xw);
+  }
+
+  // derivative or value pass of every term over (cands, lags)
+  void terms(const double* x, const double* xw, CandStore& cs, PairBufs& pb, bool deriv, double h,
+             const int* flag, double* min_s) {
+    double h2 = h * h;
+    k_body<<<nblk(W.n_aff, 64), 64, 0, st>>>(W, x, W.xhat, h2, deriv, flag, body_val, D.body_g, D.body_h);
+    if (W.n_tet) k_tet<<<nblk(W.n_tet, 64), 64, 0, st>>>(W, x, h2, deriv, flag, tet_val, D.tet_g, D.tet_h);
+    if (cs.max_pt_cap)
+      k_pairs<<<dim3(nblk(cs.max_pt_cap, 64), n_env), 64, 0, st>>>(W, xw, cs.c, 0, deriv, flag, pb.pt_val,
+                                                                   pb.pt_g, pb.pt_h, pb.pt_act, min_s);
+    if (cs.max_ee_cap)
+      k_pairs<<<dim3(nblk(cs.max_ee_cap, 64), n_env), 64, 0, st>>>(W, xw, cs.c, 1, deriv, flag, pb.ee_val,
+                                                                   pb.ee_g, pb.ee_h, pb.ee_act, min_s);
+    int max_slots = 0;
+    for (int e = 0; e < n_env; ++e) max_slots = std::max(max_slots, h_env_slot[e + 1] - h_env_slot[e]);
+    k_ground<<<dim3(nblk(max_slots, 128), n_env), 128, 0, st>>>(W, xw, cs.c, deriv, flag, pb.gnd_val,
+                                                                pb.gnd_gy, pb.gnd_hyy, min_s);
+    long long maxlag = 0;
+    for (int e = 0; e < n_env; ++e) maxlag = std::max(maxlag, dcd.pt_cap[e] + dcd.ee_cap[e]);
+    k_friction<<<dim3(nblk(maxlag, 128), n_env), 128, 0, st>>>(W, xw, W.xw0, L, h, deriv, flag, fr_val,
+                                                               D.fr_g, D.fr_h);
+    k_friction_gnd<<<dim3(nblk(max_slots, 128), n_env), 128, 0, st>>>(W, xw, W.xw0, L, h, deriv, flag,
+                                                                      frg_val, D.frg_g, D.frg_h);
+    CK(cudaGetLastError());
+  }
+
+  void energy(const double* x, CandStore& cs, PairBufs& pb, const int* flag, double* out) {
+    Terms T{body_val, tet_val, pb.pt_val, pb.ee_val, pb.gnd_val, fr_val, frg_val, nullptr};
+    k_env_energy<<<n_env, RED_THREADS, 0, st>>>(W, x, W.xhat, T, cs.c, L, flag, out);
+  }
+
+  void newton_solve(const ipc_step_config& cfg) {
+    double h = cfg.h;
+    k_newton_begin<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S, al_flag);
+    size_t smem = (size_t)(max_env_dof * max_env_dof + 2 * max_env_dof) * sizeof(double);
+    for (int it = 0; it < cfg.max_newton_iters; ++it) {
+      if (count(S.newton_active) == 0) break;
+      world_pos(W.x, W.xw);
+      broad(dcd, pb_dcd, true, W.xw, W.xw, S.newton_active);
+      k_fill_flag<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S.min_s, INFINITY, S.newton_active);
+      terms(W.x, W.xw, dcd, pb_dcd, true, h, S.newton_active, S.min_s);
+      energy(W.x, dcd, pb_dcd, S.newton_active, S.e0);
+      k_dense_solve<<<n_env, DENSE_THREADS, smem, st>>>(W, S, D_with(pb_dcd), dcd.c, L, W.x, W.xhat, W.p,
+                                                        W.grad);
+      CK(cudaGetLastError());
+      k_newton_check<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S, h, cfg.newton_tol);
+      if (count(S.ls_active) == 0) continue;
+      // CCD bound along p (ref solver.py:333-343)
+      k_axpy_env<<<nblk(W.n_dof, 256), 256, 0, st>>>(W, W.x, W.p, nullptr, S.ls_active, W.xt);
+      world_pos(W.xt, xwt);
+      k_sub<<<nblk(3 * W.n_slot, 256), 256, 0, st>>>(3 * W.n_slot, xwt, W.xw, W.dxw);
+      k_sweep_box<<<nblk(3 * W.n_slot, 256), 256, 0, st>>>(W.n_slot, W.xw, W.dxw, xlo, xhi);
+      broad(sweep, pb_sweep, false, xlo, xhi, S.ls_active);
+      k_fill_flag<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S.alpha_max, 1.0, S.ls_active);
+      if (sweep.max_pt_cap)
+        k_ccd_pairs<<<dim3(nblk(sweep.max_pt_cap, 64), n_env), 64, 0, st>>>(
+            W, W.xw, W.dxw, sweep.c, 0, cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
+      if (sweep.max_ee_cap)
+        k_ccd_pairs<<<dim3(nblk(sweep.max_ee_cap, 64), n_env), 64, 0, st>>>(
+            W, W.xw, W.dxw, sweep.c, 1, cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
+      int max_slots = 0;
+      for (int e = 0; e < n_env; ++e) max_slots = std::max(max_slots, h_env_slot[e + 1] - h_env_slot[e]);
+      k_ccd_ground<<<dim3(nblk(max_slots, 128), n_env), 128, 0, st>>>(W, W.xw, W.dxw, sweep.c,
+                                                                      cfg.ccd_conservative_factor, S.ls_active,
+                                                                      S.alpha_max);
+      k_ls_begin<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S, ls_count);
+      for (int ls = 0; ls < cfg.max_line_search_halvings + 1; ++ls) {
+        if (count(S.ls_active) == 0) break;
+        k_axpy_env<<<nblk(W.n_dof, 256), 256, 0, st>>>(W, W.x, W.p, S.alpha, S.ls_active, W.xt);
+        world_pos(W.xt, xwt);
+        terms(W.xt, xwt, sweep, pb_sweep, false, h, S.ls_active, nullptr);
+        energy(W.xt, sweep, pb_sweep, S.ls_active, S.e_new);
+        k_ls_check<<<nblk(n_env, 128), 128, 0, st>>>(W, S, ls_count, cfg.max_line_search_halvings, accepted);
+        k_copy_env<<<nblk(W.n_dof, 256), 256, 0, st>>>(W, W.xt, W.x, accepted);
+      }
+    }
+    // envs still active after the iteration cap did not converge
+    k_mark_unconverged<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S);
+  }
+
+  Derivs D_with(const PairBufs& pb) {
+    Derivs d = D;
+    d.pt_g = pb.pt_g; d.pt_h = pb.pt_h; d.ee_g = pb.ee_g; d.ee_h = pb.ee_h;
+    d.pt_act = pb.pt_act; d.ee_act = pb.ee_act;
+    d.gnd_gy = pb.gnd_gy; d.gnd_hyy = pb.gnd_hyy;
+    return d;
+  }
+};
+
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* ipc_last_error(void) { return g_err.c_str(); }
+
+int ipc_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
+  ipc_world* w = nullptr;
+  try {
+    if (ipc_device_count() == 0) return set_err("no CUDA device");
+    w = new ipc_world();
+    Pool& P = w->pool;
+    World& W = w->W;
+    int ne = d->n_env;
+    w->n_env = ne;
+    W.n_env = ne; W.n_dof = d->n_dof; W.n_vert = d->n_vert; W.n_aff = d->n_aff; W.n_tet = d->n_tet;
+    W.n_slot = d->n_slot; W.n_tri = d->n_tri; W.n_edge = d->n_edge; W.n_cbody = d->n_cbody; W.n_cons = d->n_cons;
+    W.env_dof = P.upload(d->env_dof, ne + 1);
+    W.env_vert = P.upload(d->env_vert, ne + 1);
+    W.env_aff = P.upload(d->env_aff, ne + 1);
+    W.env_tet = P.upload(d->env_tet, ne + 1);
+    W.env_slot = P.upload(d->env_slot, ne + 1);
+    W.env_tri = P.upload(d->env_tri, ne + 1);
+    W.env_edge = P.upload(d->env_edge, ne + 1);
+    W.env_cbody = P.upload(d->env_cbody, ne + 1);
+    W.env_cons = P.upload(d->env_cons, ne + 1);
+    W.env_pairs = P.upload(d->env_pairs, ne);
+    W.env_has_ground = P.upload(d->env_has_ground, ne);
+    W.env_ground_y = P.upload(d->env_ground_y, ne);
+    W.env_gravity = P.upload(d->env_gravity, 3 * ne);
+    W.env_dhat = P.upload(d->env_dhat, ne);
+    W.env_kappa = P.upload(d->env_kappa, ne);
+    W.env_kappa0 = P.upload(d->env_kappa0, ne);
+    W.env_mu = P.upload(d->env_mu, ne);
+    W.env_epsv = P.upload(d->env_eps_v, ne);
+    // per-element env ids
+    auto expand = [&](const int32_t* pre, int n) {
+      std::vector<int> v(std::max(n, 1), 0);
+      for (int e = 0; e < ne; ++e)
+        for (int i = pre[e]; i < pre[e + 1]; ++i) v[i] = e;
+      return P.upload(v.data(), v.size());
+    };
+    W.dof_env = expand(d->env_dof, d->n_dof);
+    W.vert_env = expand(d->env_vert, d->n_vert);
+    W.aff_env = expand(d->env_aff, d->n_aff);
+    W.tet_env = expand(d->env_tet, d->n_tet);
+    W.slot_env = expand(d->env_slot, d->n_slot);
+    W.cons_env = expand(d->env_cons, d->n_cons);
+    W.x = P.upload(d->x0, d->n_dof);
+    W.v = P.upload(d->v0, d->n_dof);
+    W.x_prev = P.alloc<double>(d->n_dof);
+    W.xhat = P.alloc<double>(d->n_dof);
+    W.p = P.alloc<double>(d->n_dof);
+    W.xt = P.alloc<double>(d->n_dof);
+    W.grad = P.alloc<double>(d->n_dof);
+    W.vert_dof = P.upload(d->vert_dof, d->n_vert);
+    W.vert_mass = P.upload(d->vert_mass, d->n_vert);
+    W.aff_dof = P.upload(d->aff_dof, d->n_aff);
+    W.aff_M = P.upload(d->aff_M, 144 * (size_t)d->n_aff);
+    W.aff_acc = P.upload(d->aff_acc, 12 * (size_t)d->n_aff);
+    W.aff_ortho = P.upload(d->aff_ortho, d->n_aff);
+    W.tet_dof = (const int4*)P.upload(d->tet_dof, 4 * (size_t)d->n_tet);
+    W.tet_Dminv = P.upload(d->tet_Dminv, 9 * (size_t)d->n_tet);
+    W.tet_vol = P.upload(d->tet_vol, d->n_tet);
+    W.tet_mu = P.upload(d->tet_mu, d->n_tet);
+    W.tet_lam = P.upload(d->tet_lam, d->n_tet);
+    W.tet_model = P.upload(d->tet_model, d->n_tet);
+    W.slot_aff = P.upload(d->slot_aff, d->n_slot);
+    W.slot_dof = P.upload(d->slot_dof, d->n_slot);
+    W.slot_rest = P.upload(d->slot_rest, 3 * (size_t)d->n_slot);
+    W.slot_cbody = P.upload(d->slot_cbody, d->n_slot);
+    W.tri_v = (const int3*)P.upload(d->tri_v, 3 * (size_t)d->n_tri);
+    W.tri_cbody = P.upload(d->tri_cbody, d->n_tri);
+    W.edge_v = (const int2*)P.upload(d->edge_v, 2 * (size_t)d->n_edge);
+    W.edge_cbody = P.upload(d->edge_cbody, d->n_edge);
+    W.edge_len2 = P.upload(d->edge_len2, d->n_edge);
+    W.cbody_rigid = P.upload(d->cbody_rigid, d->n_cbody);
+    W.cbody_kin = P.upload(d->cbody_kin, d->n_cbody);
+    W.cbody_excl = (const unsigned long long*)P.upload(d->cbody_excl, d->n_cbody);
+    W.cons_aff = P.upload(d->cons_aff, d->n_cons);
+    W.cons_kappa0 = P.upload(d->cons_kappa0, d->n_cons);
+    W.cons_kappa = P.upload(d->cons_kappa0, d->n_cons);
+    W.cons_mass = P.upload(d->cons_mass, d->n_cons);
+    W.cons_target = P.alloc<double>(12 * (size_t)d->n_cons);
+    W.cons_lam = P.alloc<double>(12 * (size_t)d->n_cons);
+    W.cons_lastres = P.alloc<double>(d->n_cons);
+    W.xw = P.alloc<double>(3 * (size_t)d->n_slot);
+    W.xw0 = P.alloc<double>(3 * (size_t)d->n_slot);
+    W.dxw = P.alloc<double>(3 * (size_t)d->n_slot);
+    w->xwt = P.alloc<double>(3 * (size_t)d->n_slot);
+    w->xlo = P.alloc<double>(3 * (size_t)d->n_slot);
+    w->xhi = P.alloc<double>(3 * (size_t)d->n_slot);
+    w->slot_force = P.alloc<double>(3 * (size_t)d->n_slot);
+    w->d_targets = P.alloc<double>(12 * (size_t)d->n_cons);
+    w->h_env_slot.assign(d->env_slot, d->env_slot + ne + 1);
+    w->h_env_dof.assign(d->env_dof, d->env_dof + ne + 1);
+    w->h_env_tri.assign(d->env_tri, d->env_tri + ne + 1);
+    w->h_env_edge.assign(d->env_edge, d->env_edge + ne + 1);
+    w->h_env_cbody.assign(d->env_cbody, d->env_cbody + ne + 1);
+    for (int e = 0; e < ne; ++e) {
+      w->max_env_dof = std::max(w->max_env_dof, d->env_dof[e + 1] - d->env_dof[e]);
+      if (d->env_cbody[e + 1] - d->env_cbody[e] > 64)
+        throw std::runtime_error("more than 64 collision bodies in one environment");
+    }
+    const int DENSE_MAX = 160;
+    if (w->max_env_dof > DENSE_MAX)
+      throw std::runtime_error("environment exceeds the dense-solve DoF limit (sparse PCG path not built)");
+    size_t smem = (size_t)(w->max_env_dof * w->max_env_dof + 2 * w->max_env_dof) * sizeof(double);
+    CK(cudaFuncSetAttribute(k_dense_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // env scalar state
+    EnvState& S = w->S;
+    S.e0 = P.alloc<double>(ne); S.e_new = P.alloc<double>(ne); S.alpha = P.alloc<double>(ne);
+    S.alpha_max = P.alloc<double>(ne); S.pnorm = P.alloc<double>(ne); S.prev_pnorm = P.alloc<double>(ne);
+    S.gnorm = P.alloc<double>(ne); S.min_s_before = P.alloc<double>(ne); S.min_s = P.alloc<double>(ne);
+    S.res = P.alloc<double>(ne);
+    S.small_run = P.alloc<int>(ne); S.newton_active = P.alloc<int>(ne); S.ls_active = P.alloc<int>(ne);
+    S.al_active = P.alloc<int>(ne); S.ls_failed = P.alloc<int>(ne); S.converged = P.alloc<int>(ne);
+    S.newton_iters = P.alloc<int>(ne); S.ccd_calls = P.alloc<int>(ne); S.al_outer = P.alloc<int>(ne);
+    S.err = P.alloc<int>(ne); S.any = P.alloc<int>(1);
+    w->ok = P.alloc<int>(ne); w->al_flag = S.al_active; w->accepted = P.alloc<int>(ne);
+    w->ls_count = P.alloc<int>(ne); w->d_count = P.alloc<int>(1);
+    w->env_alpha = P.alloc<double>(ne);
+    CK(cudaMallocHost(&w->h_count, sizeof(int)));
+    // capacities: exhaustive for small envs, bounded for large ones
+    std::vector<long long> ptc(ne), eec(ne);
+    for (int e = 0; e < ne; ++e) {
+      long long nv = d->env_slot[e + 1] - d->env_slot[e], nt = d->env_tri[e + 1] - d->env_tri[e];
+      long long nE = d->env_edge[e + 1] - d->env_edge[e];
+      ptc[e] = d->env_pairs[e] ? std::min(nv * nt, std::max(4096LL, 16 * (nv + nt))) : 0;
+      eec[e] = d->env_pairs[e] ? std::min(nE * nE, std::max(4096LL, 16 * nE)) : 0;
+    }
+    w->alloc_cands(w->dcd, ptc, eec);
+    w->alloc_cands(w->sweep, ptc, eec);
+    w->alloc_pairbufs(w->pb_dcd, w->dcd, true);
+    w->alloc_pairbufs(w->pb_sweep, w->sweep, false);
+    w->alloc_lags();
+    w->body_val = P.alloc<double>(d->n_aff);
+    w->D.body_g = P.alloc<double>(12 * (size_t)d->n_aff);
+    w->D.body_h = P.alloc<double>(144 * (size_t)d->n_aff);
+    w->tet_val = P.alloc<double>(d->n_tet);
+    w->D.tet_g = P.alloc<double>(12 * (size_t)d->n_tet);
+    w->D.tet_h = P.alloc<double>(PK * (size_t)d->n_tet);
+    CK(cudaStreamCreateWithFlags(&w->st, cudaStreamNonBlocking));
+    CK(cudaDeviceSynchronize());
+    *out = w;
+    return 0;
+  } catch (const std::exception& ex) {
+    delete w;
+    return set_err("%s", ex.what());
+  }
+}
+
+int ipc_world_destroy(ipc_world* w) {
+  if (w) {
+    cudaStreamSynchronize(w->st);
+    if (w->st) cudaStreamDestroy(w->st);
+    delete w;
+  }
+  return 0;
+}
+
+int ipc_world_step(ipc_world* w, const ipc_step_config* cfg, const double* targets, ipc_step_report* rep) {
+  GUARD({
+    World& W = w->W;
+    EnvState& S = w->S;
+    cudaStream_t st = w->st;
+    int ne = w->n_env;
+    double h = cfg->h;
+    if (targets && W.n_cons) {
+      w->h_targets.assign(targets, targets + 12 * (size_t)W.n_cons);
+      w->targets_set = true;
+    }
+    std::vector<double>& tg = w->h_targets;
+    k_step_begin<<<nblk(ne, 128), 128, 0, st>>>(ne, S);
+    CK(cudaMemcpyAsync(W.x_prev, W.x, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, st));
+    w->world_pos(W.x, W.xw0);
+    int* all = w->ok;
+    k_fill_int<<<nblk(ne, 128), 128, 0, st>>>(ne, all, 1);
+    w->broad(w->dcd, w->pb_dcd, true, W.xw0, W.xw0, nullptr);
+    // feasibility of the incoming state (ref solver.py:372-385)
+    k_pairs<<<dim3(nblk(w->dcd.max_pt_cap, 64), ne), 64, 0, st>>>(W, W.xw0, w->dcd.c, 0, 0, nullptr,
+                                                                  w->pb_dcd.pt_val, nullptr, nullptr, nullptr, nullptr);
+    k_pairs<<<dim3(nblk(w->dcd.max_ee_cap, 64), ne), 64, 0, st>>>(W, W.xw0, w->dcd.c, 1, 0, nullptr,
+                                                                  w->pb_dcd.ee_val, nullptr, nullptr, nullptr, nullptr);
+    int max_slots = 0;
+    for (int e = 0; e < ne; ++e) max_slots = std::max(max_slots, w->h_env_slot[e + 1] - w->h_env_slot[e]);
+    k_ground<<<dim3(nblk(max_slots, 128), ne), 128, 0, st>>>(W, W.xw0, w->dcd.c, 0, nullptr, w->pb_dcd.gnd_val,
+                                                             nullptr, nullptr, nullptr);
+    k_start_check<<<ne, 128, 0, st>>>(W, S, w->dcd.c, w->pb_dcd.pt_val, w->pb_dcd.ee_val, w->pb_dcd.gnd_val, w->ok);
+    // predictor
+    k_predictor<<<nblk(W.n_dof, 256), 256, 0, st>>>(W, h);
+    k_predictor_forces<<<nblk(std::max(W.n_vert, W.n_aff), 128), 128, 0, st>>>(W, h);
+    // fresh AL cycle per step (ref solver.py:394-400)
+    if (W.n_cons) {
+      if (!w->targets_set) throw std::runtime_error("kinematic constraint targets were never set");
+      CK(cudaMemcpyAsync(w->d_targets, tg.data(), tg.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+      k_cons_reset<<<nblk(W.n_cons, 128), 128, 0, st>>>(W, w->d_targets);
+    }
+    int fp_iters = std::max(cfg->friction_fixed_point_iters, 1);
+    for (int fp = 0; fp < fp_iters; ++fp) {
+      // lags frozen at the anchor (x_prev first, then the current iterate)
+      if (w->lags_stale) {
+        w->alloc_lags();
+        w->lags_stale = false;
+      }
+      if (fp == 0) {
+        k_lags<<<ne, BP_THREADS, 0, st>>>(W, W.xw0, w->dcd.c, w->L, w->ok);
+      } else {
+        w->world_pos(W.x, W.xw);
+        w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, w->ok);
+        k_lags<<<ne, BP_THREADS, 0, st>>>(W, W.xw, w->dcd.c, w->L, w->ok);
+      }
+      k_copy_int<<<nblk(ne, 128), 128, 0, st>>>(ne, w->ok, S.al_active);
+      for (int outer = 0; outer < cfg->al_max_outer; ++outer) {
+        if (w->count(S.al_active) == 0) break;
+        w->newton_solve(*cfg);
+        k_al_update<<<nblk(ne, 128), 128, 0, st>>>(W, S, outer);
+      }
+      k_and_not<<<nblk(ne, 128), 128, 0, st>>>(ne, w->ok, S.ls_failed);
+    }
+    // post-step distance and barrier adaptation (ref solver.py:440-450)
+    k_copy_int<<<nblk(ne, 128), 128, 0, st>>>(ne, S.err, w->accepted);
+    k_fill_int<<<nblk(ne, 128), 128, 0, st>>>(ne, w->ok, 1);
+    k_and_not<<<nblk(ne, 128), 128, 0, st>>>(ne, w->ok, w->accepted);
+    w->world_pos(W.x, W.xw);
+    w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, w->ok);
+    k_fill<<<nblk(ne, 128), 128, 0, st>>>(ne, S.min_s, INFINITY);
+    k_pairs<<<dim3(nblk(w->dcd.max_pt_cap, 64), ne), 64, 0, st>>>(W, W.xw, w->dcd.c, 0, 0, w->ok, w->pb_dcd.pt_val,
+                                                                  nullptr, nullptr, nullptr, S.min_s);
+    k_pairs<<<dim3(nblk(w->dcd.max_ee_cap, 64), ne), 64, 0, st>>>(W, W.xw, w->dcd.c, 1, 0, w->ok, w->pb_dcd.ee_val,
+                                                                  nullptr, nullptr, nullptr, S.min_s);
+    k_ground<<<dim3(nblk(max_slots, 128), ne), 128, 0, st>>>(W, W.xw, w->dcd.c, 0, w->ok, w->pb_dcd.gnd_val,
+                                                             nullptr, nullptr, S.min_s);
+    k_kappa_adapt<<<nblk(ne, 128), 128, 0, st>>>(W, S, w->ok);
+    k_finalize<<<nblk(W.n_dof, 256), 256, 0, st>>>(W, h, w->ok);
+    CK(cudaGetLastError());
+    if (rep) {
+      std::vector<int> it(ne), cc(ne), cv(ne), lf(ne), ao(ne), er(ne);
+      std::vector<double> gn(ne), mb(ne), ma(ne), kp(ne);
+      CK(cudaMemcpyAsync(it.data(), S.newton_iters, 4 * ne, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(cc.data(), S.ccd_calls, 4 * ne, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(cv.data(), S.converged, 4 * ne, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(lf.data(), S.ls_failed, 4 * ne, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(ao.data(), S.al_outer, 4 * ne, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(er.data(), S.err, 4 * ne, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(gn.data(), S.gnorm, 8 * ne, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(mb.data(), S.min_s_before, 8 * ne, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(ma.data(), S.min_s, 8 * ne, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(kp.data(), W.env_kappa, 8 * ne, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int e = 0; e < ne; ++e) {
+        rep[e].newton_iters = it[e];
+        rep[e].ccd_invocations = cc[e];
+        rep[e].converged = cv[e];
+        rep[e].line_search_failed = lf[e];
+        rep[e].al_outer = ao[e];
+        rep[e].error = er[e];
+        rep[e].final_grad_norm = gn[e];
+        rep[e].min_dist_before = std::isinf(mb[e]) ? INFINITY : std::sqrt(mb[e]);
+        rep[e].min_dist_after = ma[e];
+        rep[e].kappa = kp[e];
+      }
+    } else {
+      CK(cudaStreamSynchronize(st));
+    }
+  })
+}
+
+int ipc_world_get_state(ipc_world* w, double* x, double* v) {
+  GUARD({
+    if (x) CK(cudaMemcpyAsync(x, w->W.x, sizeof(double) * w->W.n_dof, cudaMemcpyDeviceToHost, w->st));
+    if (v) CK(cudaMemcpyAsync(v, w->W.v, sizeof(double) * w->W.n_dof, cudaMemcpyDeviceToHost, w->st));
+    CK(cudaStreamSynchronize(w->st));
+  })
+}
+
+int ipc_world_set_state(ipc_world* w, const double* x, const double* v) {
+  GUARD({
+    if (x) CK(cudaMemcpyAsync(w->W.x, x, sizeof(double) * w->W.n_dof, cudaMemcpyHostToDevice, w->st));
+    if (v) CK(cudaMemcpyAsync(w->W.v, v, sizeof(double) * w->W.n_dof, cudaMemcpyHostToDevice, w->st));
+    CK(cudaStreamSynchronize(w->st));
+  })
+}
+
+int ipc_world_state_device(ipc_world* w, double** x, double** v) {
+  if (x) *x = w->W.x;
+  if (v) *v = w->W.v;
+  return 0;
+}
+
+int ipc_world_get_kappa(ipc_world* w, double* kappa) {
+  GUARD({
+    CK(cudaMemcpy(kappa, w->W.env_kappa, sizeof(double) * w->n_env, cudaMemcpyDeviceToHost));
+  })
+}
+
+int ipc_world_set_kappa(ipc_world* w, const double* kappa) {
+  GUARD({
+    CK(cudaMemcpy(w->W.env_kappa, kappa, sizeof(double) * w->n_env, cudaMemcpyHostToDevice));
+  })
+}
+
+int ipc_world_get_constraints(ipc_world* w, double* lam, double* kappa) {
+  GUARD({
+    if (lam) CK(cudaMemcpy(lam, w->W.cons_lam, sizeof(double) * 12 * w->W.n_cons, cudaMemcpyDeviceToHost));
+    if (kappa) CK(cudaMemcpy(kappa, w->W.cons_kappa, sizeof(double) * w->W.n_cons, cudaMemcpyDeviceToHost));
+  })
+}
+
+// DCD candidates + contact derivatives at the current state (for sensing)
+static void contact_at_current(ipc_world* w) {
+  World& W = w->W;
+  int ne = w->n_env;
+  w->world_pos(W.x, W.xw);
+  w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, nullptr);
+  k_pairs<<<dim3(nblk(w->dcd.max_pt_cap, 64), ne), 64, 0, w->st>>>(W, W.xw, w->dcd.c, 0, 1, nullptr, w->pb_dcd.pt_val,
+                                                                   w->pb_dcd.pt_g, w->pb_dcd.pt_h, w->pb_dcd.pt_act,
+                                                                   nullptr);
+  k_pairs<<<dim3(nblk(w->dcd.max_ee_cap, 64), ne), 64, 0, w->st>>>(W, W.xw, w->dcd.c, 1, 1, nullptr, w->pb_dcd.ee_val,
+                                                                   w->pb_dcd.ee_g, w->pb_dcd.ee_h, w->pb_dcd.ee_act,
+                                                                   nullptr);
+  int max_slots = 0;
+  for (int e = 0; e < ne; ++e) max_slots = std::max(max_slots, w->h_env_slot[e + 1] - w->h_env_slot[e]);
+  k_ground<<<dim3(nblk(max_slots, 128), ne), 128, 0, w->st>>>(W, W.xw, w->dcd.c, 1, nullptr, w->pb_dcd.gnd_val,
+                                                              w->pb_dcd.gnd_gy, w->pb_dcd.gnd_hyy, nullptr);
+  k_slot_forces<<<nblk(W.n_slot, 128), 128, 0, w->st>>>(W, w->dcd.c, w->pb_dcd.pt_g, w->pb_dcd.pt_act,
+                                                        w->pb_dcd.ee_g, w->pb_dcd.ee_act, w->pb_dcd.gnd_gy, 1.0,
+                                                        w->slot_force);
+  CK(cudaGetLastError());
+}
+
+int ipc_world_slot_forces(ipc_world* w, double h, double* out) {
+  GUARD({
+    contact_at_current(w);
+    std::vector<double> f(3 * (size_t)w->W.n_slot);
+    CK(cudaMemcpyAsync(f.data(), w->slot_force, sizeof(double) * f.size(), cudaMemcpyDeviceToHost, w->st));
+    CK(cudaStreamSynchronize(w->st));
+    double ih = 1.0 / (h * h);
+    for (size_t i = 0; i < f.size(); ++i) out[i] = f[i] * ih;  // slot_force holds -g (h = 1 pass)
+  })
+}
+
+int ipc_world_group_forces(ipc_world* w, double h, const uint64_t* groups, int ng, double* out) {
+  GUARD({
+    contact_at_current(w);
+    size_t n = (size_t)w->n_env * ng;
+    unsigned long long* dg = w->pool.upload((const unsigned long long*)groups, n);
+    double* dout = w->pool.alloc<double>(3 * n);
+    k_group_forces<<<nblk(n, 128), 128, 0, w->st>>>(w->W, w->slot_force, dg, ng, dout);
+    CK(cudaMemcpyAsync(out, dout, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, w->st));
+    CK(cudaStreamSynchronize(w->st));
+    double ih = 1.0 / (h * h);
+    for (size_t i = 0; i < 3 * n; ++i) out[i] *= ih;
+    w->pool.free_one(dg);
+    w->pool.free_one(dout);
+  })
+}
+
+int ipc_world_candidates(ipc_world* w, int env, int which, int32_t* out, int64_t cap, int64_t* n) {
+  GUARD({
+    World& W = w->W;
+    w->world_pos(W.x, W.xw);
+    w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, nullptr);
+    int cnt = 0;
+    const int* src = which == 0 ? w->dcd.c.n_pt : (which == 1 ? w->dcd.c.n_ee : w->dcd.c.n_gnd);
+    CK(cudaMemcpy(&cnt, src + env, sizeof(int), cudaMemcpyDeviceToHost));
+    *n = cnt;
+    long long m = std::min<long long>(cnt, cap);
+    if (which == 0) {
+      long long off = 0;
+      CK(cudaMemcpy(&off, w->dcd.d_pt_off + env, sizeof(long long), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(out, w->dcd.c.pt + off, 8 * m, cudaMemcpyDeviceToHost));
+    } else if (which == 1) {
+      long long off = 0;
+      CK(cudaMemcpy(&off, w->dcd.d_ee_off + env, sizeof(long long), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(out, w->dcd.c.ee + off, 8 * m, cudaMemcpyDeviceToHost));
+    } else {
+      CK(cudaMemcpy(out, w->dcd.c.gnd + w->h_env_slot[env], 4 * m, cudaMemcpyDeviceToHost));
+    }
+  })
+}
+
+int ipc_world_min_distance(ipc_world* w, double* out) {
+  GUARD({
+    World& W = w->W;
+    int ne = w->n_env;
+    w->world_pos(W.x, W.xw);
+    w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, nullptr);
+    double* d = w->S.min_s_before;  // scratch
+    k_fill<<<nblk(ne, 128), 128, 0, w->st>>>(ne, d, INFINITY);
+    k_pairs<<<dim3(nblk(w->dcd.max_pt_cap, 64), ne), 64, 0, w->st>>>(W, W.xw, w->dcd.c, 0, 0, nullptr,
+                                                                     w->pb_dcd.pt_val, nullptr, nullptr, nullptr, d);
+    k_pairs<<<dim3(nblk(w->dcd.max_ee_cap, 64), ne), 64, 0, w->st>>>(W, W.xw, w->dcd.c, 1, 0, nullptr,
+                                                                     w->pb_dcd.ee_val, nullptr, nullptr, nullptr, d);
+    int max_slots = 0;
+    for (int e = 0; e < ne; ++e) max_slots = std::max(max_slots, w->h_env_slot[e + 1] - w->h_env_slot[e]);
+    k_ground<<<dim3(nblk(max_slots, 128), ne), 128, 0, w->st>>>(W, W.xw, w->dcd.c, 0, nullptr, w->pb_dcd.gnd_val,
+                                                                nullptr, nullptr, d);
+    std::vector<double> s(ne);
+    CK(cudaMemcpyAsync(s.data(), d, 8 * ne, cudaMemcpyDeviceToHost, w->st));
+    CK(cudaStreamSynchronize(w->st));
+    for (int e = 0; e < ne; ++e) out[e] = std::isinf(s[e]) ? INFINITY : std::sqrt(s[e]);
+  })
+}
+
+int ipc_world_group_distance(ipc_world* w, const uint64_t* ga, const uint64_t* gb, double* out) {
+  GUARD({
+    World& W = w->W;
+    int ne = w->n_env;
+    w->world_pos(W.x, W.xw);
+    w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, nullptr);
+    unsigned long long* da = w->pool.upload((const unsigned long long*)ga, ne);
+    unsigned long long* db = w->pool.upload((const unsigned long long*)gb, ne);
+    double* dout = w->pool.alloc<double>(ne);
+    k_group_distance<<<ne, 256, 0, w->st>>>(W, w->dcd.c, W.xw, da, db, dout);
+    CK(cudaMemcpyAsync(out, dout, 8 * ne, cudaMemcpyDeviceToHost, w->st));
+    CK(cudaStreamSynchronize(w->st));
+    w->pool.free_one(da);
+    w->pool.free_one(db);
+    w->pool.free_one(dout);
+  })
+}
+
+int ipc_world_ground_distance(ipc_world* w, const uint64_t* g, double* out) {
+  GUARD({
+    World& W = w->W;
+    int ne = w->n_env;
+    w->world_pos(W.x, W.xw);
+    unsigned long long* dg = w->pool.upload((const unsigned long long*)g, ne);
+    double* dout = w->pool.alloc<double>(ne);
+    k_ground_distance<<<nblk(ne, 128), 128, 0, w->st>>>(W, W.xw, dg, dout);
+    CK(cudaMemcpyAsync(out, dout, 8 * ne, cudaMemcpyDeviceToHost, w->st));
+    CK(cudaStreamSynchronize(w->st));
+    w->pool.free_one(dg);
+    w->pool.free_one(dout);
+  })
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// kernel-level entry points for parity tests
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_t_dist(int kind, long long n, const double* st, int* region, double* s, double* g, double* h) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  V3 X[4];
+  for (int a = 0; a < 4; ++a) X[a] = ld3(st + 12 * i + 3 * a);
+  bool par;
+  int r = kind == 0 ? pt_region(X[0], X[1], X[2], X[3]) : ee_region(X[0], X[1], X[2], X[3], &par);
+  double G[12], H[144];
+  for (int k = 0; k < 12; ++k) G[k] = 0.0;
+  for (int k = 0; k < 144; ++k) H[k] = 0.0;
+  int mask;
+  s[i] = dist2_derivs(kind == 0, r, X, G, H, &mask);
+  region[i] = r;
+  for (int k = 0; k < 12; ++k) g[12 * i + k] = G[k];
+  for (int k = 0; k < 144; ++k) h[144 * i + k] = H[k];
+}
+__global__ void k_t_ccd(int kind, long long n, const double* px, const double* pdx, double cons, double* a) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  V3 X[4], D[4];
+  for (int k = 0; k < 4; ++k) {
+    X[k] = ld3(px + 12 * i + 3 * k);
+    D[k] = ld3(pdx + 12 * i + 3 * k);
+  }
+  a[i] = pair_ccd_alpha(kind, X, D, cons);
+}
+template <int N>
+__global__ void k_t_psd(long long n, double* m) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) psd_project<N>(m + (long long)N * N * i, N);
+}
+__global__ void k_t_elastic(int model, long long n, const double* F, double mu, double lam, double* psi, double* P,
+                            double* H9) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  M3 f;
+  for (int k = 0; k < 9; ++k) f.m[k] = F[9 * i + k];
+  double ps, p[9], h[81];
+  if (!psi_derivs(model, f, mu, lam, &ps, p, h)) {
+    psi[i] = INFINITY;
+    return;
+  }
+  psi[i] = ps;
+  for (int k = 0; k < 9; ++k) P[9 * i + k] = p[k];
+  for (int k = 0; k < 81; ++k) H9[81 * i + k] = h[k];
+}
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  explicit DBuf(size_t n_) : n(n_) { CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T))); }
+  DBuf(const T* h, size_t n_) : DBuf(n_) {
+    if (n) CK(cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void get(T* h) const {
+    if (n) CK(cudaMemcpy(h, p, n * sizeof(T), cudaMemcpyDeviceToHost));
+  }
+  ~DBuf() { cudaFree(p); }
+};
+}  // namespace
+
+extern "C" {
+int ipc_dist2_derivs(int kind, int64_t n, const double* st, int32_t* region, double* s, double* g, double* h) {
+  GUARD({
+    DBuf<double> dst(st, 12 * n), ds(n), dg(12 * n), dh(144 * n);
+    DBuf<int> dr(n);
+    k_t_dist<<<nblk(n, 64), 64>>>(kind, n, dst.p, dr.p, ds.p, dg.p, dh.p);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    dr.get(region); ds.get(s); dg.get(g); dh.get(h);
+  })
+}
+int ipc_ccd_pairs(int kind, int64_t n, const double* px, const double* pdx, double cons, double* alpha) {
+  GUARD({
+    DBuf<double> a(px, 12 * n), b(pdx, 12 * n), o(n);
+    k_t_ccd<<<nblk(n, 64), 64>>>(kind, n, a.p, b.p, cons, o.p);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    o.get(alpha);
+  })
+}
+int ipc_psd_project(int dim, int64_t n, double* mats) {
+  GUARD({
+    DBuf<double> m(mats, (size_t)dim * dim * n);
+    if (dim == 6) k_t_psd<6><<<nblk(n, 64), 64>>>(n, m.p);
+    else if (dim == 9) k_t_psd<9><<<nblk(n, 64), 64>>>(n, m.p);
+    else if (dim == 12) k_t_psd<12><<<nblk(n, 64), 64>>>(n, m.p);
+    else throw std::runtime_error("psd_project: dim must be 6, 9 or 12");
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    m.get(mats);
+  })
+}
+int ipc_elastic_eval(int model, int64_t n, const double* F, double mu, double lam, double* psi, double* P, double* H9) {
+  GUARD({
+    DBuf<double> f(F, 9 * n), ps(n), p(9 * n), h(81 * n);
+    k_t_elastic<<<nblk(n, 64), 64>>>(model, n, f.p, mu, lam, ps.p, p.p, h.p);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    ps.get(psi); p.get(P); h.get(H9);
+  })
+}
+}  // extern "C"

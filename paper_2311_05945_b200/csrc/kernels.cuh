@@ -1,0 +1,778 @@
+// Kernels of the batched IPC time step. See DESIGN.md for the data flow.
+#pragma once
+#include "ipc_math.cuh"
+#include "world.cuh"
+
+namespace ipc {
+
+constexpr int PK = 78;  // packed upper triangle of a 12x12 block
+
+IPC_HD int pk(int i, int j) {  // i <= j
+  return i * 12 - (i * (i - 1)) / 2 + (j - i);
+}
+IPC_HD double pk_get(const double* h, int i, int j) { return i <= j ? h[pk(i, j)] : h[pk(j, i)]; }
+
+IPC_HD void atomic_min_pos(double* addr, double v) {
+  // non-negative doubles order like their int64 bit patterns
+  atomicMin(reinterpret_cast<long long*>(addr), __double_as_longlong(v));
+}
+
+// ---------------------------------------------------------------------------
+// world-space slot positions: soft slots copy their DoF, affine slots
+// p + A x0 with numpy's operation order (ref contact.py:296)
+// ---------------------------------------------------------------------------
+__global__ void k_world(World W, const double* __restrict__ x, double* __restrict__ xw) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= W.n_slot) return;
+  int d = W.slot_dof[s];
+  if (!W.slot_aff[s]) {
+    xw[3 * s] = x[d];
+    xw[3 * s + 1] = x[d + 1];
+    xw[3 * s + 2] = x[d + 2];
+    return;
+  }
+  const double* r = W.slot_rest + 3 * s;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double* a = x + d + 3 + 3 * i;
+    double m = __dadd_rn(__dadd_rn(__dmul_rn(a[0], r[0]), __dmul_rn(a[1], r[1])), __dmul_rn(a[2], r[2]));
+    xw[3 * s + i] = __dadd_rn(x[d + i], m);
+  }
+}
+
+// out = a + alpha_e * b over DoFs of envs with flag set (others copy a)
+__global__ void k_axpy_env(World W, const double* a, const double* b, const double* alpha,
+                           const int* flag, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= W.n_dof) return;
+  int e = W.dof_env[i];
+  out[i] = (flag == nullptr || flag[e]) ? __dadd_rn(a[i], __dmul_rn(alpha ? alpha[e] : 1.0, b[i])) : a[i];
+}
+
+__global__ void k_sub(int n, const double* a, const double* b, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __dsub_rn(a[i], b[i]);
+}
+
+// ---------------------------------------------------------------------------
+// broad phase: exhaustive box tests, one CTA per environment, ordered
+// compaction (lexicographic output, ref broadphase.py:162-166). Boxes:
+// query box [lo, hi] vs primitive box inflated by `margin` (ref bvh.py:306).
+// ---------------------------------------------------------------------------
+template <int NT>
+__device__ int block_ordered_offset(bool hit, int* warp_tot, int* total) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned m = __ballot_sync(0xffffffffu, hit);
+  int pre = __popc(m & ((1u << lane) - 1u));
+  if (lane == 0) warp_tot[wid] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int w = 0; w < NT / 32; ++w) {
+      int t = warp_tot[w];
+      warp_tot[w] = acc;
+      acc += t;
+    }
+    *total = acc;
+  }
+  __syncthreads();
+  return warp_tot[wid] + pre;
+}
+
+__device__ __forceinline__ bool box_hit(const double* qlo, const double* qhi, const double* plo,
+                                        const double* phi, double margin) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double pmin = __dsub_rn(plo[c], margin), pmax = __dadd_rn(phi[c], margin);
+    if (!(qlo[c] <= pmax && qhi[c] >= pmin)) return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool excluded(const World& W, int cb0, int b1, int b2) {
+  unsigned long long m = W.cbody_excl[b1];
+  return (m >> (b2 - cb0)) & 1ull;
+}
+
+constexpr int BP_THREADS = 256;
+
+// kind 0: PT, 1: EE, 2: ground
+__global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __restrict__ lo,
+                                                       const double* __restrict__ hi, Cands C,
+                                                       int kind, const int* env_mask) {
+  __shared__ int warp_tot[BP_THREADS / 32];
+  __shared__ int total;
+  int e = blockIdx.x;
+  if (env_mask && !env_mask[e]) return;
+  double margin = W.env_dhat[e];
+  int s0 = W.env_slot[e], s1 = W.env_slot[e + 1];
+  int cb0 = W.env_cbody[e];
+  if (kind == 2) {
+    int base = 0;
+    if (!W.env_has_ground[e]) {
+      if (threadIdx.x == 0) C.n_gnd[e] = 0;
+      return;
+    }
+    double lim = __dadd_rn(W.env_ground_y[e], margin);
+    int off = C.gnd_off[e];
+    for (int s = s0; s < s1; s += BP_THREADS) {
+      int v = s + threadIdx.x;
+      bool hit = v < s1 && lo[3 * v + 1] < lim && !W.cbody_kin[W.slot_cbody[v]];
+      int o = block_ordered_offset<BP_THREADS>(hit, warp_tot, &total);
+      if (hit) C.gnd[off + base + o] = v;
+      base += total;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) C.n_gnd[e] = base;
+    return;
+  }
+  if (!W.env_pairs[e]) {
+    if (threadIdx.x == 0) {
+      if (kind == 0) C.n_pt[e] = 0; else C.n_ee[e] = 0;
+    }
+    return;
+  }
+  long long cap, off;
+  long long n_items;
+  int t0, nt;
+  if (kind == 0) {
+    t0 = W.env_tri[e];
+    nt = W.env_tri[e + 1] - t0;
+    n_items = (long long)(s1 - s0) * nt;
+    off = C.pt_off[e];
+    cap = C.pt_off[e + 1] - off;
+  } else {
+    t0 = W.env_edge[e];
+    nt = W.env_edge[e + 1] - t0;
+    n_items = (long long)nt * nt;
+    off = C.ee_off[e];
+    cap = C.ee_off[e + 1] - off;
+  }
+  long long base = 0;
+  for (long long k0 = 0; k0 < n_items; k0 += BP_THREADS) {
+    long long k = k0 + threadIdx.x;
+    bool hit = false;
+    int a = 0, b = 0;
+    if (k < n_items) {
+      a = (int)(k / nt);
+      b = (int)(k - (long long)a * nt);
+      if (kind == 0) {
+        int v = s0 + a, t = t0 + b;
+        int3 tv = W.tri_v[t];
+        double plo[3], phi[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          plo[c] = fmin(fmin(lo[3 * tv.x + c], lo[3 * tv.y + c]), lo[3 * tv.z + c]);
+          phi[c] = fmax(fmax(hi[3 * tv.x + c], hi[3 * tv.y + c]), hi[3 * tv.z + c]);
+        }
+        hit = box_hit(lo + 3 * v, hi + 3 * v, plo, phi, margin);
+        if (hit) {
+          int bv = W.slot_cbody[v], bt = W.tri_cbody[t];
+          bool adj = tv.x == v || tv.y == v || tv.z == v;
+          bool same = bv == bt && W.cbody_rigid[bv];
+          hit = !(adj || same || excluded(W, cb0, bv, bt));
+        }
+        a = v;
+        b = t;
+      } else if (b > a) {
+        int i = t0 + a, j = t0 + b;
+        int2 ei = W.edge_v[i], ej = W.edge_v[j];
+        double qlo[3], qhi[3], plo[3], phi[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          qlo[c] = fmin(lo[3 * ei.x + c], lo[3 * ei.y + c]);
+          qhi[c] = fmax(hi[3 * ei.x + c], hi[3 * ei.y + c]);
+          plo[c] = fmin(lo[3 * ej.x + c], lo[3 * ej.y + c]);
+          phi[c] = fmax(hi[3 * ej.x + c], hi[3 * ej.y + c]);
+        }
+        hit = box_hit(qlo, qhi, plo, phi, margin);
+        if (hit) {
+          bool shared = ei.x == ej.x || ei.x == ej.y || ei.y == ej.x || ei.y == ej.y;
+          int ba = W.edge_cbody[i], bb = W.edge_cbody[j];
+          bool same = ba == bb && W.cbody_rigid[ba];
+          hit = !(shared || same || excluded(W, cb0, ba, bb));
+        }
+        a = i;
+        b = j;
+      }
+    }
+    int o = block_ordered_offset<BP_THREADS>(hit, warp_tot, &total);
+    if (hit) {
+      long long dst = base + o;
+      if (dst < cap) {
+        if (kind == 0) C.pt[off + dst] = make_int2(a, b);
+        else C.ee[off + dst] = make_int2(a, b);
+      }
+    }
+    base += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (base > cap) {
+      atomicExch(C.overflow, 1);
+      base = cap;
+    }
+    if (kind == 0) C.n_pt[e] = (int)base; else C.n_ee[e] = (int)base;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// element terms. Outputs per element: value, gradient, packed Hessian.
+// ---------------------------------------------------------------------------
+
+// per affine body: inertia + h² orthogonality (projected) + kinematic target
+__global__ void k_body(World W, const double* __restrict__ x, const double* __restrict__ xhat,
+                       double h2, int deriv, const int* env_flag, double* val, double* g12,
+                       double* h144) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= W.n_aff) return;
+  int e = W.aff_env[b];
+  if (env_flag && !env_flag[e]) return;
+  int o = W.aff_dof[b];
+  const double* M = W.aff_M + 144 * b;
+  double d[12];
+  for (int i = 0; i < 12; ++i) d[i] = x[o + i] - xhat[o + i];
+  double g[12];
+  double v = 0.0;
+  for (int i = 0; i < 12; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < 12; ++j) s += M[12 * i + j] * d[j];
+    g[i] = s;
+    v += d[i] * s;
+  }
+  v *= 0.5;
+  // orthogonality coeff ||A A^T - I||^2 (ref terms.py:234)
+  double c = W.aff_ortho[b];
+  M3 A;
+  for (int i = 0; i < 9; ++i) A.m[i] = x[o + 3 + i];
+  M3 Mm = m3_mul(A, m3_T(A));
+  m3_add_diag(Mm, -1.0);
+  double ov = 0.0;
+  for (int i = 0; i < 9; ++i) ov += Mm.m[i] * Mm.m[i];
+  v += h2 * c * ov;
+  double H[144];
+  if (deriv) {
+    M3 MA = m3_mul(Mm, A);
+    for (int i = 0; i < 9; ++i) g[3 + i] += h2 * 4.0 * c * MA.m[i];
+    M3 ata = m3_tmul(A, A);
+    double h9[81];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        for (int k = 0; k < 3; ++k)
+          for (int l = 0; l < 3; ++l) {
+            double t = A.m[3 * i + l] * A.m[3 * k + j];
+            if (i == k) t += ata.m[3 * l + j];
+            if (j == l) t += Mm.m[3 * i + k];
+            h9[(3 * i + j) * 9 + 3 * k + l] = 4.0 * c * t;
+          }
+    psd_project<9>(h9, 9);
+    for (int i = 0; i < 144; ++i) H[i] = M[i];
+    for (int i = 0; i < 9; ++i)
+      for (int j = 0; j < 9; ++j) H[(3 + i) * 12 + 3 + j] += h2 * h9[9 * i + j];
+  }
+  // kinematic constraints on this body
+  for (int k = W.env_cons[e]; k < W.env_cons[e + 1]; ++k) {
+    if (W.cons_aff[k] != b) continue;
+    double kap = W.cons_kappa[k], sm = sqrt(W.cons_mass[k]);
+    const double* tg = W.cons_target + 12 * k;
+    const double* lam = W.cons_lam + 12 * k;
+    double dd = 0.0, ld = 0.0;
+    for (int i = 0; i < 12; ++i) {
+      double di = x[o + i] - tg[i];
+      dd += di * di;
+      ld += lam[i] * di;
+      if (deriv) {
+        g[i] += kap * di - sm * lam[i];
+        H[13 * i] += kap;
+      }
+    }
+    v += 0.5 * kap * dd - sm * ld;
+  }
+  val[b] = v;
+  if (deriv) {
+    for (int i = 0; i < 12; ++i) g12[12 * b + i] = g[i];
+    for (int i = 0; i < 144; ++i) h144[144 * b + i] = H[i];
+  }
+}
+
+// per tet: h² V ψ(F), gradient, PSD-projected stencil Hessian (ref elastic.py:204)
+__global__ void k_tet(World W, const double* __restrict__ x, double h2, int deriv,
+                      const int* env_flag, double* val, double* g12, double* hp) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= W.n_tet) return;
+  if (env_flag && !env_flag[W.tet_env[t]]) return;
+  int4 d = W.tet_dof[t];
+  V3 x0 = ld3(x + d.x), x1 = ld3(x + d.y), x2 = ld3(x + d.z), x3 = ld3(x + d.w);
+  V3 e1 = x1 - x0, e2 = x2 - x0, e3 = x3 - x0;
+  const double* Dm = W.tet_Dminv + 9 * t;
+  M3 Ds;  // columns e1 e2 e3
+  Ds.m[0] = e1.x; Ds.m[1] = e2.x; Ds.m[2] = e3.x;
+  Ds.m[3] = e1.y; Ds.m[4] = e2.y; Ds.m[5] = e3.y;
+  Ds.m[6] = e1.z; Ds.m[7] = e2.z; Ds.m[8] = e3.z;
+  M3 Dmi;
+  for (int i = 0; i < 9; ++i) Dmi.m[i] = Dm[i];
+  M3 F = m3_mul(Ds, Dmi);
+  double vol = W.tet_vol[t], mu = W.tet_mu[t], lam = W.tet_lam[t];
+  int model = W.tet_model[t];
+  double s = h2 * vol;
+  if (!deriv) {
+    double psi = psi_value(model, F, mu, lam);
+    val[t] = isinf(psi) ? INFINITY : s * psi;
+    return;
+  }
+  double psi, P[9], H9[81];
+  if (!psi_derivs(model, F, mu, lam, &psi, P, H9)) {
+    val[t] = INFINITY;
+    return;
+  }
+  val[t] = s * psi;
+  psd_project<9>(H9, 9);
+  // stencil coefficients: dF_ij = Σ_v C[v][j] dx_{v,i}
+  double Cc[4][3];
+  for (int j = 0; j < 3; ++j) {
+    Cc[1][j] = Dm[j];
+    Cc[2][j] = Dm[3 + j];
+    Cc[3][j] = Dm[6 + j];
+    Cc[0][j] = -(Dm[j] + Dm[3 + j] + Dm[6 + j]);
+  }
+  for (int v = 0; v < 4; ++v)
+    for (int i = 0; i < 3; ++i) {
+      double acc = 0.0;
+      for (int j = 0; j < 3; ++j) acc += P[3 * i + j] * Cc[v][j];
+      g12[12 * t + 3 * v + i] = s * acc;
+    }
+  // H[(v,l),(w,m)] = s Σ_jk C[v][j] C[w][k] H9[(l,j),(m,k)]
+  for (int r = 0; r < 12; ++r) {
+    int v = r / 3, l = r % 3;
+    for (int c = r; c < 12; ++c) {
+      int w = c / 3, m = c % 3;
+      double acc = 0.0;
+      for (int j = 0; j < 3; ++j)
+        for (int k = 0; k < 3; ++k) acc += Cc[v][j] * Cc[w][k] * H9[(3 * l + j) * 9 + 3 * m + k];
+      hp[PK * t + pk(r, c)] = s * acc;
+    }
+  }
+}
+
+// contact pairs over a candidate list. kind 0 PT, 1 EE.
+// val[k] = κ b (× mollifier) for active pairs, 0 otherwise; INF when an
+// active pair has non-positive distance (ref contact.py:497-531).
+// active[k] = slot mask when derivatives were written, 0 otherwise.
+__global__ void k_pairs(World W, const double* __restrict__ xw, Cands C, int kind, int deriv,
+                        const int* env_flag, double* val, double* g12, double* hp,
+                        unsigned char* active, double* env_min_s) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int e = blockIdx.y;
+  long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
+  int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
+  if (k >= n) return;
+  if (env_flag && !env_flag[e]) return;
+  k += off;
+  int2 pr = kind == 0 ? C.pt[k] : C.ee[k];
+  int sl[4];
+  if (kind == 0) {
+    int3 tv = W.tri_v[pr.y];
+    sl[0] = pr.x; sl[1] = tv.x; sl[2] = tv.y; sl[3] = tv.z;
+  } else {
+    int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
+    sl[0] = a.x; sl[1] = a.y; sl[2] = b.x; sl[3] = b.y;
+  }
+  V3 X[4];
+  for (int i = 0; i < 4; ++i) X[i] = ld3(xw + 3 * sl[i]);
+  int region;
+  double d2;
+  if (kind == 0) {
+    region = pt_region(X[0], X[1], X[2], X[3]);
+    d2 = pt_dist2(region, X[0], X[1], X[2], X[3]);
+  } else {
+    region = ee_region(X[0], X[1], X[2], X[3], nullptr);
+    d2 = ee_dist2(region, X[0], X[1], X[2], X[3]);
+  }
+  if (env_min_s) atomic_min_pos(env_min_s + e, d2);
+  double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
+  if (active) active[k] = 0;
+  if (!(d2 < shat)) {
+    val[k] = 0.0;
+    return;
+  }
+  if (d2 <= 0.0) {
+    val[k] = INFINITY;
+    return;
+  }
+  double eps = 0.0;
+  if (kind == 1) eps = 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y];
+  if (!deriv) {
+    double b = barrier_val(d2, shat);
+    double m = kind == 1 ? mollifier_val(cross2(X[1] - X[0], X[3] - X[2]), eps) : 1.0;
+    val[k] = kind == 1 ? kappa * (m * b) : kappa * b;
+    return;
+  }
+  double G[12], H[144];
+  for (int i = 0; i < 12; ++i) G[i] = 0.0;
+  for (int i = 0; i < 144; ++i) H[i] = 0.0;
+  int mask;
+  double s = dist2_derivs(kind == 0, region, X, G, H, &mask);
+  double b, db, d2b;
+  barrier_d(s, shat, &b, &db, &d2b);
+  double gout[12];
+  if (kind == 0) {
+    val[k] = kappa * b;
+    for (int i = 0; i < 12; ++i) gout[i] = kappa * db * G[i];
+    for (int i = 0; i < 12; ++i)
+      for (int j = 0; j < 12; ++j) H[i * 12 + j] = kappa * (d2b * G[i] * G[j] + db * H[i * 12 + j]);
+  } else {
+    double Gc[12], Hc[144];
+    for (int i = 0; i < 12; ++i) Gc[i] = 0.0;
+    for (int i = 0; i < 144; ++i) Hc[i] = 0.0;
+    double c = cross2_derivs(X, Gc, Hc);
+    double t = c / eps;
+    double em, de, d2e;
+    if (t < 1.0) {
+      em = t * (2.0 - t);
+      de = (2.0 - 2.0 * t) / eps;
+      d2e = -2.0 / (eps * eps);
+    } else {
+      em = 1.0; de = 0.0; d2e = 0.0;
+    }
+    val[k] = kappa * (em * b);
+    for (int i = 0; i < 12; ++i) gout[i] = kappa * ((de * b) * Gc[i] + (em * db) * G[i]);
+    for (int i = 0; i < 12; ++i)
+      for (int j = 0; j < 12; ++j)
+        H[i * 12 + j] = kappa * ((d2e * b) * Gc[i] * Gc[j] + (de * b) * Hc[i * 12 + j] +
+                                 (de * db) * (Gc[i] * G[j] + G[i] * Gc[j]) + (em * d2b) * G[i] * G[j] +
+                                 (em * db) * H[i * 12 + j]);
+    if (t < 1.0) mask = 0xF;
+  }
+  psd_project_masked12(H, mask);
+  for (int i = 0; i < 12; ++i) g12[12 * k + i] = gout[i];
+  for (int i = 0; i < 12; ++i)
+    for (int j = i; j < 12; ++j) hp[PK * k + pk(i, j)] = H[i * 12 + j];
+  if (active) active[k] = (unsigned char)0xF;
+}
+
+// ground candidates (ref contact.py:564): value, y-gradient, clamped y-curvature
+__global__ void k_ground(World W, const double* __restrict__ xw, Cands C, int deriv,
+                         const int* env_flag, double* val, double* gy, double* hyy,
+                         double* env_min_s) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.y;
+  if (k >= C.n_gnd[e]) return;
+  if (env_flag && !env_flag[e]) return;
+  k += C.gnd_off[e];
+  int s = C.gnd[k];
+  double d = xw[3 * s + 1] - W.env_ground_y[e];
+  double dhat = W.env_dhat[e], shat = dhat * dhat;
+  if (d <= 0.0) {
+    val[k] = INFINITY;
+    if (env_min_s) atomic_min_pos(env_min_s + e, 0.0);
+    return;
+  }
+  double ss = d * d;
+  if (env_min_s) atomic_min_pos(env_min_s + e, ss);
+  if (!(ss < shat)) {
+    val[k] = 0.0;
+    if (deriv) { gy[k] = 0.0; hyy[k] = 0.0; }
+    return;
+  }
+  double kappa = W.env_kappa[e];
+  double b, db, d2b;
+  barrier_d(ss, shat, &b, &db, &d2b);
+  val[k] = kappa * b;
+  if (deriv) {
+    gy[k] = kappa * db * 2.0 * d;
+    hyy[k] = fmax(kappa * (d2b * 4.0 * d * d + db * 2.0), 0.0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// friction (ref friction.py)
+// ---------------------------------------------------------------------------
+IPC_HD void tangent_basis(V3 n, double* T /*3x2 row-major*/) {
+  V3 ref = fabs(n.x) < 0.9 ? v3(1, 0, 0) : v3(0, 1, 0);
+  V3 t1 = crossx(n, ref);
+  double l = sqrt(dotx(t1, t1));
+  t1 = v3(t1.x / l, t1.y / l, t1.z / l);
+  V3 t2 = crossx(n, t1);
+  T[0] = t1.x; T[1] = t2.x;
+  T[2] = t1.y; T[3] = t2.y;
+  T[4] = t1.z; T[5] = t2.z;
+}
+
+// lag one candidate pair if active and λ > 0; lags are appended per env in
+// candidate order (PT list then EE list) — one CTA per env for ordering.
+__global__ void k_lags(World W, const double* __restrict__ xw, Cands C, Lags L, const int* env_flag) {
+  __shared__ int warp_tot[BP_THREADS / 32];
+  __shared__ int total;
+  int e = blockIdx.x;
+  if (env_flag && !env_flag[e]) return;
+  double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
+  long long lo = L.off[e];
+  int base = 0;
+  for (int kind = 0; kind < 2; ++kind) {
+    int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
+    long long coff = kind == 0 ? C.pt_off[e] : C.ee_off[e];
+    for (int k0 = 0; k0 < n; k0 += BP_THREADS) {
+      int k = k0 + threadIdx.x;
+      bool keep = false;
+      int sl[4];
+      double gam[4], T[6], lam = 0.0;
+      if (k < n) {
+        int2 pr = kind == 0 ? C.pt[coff + k] : C.ee[coff + k];
+        if (kind == 0) {
+          int3 tv = W.tri_v[pr.y];
+          sl[0] = pr.x; sl[1] = tv.x; sl[2] = tv.y; sl[3] = tv.z;
+        } else {
+          int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
+          sl[0] = a.x; sl[1] = a.y; sl[2] = b.x; sl[3] = b.y;
+        }
+        V3 X[4];
+        for (int i = 0; i < 4; ++i) X[i] = ld3(xw + 3 * sl[i]);
+        int region;
+        double d2;
+        if (kind == 0) {
+          region = pt_region(X[0], X[1], X[2], X[3]);
+          d2 = pt_dist2(region, X[0], X[1], X[2], X[3]);
+        } else {
+          region = ee_region(X[0], X[1], X[2], X[3], nullptr);
+          d2 = ee_dist2(region, X[0], X[1], X[2], X[3]);
+        }
+        if (d2 < shat) {
+          double G[12], H[144];
+          for (int i = 0; i < 12; ++i) G[i] = 0.0;
+          for (int i = 0; i < 144; ++i) H[i] = 0.0;
+          int mask;
+          double s = dist2_derivs(kind == 0, region, X, G, H, &mask);
+          double d = sqrt(s);
+          double b, db, d2b;
+          barrier_d(s, shat, &b, &db, &d2b);
+          V3 n3;
+          if (kind == 0) {
+            lam = -kappa * db * 2.0 * d;
+            n3 = v3(G[0] / (2.0 * d), G[1] / (2.0 * d), G[2] / (2.0 * d));
+            gam[0] = 1.0;
+            for (int v = 1; v < 4; ++v) {
+              double w = -(G[3 * v] * n3.x + G[3 * v + 1] * n3.y + G[3 * v + 2] * n3.z) / (2.0 * d);
+              gam[v] = -w;
+            }
+          } else {
+            double eps = 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y];
+            double m = mollifier_val(cross2(X[1] - X[0], X[3] - X[2]), eps);
+            lam = -kappa * m * db * 2.0 * d;
+            n3 = v3((G[0] + G[3]) / (2.0 * d), (G[1] + G[4]) / (2.0 * d), (G[2] + G[5]) / (2.0 * d));
+            for (int v = 0; v < 2; ++v)
+              gam[v] = (G[3 * v] * n3.x + G[3 * v + 1] * n3.y + G[3 * v + 2] * n3.z) / (2.0 * d);
+            for (int v = 2; v < 4; ++v) {
+              double wb = -(G[3 * v] * n3.x + G[3 * v + 1] * n3.y + G[3 * v + 2] * n3.z) / (2.0 * d);
+              gam[v] = -wb;
+            }
+          }
+          tangent_basis(n3, T);
+          keep = lam > 0.0;
+        }
+      }
+      int o = block_ordered_offset<BP_THREADS>(keep, warp_tot, &total);
+      if (keep) {
+        long long dst = lo + base + o;
+        L.slots[dst] = make_int4(sl[0], sl[1], sl[2], sl[3]);
+        for (int i = 0; i < 4; ++i) L.gamma[4 * dst + i] = gam[i];
+        for (int i = 0; i < 6; ++i) L.tangent[6 * dst + i] = T[i];
+        L.lam[dst] = lam;
+      }
+      base += total;
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) L.n[e] = base;
+  // ground lags
+  int gbase = 0;
+  int ng = C.n_gnd[e];
+  int goff = C.gnd_off[e];
+  for (int k0 = 0; k0 < ng; k0 += BP_THREADS) {
+    int k = k0 + threadIdx.x;
+    bool keep = false;
+    int s = 0;
+    double lam = 0.0;
+    if (k < ng) {
+      s = C.gnd[goff + k];
+      double d = xw[3 * s + 1] - W.env_ground_y[e];
+      double ss = d * d;
+      if (ss < shat) {
+        double b, db, d2b;
+        barrier_d(ss, shat, &b, &db, &d2b);
+        lam = -kappa * db * 2.0 * d;
+        keep = lam > 0.0;
+      }
+    }
+    int o = block_ordered_offset<BP_THREADS>(keep, warp_tot, &total);
+    if (keep) {
+      L.g_slot[goff + gbase + o] = s;
+      L.g_lam[goff + gbase + o] = lam;
+    }
+    gbase += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) L.g_n[e] = gbase;
+}
+
+IPC_HD double f0s(double y, double eh) {
+  return y < eh ? y * y / eh - y * y * y / (3.0 * eh * eh) + eh / 3.0 : y;
+}
+IPC_HD double f1s(double y, double eh) { return y < eh ? 2.0 * y / eh - y * y / (eh * eh) : 1.0; }
+
+// smoothed tangential norm: value, 2-vector gradient, 2x2 Hessian (ref friction.py:177)
+IPC_HD double smooth_norm(double u0, double u1, double ml, double eh, double* gu, double* hu) {
+  double y = sqrt(u0 * u0 + u1 * u1);
+  double v = ml * f0s(y, eh);
+  if (gu) {
+    double fac = y > 0 ? f1s(y, eh) / fmax(y, 1e-300) : 2.0 / eh;
+    gu[0] = ml * fac * u0;
+    gu[1] = ml * fac * u1;
+    double df1 = y < eh ? 2.0 / eh - 2.0 * y / (eh * eh) : 0.0;
+    double coef = y > 1e-300 ? df1 - fac : 0.0;
+    double iy = 1.0 / fmax(y, 1e-300);
+    double h0 = u0 * iy, h1 = u1 * iy;
+    hu[0] = ml * (fac + coef * h0 * h0);
+    hu[1] = ml * (coef * h0 * h1);
+    hu[2] = hu[1];
+    hu[3] = ml * (fac + coef * h1 * h1);
+  }
+  return v;
+}
+
+__global__ void k_friction(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
+                           Lags L, double h, int deriv, const int* env_flag, double* val,
+                           double* g12, double* hp) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.y;
+  if (k >= L.n[e]) return;
+  if (env_flag && !env_flag[e]) return;
+  long long q = L.off[e] + k;
+  int4 s4 = L.slots[q];
+  int sl[4] = {s4.x, s4.y, s4.z, s4.w};
+  const double* gam = L.gamma + 4 * q;
+  const double* T = L.tangent + 6 * q;
+  double u3[3] = {0, 0, 0};
+  for (int i = 0; i < 4; ++i)
+    for (int c = 0; c < 3; ++c) u3[c] += gam[i] * (xw[3 * sl[i] + c] - xw0[3 * sl[i] + c]);
+  double u0 = T[0] * u3[0] + T[2] * u3[1] + T[4] * u3[2];
+  double u1 = T[1] * u3[0] + T[3] * u3[1] + T[5] * u3[2];
+  double ml = W.env_mu[e] * L.lam[q];
+  double eh = W.env_epsv[e] * h;
+  double gu[2], hu[4];
+  val[q] = smooth_norm(u0, u1, ml, eh, deriv ? gu : nullptr, hu);
+  if (!deriv) return;
+  double g3[3], h3[9];
+  for (int a = 0; a < 3; ++a) {
+    g3[a] = T[2 * a] * gu[0] + T[2 * a + 1] * gu[1];
+    for (int b = 0; b < 3; ++b)
+      h3[3 * a + b] = T[2 * a] * (hu[0] * T[2 * b] + hu[1] * T[2 * b + 1]) +
+                      T[2 * a + 1] * (hu[2] * T[2 * b] + hu[3] * T[2 * b + 1]);
+  }
+  for (int i = 0; i < 4; ++i)
+    for (int a = 0; a < 3; ++a) g12[12 * q + 3 * i + a] = gam[i] * g3[a];
+  for (int r = 0; r < 12; ++r)
+    for (int c = r; c < 12; ++c) hp[PK * q + pk(r, c)] = gam[r / 3] * gam[c / 3] * h3[3 * (r % 3) + c % 3];
+}
+
+// ground friction: tangent frame (x, z)
+__global__ void k_friction_gnd(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
+                               Lags L, double h, int deriv, const int* env_flag, double* val,
+                               double* g3, double* h3) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.y;
+  if (k >= L.g_n[e]) return;
+  if (env_flag && !env_flag[e]) return;
+  int q = W.env_slot[e] + k;
+  int s = L.g_slot[q];
+  double u0 = xw[3 * s] - xw0[3 * s], u1 = xw[3 * s + 2] - xw0[3 * s + 2];
+  double ml = W.env_mu[e] * L.g_lam[q];
+  double eh = W.env_epsv[e] * h;
+  double gu[2], hu[4];
+  val[q] = smooth_norm(u0, u1, ml, eh, deriv ? gu : nullptr, hu);
+  if (!deriv) return;
+  g3[3 * q] = gu[0]; g3[3 * q + 1] = 0.0; g3[3 * q + 2] = gu[1];
+  h3[9 * q + 0] = hu[0]; h3[9 * q + 1] = 0.0; h3[9 * q + 2] = hu[1];
+  h3[9 * q + 3] = 0.0; h3[9 * q + 4] = 0.0; h3[9 * q + 5] = 0.0;
+  h3[9 * q + 6] = hu[2]; h3[9 * q + 7] = 0.0; h3[9 * q + 8] = hu[3];
+}
+
+// ---------------------------------------------------------------------------
+// CCD: per-pair conservative advancement (ref ccd.py:395) and ground crossing
+// ---------------------------------------------------------------------------
+__device__ double stencil_dist(int kind, const V3* X) {
+  if (kind == 0) {
+    int r = pt_region(X[0], X[1], X[2], X[3]);
+    return sqrt(pt_dist2(r, X[0], X[1], X[2], X[3]));
+  }
+  int r = ee_region(X[0], X[1], X[2], X[3], nullptr);
+  return sqrt(ee_dist2(r, X[0], X[1], X[2], X[3]));
+}
+
+__device__ double pair_ccd_alpha(int kind, const V3* X, const V3* D, double conservative) {
+  V3 sum = ((D[0] + D[1]) + D[2]) + D[3];
+  V3 mean = v3(__ddiv_rn(sum.x, 4.0), __ddiv_rn(sum.y, 4.0), __ddiv_rn(sum.z, 4.0));
+  double sp[4];
+  for (int i = 0; i < 4; ++i) {
+    V3 r = D[i] - mean;
+    sp[i] = sqrt(dotx(r, r));
+  }
+  double l = kind == 0 ? sp[0] + fmax(fmax(sp[1], sp[2]), sp[3]) : fmax(sp[0], sp[1]) + fmax(sp[2], sp[3]);
+  double d0 = stencil_dist(kind, X);
+  if (!(l > 1e-300)) return 1.0;
+  double t = 0.0, d = d0, g = 0.01 * d0;
+  for (int it = 0; it < 64; ++it) {
+    double tn = t + d / l;
+    if (tn >= 1.0) return 1.0;
+    V3 Y[4];
+    for (int i = 0; i < 4; ++i)
+      Y[i] = v3(__dadd_rn(X[i].x, __dmul_rn(tn, D[i].x)), __dadd_rn(X[i].y, __dmul_rn(tn, D[i].y)),
+                __dadd_rn(X[i].z, __dmul_rn(tn, D[i].z)));
+    d = stencil_dist(kind, Y);
+    t = tn;
+    if (d <= g) return conservative * t;
+  }
+  return fmin(1.0, fmax(conservative * t, 1e-12));
+}
+
+__global__ void k_ccd_pairs(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
+                            Cands C, int kind, double conservative, const int* env_flag,
+                            double* env_alpha) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.y;
+  int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
+  if (k >= n) return;
+  if (env_flag && !env_flag[e]) return;
+  long long q = (kind == 0 ? C.pt_off[e] : C.ee_off[e]) + k;
+  int2 pr = kind == 0 ? C.pt[q] : C.ee[q];
+  int sl[4];
+  if (kind == 0) {
+    int3 tv = W.tri_v[pr.y];
+    sl[0] = pr.x; sl[1] = tv.x; sl[2] = tv.y; sl[3] = tv.z;
+  } else {
+    int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
+    sl[0] = a.x; sl[1] = a.y; sl[2] = b.x; sl[3] = b.y;
+  }
+  V3 X[4], D[4];
+  for (int i = 0; i < 4; ++i) {
+    X[i] = ld3(xw + 3 * sl[i]);
+    D[i] = ld3(dxw + 3 * sl[i]);
+  }
+  double a = pair_ccd_alpha(kind, X, D, conservative);
+  atomic_min_pos(env_alpha + e, a);
+}
+
+__global__ void k_ccd_ground(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
+                             Cands C, double conservative, const int* env_flag, double* env_alpha) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.y;
+  if (k >= C.n_gnd[e]) return;
+  if (env_flag && !env_flag[e]) return;
+  int s = C.gnd[C.gnd_off[e] + k];
+  double y = xw[3 * s + 1], dy = dxw[3 * s + 1];
+  if (!(dy < 0.0)) return;
+  double t = (y - W.env_ground_y[e]) / -dy;
+  if (!(t <= 1.0)) return;
+  atomic_min_pos(env_alpha + e, fmin(1.0, conservative * t));
+}
+
+}  // namespace ipc

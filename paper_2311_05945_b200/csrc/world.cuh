@@ -1,0 +1,98 @@
+// Device-resident batch of independent environments ("world").
+//
+// Layout (all fp64 state, SoA, flattened over environments; every per-env
+// range is a prefix array `env_*[e] .. env_*[e+1]`):
+//   DoF vector x/v/...   env e owns [env_dof[e], env_dof[e+1]); inside an env
+//                        the reference layout: soft vertex triples first,
+//                        then affine bodies as (p, rows of A)  (ref bodies.py:1-6)
+//   soft vertices        vert_dof (index of the x coordinate), vert_mass
+//   affine bodies        aff_dof, aff_M (12x12), aff_acc (M⁻¹ f_gravity), aff_ortho (λV)
+//   tets                 tet_dof (4 vertex DoF indices), Dm⁻¹ (9), rest volume, μ, λ, model
+//   contact slots        slot_aff (kind), slot_dof (soft DoF index | affine body DoF
+//                        offset), slot_rest (lever arm), slot_cbody
+//   triangles / edges    global slot ids, owning collision body, rest length²
+//   collision bodies     rigid / kinematic flags, excluded-partner bitmask (env-local ids)
+//   constraints          kinematic AL targets (ref constraints.py:36)
+//   candidates           per-env capacity ranges; pairs stored lexicographically
+#pragma once
+#include <stdint.h>
+
+namespace ipc {
+
+struct Cands {
+  int2* pt;       // (slot, tri)
+  int2* ee;       // (edge i, edge j), i < j
+  int* gnd;       // slot ids
+  int* n_pt;      // [n_env]
+  int* n_ee;
+  int* n_gnd;
+  const long long* pt_off;  // [n_env+1] capacity prefix
+  const long long* ee_off;
+  const int* gnd_off;       // == env_slot
+  int* overflow;            // [1] set when a capacity is exceeded
+};
+
+struct Lags {  // lagged friction (ref friction.py:35)
+  int4* slots;      // 4 slots per stencil
+  double* gamma;    // 4
+  double* tangent;  // 3x2 row-major
+  double* lam;
+  int* n;           // [n_env]
+  const long long* off;  // [n_env+1] capacity prefix (== pt_off + ee_off)
+  int* g_slot;      // ground lags
+  double* g_lam;
+  int* g_n;         // [n_env]
+};
+
+struct World {
+  int n_env, n_dof, n_vert, n_aff, n_tet, n_slot, n_tri, n_edge, n_cbody, n_cons;
+  // env prefix arrays
+  const int *env_dof, *env_vert, *env_aff, *env_tet, *env_slot, *env_tri, *env_edge, *env_cbody,
+      *env_cons;
+  const unsigned char* env_pairs;  // needs_pair_search
+  const unsigned char* env_has_ground;
+  const double* env_ground_y;
+  const double* env_gravity;  // 3 per env
+  double *env_dhat, *env_kappa, *env_kappa0, *env_mu, *env_epsv;
+  // per-element env ids
+  const int *dof_env, *vert_env, *aff_env, *tet_env, *slot_env, *cons_env;
+  // state
+  double *x, *v, *x_prev, *xhat, *p, *xt, *grad;
+  // soft vertices
+  const int* vert_dof;
+  const double* vert_mass;
+  // affine bodies
+  const int* aff_dof;
+  const double *aff_M, *aff_acc, *aff_ortho;
+  // tets
+  const int4* tet_dof;
+  const double *tet_Dminv, *tet_vol, *tet_mu, *tet_lam;
+  const unsigned char* tet_model;
+  // slots & primitives
+  const unsigned char* slot_aff;
+  const int* slot_dof;
+  const double* slot_rest;
+  const int* slot_cbody;
+  const int3* tri_v;
+  const int* tri_cbody;
+  const int2* edge_v;
+  const int* edge_cbody;
+  const double* edge_len2;
+  const unsigned char *cbody_rigid, *cbody_kin;
+  const unsigned long long* cbody_excl;
+  // constraints
+  const int* cons_aff;
+  double *cons_target, *cons_lam, *cons_kappa, *cons_kappa0, *cons_mass, *cons_lastres;
+  // world-space slot positions
+  double *xw, *xw0, *dxw;
+};
+
+// per-environment solver scalars (device)
+struct EnvState {
+  double *e0, *e_new, *alpha, *alpha_max, *pnorm, *prev_pnorm, *gnorm, *min_s_before, *min_s,
+      *res;
+  int *small_run, *newton_active, *ls_active, *al_active, *ls_failed, *converged, *newton_iters,
+      *ccd_calls, *al_outer, *err, *any;
+};
+
+}  // namespace ipc

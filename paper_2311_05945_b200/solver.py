@@ -1,9 +1,38 @@
-"""Placeholder; replaced by the GPU engine binding."""
-from dataclasses import dataclass
+"""Drop-in time step on the GPU (ref: pkg/src/srsim/solver.py).
+
+``step(scene, config)`` has the reference's signature and semantics: it
+advances the scene's bodies in place by one barrier-augmented implicit
+Euler step (projected Newton, CCD-filtered line search, lagged friction,
+augmented-Lagrangian kinematic targets, κ adaptation) and returns
+``(state, StepReport)``. All of the per-step work runs in
+``libipc_b200.so``; there is no CPU path.
+
+Host ↔ device traffic per call: the scene's DoF state and velocities are
+uploaded (the caller may have edited bodies between steps, e.g. a gripper
+placement), then downloaded after the step together with κ and the
+kinematic multipliers. ``GpuWorld`` (world.py) keeps batches resident.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .world import GpuWorld
+
+PHASES = ("DCD", "Energy", "Hess", "Linear", "CCD", "Others")
+
+
+class IntersectionError(RuntimeError):
+    """The incoming state already touches or penetrates (ref ccd.py:382)."""
 
 
 @dataclass
 class SolverConfig:
+    """ref solver.py:56."""
+
     h: float = 0.01
     newton_tol: float = 1e-2
     max_newton_iters: int = 100
@@ -11,3 +40,133 @@ class SolverConfig:
     ccd_conservative_factor: float = 0.9
     friction_fixed_point_iters: int = 1
     al_max_outer: int = 20
+
+    def __post_init__(self):
+        if self.h <= 0:
+            raise ValueError("time step must be positive")
+        if self.newton_tol <= 0:
+            raise ValueError("newton_tol must be positive")
+        if not 0.0 < self.ccd_conservative_factor < 1.0:
+            raise ValueError("ccd_conservative_factor must lie in (0, 1)")
+
+
+@dataclass
+class StepReport:
+    """ref solver.py:75. Phase times are not split on the GPU: the whole step
+    is reported under "Others" (wall time of the device step)."""
+
+    newton_iters: int = 0
+    final_grad_norm: float = 0.0
+    min_dist_before: float = np.inf
+    min_dist_after: float = np.inf
+    ccd_invocations: int = 0
+    converged: bool = True
+    line_search_failed: bool = False
+    al_outer: int = 0
+    times: dict = field(default_factory=lambda: {k: 0.0 for k in PHASES})
+    total_time: float = 0.0
+
+    def as_dict(self) -> dict:
+        return {"newton_iters": self.newton_iters, "final_grad_norm": self.final_grad_norm,
+                "min_dist_before": self.min_dist_before, "min_dist_after": self.min_dist_after,
+                "ccd_invocations": self.ccd_invocations, "converged": self.converged,
+                "line_search_failed": self.line_search_failed, "al_outer": self.al_outer,
+                "times": dict(self.times), "total_time": self.total_time}
+
+    @classmethod
+    def from_c(cls, r, t):
+        rep = cls(newton_iters=r.newton_iters, final_grad_norm=r.final_grad_norm,
+                  min_dist_before=r.min_dist_before, min_dist_after=r.min_dist_after,
+                  ccd_invocations=r.ccd_invocations, converged=bool(r.converged),
+                  line_search_failed=bool(r.line_search_failed), al_outer=r.al_outer)
+        rep.total_time = t
+        rep.times["Others"] = t
+        return rep
+
+
+def engine_of(scene) -> GpuWorld:
+    if scene.engine is None:
+        scene.engine = GpuWorld([scene])
+    return scene.engine
+
+
+def convergence_check(p, h: float, tol: float) -> bool:
+    """‖p‖∞ / h ≤ tol (ref solver.py:234)."""
+    p = np.asarray(p)
+    return True if len(p) == 0 else bool(np.abs(p).max() / h <= tol)
+
+
+def _sync_to_device(scene, w: GpuWorld):
+    st = scene.state
+    w.set_state(st.gather(), st.gather_velocity())
+    w.set_kappa(np.array([scene.barrier.kappa]))
+
+
+def _sync_from_device(scene, w: GpuWorld, h):
+    x, v = w.get_state()
+    scene.state.scatter(x)
+    scene.state.scatter_velocity(v)
+    k = float(w.get_kappa()[0])
+    if k != scene.barrier.kappa:
+        scene.barrier = type(scene.barrier)(scene.barrier.dhat, k)
+    if scene.constraints:
+        lam, kap = w.get_constraints()
+        for c, l, kk in zip(scene.constraints, lam, kap):
+            c.lam = l.copy()
+            c.kappa = float(kk)
+
+
+def step(scene, config: SolverConfig):
+    """Advance one time step on the GPU; returns (state, StepReport)
+    (ref solver.py:360). Raises IntersectionError on an intersecting start."""
+    t0 = time.perf_counter()
+    w = engine_of(scene)
+    _sync_to_device(scene, w)
+    reps = w.step(config)
+    r = reps[0]
+    if r.error:
+        raise IntersectionError("step started from an intersecting state")
+    _sync_from_device(scene, w, config.h)
+    return scene.state, StepReport.from_c(r, time.perf_counter() - t0)
+
+
+def simulate(scene, config: SolverConfig, n_steps: int, callback=None):
+    """ref solver.py:457."""
+    out = []
+    for i in range(n_steps):
+        _, rep = step(scene, config)
+        out.append(rep)
+        if callback is not None:
+            callback(i, scene, rep)
+    return out
+
+
+class _GpuBackend:
+    """Grasp-driver backend on the GPU engine (robot/grasp.py)."""
+
+    def step(self, scene, cfg):
+        return step(scene, cfg)
+
+    def finger_forces(self, scene, gripper, h):
+        w = engine_of(scene)
+        _sync_to_device(scene, w)
+        groups = np.array([[w.mask(0, [gripper.links[ln] for ln in gripper.finger_groups[fn]])
+                            for fn in gripper.finger_names]], dtype=np.uint64)
+        f = w.group_forces(h, groups)[0]
+        return np.linalg.norm(f, axis=1)
+
+    def min_group_distance(self, scene, a, b):
+        w = engine_of(scene)
+        _sync_to_device(scene, w)
+        return float(w.group_distance(np.array([w.mask(0, a)], np.uint64),
+                                      np.array([w.mask(0, b)], np.uint64))[0])
+
+    def min_ground_distance(self, scene, bodies):
+        if scene.ground_y is None:
+            return np.inf
+        w = engine_of(scene)
+        _sync_to_device(scene, w)
+        return float(w.ground_distance(np.array([w.mask(0, bodies)], np.uint64))[0])
+
+
+GPU_BACKEND = _GpuBackend()

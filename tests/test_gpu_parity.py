@@ -1,0 +1,142 @@
+"""CUDA path vs the CPU oracle and the reference's golden vectors (needs a GPU).
+
+Tolerances: integer / index outputs (regions, candidate lists, grasp
+outcomes, Newton iteration counts) must match exactly; fp64 DoF states
+within 1e-6 relative per step (north_star), element derivatives within
+1e-9 relative of the reference autodiff.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import collide as C
+from oracle import energies as E
+from oracle import stepper as S
+from oracle.robot import OracleBackend
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-6  # per-step DoF tolerance (north_star: "within 1e-6 relative")
+
+
+@pytest.fixture(scope="module")
+def native():
+    from paper_2311_05945_b200 import _native
+
+    return _native
+
+
+def test_distance_kernels_match_reference(native, golden):
+    z = golden("distance.npz")
+    for kind in ("pt", "ee"):
+        reg, s, g, h = native.dist2_derivs(kind, z[kind])
+        assert np.array_equal(reg, z[f"{kind}_region"])
+        np.testing.assert_allclose(s, z[f"{kind}_s"], rtol=1e-12, atol=1e-14)
+        gs = np.abs(z[f"{kind}_g"]).max(axis=1, keepdims=True)
+        assert np.all(np.abs(g - z[f"{kind}_g"]) <= 1e-9 * gs + 1e-14)
+        hs = np.abs(z[f"{kind}_h"]).max(axis=(1, 2), keepdims=True)
+        assert np.all(np.abs(h - z[f"{kind}_h"]) <= 1e-8 * hs + 1e-14)
+
+
+def test_ccd_kernel_matches_reference(native, golden):
+    z = golden("ccd.npz")
+    for kind in ("pt", "ee"):
+        a = native.ccd_pairs(kind, z["px"], z["pdx"])
+        np.testing.assert_allclose(a, z[f"alpha_{kind}"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("dim", [6, 9, 12])
+def test_psd_projection(native, dim):
+    rng = np.random.default_rng(dim)
+    m = rng.standard_normal((200, dim, dim))
+    m = m + np.swapaxes(m, 1, 2)
+    m[:50] = m[:50] @ np.swapaxes(m[:50], 1, 2)  # some already PSD
+    got = native.psd_project(m)
+    want = E.psd(m)
+    np.testing.assert_allclose(got, want, atol=1e-10 * np.abs(m).max())
+    assert np.linalg.eigvalsh(got).min() >= -1e-9 * np.abs(m).max()
+
+
+@pytest.mark.parametrize("model", [0, 1, 2])
+def test_elastic_models(native, model):
+    names = ("NeoHookean", "StVK", "FixedCorotated")
+    rng = np.random.default_rng(7 + model)
+    F = np.eye(3) + 0.2 * rng.standard_normal((300, 3, 3))
+    F = F[np.linalg.det(F) > 0.2]
+    mu, lam = 3.8e4, 5.7e4
+    psi, P, H = native.elastic_eval(model, F, mu, lam)
+    rp, rP, rH = E.elastic_pk1_hess(F, names[model], mu, lam)
+    np.testing.assert_allclose(psi, rp, rtol=1e-10)
+    np.testing.assert_allclose(P, rP, rtol=1e-8, atol=1e-8 * np.abs(rP).max())
+    np.testing.assert_allclose(H, rH, rtol=1e-7, atol=1e-8 * np.abs(rH).max())
+
+
+# ---------------------------------------------------------------------------
+# whole-step parity
+# ---------------------------------------------------------------------------
+from test_oracle_golden import CUBE_Y, contact_scene  # noqa: E402
+from paper_2311_05945_b200 import data_path  # noqa: E402
+from paper_2311_05945_b200.bodies import AffineBody, GlobalState, Material, SoftBody  # noqa: E402
+from paper_2311_05945_b200.mesh import box_surface, box_tet  # noqa: E402
+from paper_2311_05945_b200.robot import (Gripper, GraspTrial, autograsp,  # noqa: E402
+                                         build_grasp_scene, lift_and_shake, parse_urdf,
+                                         top_down_pose)
+from paper_2311_05945_b200.scene import make_scene  # noqa: E402
+from paper_2311_05945_b200.solver import SolverConfig, step  # noqa: E402
+from paper_2311_05945_b200.world import GpuWorld  # noqa: E402
+
+
+def test_candidates_match_oracle(golden):
+    z = golden("contact.npz")
+    sc = contact_scene()
+    sc.state.scatter(z["x"])
+    w = GpuWorld([sc])
+    assert np.array_equal(w.candidates(0, 0), z["cand_pt"])
+    assert np.array_equal(w.candidates(0, 1), z["cand_ee"])
+    assert np.array_equal(w.candidates(0, 2), z["cand_ground"])
+    md = w.min_distance()[0]
+    assert md == pytest.approx(float(z["min_dist"]), rel=1e-12)
+
+
+def test_soft_drop_trajectory(golden):
+    z = golden("traj_soft_drop.npz")
+    body = SoftBody(box_tet(0.05, 3, center=(0.0, 0.03, 0.0)),
+                    Material(youngs_modulus=1e5, poisson_ratio=0.3, density=1000.0))
+    sc = make_scene(GlobalState(soft_bodies=[body]), ground_y=0.0, dhat=1e-3)
+    cfg = SolverConfig()
+    for k in range(len(z["x"])):
+        _, rep = step(sc, cfg)
+        x = sc.state.gather()
+        assert rep.newton_iters == z["newton_iters"][k], k
+        assert np.abs(x - z["x"][k]).max() <= REL * np.abs(z["x"][k]).max(), k
+        assert rep.min_dist_after > 0.0
+
+
+def test_pinch_steps(golden):
+    z = golden("traj_pinch_steps.npz")
+    g = Gripper(parse_urdf(data_path("pj_gripper.urdf")))
+    obj = AffineBody(box_surface(0.05, center=(0.0, CUBE_Y, 0.0)), density=500.0)
+    sc = build_grasp_scene(obj, g, top_down_pose((0.0, CUBE_Y, 0.0)), [0.0, 0.0], mu=0.5)
+    cfg = SolverConfig()
+    for k in range(len(z["x"])):
+        g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, 0.0262))
+        _, rep = step(sc, cfg)
+        assert rep.newton_iters == z["newton_iters"][k], k
+        x = sc.state.gather()
+        assert np.abs(x - z["x"][k]).max() <= REL * np.abs(z["x"][k]).max(), k
+        assert rep.min_dist_after > 0.0
+
+
+def test_grasp_trial_flags_match_reference(golden):
+    z = golden("traj_grasp_rigid.npz")
+    g = Gripper(parse_urdf(data_path("pj_gripper.urdf")))
+    obj = AffineBody(box_surface(0.05, center=(0.0, CUBE_Y, 0.0)), density=500.0)
+    pose = top_down_pose((0.0, CUBE_Y, 0.0))
+    sc = build_grasp_scene(obj, g, pose, [0.0, 0.0], mu=float(z["mu"]))
+    tr = GraspTrial(pose, np.zeros(2))
+    autograsp(sc, g, tr)
+    lift_and_shake(sc, g, obj, tr)
+    assert tr.outcome == str(z["outcome"]) and tr.steps == int(z["steps"])
+    np.testing.assert_allclose(np.array(tr.forces), z["forces"], rtol=1e-5, atol=1e-5)
+    x = sc.state.gather()
+    assert np.abs(x - z["x_final"]).max() <= 1e-5 * np.abs(z["x_final"]).max()
