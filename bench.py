@@ -1,0 +1,319 @@
+"""Benchmark: batched grasp-scene time steps (BASELINE.json config 3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--envs E] [--impl ours|reference]
+
+One *step* = one implicit time step of every environment in the batch
+(parallel grasp generation: E gripper + rigid-object envs per GPU, weak
+scaling). Metric: env-steps/s over all ranks. `value` runs the device-resident
+command stream (no host inputs); `e2e` runs the same steps through the public
+Python API with host targets uploaded and the state read back every step.
+`--impl reference` times the CPU oracle (numpy restatement of the reference
+path, oracle/) on a bounded sample of the same environments with every host
+core. For N > 1 launch with torchrun; one process per GPU, envs sharded by
+rank, NCCL only to gather the timings.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "env-steps/sec (batched grasp scenes)"
+UNIT = "env-steps/s"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lr = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, lr
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the oracle on a bounded sample (multiprocess, one env subset per worker)
+# ---------------------------------------------------------------------------
+
+
+def _cpu_worker(args):
+    sample, worker, n_workers, seed, warmup, steps = args
+    sys.path.insert(0, ROOT)
+    from oracle import stepper as OS
+    from paper_2311_05945_b200 import workloads as WL
+
+    scenes, grippers, half, poses = WL.grasp_batch(sample, seed=seed)
+    sched = WL.schedule(grippers, half, poses, warmup + steps)
+    nl = len(grippers[0].links)
+    mine = list(range(worker, sample, n_workers))
+    lays = {e: OS.Layout(scenes[e]) for e in mine}
+    cfg = OS.Config()
+    t_timed, newton = 0.0, 0
+    for k in range(warmup + steps):
+        tgt = sched[k].reshape(sample, nl, 12)
+        t0 = time.perf_counter()
+        for e in mine:
+            for c, t12 in zip(scenes[e].constraints, tgt[e]):
+                c.body.target_q = t12
+            r = OS.step(scenes[e], cfg, lays[e])
+            if k >= warmup:
+                newton += r.newton_iters
+        if k >= warmup:
+            t_timed += time.perf_counter() - t0
+    return len(mine) * steps, t_timed, newton
+
+
+def cpu_arm(sample, seed, warmup, steps, cores):
+    import multiprocessing as mp
+
+    n_workers = min(cores, sample)
+    jobs = [(sample, w, n_workers, seed, warmup, steps) for w in range(n_workers)]
+    with mp.get_context("spawn").Pool(n_workers) as pool:
+        res = pool.map(_cpu_worker, jobs)
+    env_steps = sum(r[0] for r in res)
+    t = max(r[1] for r in res)
+    return env_steps / t, t, sum(r[2] for r in res), n_workers
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.p is None:
+            return
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                self.rows.append(f)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# roofline models (algorithmic bytes per launch)
+# ---------------------------------------------------------------------------
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            m = json.load(fh)
+        return float(m["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--envs", type=int, default=1024, help="environments per GPU")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="envs in the CPU sample (0 = 2x cores)")
+    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    ws, rank, lr = _dist()
+    K, W = args.steps, max(args.warmup, 3)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cores = _cores()
+        sample = args.cpu_sample or 2 * cores
+        ksteps = min(K, args.cpu_steps)
+        v, t, newton, used = cpu_arm(sample, args.seed, W, ksteps, cores)
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": ksteps, "warmup": W, "ms_per_step": 1e3 * t / ksteps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": "config3 parallel grasp generation (CPU oracle sample)",
+                           "envs_sampled": sample, "seed": args.seed},
+                "newton_iters_per_s": newton / t,
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": used, "kind": "port",
+                                 "sample": f"first {sample} envs of the batch, {ksteps} steps after "
+                                           f"{W} warm-up steps"},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    from paper_2311_05945_b200 import _native
+    from paper_2311_05945_b200 import workloads as WL
+    from paper_2311_05945_b200.solver import SolverConfig
+    from paper_2311_05945_b200.world import GpuWorld
+
+    lib = _native.load()
+    _native.check(lib.ipc_set_device(lr))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(lr)
+        dist.init_process_group("nccl")
+    cfg = SolverConfig()
+    E = args.envs
+    seed = args.seed + 1000 * rank
+    scenes, grippers, half, poses = WL.grasp_batch(E, seed=seed)
+    sched = WL.schedule(grippers, half, poses, W + K)
+    world = GpuWorld(scenes)
+    world.upload_schedule(sched)
+
+    # warm-up with full per-kernel profiling to identify the dominant kernel
+    world.profile(True)
+    for k in range(W):
+        world.step_scheduled(cfg, k, want_reports=False)
+    prof, _ = world.profile_read()
+    dom = max(prof, key=lambda n: prof[n][0])
+    if os.environ.get("BENCH_PROFILE"):
+        for n, (ms, c) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
+            print(f"[warmup profile] {n:14s} {ms:9.2f} ms {c:6d} launches "
+                  f"{1e3 * ms / max(c, 1):9.1f} us/launch", file=sys.stderr)
+
+    # timed region: device-resident inputs, L2 flushed between steps
+    world.profile(True, kernels=[dom])
+    t_ms, newton = [], 0
+    with Clocks(lr) as clk:
+        for k in range(W, W + K):
+            world.flush_l2()
+            world.mark(0)
+            reps = world.step_scheduled(cfg, k)
+            world.mark(1)
+            t_ms.append(world.elapsed_ms(0, 1))
+            newton += sum(r.newton_iters for r in reps)
+            if os.environ.get("BENCH_PROFILE"):
+                it = [r.newton_iters for r in reps]
+                print(f"[step {k}] {t_ms[-1]:8.2f} ms newton mean {np.mean(it):.2f} max {max(it)} "
+                      f"al max {max(r.al_outer for r in reps)}", file=sys.stderr)
+    prof, launches = world.profile_read()
+    total_ms = float(np.sum(t_ms))
+    final_err = sum(r.error + r.line_search_failed for r in reps)
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        tt = torch.tensor([total_ms, float(newton)], device=f"cuda:{lr}", dtype=torch.float64)
+        g = [torch.zeros_like(tt) for _ in range(ws)]
+        dist.all_gather(g, tt)
+        total_ms = max(float(x[0]) for x in g)
+        newton = sum(float(x[1]) for x in g)
+    value = E * ws * K / (total_ms * 1e-3)
+
+    # end-to-end through the public API: host targets in, state out, every step
+    scenes2, gr2, half2, poses2 = WL.grasp_batch(E, seed=seed)
+    w2 = GpuWorld(scenes2)
+    for k in range(W):
+        w2.step(cfg, targets=sched[k], want_reports=False)
+    w2.sync()
+    t0 = time.perf_counter()
+    for k in range(W, W + K):
+        w2.step(cfg, targets=sched[k], want_reports=True)
+        x, v = w2.get_state()
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        tt = torch.tensor([e2e_s], device=f"cuda:{lr}", dtype=torch.float64)
+        g = [torch.zeros_like(tt) for _ in range(ws)]
+        dist.all_gather(g, tt)
+        e2e_s = max(float(x[0]) for x in g)
+    e2e = E * ws * K / e2e_s
+    h2d = 12 * 8 * world.n_cons
+    d2h = 2 * 8 * world.n_dof
+
+    # roofline of the dominant kernel: algorithmic bytes / measured launch time
+    ms_dom, cnt_dom = prof[dom]
+    peak, peak_kind = _peaks()
+    algo = _algo_bytes(dom, world)
+    avg_s = (ms_dom / max(cnt_dom, 1)) * 1e-3
+    achieved = algo / avg_s / 1e9 if avg_s > 0 else 0.0
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+            "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config3 parallel grasp generation: per GPU "
+                                   f"{E} envs of gripper + rigid object (boxes/spheres), "
+                                   "scripted squeeze-and-lift command stream",
+                       "envs_per_gpu": E, "seed": args.seed, "l2": "flushed between timed steps"},
+            "newton_iters_per_s": newton / (total_ms * 1e-3),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "launches": cnt_dom, "avg_launch_us": avg_s * 1e6,
+                         "share_of_step": ms_dom / total_ms if total_ms else None},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches, "clocks": clk.summary(), "failed_envs_last_step": final_err}
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cores = _cores()
+        sample = args.cpu_sample or 2 * cores
+        v, t, _, used = cpu_arm(sample, args.seed, W, min(K, args.cpu_steps), cores)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": used, "kind": "port",
+                                "sample": f"first {sample} envs, {min(K, args.cpu_steps)} steps "
+                                          f"after {W} warm-up steps, oracle/ numpy port"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _algo_bytes(kernel, world):
+    """Algorithmic DRAM bytes of one launch of `kernel` over the whole batch
+    (DESIGN.md §Roofline): the minimum each launch must move."""
+    p = world.packed
+    ns, nt, ne, nd = p.n("slot"), p.n("tri"), p.n("edge"), p.n("dof")
+    if kernel.startswith("broad"):
+        # slot boxes (lo, hi) + primitive index lists, read once
+        return ns * 48 + nt * 16 + ne * 12
+    if kernel in ("dense_solve",):
+        return nd * 8 * 4 + p.n("aff") * (144 + 12) * 8
+    if kernel.startswith("pairs"):
+        return ns * 24 + (nt * 12 + ne * 8)
+    return nd * 8 * 2
+
+
+if __name__ == "__main__":
+    main()

@@ -80,6 +80,17 @@ int ipc_world_destroy(ipc_world *w);
  * or NULL to keep the previous targets. reports: n_env entries or NULL. */
 int ipc_world_step(ipc_world *w, const ipc_step_config *cfg, const double *cons_targets,
                    ipc_step_report *reports);
+/* As ipc_world_step; enable (n_env bytes, or NULL = all) selects the
+ * environments to advance — disabled ones keep their state untouched. */
+int ipc_world_step_ex(ipc_world *w, const ipc_step_config *cfg, const double *cons_targets,
+                      const uint8_t *enable, ipc_step_report *reports);
+
+/* Device-resident command stream: n_steps rows of 12*n_cons targets
+ * uploaded once; ipc_world_step_scheduled(k) steps with row k (no host
+ * input). */
+int ipc_world_upload_schedule(ipc_world *w, const double *targets, int n_steps);
+int ipc_world_step_scheduled(ipc_world *w, const ipc_step_config *cfg, int k, const uint8_t *enable,
+                             ipc_step_report *reports);
 
 /* State transfer, host buffers (replaces GlobalState.gather/scatter). */
 int ipc_world_get_state(ipc_world *w, double *x, double *v);
@@ -118,6 +129,21 @@ int ipc_world_ground_distance(ipc_world *w, const uint64_t *group, double *out);
  * (ref robot/sensing.py:52 body_contact_force / :61 finger_forces). */
 int ipc_world_group_forces(ipc_world *w, double h, const uint64_t *groups, int n_groups,
                            double *out);
+
+/* Bind the calling thread to a CUDA device (one process per GPU). */
+int ipc_set_device(int device);
+
+/* Instrumentation for the benchmark: per-kernel CUDA-event timing on the
+ * world's stream (kernel ids: 0 broad-DCD, 1 broad-CCD, 2 pairs-deriv,
+ * 3 pairs-value, 4 tet, 5 body, 6 ground, 7 friction, 8 energy-reduce,
+ * 9 dense-solve, 10 ccd, 11 lags, 12 world-pos, 13 sensing, 14 misc;
+ * 15 ids), launch counting, L2 flush and stream markers. */
+int ipc_world_profile(ipc_world *w, int on, uint32_t kernel_mask);
+int ipc_world_profile_read(ipc_world *w, double *ms, int64_t *count, int64_t *launches);
+int ipc_world_flush_l2(ipc_world *w, int64_t bytes);
+int ipc_world_mark(ipc_world *w, int slot);
+int ipc_world_elapsed(ipc_world *w, int a, int b, double *ms);
+int ipc_world_sync(ipc_world *w);
 
 /* Kernel-level entry points used by the parity tests (host buffers).
  * ipc_dist2_derivs: n stencils (12 doubles each) -> region, s, grad 12, hess 144

@@ -64,6 +64,11 @@ SIGNATURES = {
     "ipc_world_destroy": (C.c_int, [C.c_void_p]),
     "ipc_world_step": (C.c_int, [C.c_void_p, C.POINTER(StepConfig), _f64p,
                                  C.POINTER(StepReportC)]),
+    "ipc_world_step_ex": (C.c_int, [C.c_void_p, C.POINTER(StepConfig), _f64p, _u8p,
+                                    C.POINTER(StepReportC)]),
+    "ipc_world_upload_schedule": (C.c_int, [C.c_void_p, _f64p, C.c_int]),
+    "ipc_world_step_scheduled": (C.c_int, [C.c_void_p, C.POINTER(StepConfig), C.c_int, _u8p,
+                                           C.POINTER(StepReportC)]),
     "ipc_world_get_state": (C.c_int, [C.c_void_p, _f64p, _f64p]),
     "ipc_world_set_state": (C.c_int, [C.c_void_p, _f64p, _f64p]),
     "ipc_world_state_device": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p),
@@ -77,12 +82,23 @@ SIGNATURES = {
     "ipc_world_group_distance": (C.c_int, [C.c_void_p, _u64p, _u64p, _f64p]),
     "ipc_world_ground_distance": (C.c_int, [C.c_void_p, _u64p, _f64p]),
     "ipc_world_group_forces": (C.c_int, [C.c_void_p, C.c_double, _u64p, C.c_int, _f64p]),
+    "ipc_set_device": (C.c_int, [C.c_int]),
+    "ipc_world_profile": (C.c_int, [C.c_void_p, C.c_int, C.c_uint32]),
+    "ipc_world_profile_read": (C.c_int, [C.c_void_p, _f64p, _i64p, _i64p]),
+    "ipc_world_flush_l2": (C.c_int, [C.c_void_p, C.c_int64]),
+    "ipc_world_mark": (C.c_int, [C.c_void_p, C.c_int]),
+    "ipc_world_elapsed": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _f64p]),
+    "ipc_world_sync": (C.c_int, [C.c_void_p]),
     "ipc_dist2_derivs": (C.c_int, [C.c_int, C.c_int64, _f64p, _i32p, _f64p, _f64p, _f64p]),
     "ipc_ccd_pairs": (C.c_int, [C.c_int, C.c_int64, _f64p, _f64p, C.c_double, _f64p]),
     "ipc_psd_project": (C.c_int, [C.c_int, C.c_int64, _f64p]),
     "ipc_elastic_eval": (C.c_int, [C.c_int, C.c_int64, _f64p, C.c_double, C.c_double, _f64p,
                                    _f64p, _f64p]),
 }
+
+KERNEL_IDS = ("broad_dcd", "broad_ccd", "pairs_deriv", "pairs_value", "tet", "body", "ground",
+              "friction", "energy_reduce", "dense_solve", "ccd", "lags", "world_pos", "sensing",
+              "misc")
 
 _lib = None
 

@@ -45,6 +45,80 @@ static int set_err(const char* fmt, ...) {
 
 static inline int nblk(long long n, int t) { return (int)std::max<long long>(1, (n + t - 1) / t); }
 
+// ---------------------------------------------------------------------------
+// launch accounting + optional per-kernel CUDA-event timing
+// ---------------------------------------------------------------------------
+enum Kid {
+  K_BROAD_DCD = 0, K_BROAD_SWEEP, K_PAIRS_D, K_PAIRS_V, K_TET, K_BODY, K_GROUND, K_FRICTION, K_ENERGY,
+  K_DENSE, K_CCD, K_LAGS, K_WORLD, K_SENSE, K_MISC, NKID
+};
+struct Prof {
+  bool on = false;
+  unsigned mask = ~0u;
+  long long launches = 0;
+  struct Rec {
+    int kid;
+    cudaEvent_t a, b;
+  };
+  std::vector<cudaEvent_t> pool;
+  std::vector<Rec> pending;
+  Rec cur{};
+  double ms[NKID] = {};
+  long long cnt[NKID] = {};
+  cudaEvent_t ev() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void resolve() {
+    for (auto& r : pending) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, r.a, r.b));
+      ms[r.kid] += t;
+      cnt[r.kid] += 1;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    pending.clear();
+  }
+  ~Prof() {
+    for (auto& r : pending) { pool.push_back(r.a); pool.push_back(r.b); }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+static thread_local Prof* g_prof = nullptr;
+static inline void prof_begin(int kid, cudaStream_t s) {
+  Prof* p = g_prof;
+  if (!p) return;
+  p->launches++;
+  if (p->on && ((p->mask >> kid) & 1u)) {
+    p->cur.kid = kid;
+    p->cur.a = p->ev();
+    CK(cudaEventRecord(p->cur.a, s));
+  } else {
+    p->cur.kid = -1;
+  }
+}
+static inline void prof_end(int kid, cudaStream_t s) {
+  Prof* p = g_prof;
+  if (!p || p->cur.kid < 0) return;
+  p->cur.b = p->ev();
+  CK(cudaEventRecord(p->cur.b, s));
+  p->pending.push_back(p->cur);
+  p->cur.kid = -1;
+}
+#define IPC_LAUNCH(kid, stream, kern, grid, block, smem, ...) \
+  do {                                                        \
+    prof_begin((kid), (stream));                              \
+    kern<<<grid, block, smem, stream>>>(__VA_ARGS__);         \
+    prof_end((kid), (stream));                                \
+  } while (0)
+
 namespace ipc {
 __global__ void k_mark_unconverged(int n_env, EnvState S) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -63,6 +137,10 @@ __global__ void k_step_begin(int n_env, EnvState S) {
 __global__ void k_start_check(World W, EnvState S, Cands C, const double* ptv, const double* eev,
                               const double* gv, int* ok) {
   int e = blockIdx.x;
+  if (!ok[e]) {
+    if (threadIdx.x == 0) S.err[e] = 0;
+    return;
+  }
   int bad = 0;
   for (int k = threadIdx.x; k < C.n_pt[e]; k += blockDim.x) bad |= isinf(ptv[C.pt_off[e] + k]);
   for (int k = threadIdx.x; k < C.n_ee[e]; k += blockDim.x) bad |= isinf(eev[C.ee_off[e] + k]);
@@ -242,7 +320,7 @@ struct ipc_world {
   double *body_val = nullptr, *tet_val = nullptr, *fr_val = nullptr, *frg_val = nullptr;
   double *xlo = nullptr, *xhi = nullptr, *xwt = nullptr;
   double *env_alpha = nullptr;
-  int *ok = nullptr, *al_flag = nullptr, *accepted = nullptr, *ls_count = nullptr, *d_count = nullptr;
+  int *enable = nullptr, *ok = nullptr, *al_flag = nullptr, *accepted = nullptr, *ls_count = nullptr, *d_count = nullptr;
   int* h_count = nullptr;  // pinned
   double* slot_force = nullptr;
   double* d_targets = nullptr;
@@ -250,13 +328,22 @@ struct ipc_world {
   std::vector<double> h_targets;
   bool targets_set = false;
   cudaStream_t st = 0;
+  Prof prof;
+  int n_sm = 148;
+  long long* work[2] = {nullptr, nullptr};
+  int* work_env[2] = {nullptr, nullptr};
+  int* work_n = nullptr;
+  double* flush_buf = nullptr;
+  double* sched = nullptr;
+  int sched_steps = 0;
+  std::vector<cudaEvent_t> marks;
 
   ~ipc_world() {
     if (h_count) cudaFreeHost(h_count);
   }
 
   int count(const int* flag) {
-    k_count<<<1, 256, 0, st>>>(n_env, flag, d_count);
+    IPC_LAUNCH(K_MISC, st, k_count, 1, 256, 0, n_env, flag, d_count);
     CK(cudaMemcpyAsync(h_count, d_count, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return *h_count;
@@ -289,6 +376,18 @@ struct ipc_world {
       cs.c.n_gnd = pool.alloc<int>(n_env);
       cs.c.gnd_off = W.env_slot;
       cs.c.overflow = pool.alloc<int>(1);
+      cs.c.pre_pt = pool.alloc<int>(n_env + 1);
+      cs.c.pre_ee = pool.alloc<int>(n_env + 1);
+      cs.c.pre_gnd = pool.alloc<int>(n_env + 1);
+    }
+    if (&cs == &dcd) {  // derivative work lists track the DCD capacity
+      for (int k = 0; k < 2; ++k) {
+        if (work[k]) { pool.free_one(work[k]); pool.free_one(work_env[k]); }
+        long long n = k == 0 ? cs.pt_total : cs.ee_total;
+        work[k] = pool.alloc<long long>(n);
+        work_env[k] = pool.alloc<int>(n);
+      }
+      if (!work_n) work_n = pool.alloc<int>(2);
     }
   }
 
@@ -337,6 +436,8 @@ struct ipc_world {
       frg_val = pool.alloc<double>(W.n_slot);
       D.frg_g = pool.alloc<double>(3 * W.n_slot);
       D.frg_h = pool.alloc<double>(9 * W.n_slot);
+      L.pre = pool.alloc<int>(n_env + 1);
+      L.g_pre = pool.alloc<int>(n_env + 1);
     }
     fr_val = pool.alloc<double>(tot);
     D.fr_g = pool.alloc<double>(12 * tot);
@@ -348,13 +449,18 @@ struct ipc_world {
              const int* env_mask) {
     for (int attempt = 0; attempt < 8; ++attempt) {
       CK(cudaMemsetAsync(cs.c.overflow, 0, sizeof(int), st));
-      for (int kind = 0; kind < 3; ++kind) k_broad<<<n_env, BP_THREADS, 0, st>>>(W, lo, hi, cs.c, kind, env_mask);
+      for (int kind = 0; kind < 3; ++kind) IPC_LAUNCH((&cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD), st, k_broad, n_env, BP_THREADS, 0, W, lo, hi, cs.c, kind, env_mask);
       CK(cudaGetLastError());
       int ov = 0;
       CK(cudaMemcpyAsync(h_count, cs.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       ov = *h_count;
-      if (!ov) return;
+      if (!ov) {
+        IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_pt, env_mask, cs.c.pre_pt);
+        IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_ee, env_mask, cs.c.pre_ee);
+        IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_gnd, env_mask, cs.c.pre_gnd);
+        return;
+      }
       // grow: read counts are clipped, so grow every env capacity 4x
       std::vector<long long> ptc = cs.pt_cap, eec = cs.ee_cap;
       for (int e = 0; e < n_env; ++e) {
@@ -370,87 +476,94 @@ struct ipc_world {
     throw std::runtime_error("broad phase capacity overflow persists");
   }
 
+  // contact pairs of (cs): light distance/value pass over every candidate of
+  // the envs flagged at the last broad phase, then (deriv) the heavy
+  // derivative pass over the compacted active list
+  void pairs(const double* xw, CandStore& cs, PairBufs& pb, int deriv, double* min_s, int kid) {
+    for (int kind = 0; kind < 2; ++kind) {
+      long long cap = kind == 0 ? cs.pt_total : cs.ee_total;
+      if (!cap) continue;
+      if (deriv) CK(cudaMemsetAsync(work_n + kind, 0, sizeof(int), st));
+      IPC_LAUNCH(kid, st, k_pair_dist, n_sm * 8, 128, 0, W, xw, cs.c, kind, deriv, kind == 0 ? pb.pt_val : pb.ee_val,
+                 kind == 0 ? pb.pt_act : pb.ee_act, min_s, work[kind], work_env[kind], work_n + kind);
+      if (deriv)
+        IPC_LAUNCH(kid == K_SENSE ? K_SENSE : K_PAIRS_D, st, k_pair_hess, n_sm * 4, 64, 0, W, xw, cs.c, kind,
+                   work[kind], work_env[kind], work_n + kind, kind == 0 ? pb.pt_g : pb.ee_g,
+                   kind == 0 ? pb.pt_h : pb.ee_h, kind == 0 ? pb.pt_act : pb.ee_act);
+    }
+  }
+
   void world_pos(const double* x, double* xw) {
-    k_world<<<nblk(W.n_slot, 256), 256, 0, st>>>(W, x, xw);
+    IPC_LAUNCH(K_WORLD, st, k_world, nblk(W.n_slot, 256), 256, 0, W, x, xw);
   }
 
   // derivative or value pass of every term over (cands, lags)
   void terms(const double* x, const double* xw, CandStore& cs, PairBufs& pb, bool deriv, double h,
              const int* flag, double* min_s) {
     double h2 = h * h;
-    k_body<<<nblk(W.n_aff, 64), 64, 0, st>>>(W, x, W.xhat, h2, deriv, flag, body_val, D.body_g, D.body_h);
-    if (W.n_tet) k_tet<<<nblk(W.n_tet, 64), 64, 0, st>>>(W, x, h2, deriv, flag, tet_val, D.tet_g, D.tet_h);
-    if (cs.max_pt_cap)
-      k_pairs<<<dim3(nblk(cs.max_pt_cap, 64), n_env), 64, 0, st>>>(W, xw, cs.c, 0, deriv, flag, pb.pt_val,
-                                                                   pb.pt_g, pb.pt_h, pb.pt_act, min_s);
-    if (cs.max_ee_cap)
-      k_pairs<<<dim3(nblk(cs.max_ee_cap, 64), n_env), 64, 0, st>>>(W, xw, cs.c, 1, deriv, flag, pb.ee_val,
-                                                                   pb.ee_g, pb.ee_h, pb.ee_act, min_s);
+    IPC_LAUNCH(K_BODY, st, k_body, nblk(W.n_aff, 64), 64, 0, W, x, W.xhat, h2, deriv, flag, body_val, D.body_g, D.body_h);
+    if (W.n_tet) IPC_LAUNCH(K_TET, st, k_tet, nblk(W.n_tet, 64), 64, 0, W, x, h2, deriv, flag, tet_val, D.tet_g, D.tet_h);
+    pairs(xw, cs, pb, deriv, min_s, K_PAIRS_V);
     int max_slots = 0;
     for (int e = 0; e < n_env; ++e) max_slots = std::max(max_slots, h_env_slot[e + 1] - h_env_slot[e]);
-    k_ground<<<dim3(nblk(max_slots, 128), n_env), 128, 0, st>>>(W, xw, cs.c, deriv, flag, pb.gnd_val,
+    IPC_LAUNCH(K_GROUND, st, k_ground, dim3(nblk(max_slots, 128), n_env), 128, 0, W, xw, cs.c, deriv, flag, pb.gnd_val,
                                                                 pb.gnd_gy, pb.gnd_hyy, min_s);
-    long long maxlag = 0;
-    for (int e = 0; e < n_env; ++e) maxlag = std::max(maxlag, dcd.pt_cap[e] + dcd.ee_cap[e]);
-    k_friction<<<dim3(nblk(maxlag, 128), n_env), 128, 0, st>>>(W, xw, W.xw0, L, h, deriv, flag, fr_val,
-                                                               D.fr_g, D.fr_h);
-    k_friction_gnd<<<dim3(nblk(max_slots, 128), n_env), 128, 0, st>>>(W, xw, W.xw0, L, h, deriv, flag,
+    IPC_LAUNCH(K_FRICTION, st, k_friction, n_sm * 4, 128, 0, W, xw, W.xw0, L, h, deriv, flag, fr_val, D.fr_g, D.fr_h);
+    IPC_LAUNCH(K_FRICTION, st, k_friction_gnd, dim3(nblk(max_slots, 128), n_env), 128, 0, W, xw, W.xw0, L, h, deriv, flag,
                                                                       frg_val, D.frg_g, D.frg_h);
     CK(cudaGetLastError());
   }
 
   void energy(const double* x, CandStore& cs, PairBufs& pb, const int* flag, double* out) {
     Terms T{body_val, tet_val, pb.pt_val, pb.ee_val, pb.gnd_val, fr_val, frg_val, nullptr};
-    k_env_energy<<<n_env, RED_THREADS, 0, st>>>(W, x, W.xhat, T, cs.c, L, flag, out);
+    IPC_LAUNCH(K_ENERGY, st, k_env_energy, n_env, RED_THREADS, 0, W, x, W.xhat, T, cs.c, L, flag, out);
   }
 
   void newton_solve(const ipc_step_config& cfg) {
     double h = cfg.h;
-    k_newton_begin<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S, al_flag);
+    IPC_LAUNCH(K_MISC, st, k_newton_begin, nblk(n_env, 128), 128, 0, n_env, S, al_flag);
     size_t smem = (size_t)(max_env_dof * max_env_dof + 2 * max_env_dof) * sizeof(double);
     for (int it = 0; it < cfg.max_newton_iters; ++it) {
       if (count(S.newton_active) == 0) break;
       world_pos(W.x, W.xw);
       broad(dcd, pb_dcd, true, W.xw, W.xw, S.newton_active);
-      k_fill_flag<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S.min_s, INFINITY, S.newton_active);
+      IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.min_s, INFINITY, S.newton_active);
       terms(W.x, W.xw, dcd, pb_dcd, true, h, S.newton_active, S.min_s);
       energy(W.x, dcd, pb_dcd, S.newton_active, S.e0);
-      k_dense_solve<<<n_env, DENSE_THREADS, smem, st>>>(W, S, D_with(pb_dcd), dcd.c, L, W.x, W.xhat, W.p,
+      IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, smem, W, S, D_with(pb_dcd), dcd.c, L, W.x, W.xhat, W.p,
                                                         W.grad);
       CK(cudaGetLastError());
-      k_newton_check<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S, h, cfg.newton_tol);
+      IPC_LAUNCH(K_MISC, st, k_newton_check, nblk(n_env, 128), 128, 0, n_env, S, h, cfg.newton_tol);
       if (count(S.ls_active) == 0) continue;
       // CCD bound along p (ref solver.py:333-343)
-      k_axpy_env<<<nblk(W.n_dof, 256), 256, 0, st>>>(W, W.x, W.p, nullptr, S.ls_active, W.xt);
+      IPC_LAUNCH(K_MISC, st, k_axpy_env, nblk(W.n_dof, 256), 256, 0, W, W.x, W.p, nullptr, S.ls_active, W.xt);
       world_pos(W.xt, xwt);
-      k_sub<<<nblk(3 * W.n_slot, 256), 256, 0, st>>>(3 * W.n_slot, xwt, W.xw, W.dxw);
-      k_sweep_box<<<nblk(3 * W.n_slot, 256), 256, 0, st>>>(W.n_slot, W.xw, W.dxw, xlo, xhi);
+      IPC_LAUNCH(K_MISC, st, k_sub, nblk(3 * W.n_slot, 256), 256, 0, 3 * W.n_slot, xwt, W.xw, W.dxw);
+      IPC_LAUNCH(K_MISC, st, k_sweep_box, nblk(3 * W.n_slot, 256), 256, 0, W.n_slot, W.xw, W.dxw, xlo, xhi);
       broad(sweep, pb_sweep, false, xlo, xhi, S.ls_active);
-      k_fill_flag<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S.alpha_max, 1.0, S.ls_active);
-      if (sweep.max_pt_cap)
-        k_ccd_pairs<<<dim3(nblk(sweep.max_pt_cap, 64), n_env), 64, 0, st>>>(
-            W, W.xw, W.dxw, sweep.c, 0, cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
-      if (sweep.max_ee_cap)
-        k_ccd_pairs<<<dim3(nblk(sweep.max_ee_cap, 64), n_env), 64, 0, st>>>(
-            W, W.xw, W.dxw, sweep.c, 1, cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
+      IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.alpha_max, 1.0, S.ls_active);
+      for (int kind = 0; kind < 2; ++kind)
+        if (kind == 0 ? sweep.pt_total : sweep.ee_total)
+          IPC_LAUNCH(K_CCD, st, k_ccd_pairs, n_sm * 8, 64, 0, W, W.xw, W.dxw, sweep.c, kind,
+                     cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
       int max_slots = 0;
       for (int e = 0; e < n_env; ++e) max_slots = std::max(max_slots, h_env_slot[e + 1] - h_env_slot[e]);
-      k_ccd_ground<<<dim3(nblk(max_slots, 128), n_env), 128, 0, st>>>(W, W.xw, W.dxw, sweep.c,
+      IPC_LAUNCH(K_CCD, st, k_ccd_ground, dim3(nblk(max_slots, 128), n_env), 128, 0, W, W.xw, W.dxw, sweep.c,
                                                                       cfg.ccd_conservative_factor, S.ls_active,
                                                                       S.alpha_max);
-      k_ls_begin<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S, ls_count);
+      IPC_LAUNCH(K_MISC, st, k_ls_begin, nblk(n_env, 128), 128, 0, n_env, S, ls_count);
       for (int ls = 0; ls < cfg.max_line_search_halvings + 1; ++ls) {
         if (count(S.ls_active) == 0) break;
-        k_axpy_env<<<nblk(W.n_dof, 256), 256, 0, st>>>(W, W.x, W.p, S.alpha, S.ls_active, W.xt);
+        IPC_LAUNCH(K_MISC, st, k_axpy_env, nblk(W.n_dof, 256), 256, 0, W, W.x, W.p, S.alpha, S.ls_active, W.xt);
         world_pos(W.xt, xwt);
         terms(W.xt, xwt, sweep, pb_sweep, false, h, S.ls_active, nullptr);
         energy(W.xt, sweep, pb_sweep, S.ls_active, S.e_new);
-        k_ls_check<<<nblk(n_env, 128), 128, 0, st>>>(W, S, ls_count, cfg.max_line_search_halvings, accepted);
-        k_copy_env<<<nblk(W.n_dof, 256), 256, 0, st>>>(W, W.xt, W.x, accepted);
+        IPC_LAUNCH(K_MISC, st, k_ls_check, nblk(n_env, 128), 128, 0, W, S, ls_count, cfg.max_line_search_halvings, accepted);
+        IPC_LAUNCH(K_MISC, st, k_copy_env, nblk(W.n_dof, 256), 256, 0, W, W.xt, W.x, accepted);
       }
     }
     // envs still active after the iteration cap did not converge
-    k_mark_unconverged<<<nblk(n_env, 128), 128, 0, st>>>(n_env, S);
+    IPC_LAUNCH(K_MISC, st, k_mark_unconverged, nblk(n_env, 128), 128, 0, n_env, S);
   }
 
   Derivs D_with(const PairBufs& pb) {
@@ -549,6 +662,23 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     W.cbody_rigid = P.upload(d->cbody_rigid, d->n_cbody);
     W.cbody_kin = P.upload(d->cbody_kin, d->n_cbody);
     W.cbody_excl = (const unsigned long long*)P.upload(d->cbody_excl, d->n_cbody);
+    {
+      // contiguous per-body primitive ranges (slots/tris/edges are emitted body by body)
+      auto ranges = [&](const int32_t* owner, int n) {
+        std::vector<int> pre(d->n_cbody + 1, 0);
+        for (int i = 0; i < n; ++i) pre[owner[i] + 1]++;
+        for (int b = 0; b < d->n_cbody; ++b) pre[b + 1] += pre[b];
+        for (int i = 1; i < n; ++i)
+          if (owner[i] < owner[i - 1]) throw std::runtime_error("primitives not grouped by body");
+        return P.upload(pre.data(), pre.size());
+      };
+      W.cbody_slot = ranges(d->slot_cbody, d->n_slot);
+      W.cbody_tri = ranges(d->tri_cbody, d->n_tri);
+      W.cbody_edge = ranges(d->edge_cbody, d->n_edge);
+      int dev = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&w->n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
     W.cons_aff = P.upload(d->cons_aff, d->n_cons);
     W.cons_kappa0 = P.upload(d->cons_kappa0, d->n_cons);
     W.cons_kappa = P.upload(d->cons_kappa0, d->n_cons);
@@ -589,6 +719,7 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     S.al_active = P.alloc<int>(ne); S.ls_failed = P.alloc<int>(ne); S.converged = P.alloc<int>(ne);
     S.newton_iters = P.alloc<int>(ne); S.ccd_calls = P.alloc<int>(ne); S.al_outer = P.alloc<int>(ne);
     S.err = P.alloc<int>(ne); S.any = P.alloc<int>(1);
+    w->enable = P.alloc<int>(ne);
     w->ok = P.alloc<int>(ne); w->al_flag = S.al_active; w->accepted = P.alloc<int>(ne);
     w->ls_count = P.alloc<int>(ne); w->d_count = P.alloc<int>(1);
     w->env_alpha = P.alloc<double>(ne);
@@ -625,6 +756,8 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
 int ipc_world_destroy(ipc_world* w) {
   if (w) {
     cudaStreamSynchronize(w->st);
+    if (g_prof == &w->prof) g_prof = nullptr;
+    for (auto e : w->marks) cudaEventDestroy(e);
     if (w->st) cudaStreamDestroy(w->st);
     delete w;
   }
@@ -632,41 +765,75 @@ int ipc_world_destroy(ipc_world* w) {
 }
 
 int ipc_world_step(ipc_world* w, const ipc_step_config* cfg, const double* targets, ipc_step_report* rep) {
+  return ipc_world_step_ex(w, cfg, targets, nullptr, rep);
+}
+
+static int step_impl(ipc_world* w, const ipc_step_config* cfg, const double* targets, int sched_k,
+                     const uint8_t* enable, ipc_step_report* rep);
+
+int ipc_world_step_ex(ipc_world* w, const ipc_step_config* cfg, const double* targets, const uint8_t* enable,
+                      ipc_step_report* rep) {
+  return step_impl(w, cfg, targets, -1, enable, rep);
+}
+
+int ipc_world_upload_schedule(ipc_world* w, const double* targets, int n_steps) {
   GUARD({
+    if (w->sched) w->pool.free_one(w->sched);
+    w->sched = w->pool.upload(targets, 12 * (size_t)w->W.n_cons * n_steps);
+    w->sched_steps = n_steps;
+  })
+}
+
+int ipc_world_step_scheduled(ipc_world* w, const ipc_step_config* cfg, int k, const uint8_t* enable,
+                             ipc_step_report* rep) {
+  if (k < 0 || k >= w->sched_steps) return set_err("schedule index %d out of range", k);
+  return step_impl(w, cfg, nullptr, k, enable, rep);
+}
+
+static int step_impl(ipc_world* w, const ipc_step_config* cfg, const double* targets, int sched_k,
+                     const uint8_t* enable, ipc_step_report* rep) {
+  GUARD({
+    g_prof = &w->prof;
     World& W = w->W;
     EnvState& S = w->S;
     cudaStream_t st = w->st;
     int ne = w->n_env;
     double h = cfg->h;
     if (targets && W.n_cons) {
-      w->h_targets.assign(targets, targets + 12 * (size_t)W.n_cons);
+      CK(cudaMemcpyAsync(w->d_targets, targets, 12 * sizeof(double) * W.n_cons, cudaMemcpyHostToDevice, st));
+      w->targets_set = true;
+    } else if (sched_k >= 0 && W.n_cons) {
+      CK(cudaMemcpyAsync(w->d_targets, w->sched + 12 * (size_t)W.n_cons * sched_k, 12 * sizeof(double) * W.n_cons,
+                         cudaMemcpyDeviceToDevice, st));
       w->targets_set = true;
     }
-    std::vector<double>& tg = w->h_targets;
-    k_step_begin<<<nblk(ne, 128), 128, 0, st>>>(ne, S);
+    IPC_LAUNCH(K_MISC, st, k_step_begin, nblk(ne, 128), 128, 0, ne, S);
     CK(cudaMemcpyAsync(W.x_prev, W.x, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, st));
     w->world_pos(W.x, W.xw0);
-    int* all = w->ok;
-    k_fill_int<<<nblk(ne, 128), 128, 0, st>>>(ne, all, 1);
-    w->broad(w->dcd, w->pb_dcd, true, W.xw0, W.xw0, nullptr);
+    if (enable) {
+      std::vector<int> en(ne);
+      for (int e = 0; e < ne; ++e) en[e] = enable[e] ? 1 : 0;
+      CK(cudaMemcpyAsync(w->enable, en.data(), 4 * ne, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    } else {
+      IPC_LAUNCH(K_MISC, st, k_fill_int, nblk(ne, 128), 128, 0, ne, w->enable, 1);
+    }
+    IPC_LAUNCH(K_MISC, st, k_copy_int, nblk(ne, 128), 128, 0, ne, w->enable, w->ok);
+    w->broad(w->dcd, w->pb_dcd, true, W.xw0, W.xw0, w->ok);
     // feasibility of the incoming state (ref solver.py:372-385)
-    k_pairs<<<dim3(nblk(w->dcd.max_pt_cap, 64), ne), 64, 0, st>>>(W, W.xw0, w->dcd.c, 0, 0, nullptr,
-                                                                  w->pb_dcd.pt_val, nullptr, nullptr, nullptr, nullptr);
-    k_pairs<<<dim3(nblk(w->dcd.max_ee_cap, 64), ne), 64, 0, st>>>(W, W.xw0, w->dcd.c, 1, 0, nullptr,
-                                                                  w->pb_dcd.ee_val, nullptr, nullptr, nullptr, nullptr);
+    w->pairs(W.xw0, w->dcd, w->pb_dcd, 0, nullptr, K_PAIRS_V);
     int max_slots = 0;
     for (int e = 0; e < ne; ++e) max_slots = std::max(max_slots, w->h_env_slot[e + 1] - w->h_env_slot[e]);
-    k_ground<<<dim3(nblk(max_slots, 128), ne), 128, 0, st>>>(W, W.xw0, w->dcd.c, 0, nullptr, w->pb_dcd.gnd_val,
+    IPC_LAUNCH(K_GROUND, st, k_ground, dim3(nblk(max_slots, 128), ne), 128, 0, W, W.xw0, w->dcd.c, 0, w->ok, w->pb_dcd.gnd_val,
                                                              nullptr, nullptr, nullptr);
-    k_start_check<<<ne, 128, 0, st>>>(W, S, w->dcd.c, w->pb_dcd.pt_val, w->pb_dcd.ee_val, w->pb_dcd.gnd_val, w->ok);
+    IPC_LAUNCH(K_MISC, st, k_start_check, ne, 128, 0, W, S, w->dcd.c, w->pb_dcd.pt_val, w->pb_dcd.ee_val, w->pb_dcd.gnd_val, w->ok);
     // predictor
-    k_predictor<<<nblk(W.n_dof, 256), 256, 0, st>>>(W, h);
-    k_predictor_forces<<<nblk(std::max(W.n_vert, W.n_aff), 128), 128, 0, st>>>(W, h);
+    IPC_LAUNCH(K_MISC, st, k_predictor, nblk(W.n_dof, 256), 256, 0, W, h);
+    IPC_LAUNCH(K_MISC, st, k_predictor_forces, nblk(std::max(W.n_vert, W.n_aff), 128), 128, 0, W, h);
     // fresh AL cycle per step (ref solver.py:394-400)
     if (W.n_cons) {
       if (!w->targets_set) throw std::runtime_error("kinematic constraint targets were never set");
-      CK(cudaMemcpyAsync(w->d_targets, tg.data(), tg.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-      k_cons_reset<<<nblk(W.n_cons, 128), 128, 0, st>>>(W, w->d_targets);
+      IPC_LAUNCH(K_MISC, st, k_cons_reset, nblk(W.n_cons, 128), 128, 0, W, w->d_targets);
     }
     int fp_iters = std::max(cfg->friction_fixed_point_iters, 1);
     for (int fp = 0; fp < fp_iters; ++fp) {
@@ -676,35 +843,35 @@ int ipc_world_step(ipc_world* w, const ipc_step_config* cfg, const double* targe
         w->lags_stale = false;
       }
       if (fp == 0) {
-        k_lags<<<ne, BP_THREADS, 0, st>>>(W, W.xw0, w->dcd.c, w->L, w->ok);
+        IPC_LAUNCH(K_LAGS, st, k_lags, ne, BP_THREADS, 0, W, W.xw0, w->dcd.c, w->L, w->ok);
+        IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, ne, w->L.n, w->ok, w->L.pre);
+        IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, ne, w->L.g_n, w->ok, w->L.g_pre);
       } else {
         w->world_pos(W.x, W.xw);
         w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, w->ok);
-        k_lags<<<ne, BP_THREADS, 0, st>>>(W, W.xw, w->dcd.c, w->L, w->ok);
+        IPC_LAUNCH(K_LAGS, st, k_lags, ne, BP_THREADS, 0, W, W.xw, w->dcd.c, w->L, w->ok);
+        IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, ne, w->L.n, w->ok, w->L.pre);
+        IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, ne, w->L.g_n, w->ok, w->L.g_pre);
       }
-      k_copy_int<<<nblk(ne, 128), 128, 0, st>>>(ne, w->ok, S.al_active);
+      IPC_LAUNCH(K_MISC, st, k_copy_int, nblk(ne, 128), 128, 0, ne, w->ok, S.al_active);
       for (int outer = 0; outer < cfg->al_max_outer; ++outer) {
         if (w->count(S.al_active) == 0) break;
         w->newton_solve(*cfg);
-        k_al_update<<<nblk(ne, 128), 128, 0, st>>>(W, S, outer);
+        IPC_LAUNCH(K_MISC, st, k_al_update, nblk(ne, 128), 128, 0, W, S, outer);
       }
-      k_and_not<<<nblk(ne, 128), 128, 0, st>>>(ne, w->ok, S.ls_failed);
+      IPC_LAUNCH(K_MISC, st, k_and_not, nblk(ne, 128), 128, 0, ne, w->ok, S.ls_failed);
     }
     // post-step distance and barrier adaptation (ref solver.py:440-450)
-    k_copy_int<<<nblk(ne, 128), 128, 0, st>>>(ne, S.err, w->accepted);
-    k_fill_int<<<nblk(ne, 128), 128, 0, st>>>(ne, w->ok, 1);
-    k_and_not<<<nblk(ne, 128), 128, 0, st>>>(ne, w->ok, w->accepted);
+    IPC_LAUNCH(K_MISC, st, k_copy_int, nblk(ne, 128), 128, 0, ne, w->enable, w->ok);
+    IPC_LAUNCH(K_MISC, st, k_and_not, nblk(ne, 128), 128, 0, ne, w->ok, S.err);
     w->world_pos(W.x, W.xw);
     w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, w->ok);
-    k_fill<<<nblk(ne, 128), 128, 0, st>>>(ne, S.min_s, INFINITY);
-    k_pairs<<<dim3(nblk(w->dcd.max_pt_cap, 64), ne), 64, 0, st>>>(W, W.xw, w->dcd.c, 0, 0, w->ok, w->pb_dcd.pt_val,
-                                                                  nullptr, nullptr, nullptr, S.min_s);
-    k_pairs<<<dim3(nblk(w->dcd.max_ee_cap, 64), ne), 64, 0, st>>>(W, W.xw, w->dcd.c, 1, 0, w->ok, w->pb_dcd.ee_val,
-                                                                  nullptr, nullptr, nullptr, S.min_s);
-    k_ground<<<dim3(nblk(max_slots, 128), ne), 128, 0, st>>>(W, W.xw, w->dcd.c, 0, w->ok, w->pb_dcd.gnd_val,
+    IPC_LAUNCH(K_MISC, st, k_fill, nblk(ne, 128), 128, 0, ne, S.min_s, INFINITY);
+    w->pairs(W.xw, w->dcd, w->pb_dcd, 0, S.min_s, K_PAIRS_V);
+    IPC_LAUNCH(K_GROUND, st, k_ground, dim3(nblk(max_slots, 128), ne), 128, 0, W, W.xw, w->dcd.c, 0, w->ok, w->pb_dcd.gnd_val,
                                                              nullptr, nullptr, S.min_s);
-    k_kappa_adapt<<<nblk(ne, 128), 128, 0, st>>>(W, S, w->ok);
-    k_finalize<<<nblk(W.n_dof, 256), 256, 0, st>>>(W, h, w->ok);
+    IPC_LAUNCH(K_MISC, st, k_kappa_adapt, nblk(ne, 128), 128, 0, W, S, w->ok);
+    IPC_LAUNCH(K_MISC, st, k_finalize, nblk(W.n_dof, 256), 256, 0, W, h, w->ok);
     CK(cudaGetLastError());
     if (rep) {
       std::vector<int> it(ne), cc(ne), cv(ne), lf(ne), ao(ne), er(ne);
@@ -738,8 +905,67 @@ int ipc_world_step(ipc_world* w, const ipc_step_config* cfg, const double* targe
   })
 }
 
+int ipc_set_device(int device) {
+  GUARD({ CK(cudaSetDevice(device)); })
+}
+
+int ipc_world_profile(ipc_world* w, int on, uint32_t kernel_mask) {
+  GUARD({
+    CK(cudaStreamSynchronize(w->st));
+    w->prof.resolve();
+    w->prof.on = on != 0;
+    w->prof.mask = kernel_mask;
+    for (int k = 0; k < NKID; ++k) { w->prof.ms[k] = 0.0; w->prof.cnt[k] = 0; }
+    w->prof.launches = 0;
+  })
+}
+
+int ipc_world_profile_read(ipc_world* w, double* ms, int64_t* count, int64_t* launches) {
+  GUARD({
+    CK(cudaStreamSynchronize(w->st));
+    w->prof.resolve();
+    for (int k = 0; k < NKID; ++k) {
+      if (ms) ms[k] = w->prof.ms[k];
+      if (count) count[k] = w->prof.cnt[k];
+    }
+    if (launches) *launches = w->prof.launches;
+  })
+}
+
+int ipc_world_flush_l2(ipc_world* w, int64_t bytes) {
+  GUARD({
+    if (!w->flush_buf) w->flush_buf = w->pool.alloc<double>((size_t)bytes / 8);
+    CK(cudaMemsetAsync(w->flush_buf, 0xA5, (size_t)bytes, w->st));
+  })
+}
+
+int ipc_world_mark(ipc_world* w, int slot) {
+  GUARD({
+    while ((int)w->marks.size() <= slot) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      w->marks.push_back(e);
+    }
+    CK(cudaEventRecord(w->marks[slot], w->st));
+  })
+}
+
+int ipc_world_elapsed(ipc_world* w, int a, int b, double* ms) {
+  GUARD({
+    CK(cudaEventSynchronize(w->marks[b]));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, w->marks[a], w->marks[b]));
+    *ms = t;
+  })
+}
+
+int ipc_world_sync(ipc_world* w) {
+  GUARD({ CK(cudaStreamSynchronize(w->st)); })
+}
+
 int ipc_world_get_state(ipc_world* w, double* x, double* v) {
   GUARD({
+    g_prof = &w->prof;
     if (x) CK(cudaMemcpyAsync(x, w->W.x, sizeof(double) * w->W.n_dof, cudaMemcpyDeviceToHost, w->st));
     if (v) CK(cudaMemcpyAsync(v, w->W.v, sizeof(double) * w->W.n_dof, cudaMemcpyDeviceToHost, w->st));
     CK(cudaStreamSynchronize(w->st));
@@ -748,6 +974,7 @@ int ipc_world_get_state(ipc_world* w, double* x, double* v) {
 
 int ipc_world_set_state(ipc_world* w, const double* x, const double* v) {
   GUARD({
+    g_prof = &w->prof;
     if (x) CK(cudaMemcpyAsync(w->W.x, x, sizeof(double) * w->W.n_dof, cudaMemcpyHostToDevice, w->st));
     if (v) CK(cudaMemcpyAsync(w->W.v, v, sizeof(double) * w->W.n_dof, cudaMemcpyHostToDevice, w->st));
     CK(cudaStreamSynchronize(w->st));
@@ -762,18 +989,21 @@ int ipc_world_state_device(ipc_world* w, double** x, double** v) {
 
 int ipc_world_get_kappa(ipc_world* w, double* kappa) {
   GUARD({
+    g_prof = &w->prof;
     CK(cudaMemcpy(kappa, w->W.env_kappa, sizeof(double) * w->n_env, cudaMemcpyDeviceToHost));
   })
 }
 
 int ipc_world_set_kappa(ipc_world* w, const double* kappa) {
   GUARD({
+    g_prof = &w->prof;
     CK(cudaMemcpy(w->W.env_kappa, kappa, sizeof(double) * w->n_env, cudaMemcpyHostToDevice));
   })
 }
 
 int ipc_world_get_constraints(ipc_world* w, double* lam, double* kappa) {
   GUARD({
+    g_prof = &w->prof;
     if (lam) CK(cudaMemcpy(lam, w->W.cons_lam, sizeof(double) * 12 * w->W.n_cons, cudaMemcpyDeviceToHost));
     if (kappa) CK(cudaMemcpy(kappa, w->W.cons_kappa, sizeof(double) * w->W.n_cons, cudaMemcpyDeviceToHost));
   })
@@ -785,17 +1015,12 @@ static void contact_at_current(ipc_world* w) {
   int ne = w->n_env;
   w->world_pos(W.x, W.xw);
   w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, nullptr);
-  k_pairs<<<dim3(nblk(w->dcd.max_pt_cap, 64), ne), 64, 0, w->st>>>(W, W.xw, w->dcd.c, 0, 1, nullptr, w->pb_dcd.pt_val,
-                                                                   w->pb_dcd.pt_g, w->pb_dcd.pt_h, w->pb_dcd.pt_act,
-                                                                   nullptr);
-  k_pairs<<<dim3(nblk(w->dcd.max_ee_cap, 64), ne), 64, 0, w->st>>>(W, W.xw, w->dcd.c, 1, 1, nullptr, w->pb_dcd.ee_val,
-                                                                   w->pb_dcd.ee_g, w->pb_dcd.ee_h, w->pb_dcd.ee_act,
-                                                                   nullptr);
+  w->pairs(W.xw, w->dcd, w->pb_dcd, 1, nullptr, K_SENSE);
   int max_slots = 0;
   for (int e = 0; e < ne; ++e) max_slots = std::max(max_slots, w->h_env_slot[e + 1] - w->h_env_slot[e]);
-  k_ground<<<dim3(nblk(max_slots, 128), ne), 128, 0, w->st>>>(W, W.xw, w->dcd.c, 1, nullptr, w->pb_dcd.gnd_val,
+  IPC_LAUNCH(K_GROUND, w->st, k_ground, dim3(nblk(max_slots, 128), ne), 128, 0, W, W.xw, w->dcd.c, 1, nullptr, w->pb_dcd.gnd_val,
                                                               w->pb_dcd.gnd_gy, w->pb_dcd.gnd_hyy, nullptr);
-  k_slot_forces<<<nblk(W.n_slot, 128), 128, 0, w->st>>>(W, w->dcd.c, w->pb_dcd.pt_g, w->pb_dcd.pt_act,
+  IPC_LAUNCH(K_SENSE, w->st, k_slot_forces, nblk(W.n_slot, 128), 128, 0, W, w->dcd.c, w->pb_dcd.pt_g, w->pb_dcd.pt_act,
                                                         w->pb_dcd.ee_g, w->pb_dcd.ee_act, w->pb_dcd.gnd_gy, 1.0,
                                                         w->slot_force);
   CK(cudaGetLastError());
@@ -803,6 +1028,7 @@ static void contact_at_current(ipc_world* w) {
 
 int ipc_world_slot_forces(ipc_world* w, double h, double* out) {
   GUARD({
+    g_prof = &w->prof;
     contact_at_current(w);
     std::vector<double> f(3 * (size_t)w->W.n_slot);
     CK(cudaMemcpyAsync(f.data(), w->slot_force, sizeof(double) * f.size(), cudaMemcpyDeviceToHost, w->st));
@@ -814,11 +1040,12 @@ int ipc_world_slot_forces(ipc_world* w, double h, double* out) {
 
 int ipc_world_group_forces(ipc_world* w, double h, const uint64_t* groups, int ng, double* out) {
   GUARD({
+    g_prof = &w->prof;
     contact_at_current(w);
     size_t n = (size_t)w->n_env * ng;
     unsigned long long* dg = w->pool.upload((const unsigned long long*)groups, n);
     double* dout = w->pool.alloc<double>(3 * n);
-    k_group_forces<<<nblk(n, 128), 128, 0, w->st>>>(w->W, w->slot_force, dg, ng, dout);
+    IPC_LAUNCH(K_SENSE, w->st, k_group_forces, nblk(n, 128), 128, 0, w->W, w->slot_force, dg, ng, dout);
     CK(cudaMemcpyAsync(out, dout, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, w->st));
     CK(cudaStreamSynchronize(w->st));
     double ih = 1.0 / (h * h);
@@ -830,6 +1057,7 @@ int ipc_world_group_forces(ipc_world* w, double h, const uint64_t* groups, int n
 
 int ipc_world_candidates(ipc_world* w, int env, int which, int32_t* out, int64_t cap, int64_t* n) {
   GUARD({
+    g_prof = &w->prof;
     World& W = w->W;
     w->world_pos(W.x, W.xw);
     w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, nullptr);
@@ -854,19 +1082,17 @@ int ipc_world_candidates(ipc_world* w, int env, int which, int32_t* out, int64_t
 
 int ipc_world_min_distance(ipc_world* w, double* out) {
   GUARD({
+    g_prof = &w->prof;
     World& W = w->W;
     int ne = w->n_env;
     w->world_pos(W.x, W.xw);
     w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, nullptr);
     double* d = w->S.min_s_before;  // scratch
-    k_fill<<<nblk(ne, 128), 128, 0, w->st>>>(ne, d, INFINITY);
-    k_pairs<<<dim3(nblk(w->dcd.max_pt_cap, 64), ne), 64, 0, w->st>>>(W, W.xw, w->dcd.c, 0, 0, nullptr,
-                                                                     w->pb_dcd.pt_val, nullptr, nullptr, nullptr, d);
-    k_pairs<<<dim3(nblk(w->dcd.max_ee_cap, 64), ne), 64, 0, w->st>>>(W, W.xw, w->dcd.c, 1, 0, nullptr,
-                                                                     w->pb_dcd.ee_val, nullptr, nullptr, nullptr, d);
+    IPC_LAUNCH(K_MISC, w->st, k_fill, nblk(ne, 128), 128, 0, ne, d, INFINITY);
+    w->pairs(W.xw, w->dcd, w->pb_dcd, 0, d, K_PAIRS_V);
     int max_slots = 0;
     for (int e = 0; e < ne; ++e) max_slots = std::max(max_slots, w->h_env_slot[e + 1] - w->h_env_slot[e]);
-    k_ground<<<dim3(nblk(max_slots, 128), ne), 128, 0, w->st>>>(W, W.xw, w->dcd.c, 0, nullptr, w->pb_dcd.gnd_val,
+    IPC_LAUNCH(K_GROUND, w->st, k_ground, dim3(nblk(max_slots, 128), ne), 128, 0, W, W.xw, w->dcd.c, 0, nullptr, w->pb_dcd.gnd_val,
                                                                 nullptr, nullptr, d);
     std::vector<double> s(ne);
     CK(cudaMemcpyAsync(s.data(), d, 8 * ne, cudaMemcpyDeviceToHost, w->st));
@@ -877,6 +1103,7 @@ int ipc_world_min_distance(ipc_world* w, double* out) {
 
 int ipc_world_group_distance(ipc_world* w, const uint64_t* ga, const uint64_t* gb, double* out) {
   GUARD({
+    g_prof = &w->prof;
     World& W = w->W;
     int ne = w->n_env;
     w->world_pos(W.x, W.xw);
@@ -884,7 +1111,7 @@ int ipc_world_group_distance(ipc_world* w, const uint64_t* ga, const uint64_t* g
     unsigned long long* da = w->pool.upload((const unsigned long long*)ga, ne);
     unsigned long long* db = w->pool.upload((const unsigned long long*)gb, ne);
     double* dout = w->pool.alloc<double>(ne);
-    k_group_distance<<<ne, 256, 0, w->st>>>(W, w->dcd.c, W.xw, da, db, dout);
+    IPC_LAUNCH(K_SENSE, w->st, k_group_distance, ne, 256, 0, W, w->dcd.c, W.xw, da, db, dout);
     CK(cudaMemcpyAsync(out, dout, 8 * ne, cudaMemcpyDeviceToHost, w->st));
     CK(cudaStreamSynchronize(w->st));
     w->pool.free_one(da);
@@ -895,12 +1122,13 @@ int ipc_world_group_distance(ipc_world* w, const uint64_t* ga, const uint64_t* g
 
 int ipc_world_ground_distance(ipc_world* w, const uint64_t* g, double* out) {
   GUARD({
+    g_prof = &w->prof;
     World& W = w->W;
     int ne = w->n_env;
     w->world_pos(W.x, W.xw);
     unsigned long long* dg = w->pool.upload((const unsigned long long*)g, ne);
     double* dout = w->pool.alloc<double>(ne);
-    k_ground_distance<<<nblk(ne, 128), 128, 0, w->st>>>(W, W.xw, dg, dout);
+    IPC_LAUNCH(K_SENSE, w->st, k_ground_distance, nblk(ne, 128), 128, 0, W, W.xw, dg, dout);
     CK(cudaMemcpyAsync(out, dout, 8 * ne, cudaMemcpyDeviceToHost, w->st));
     CK(cudaStreamSynchronize(w->st));
     w->pool.free_one(dg);

@@ -436,6 +436,138 @@ IPC_HD bool chol_pd(const double* A, int ld) {
   return true;
 }
 
+// Symmetric eigen-decomposition, V (N x N, row-major) holds A on entry and the
+// eigenvectors (columns) on exit, d the eigenvalues. Householder reduction to
+// tridiagonal form followed by the implicit QL iteration (the classical
+// tred2/tql2 pair): O(N³) with a small constant, ~10x fewer flops than
+// cyclic Jacobi at N = 12.
+template <int N>
+IPC_HD void sym_eigen(double* V, double* d, double* e) {
+  for (int j = 0; j < N; ++j) d[j] = V[(N - 1) * N + j];
+  for (int i = N - 1; i > 0; --i) {
+    double scale = 0.0, h = 0.0;
+    for (int k = 0; k < i; ++k) scale += fabs(d[k]);
+    if (scale == 0.0) {
+      e[i] = d[i - 1];
+      for (int j = 0; j < i; ++j) {
+        d[j] = V[(i - 1) * N + j];
+        V[i * N + j] = 0.0;
+        V[j * N + i] = 0.0;
+      }
+    } else {
+      for (int k = 0; k < i; ++k) {
+        d[k] /= scale;
+        h += d[k] * d[k];
+      }
+      double f = d[i - 1];
+      double g = sqrt(h);
+      if (f > 0) g = -g;
+      e[i] = scale * g;
+      h -= f * g;
+      d[i - 1] = f - g;
+      for (int j = 0; j < i; ++j) e[j] = 0.0;
+      for (int j = 0; j < i; ++j) {
+        f = d[j];
+        V[j * N + i] = f;
+        g = e[j] + V[j * N + j] * f;
+        for (int k = j + 1; k <= i - 1; ++k) {
+          g += V[k * N + j] * d[k];
+          e[k] += V[k * N + j] * f;
+        }
+        e[j] = g;
+      }
+      f = 0.0;
+      for (int j = 0; j < i; ++j) {
+        e[j] /= h;
+        f += e[j] * d[j];
+      }
+      double hh = f / (h + h);
+      for (int j = 0; j < i; ++j) e[j] -= hh * d[j];
+      for (int j = 0; j < i; ++j) {
+        f = d[j];
+        g = e[j];
+        for (int k = j; k <= i - 1; ++k) V[k * N + j] -= (f * e[k] + g * d[k]);
+        d[j] = V[(i - 1) * N + j];
+        V[i * N + j] = 0.0;
+      }
+    }
+    d[i] = h;
+  }
+  for (int i = 0; i < N - 1; ++i) {
+    V[(N - 1) * N + i] = V[i * N + i];
+    V[i * N + i] = 1.0;
+    double h = d[i + 1];
+    if (h != 0.0) {
+      for (int k = 0; k <= i; ++k) d[k] = V[k * N + i + 1] / h;
+      for (int j = 0; j <= i; ++j) {
+        double g = 0.0;
+        for (int k = 0; k <= i; ++k) g += V[k * N + i + 1] * V[k * N + j];
+        for (int k = 0; k <= i; ++k) V[k * N + j] -= g * d[k];
+      }
+    }
+    for (int k = 0; k <= i; ++k) V[k * N + i + 1] = 0.0;
+  }
+  for (int j = 0; j < N; ++j) {
+    d[j] = V[(N - 1) * N + j];
+    V[(N - 1) * N + j] = 0.0;
+  }
+  V[(N - 1) * N + N - 1] = 1.0;
+  e[0] = 0.0;
+  // implicit QL
+  for (int i = 1; i < N; ++i) e[i - 1] = e[i];
+  e[N - 1] = 0.0;
+  double f = 0.0, tst1 = 0.0;
+  const double eps = 2.220446049250313e-16;
+  for (int l = 0; l < N; ++l) {
+    tst1 = fmax(tst1, fabs(d[l]) + fabs(e[l]));
+    int m = l;
+    while (m < N - 1) {
+      if (fabs(e[m]) <= eps * tst1) break;
+      ++m;
+    }
+    if (m > l) {
+      for (int iter = 0; iter < 60; ++iter) {
+        double g = d[l];
+        double p = (d[l + 1] - g) / (2.0 * e[l]);
+        double r = hypot(p, 1.0);
+        if (p < 0) r = -r;
+        d[l] = e[l] / (p + r);
+        d[l + 1] = e[l] * (p + r);
+        double dl1 = d[l + 1];
+        double h = g - d[l];
+        for (int i = l + 2; i < N; ++i) d[i] -= h;
+        f += h;
+        p = d[m];
+        double c = 1.0, c2 = 1.0, c3 = 1.0, el1 = e[l + 1], s = 0.0, s2 = 0.0;
+        for (int i = m - 1; i >= l; --i) {
+          c3 = c2;
+          c2 = c;
+          s2 = s;
+          g = c * e[i];
+          h = c * p;
+          r = hypot(p, e[i]);
+          e[i + 1] = s * r;
+          s = e[i] / r;
+          c = p / r;
+          p = c * d[i] - s * g;
+          d[i + 1] = h + s * (c * g + s * d[i]);
+          for (int k = 0; k < N; ++k) {
+            h = V[k * N + i + 1];
+            V[k * N + i + 1] = s * V[k * N + i] + c * h;
+            V[k * N + i] = c * V[k * N + i] - s * h;
+          }
+        }
+        p = -s * s2 * c3 * el1 * e[l] / dl1;
+        e[l] = s * p;
+        d[l] = c * p;
+        if (!(fabs(e[l]) > eps * tst1)) break;
+      }
+    }
+    d[l] = d[l] + f;
+    e[l] = 0.0;
+  }
+}
+
 // In-place: A <- V max(Λ,0) Vᵀ. Symmetrizes first (ref spd.py:8).
 template <int N>
 IPC_HD void psd_project(double* A, int ld) {
@@ -445,51 +577,15 @@ IPC_HD void psd_project(double* A, int ld) {
       A[i * ld + j] = A[j * ld + i] = s;
     }
   if (chol_pd<N>(A, ld)) return;  // already positive definite: projection is the identity
-  double a[N * N], V[N * N];
+  double V[N * N], d[N], e[N];
   for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N; ++j) {
-      a[i * N + j] = A[i * ld + j];
-      V[i * N + j] = (i == j) ? 1.0 : 0.0;
-    }
-  for (int sweep = 0; sweep < 30; ++sweep) {
-    double off = 0.0, diag = 0.0;
-    for (int i = 0; i < N; ++i) {
-      diag += a[i * N + i] * a[i * N + i];
-      for (int j = i + 1; j < N; ++j) off += a[i * N + j] * a[i * N + j];
-    }
-    if (off <= 1e-34 * (diag + off) || off == 0.0) break;
-    for (int p = 0; p < N - 1; ++p)
-      for (int q = p + 1; q < N; ++q) {
-        double apq = a[p * N + q];
-        if (apq == 0.0) continue;
-        double app = a[p * N + p], aqq = a[q * N + q];
-        if (fabs(apq) < 1e-300) continue;
-        double theta = (aqq - app) / (2.0 * apq);
-        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-        for (int k = 0; k < N; ++k) {
-          double akp = a[k * N + p], akq = a[k * N + q];
-          a[k * N + p] = c * akp - s * akq;
-          a[k * N + q] = s * akp + c * akq;
-        }
-        for (int k = 0; k < N; ++k) {
-          double apk = a[p * N + k], aqk = a[q * N + k];
-          a[p * N + k] = c * apk - s * aqk;
-          a[q * N + k] = s * apk + c * aqk;
-        }
-        for (int k = 0; k < N; ++k) {
-          double vkp = V[k * N + p], vkq = V[k * N + q];
-          V[k * N + p] = c * vkp - s * vkq;
-          V[k * N + q] = s * vkp + c * vkq;
-        }
-      }
-  }
-  double lam[N];
-  for (int i = 0; i < N; ++i) lam[i] = fmax(a[i * N + i], 0.0);
+    for (int j = 0; j < N; ++j) V[i * N + j] = A[i * ld + j];
+  sym_eigen<N>(V, d, e);
+  for (int i = 0; i < N; ++i) d[i] = fmax(d[i], 0.0);
   for (int i = 0; i < N; ++i)
     for (int j = i; j < N; ++j) {
       double s = 0.0;
-      for (int k = 0; k < N; ++k) s += V[i * N + k] * lam[k] * V[j * N + k];
+      for (int k = 0; k < N; ++k) s += V[i * N + k] * d[k] * V[j * N + k];
       A[i * ld + j] = A[j * ld + i] = s;
     }
 }

@@ -96,17 +96,36 @@ __device__ __forceinline__ bool excluded(const World& W, int cb0, int b1, int b2
 
 constexpr int BP_THREADS = 256;
 
-// kind 0: PT, 1: EE, 2: ground
+// kind 0: PT, 1: EE, 2: ground. One CTA per environment. Work items are
+// (row primitive, collision body) pairs in lexicographic order; an item is
+// skipped when the pair is excluded (same rigid body, excluded bodies) or
+// when the row's box misses the body's box inflated by `margin` — exact,
+// because every primitive's inflated box lies inside its body's inflated
+// box. Surviving items test the body's primitives in index order, so the
+// output stays in the reference's lexicographic order.
+constexpr int MAX_BODIES = 64;
+
+__device__ __forceinline__ bool cull_item(const World& W, int cb0, int rb, int B, const double* qlo,
+                                          const double* qhi, const double* blo, const double* bhi,
+                                          double margin) {
+  int gb = cb0 + B;
+  if (gb == rb && W.cbody_rigid[rb]) return true;
+  if (excluded(W, cb0, rb, gb)) return true;
+  return !box_hit(qlo, qhi, blo + 3 * B, bhi + 3 * B, margin);
+}
+
 __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __restrict__ lo,
                                                        const double* __restrict__ hi, Cands C,
                                                        int kind, const int* env_mask) {
   __shared__ int warp_tot[BP_THREADS / 32];
   __shared__ int total;
+  __shared__ double blo[3 * MAX_BODIES], bhi[3 * MAX_BODIES];
+  __shared__ int cnt[BP_THREADS];
   int e = blockIdx.x;
   if (env_mask && !env_mask[e]) return;
   double margin = W.env_dhat[e];
   int s0 = W.env_slot[e], s1 = W.env_slot[e + 1];
-  int cb0 = W.env_cbody[e];
+  int cb0 = W.env_cbody[e], nb = W.env_cbody[e + 1] - cb0;
   if (kind == 2) {
     int base = 0;
     if (!W.env_has_ground[e]) {
@@ -132,80 +151,147 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
     }
     return;
   }
+  // body boxes: one warp per body
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int B = wid; B < nb; B += BP_THREADS / 32) {
+    int a0 = W.cbody_slot[cb0 + B], a1 = W.cbody_slot[cb0 + B + 1];
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int v = a0 + lane; v < a1; v += 32)
+      for (int c = 0; c < 3; ++c) {
+        mn[c] = fmin(mn[c], lo[3 * v + c]);
+        mx[c] = fmax(mx[c], hi[3 * v + c]);
+      }
+    for (int o = 16; o > 0; o >>= 1)
+      for (int c = 0; c < 3; ++c) {
+        mn[c] = fmin(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+        mx[c] = fmax(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+      }
+    if (lane == 0)
+      for (int c = 0; c < 3; ++c) {
+        blo[3 * B + c] = mn[c];
+        bhi[3 * B + c] = mx[c];
+      }
+  }
+  __syncthreads();
   long long cap, off;
-  long long n_items;
-  int t0, nt;
+  int r0, nrow;
   if (kind == 0) {
-    t0 = W.env_tri[e];
-    nt = W.env_tri[e + 1] - t0;
-    n_items = (long long)(s1 - s0) * nt;
+    r0 = s0;
+    nrow = s1 - s0;
     off = C.pt_off[e];
     cap = C.pt_off[e + 1] - off;
   } else {
-    t0 = W.env_edge[e];
-    nt = W.env_edge[e + 1] - t0;
-    n_items = (long long)nt * nt;
+    r0 = W.env_edge[e];
+    nrow = W.env_edge[e + 1] - r0;
     off = C.ee_off[e];
     cap = C.ee_off[e + 1] - off;
   }
+  long long n_items = (long long)nrow * nb;
   long long base = 0;
-  for (long long k0 = 0; k0 < n_items; k0 += BP_THREADS) {
-    long long k = k0 + threadIdx.x;
-    bool hit = false;
-    int a = 0, b = 0;
-    if (k < n_items) {
-      a = (int)(k / nt);
-      b = (int)(k - (long long)a * nt);
+  for (long long i0 = 0; i0 < n_items; i0 += BP_THREADS) {
+    long long it = i0 + threadIdx.x;
+    int row = 0, B = 0, c0 = 0, c1 = 0;
+    double qlo[3], qhi[3];
+    int rb = 0;
+    int2 er = make_int2(0, 0);
+    bool live = false;
+    if (it < n_items) {
+      row = r0 + (int)(it / nb);
+      B = (int)(it % nb);
       if (kind == 0) {
-        int v = s0 + a, t = t0 + b;
-        int3 tv = W.tri_v[t];
-        double plo[3], phi[3];
-#pragma unroll
+        rb = W.slot_cbody[row];
         for (int c = 0; c < 3; ++c) {
-          plo[c] = fmin(fmin(lo[3 * tv.x + c], lo[3 * tv.y + c]), lo[3 * tv.z + c]);
-          phi[c] = fmax(fmax(hi[3 * tv.x + c], hi[3 * tv.y + c]), hi[3 * tv.z + c]);
+          qlo[c] = lo[3 * row + c];
+          qhi[c] = hi[3 * row + c];
         }
-        hit = box_hit(lo + 3 * v, hi + 3 * v, plo, phi, margin);
-        if (hit) {
-          int bv = W.slot_cbody[v], bt = W.tri_cbody[t];
-          bool adj = tv.x == v || tv.y == v || tv.z == v;
-          bool same = bv == bt && W.cbody_rigid[bv];
-          hit = !(adj || same || excluded(W, cb0, bv, bt));
-        }
-        a = v;
-        b = t;
-      } else if (b > a) {
-        int i = t0 + a, j = t0 + b;
-        int2 ei = W.edge_v[i], ej = W.edge_v[j];
-        double qlo[3], qhi[3], plo[3], phi[3];
-#pragma unroll
+        c0 = W.cbody_tri[cb0 + B];
+        c1 = W.cbody_tri[cb0 + B + 1];
+      } else {
+        rb = W.edge_cbody[row];
+        er = W.edge_v[row];
         for (int c = 0; c < 3; ++c) {
-          qlo[c] = fmin(lo[3 * ei.x + c], lo[3 * ei.y + c]);
-          qhi[c] = fmax(hi[3 * ei.x + c], hi[3 * ei.y + c]);
-          plo[c] = fmin(lo[3 * ej.x + c], lo[3 * ej.y + c]);
-          phi[c] = fmax(hi[3 * ej.x + c], hi[3 * ej.y + c]);
+          qlo[c] = fmin(lo[3 * er.x + c], lo[3 * er.y + c]);
+          qhi[c] = fmax(hi[3 * er.x + c], hi[3 * er.y + c]);
         }
-        hit = box_hit(qlo, qhi, plo, phi, margin);
-        if (hit) {
-          bool shared = ei.x == ej.x || ei.x == ej.y || ei.y == ej.x || ei.y == ej.y;
-          int ba = W.edge_cbody[i], bb = W.edge_cbody[j];
-          bool same = ba == bb && W.cbody_rigid[ba];
-          hit = !(shared || same || excluded(W, cb0, ba, bb));
+        c0 = max(W.cbody_edge[cb0 + B], row + 1);
+        c1 = W.cbody_edge[cb0 + B + 1];
+      }
+      live = c0 < c1 && !cull_item(W, cb0, rb, B, qlo, qhi, blo, bhi, margin);
+    }
+    // pass 1: count hits of this item
+    int n_hit = 0;
+    if (live) {
+      for (int t = c0; t < c1; ++t) {
+        bool hit;
+        if (kind == 0) {
+          int3 tv = W.tri_v[t];
+          double plo[3], phi[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            plo[c] = fmin(fmin(lo[3 * tv.x + c], lo[3 * tv.y + c]), lo[3 * tv.z + c]);
+            phi[c] = fmax(fmax(hi[3 * tv.x + c], hi[3 * tv.y + c]), hi[3 * tv.z + c]);
+          }
+          hit = box_hit(qlo, qhi, plo, phi, margin) && !(tv.x == row || tv.y == row || tv.z == row);
+        } else {
+          int2 ej = W.edge_v[t];
+          double plo[3], phi[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            plo[c] = fmin(lo[3 * ej.x + c], lo[3 * ej.y + c]);
+            phi[c] = fmax(hi[3 * ej.x + c], hi[3 * ej.y + c]);
+          }
+          hit = box_hit(qlo, qhi, plo, phi, margin) &&
+                !(er.x == ej.x || er.x == ej.y || er.y == ej.x || er.y == ej.y);
         }
-        a = i;
-        b = j;
+        n_hit += hit;
       }
     }
-    int o = block_ordered_offset<BP_THREADS>(hit, warp_tot, &total);
-    if (hit) {
-      long long dst = base + o;
-      if (dst < cap) {
-        if (kind == 0) C.pt[off + dst] = make_int2(a, b);
-        else C.ee[off + dst] = make_int2(a, b);
-      }
-    }
-    base += total;
+    // exclusive scan of per-item counts (item order = output order)
+    cnt[threadIdx.x] = n_hit;
     __syncthreads();
+    for (int o = 1; o < BP_THREADS; o <<= 1) {
+      int v = threadIdx.x >= o ? cnt[threadIdx.x - o] : 0;
+      __syncthreads();
+      cnt[threadIdx.x] += v;
+      __syncthreads();
+    }
+    long long dst = base + cnt[threadIdx.x] - n_hit;
+    long long chunk_total = cnt[BP_THREADS - 1];
+    __syncthreads();
+    // pass 2: write
+    if (n_hit) {
+      for (int t = c0; t < c1; ++t) {
+        bool hit;
+        if (kind == 0) {
+          int3 tv = W.tri_v[t];
+          double plo[3], phi[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            plo[c] = fmin(fmin(lo[3 * tv.x + c], lo[3 * tv.y + c]), lo[3 * tv.z + c]);
+            phi[c] = fmax(fmax(hi[3 * tv.x + c], hi[3 * tv.y + c]), hi[3 * tv.z + c]);
+          }
+          hit = box_hit(qlo, qhi, plo, phi, margin) && !(tv.x == row || tv.y == row || tv.z == row);
+        } else {
+          int2 ej = W.edge_v[t];
+          double plo[3], phi[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            plo[c] = fmin(lo[3 * ej.x + c], lo[3 * ej.y + c]);
+            phi[c] = fmax(hi[3 * ej.x + c], hi[3 * ej.y + c]);
+          }
+          hit = box_hit(qlo, qhi, plo, phi, margin) &&
+                !(er.x == ej.x || er.x == ej.y || er.y == ej.x || er.y == ej.y);
+        }
+        if (hit) {
+          if (dst < cap) {
+            if (kind == 0) C.pt[off + dst] = make_int2(row, t);
+            else C.ee[off + dst] = make_int2(row, t);
+          }
+          ++dst;
+        }
+      }
+    }
+    base += chunk_total;
   }
   if (threadIdx.x == 0) {
     if (base > cap) {
@@ -214,6 +300,41 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
     }
     if (kind == 0) C.n_pt[e] = (int)base; else C.n_ee[e] = (int)base;
   }
+}
+
+// per-env exclusive prefix of candidate counts over flagged envs (one CTA);
+// pre has n_env + 1 entries, pre[n_env] = total
+__global__ void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
+  __shared__ int part[1024];
+  int tid = threadIdx.x, nt = blockDim.x;
+  int per = (n_env + nt - 1) / nt;
+  int a = tid * per, b = min(n_env, a + per);
+  int s = 0;
+  for (int e = a; e < b; ++e) s += (flag == nullptr || flag[e]) ? cnt[e] : 0;
+  part[tid] = s;
+  __syncthreads();
+  for (int o = 1; o < nt; o <<= 1) {
+    int v = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  int run = part[tid] - s;
+  for (int e = a; e < b; ++e) {
+    pre[e] = run;
+    run += (flag == nullptr || flag[e]) ? cnt[e] : 0;
+  }
+  if (tid == nt - 1) pre[n_env] = part[nt - 1];
+}
+
+// env owning flattened item g: pre[e] <= g < pre[e+1] (last such e)
+__device__ __forceinline__ int find_env(const int* __restrict__ pre, int n_env, int g) {
+  int lo = 0, hi = n_env;  // invariant: pre[lo] <= g < pre[hi]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (pre[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
 }
 
 // ---------------------------------------------------------------------------
@@ -354,22 +475,13 @@ __global__ void k_tet(World W, const double* __restrict__ x, double h2, int deri
   }
 }
 
-// contact pairs over a candidate list. kind 0 PT, 1 EE.
-// val[k] = κ b (× mollifier) for active pairs, 0 otherwise; INF when an
-// active pair has non-positive distance (ref contact.py:497-531).
-// active[k] = slot mask when derivatives were written, 0 otherwise.
-__global__ void k_pairs(World W, const double* __restrict__ xw, Cands C, int kind, int deriv,
-                        const int* env_flag, double* val, double* g12, double* hp,
-                        unsigned char* active, double* env_min_s) {
-  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  int e = blockIdx.y;
-  long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
-  int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
-  if (k >= n) return;
-  if (env_flag && !env_flag[e]) return;
-  k += off;
-  int2 pr = kind == 0 ? C.pt[k] : C.ee[k];
-  int sl[4];
+// Contact pairs, pass 1 (light, every candidate of every flagged env):
+// region + squared distance, value κ b (× mollifier) for active pairs, 0
+// otherwise, INF when an active pair has non-positive distance
+// (ref contact.py:497-531); min distance stats. In the derivative pass the
+// active pairs are appended to a work list for pass 2. Persistent
+// grid-stride over the flattened candidate index (prefix C.pre_*).
+__device__ __forceinline__ void pair_slots(const World& W, int kind, int2 pr, int* sl) {
   if (kind == 0) {
     int3 tv = W.tri_v[pr.y];
     sl[0] = pr.x; sl[1] = tv.x; sl[2] = tv.y; sl[3] = tv.z;
@@ -377,77 +489,112 @@ __global__ void k_pairs(World W, const double* __restrict__ xw, Cands C, int kin
     int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
     sl[0] = a.x; sl[1] = a.y; sl[2] = b.x; sl[3] = b.y;
   }
-  V3 X[4];
-  for (int i = 0; i < 4; ++i) X[i] = ld3(xw + 3 * sl[i]);
-  int region;
-  double d2;
-  if (kind == 0) {
-    region = pt_region(X[0], X[1], X[2], X[3]);
-    d2 = pt_dist2(region, X[0], X[1], X[2], X[3]);
-  } else {
-    region = ee_region(X[0], X[1], X[2], X[3], nullptr);
-    d2 = ee_dist2(region, X[0], X[1], X[2], X[3]);
-  }
-  if (env_min_s) atomic_min_pos(env_min_s + e, d2);
-  double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
-  if (active) active[k] = 0;
-  if (!(d2 < shat)) {
-    val[k] = 0.0;
-    return;
-  }
-  if (d2 <= 0.0) {
-    val[k] = INFINITY;
-    return;
-  }
-  double eps = 0.0;
-  if (kind == 1) eps = 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y];
-  if (!deriv) {
-    double b = barrier_val(d2, shat);
-    double m = kind == 1 ? mollifier_val(cross2(X[1] - X[0], X[3] - X[2]), eps) : 1.0;
-    val[k] = kind == 1 ? kappa * (m * b) : kappa * b;
-    return;
-  }
-  double G[12], H[144];
-  for (int i = 0; i < 12; ++i) G[i] = 0.0;
-  for (int i = 0; i < 144; ++i) H[i] = 0.0;
-  int mask;
-  double s = dist2_derivs(kind == 0, region, X, G, H, &mask);
-  double b, db, d2b;
-  barrier_d(s, shat, &b, &db, &d2b);
-  double gout[12];
-  if (kind == 0) {
-    val[k] = kappa * b;
-    for (int i = 0; i < 12; ++i) gout[i] = kappa * db * G[i];
-    for (int i = 0; i < 12; ++i)
-      for (int j = 0; j < 12; ++j) H[i * 12 + j] = kappa * (d2b * G[i] * G[j] + db * H[i * 12 + j]);
-  } else {
-    double Gc[12], Hc[144];
-    for (int i = 0; i < 12; ++i) Gc[i] = 0.0;
-    for (int i = 0; i < 144; ++i) Hc[i] = 0.0;
-    double c = cross2_derivs(X, Gc, Hc);
-    double t = c / eps;
-    double em, de, d2e;
-    if (t < 1.0) {
-      em = t * (2.0 - t);
-      de = (2.0 - 2.0 * t) / eps;
-      d2e = -2.0 / (eps * eps);
+}
+
+__global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int kind, int deriv,
+                            double* val, unsigned char* active, double* env_min_s, long long* work,
+                            int* work_env, int* work_n) {
+  const int* pre = kind == 0 ? C.pre_pt : C.pre_ee;
+  int total = pre[W.n_env];
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    int e = find_env(pre, W.n_env, g);
+    long long q = (kind == 0 ? C.pt_off[e] : C.ee_off[e]) + (g - pre[e]);
+    int2 pr = kind == 0 ? C.pt[q] : C.ee[q];
+    int sl[4];
+    pair_slots(W, kind, pr, sl);
+    V3 X[4];
+    for (int i = 0; i < 4; ++i) X[i] = ld3(xw + 3 * sl[i]);
+    double d2;
+    if (kind == 0) {
+      int r = pt_region(X[0], X[1], X[2], X[3]);
+      d2 = pt_dist2(r, X[0], X[1], X[2], X[3]);
     } else {
-      em = 1.0; de = 0.0; d2e = 0.0;
+      int r = ee_region(X[0], X[1], X[2], X[3], nullptr);
+      d2 = ee_dist2(r, X[0], X[1], X[2], X[3]);
     }
-    val[k] = kappa * (em * b);
-    for (int i = 0; i < 12; ++i) gout[i] = kappa * ((de * b) * Gc[i] + (em * db) * G[i]);
-    for (int i = 0; i < 12; ++i)
-      for (int j = 0; j < 12; ++j)
-        H[i * 12 + j] = kappa * ((d2e * b) * Gc[i] * Gc[j] + (de * b) * Hc[i * 12 + j] +
-                                 (de * db) * (Gc[i] * G[j] + G[i] * Gc[j]) + (em * d2b) * G[i] * G[j] +
-                                 (em * db) * H[i * 12 + j]);
-    if (t < 1.0) mask = 0xF;
+    if (env_min_s) atomic_min_pos(env_min_s + e, d2);
+    double dhat = W.env_dhat[e], shat = dhat * dhat;
+    if (active) active[q] = 0;
+    if (!(d2 < shat)) {
+      val[q] = 0.0;
+      continue;
+    }
+    if (d2 <= 0.0) {
+      val[q] = INFINITY;
+      continue;
+    }
+    double kappa = W.env_kappa[e];
+    double b = barrier_val(d2, shat);
+    double m = 1.0;
+    if (kind == 1) m = mollifier_val(cross2(X[1] - X[0], X[3] - X[2]), 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y]);
+    val[q] = kind == 1 ? kappa * (m * b) : kappa * b;
+    if (deriv) {
+      int slot = atomicAdd(work_n, 1);
+      work[slot] = q;
+      work_env[slot] = e;
+    }
   }
-  psd_project_masked12(H, mask);
-  for (int i = 0; i < 12; ++i) g12[12 * k + i] = gout[i];
-  for (int i = 0; i < 12; ++i)
-    for (int j = i; j < 12; ++j) hp[PK * k + pk(i, j)] = H[i * 12 + j];
-  if (active) active[k] = (unsigned char)0xF;
+}
+
+// Contact pairs, pass 2 (heavy, active pairs only): closed-form distance
+// derivatives, barrier chain rule, mollifier product rule, PSD projection.
+// Values were written by pass 1; the value term is recomputed from the same
+// formulas here for the derivative distance s (ref contact.py:505-556).
+__global__ void __launch_bounds__(64) k_pair_hess(World W, const double* __restrict__ xw, Cands C, int kind,
+                                                  const long long* work, const int* work_env, const int* work_n,
+                                                  double* g12, double* hp, unsigned char* active) {
+  int total = *work_n;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < total; w += gridDim.x * blockDim.x) {
+    long long k = work[w];
+    int e = work_env[w];
+    int2 pr = kind == 0 ? C.pt[k] : C.ee[k];
+    int sl[4];
+    pair_slots(W, kind, pr, sl);
+    V3 X[4];
+    for (int i = 0; i < 4; ++i) X[i] = ld3(xw + 3 * sl[i]);
+    int region = kind == 0 ? pt_region(X[0], X[1], X[2], X[3]) : ee_region(X[0], X[1], X[2], X[3], nullptr);
+    double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
+    double G[12], H[144];
+    for (int i = 0; i < 12; ++i) G[i] = 0.0;
+    for (int i = 0; i < 144; ++i) H[i] = 0.0;
+    int mask;
+    double s = dist2_derivs(kind == 0, region, X, G, H, &mask);
+    double b, db, d2b;
+    barrier_d(s, shat, &b, &db, &d2b);
+    double gout[12];
+    if (kind == 0) {
+      for (int i = 0; i < 12; ++i) gout[i] = kappa * db * G[i];
+      for (int i = 0; i < 12; ++i)
+        for (int j = 0; j < 12; ++j) H[i * 12 + j] = kappa * (d2b * G[i] * G[j] + db * H[i * 12 + j]);
+    } else {
+      double eps = 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y];
+      double Gc[12], Hc[144];
+      for (int i = 0; i < 12; ++i) Gc[i] = 0.0;
+      for (int i = 0; i < 144; ++i) Hc[i] = 0.0;
+      double c = cross2_derivs(X, Gc, Hc);
+      double t = c / eps;
+      double em, de, d2e;
+      if (t < 1.0) {
+        em = t * (2.0 - t);
+        de = (2.0 - 2.0 * t) / eps;
+        d2e = -2.0 / (eps * eps);
+      } else {
+        em = 1.0; de = 0.0; d2e = 0.0;
+      }
+      for (int i = 0; i < 12; ++i) gout[i] = kappa * ((de * b) * Gc[i] + (em * db) * G[i]);
+      for (int i = 0; i < 12; ++i)
+        for (int j = 0; j < 12; ++j)
+          H[i * 12 + j] = kappa * ((d2e * b) * Gc[i] * Gc[j] + (de * b) * Hc[i * 12 + j] +
+                                   (de * db) * (Gc[i] * G[j] + G[i] * Gc[j]) + (em * d2b) * G[i] * G[j] +
+                                   (em * db) * H[i * 12 + j]);
+      if (t < 1.0) mask = 0xF;
+    }
+    psd_project_masked12(H, mask);
+    for (int i = 0; i < 12; ++i) g12[12 * k + i] = gout[i];
+    for (int i = 0; i < 12; ++i)
+      for (int j = i; j < 12; ++j) hp[PK * k + pk(i, j)] = H[i * 12 + j];
+    active[k] = (unsigned char)0xF;
+  }
 }
 
 // ground candidates (ref contact.py:564): value, y-gradient, clamped y-curvature
@@ -642,10 +789,11 @@ IPC_HD double smooth_norm(double u0, double u1, double ml, double eh, double* gu
 __global__ void k_friction(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
                            Lags L, double h, int deriv, const int* env_flag, double* val,
                            double* g12, double* hp) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  int e = blockIdx.y;
-  if (k >= L.n[e]) return;
-  if (env_flag && !env_flag[e]) return;
+  int total = L.pre[W.n_env];
+  for (int gi = blockIdx.x * blockDim.x + threadIdx.x; gi < total; gi += gridDim.x * blockDim.x) {
+  int e = find_env(L.pre, W.n_env, gi);
+  if (env_flag && !env_flag[e]) continue;
+  int k = gi - L.pre[e];
   long long q = L.off[e] + k;
   int4 s4 = L.slots[q];
   int sl[4] = {s4.x, s4.y, s4.z, s4.w};
@@ -660,7 +808,7 @@ __global__ void k_friction(World W, const double* __restrict__ xw, const double*
   double eh = W.env_epsv[e] * h;
   double gu[2], hu[4];
   val[q] = smooth_norm(u0, u1, ml, eh, deriv ? gu : nullptr, hu);
-  if (!deriv) return;
+  if (!deriv) continue;
   double g3[3], h3[9];
   for (int a = 0; a < 3; ++a) {
     g3[a] = T[2 * a] * gu[0] + T[2 * a + 1] * gu[1];
@@ -672,6 +820,7 @@ __global__ void k_friction(World W, const double* __restrict__ xw, const double*
     for (int a = 0; a < 3; ++a) g12[12 * q + 3 * i + a] = gam[i] * g3[a];
   for (int r = 0; r < 12; ++r)
     for (int c = r; c < 12; ++c) hp[PK * q + pk(r, c)] = gam[r / 3] * gam[c / 3] * h3[3 * (r % 3) + c % 3];
+  }
 }
 
 // ground friction: tangent frame (x, z)
@@ -737,28 +886,23 @@ __device__ double pair_ccd_alpha(int kind, const V3* X, const V3* D, double cons
 __global__ void k_ccd_pairs(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
                             Cands C, int kind, double conservative, const int* env_flag,
                             double* env_alpha) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  int e = blockIdx.y;
-  int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
-  if (k >= n) return;
-  if (env_flag && !env_flag[e]) return;
-  long long q = (kind == 0 ? C.pt_off[e] : C.ee_off[e]) + k;
-  int2 pr = kind == 0 ? C.pt[q] : C.ee[q];
-  int sl[4];
-  if (kind == 0) {
-    int3 tv = W.tri_v[pr.y];
-    sl[0] = pr.x; sl[1] = tv.x; sl[2] = tv.y; sl[3] = tv.z;
-  } else {
-    int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
-    sl[0] = a.x; sl[1] = a.y; sl[2] = b.x; sl[3] = b.y;
+  const int* pre = kind == 0 ? C.pre_pt : C.pre_ee;
+  int total = pre[W.n_env];
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    int e = find_env(pre, W.n_env, g);
+    if (env_flag && !env_flag[e]) continue;
+    long long q = (kind == 0 ? C.pt_off[e] : C.ee_off[e]) + (g - pre[e]);
+    int2 pr = kind == 0 ? C.pt[q] : C.ee[q];
+    int sl[4];
+    pair_slots(W, kind, pr, sl);
+    V3 X[4], D[4];
+    for (int i = 0; i < 4; ++i) {
+      X[i] = ld3(xw + 3 * sl[i]);
+      D[i] = ld3(dxw + 3 * sl[i]);
+    }
+    double a = pair_ccd_alpha(kind, X, D, conservative);
+    if (a < 1.0) atomic_min_pos(env_alpha + e, a);
   }
-  V3 X[4], D[4];
-  for (int i = 0; i < 4; ++i) {
-    X[i] = ld3(xw + 3 * sl[i]);
-    D[i] = ld3(dxw + 3 * sl[i]);
-  }
-  double a = pair_ccd_alpha(kind, X, D, conservative);
-  atomic_min_pos(env_alpha + e, a);
 }
 
 __global__ void k_ccd_ground(World W, const double* __restrict__ xw, const double* __restrict__ dxw,

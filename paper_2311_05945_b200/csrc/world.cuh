@@ -30,6 +30,7 @@ struct Cands {
   const long long* ee_off;
   const int* gnd_off;       // == env_slot
   int* overflow;            // [1] set when a capacity is exceeded
+  int *pre_pt, *pre_ee, *pre_gnd;  // [n_env+1] prefix of counts over flagged envs
 };
 
 struct Lags {  // lagged friction (ref friction.py:35)
@@ -42,6 +43,7 @@ struct Lags {  // lagged friction (ref friction.py:35)
   int* g_slot;      // ground lags
   double* g_lam;
   int* g_n;         // [n_env]
+  int *pre, *g_pre;  // [n_env+1] prefix of lag counts
 };
 
 struct World {
@@ -80,6 +82,7 @@ struct World {
   const double* edge_len2;
   const unsigned char *cbody_rigid, *cbody_kin;
   const unsigned long long* cbody_excl;
+  const int *cbody_slot, *cbody_tri, *cbody_edge;  // [n_cbody+1] contiguous primitive ranges
   // constraints
   const int* cons_aff;
   double *cons_target, *cons_lam, *cons_kappa, *cons_kappa0, *cons_mass, *cons_lastres;

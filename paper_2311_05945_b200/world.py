@@ -216,13 +216,32 @@ class GpuWorld:
         return _f64(np.concatenate(out)) if out else self._targets
 
     # -- stepping ----------------------------------------------------------
-    def step(self, cfg, targets=None, want_reports=True):
+    def step(self, cfg, targets=None, want_reports=True, enable=None):
+        """Advance every (enabled) env one step. targets: 12 per kinematic
+        constraint; None reads the scenes' bodies' target_q."""
         c = N.StepConfig(cfg.h, cfg.newton_tol, cfg.max_newton_iters, cfg.max_line_search_halvings,
                          cfg.ccd_conservative_factor, cfg.friction_fixed_point_iters,
                          cfg.al_max_outer)
         t = self.constraint_targets() if targets is None else _f64(targets)
         reps = (N.StepReportC * self.n_env)() if want_reports else None
-        N.check(self.lib.ipc_world_step(self.handle, C.byref(c), N.ptr(t, N._f64p), reps))
+        keep = None if enable is None else _u8(enable)
+        en = None if keep is None else N.ptr(keep, N._u8p)
+        N.check(self.lib.ipc_world_step_ex(self.handle, C.byref(c), N.ptr(t, N._f64p), en, reps))
+        return reps
+
+    def upload_schedule(self, targets):
+        """Device-resident command stream: (n_steps, 12*n_cons) targets."""
+        t = _f64(targets)
+        N.check(self.lib.ipc_world_upload_schedule(self.handle, N.ptr(t, N._f64p), len(targets)))
+
+    def step_scheduled(self, cfg, k, want_reports=True, enable=None):
+        c = N.StepConfig(cfg.h, cfg.newton_tol, cfg.max_newton_iters, cfg.max_line_search_halvings,
+                         cfg.ccd_conservative_factor, cfg.friction_fixed_point_iters,
+                         cfg.al_max_outer)
+        reps = (N.StepReportC * self.n_env)() if want_reports else None
+        keep = None if enable is None else _u8(enable)
+        en = None if keep is None else N.ptr(keep, N._u8p)
+        N.check(self.lib.ipc_world_step_scheduled(self.handle, C.byref(c), int(k), en, reps))
         return reps
 
     # -- queries -----------------------------------------------------------
@@ -275,3 +294,31 @@ class GpuWorld:
         N.check(self.lib.ipc_world_ground_distance(self.handle, N.ptr(a, N._u64p),
                                                    N.ptr(out, N._f64p)))
         return out
+
+    # -- instrumentation (bench.py) -----------------------------------------
+    def profile(self, on=True, kernels=None):
+        """Per-kernel CUDA-event timing on the world's stream; kernels: names
+        from _native.KERNEL_IDS (None = all)."""
+        mask = 0xFFFFFFFF if kernels is None else sum(1 << N.KERNEL_IDS.index(k) for k in kernels)
+        N.check(self.lib.ipc_world_profile(self.handle, 1 if on else 0, mask))
+
+    def profile_read(self):
+        nk = len(N.KERNEL_IDS)
+        ms, cnt, launches = np.zeros(nk), np.zeros(nk, np.int64), C.c_int64()
+        N.check(self.lib.ipc_world_profile_read(self.handle, N.ptr(ms, N._f64p),
+                                                N.ptr(cnt, N._i64p), C.byref(launches)))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(N.KERNEL_IDS)}, launches.value
+
+    def flush_l2(self, nbytes=256 << 20):
+        N.check(self.lib.ipc_world_flush_l2(self.handle, int(nbytes)))
+
+    def mark(self, slot):
+        N.check(self.lib.ipc_world_mark(self.handle, slot))
+
+    def elapsed_ms(self, a, b):
+        out = C.c_double()
+        N.check(self.lib.ipc_world_elapsed(self.handle, a, b, C.byref(out)))
+        return out.value
+
+    def sync(self):
+        N.check(self.lib.ipc_world_sync(self.handle))

@@ -1,0 +1,75 @@
+"""Batched environments on one GPU vs per-environment CPU oracle runs."""
+
+import numpy as np
+import pytest
+
+from oracle import stepper as S
+from oracle.robot import OracleBackend
+
+pytestmark = pytest.mark.gpu
+
+
+def test_scheduled_batch_matches_oracle_per_env():
+    """Config 3 workload: every env of a batch tracks its own oracle run
+    step by step (DoFs within 1e-6 relative, same Newton iteration counts)."""
+    from paper_2311_05945_b200 import workloads as WL
+    from paper_2311_05945_b200.solver import SolverConfig
+    from paper_2311_05945_b200.world import GpuWorld
+
+    E, K = 6, 14
+    scenes, grippers, half, poses = WL.grasp_batch(E, seed=3)
+    sched = WL.schedule(grippers, half, poses, K)
+    ref_scenes, _, _, _ = WL.grasp_batch(E, seed=3)
+    w = GpuWorld(scenes)
+    w.upload_schedule(sched)
+    lays = [S.Layout(s) for s in ref_scenes]
+    nl = len(grippers[0].links)
+    off = w.packed.pre["dof"]
+    for k in range(K):
+        reps = w.step_scheduled(SolverConfig(), k)
+        x, _ = w.get_state()
+        tg = sched[k].reshape(E, nl, 12)
+        for e in range(E):
+            for c, t in zip(ref_scenes[e].constraints, tg[e]):
+                c.body.target_q = t
+            r = S.step(ref_scenes[e], S.Config(), lays[e])
+            xr = ref_scenes[e].state.gather()
+            xe = x[off[e]:off[e + 1]]
+            assert reps[e].newton_iters == r.newton_iters, (k, e)
+            assert np.abs(xe - xr).max() <= 1e-6 * np.abs(xr).max(), (k, e)
+            assert reps[e].min_dist_after > 0.0
+
+
+def test_batch_grasp_outcomes_match_oracle():
+    """Full AutoGrasp/lift/shake programs for several envs in one batch give
+    the same outcome flags and step counts as the oracle run one at a time."""
+    from paper_2311_05945_b200 import data_path
+    from paper_2311_05945_b200.bodies import AffineBody
+    from paper_2311_05945_b200.mesh import box_surface
+    from paper_2311_05945_b200.robot import (Gripper, GraspTrial, autograsp, build_grasp_scene,
+                                             lift_and_shake, parse_urdf, top_down_pose)
+    from paper_2311_05945_b200.robot.batch import BatchGrasp
+
+    cy = 0.02515
+    cases = [(0.05, 0.0, 0.5), (0.04, 0.3, 0.4), (0.05, 0.0, 0.0), (0.05, 0.0, 0.4)]
+    model = parse_urdf(data_path("pj_gripper.urdf"))
+    objs, poses = [], []
+    for size, yaw, _ in cases:
+        objs.append(AffineBody(box_surface(size, center=(0.0, cy, 0.0)), density=500.0))
+        poses.append(top_down_pose((0.0, cy, 0.0), yaw=yaw))
+    # last case: gripper far above the cube -> fingers meet -> NeverHeld
+    poses[3] = top_down_pose((0.0, 0.3, 0.0))
+    mus = [c[2] for c in cases]
+    bg = BatchGrasp(model, objs, np.array(poses), np.zeros((len(cases), 2)), mu=mus)
+    out = bg.run()
+    for e, (size, yaw, mu) in enumerate(cases):
+        g = Gripper(model)
+        o = AffineBody(box_surface(size, center=(0.0, cy, 0.0)), density=500.0)
+        sc = build_grasp_scene(o, g, poses[e], [0.0, 0.0], mu=mu)
+        tr = GraspTrial(poses[e], np.zeros(2))
+        be = OracleBackend()
+        autograsp(sc, g, tr, backend=be)
+        lift_and_shake(sc, g, o, tr, backend=be)
+        assert out[e] == tr.outcome, (e, out[e], tr.outcome)
+        assert bg.steps[e] == tr.steps, (e, bg.steps[e], tr.steps)
+        np.testing.assert_allclose(np.array(bg.forces[e]), np.array(tr.forces), rtol=1e-3, atol=1e-4)
