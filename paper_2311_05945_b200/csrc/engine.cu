@@ -12,7 +12,9 @@
 #include <vector>
 
 #include "../../include/ipc_b200.h"
-#include "solve.cuh"
+#include <cub/cub.cuh>
+
+#include "sparse.cuh"
 
 using namespace ipc;
 
@@ -419,6 +421,7 @@ struct ipc_world {
     std::vector<long long> lo(n_env + 1, 0);
     for (int e = 0; e < n_env; ++e) lo[e + 1] = lo[e] + dcd.pt_cap[e] + dcd.ee_cap[e];
     long long tot = lo[n_env];
+    lag_total = tot;
     for (void* p : {(void*)d_lag_off, (void*)L.slots, (void*)L.gamma, (void*)L.tangent, (void*)L.lam,
                     (void*)fr_val, (void*)D.fr_g, (void*)D.fr_h})
       if (p) pool.free_one(p);
@@ -530,8 +533,11 @@ struct ipc_world {
       IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.min_s, INFINITY, S.newton_active);
       terms(W.x, W.xw, dcd, pb_dcd, true, h, S.newton_active, S.min_s);
       energy(W.x, dcd, pb_dcd, S.newton_active, S.e0);
-      IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, smem, W, S, D_with(pb_dcd), dcd.c, L, W.x, W.xhat, W.p,
-                                                        W.grad);
+      if (sparse)
+        sparse_solve(cfg);
+      else
+        IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, smem, W, S, D_with(pb_dcd), dcd.c, L, W.x,
+                   W.xhat, W.p, W.grad);
       CK(cudaGetLastError());
       IPC_LAUNCH(K_MISC, st, k_newton_check, nblk(n_env, 128), 128, 0, n_env, S, h, cfg.newton_tol);
       if (count(S.ls_active) == 0) continue;
@@ -564,6 +570,173 @@ struct ipc_world {
     }
     // envs still active after the iteration cap did not converge
     IPC_LAUNCH(K_MISC, st, k_mark_unconverged, nblk(n_env, 128), 128, 0, n_env, S);
+  }
+
+  // ---------------- sparse path (large environments) ----------------
+  bool sparse = false;
+  Pcg pcg{};
+  int* d_counts = nullptr;
+  long long* d_offs = nullptr;
+  long long n_el_cap = 0, items_cap = 0;
+  unsigned long long *keys = nullptr, *keys_sorted = nullptr;
+  double* vals = nullptr;
+  int *idx = nullptr, *perm = nullptr, *heads = nullptr;
+  long long *uidx = nullptr, *seg_start = nullptr;
+  unsigned* bcol = nullptr;
+  double* bval = nullptr;
+  int *row_cnt = nullptr, *row_first = nullptr, *bpos = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_tmp_bytes = 0;
+  long long lag_total = 0;
+  double* g_asm = nullptr;
+  int pcg_max_iters = 20000;
+  double pcg_rtol = 1e-12;
+  long long* h_ll = nullptr;  // pinned scalars
+
+  void setup_sparse(const ipc_world_desc* d) {
+    int nn = d->n_dof / 3;
+    std::vector<int> node_env(nn), chunk_env, c0, c1, env_chunk(n_env + 1, 0);
+    const int CH = 256;
+    for (int e = 0; e < n_env; ++e) {
+      int a = d->env_dof[e] / 3, b = d->env_dof[e + 1] / 3;
+      for (int i = a; i < b; ++i) node_env[i] = e;
+      env_chunk[e] = (int)chunk_env.size();
+      for (int s = a; s < b; s += CH) {
+        chunk_env.push_back(e);
+        c0.push_back(s);
+        c1.push_back(std::min(b, s + CH));
+      }
+    }
+    env_chunk[n_env] = (int)chunk_env.size();
+    pcg.n_node = nn;
+    pcg.n_chunk = (int)chunk_env.size();
+    pcg.node_env = pool.upload(node_env.data(), nn);
+    pcg.chunk_env = pool.upload(chunk_env.data(), chunk_env.size());
+    pcg.chunk_n0 = pool.upload(c0.data(), c0.size());
+    pcg.chunk_n1 = pool.upload(c1.data(), c1.size());
+    pcg.env_chunk = pool.upload(env_chunk.data(), env_chunk.size());
+    pcg.x = pool.alloc<double>(d->n_dof);
+    pcg.r = pool.alloc<double>(d->n_dof);
+    pcg.z = pool.alloc<double>(d->n_dof);
+    pcg.p = pool.alloc<double>(d->n_dof);
+    pcg.Ap = pool.alloc<double>(d->n_dof);
+    pcg.Minv = pool.alloc<double>(9 * (size_t)nn);
+    pcg.part = pool.alloc<double>(2 * (size_t)std::max(pcg.n_chunk, 1));
+    pcg.env_rz = pool.alloc<double>(n_env);
+    pcg.env_rz_new = pool.alloc<double>(n_env);
+    pcg.env_pap = pool.alloc<double>(n_env);
+    pcg.env_bb = pool.alloc<double>(n_env);
+    pcg.env_rr = pool.alloc<double>(n_env);
+    pcg.env_live = pool.alloc<int>(n_env);
+    row_cnt = pool.alloc<int>(nn);
+    row_first = pool.alloc<int>(nn);
+    g_asm = pool.alloc<double>(d->n_dof);
+    CK(cudaMallocHost(&h_ll, 4 * sizeof(long long)));
+  }
+
+  template <typename T>
+  void grow(T*& p, long long& cap_track, long long need, long long mult = 1) {
+    (void)cap_track;
+    if (p) pool.free_one(p);
+    p = pool.alloc<T>((size_t)(need * mult));
+  }
+
+  void ensure_cub(size_t need) {
+    if (need > cub_tmp_bytes) {
+      if (cub_tmp) pool.free_one(cub_tmp);
+      cub_tmp = pool.alloc<char>(need);
+      cub_tmp_bytes = need;
+    }
+  }
+
+  // assemble the BSR Newton system of every active env and solve it with
+  // block-Jacobi PCG; writes W.p, W.grad, S.pnorm, S.gnorm
+  void sparse_solve(const ipc_step_config& cfg) {
+    (void)cfg;
+    ElemSpace sp{W.n_vert, W.n_aff, W.n_tet, dcd.pt_total, dcd.ee_total, W.n_slot, lag_total, W.n_slot};
+    long long n_el = sp.n_vert + sp.n_aff + sp.n_tet + sp.n_pt + sp.n_ee + sp.n_gnd + sp.n_fr + sp.n_frg;
+    if (n_el > n_el_cap) {
+      if (d_counts) { pool.free_one(d_counts); pool.free_one(d_offs); }
+      d_counts = pool.alloc<int>(n_el);
+      d_offs = pool.alloc<long long>(n_el);
+      n_el_cap = n_el;
+    }
+    AsmIn A{W, S, D_with(pb_dcd), dcd.c, L, W.x, W.xhat, sp};
+    IPC_LAUNCH(K_DENSE, st, k_asm_count, n_sm * 8, 128, 0, A, d_counts);
+    size_t need = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, need, d_counts, d_offs, n_el, st));
+    ensure_cub(need);
+    CK(cub::DeviceScan::ExclusiveSum(cub_tmp, need, d_counts, d_offs, n_el, st));
+    CK(cudaMemcpyAsync(h_ll, d_offs + n_el - 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    int last = 0;
+    CK(cudaMemcpyAsync(h_count, d_counts + n_el - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    last = *h_count;
+    long long n_items = h_ll[0] + last;
+    if (n_items > items_cap) {
+      for (void* q : {(void*)keys, (void*)keys_sorted, (void*)vals, (void*)idx, (void*)perm, (void*)heads,
+                      (void*)uidx, (void*)seg_start, (void*)bcol, (void*)bval, (void*)bpos})
+        if (q) pool.free_one(q);
+      long long c = std::max(n_items + n_items / 2, 1LL << 16);
+      keys = pool.alloc<unsigned long long>(c);
+      keys_sorted = pool.alloc<unsigned long long>(c);
+      vals = pool.alloc<double>(9 * c);
+      idx = pool.alloc<int>(c);
+      perm = pool.alloc<int>(c);
+      heads = pool.alloc<int>(c);
+      uidx = pool.alloc<long long>(c);
+      seg_start = pool.alloc<long long>(c);
+      bcol = pool.alloc<unsigned>(c);
+      bval = pool.alloc<double>(9 * c);
+      bpos = pool.alloc<int>(c);
+      items_cap = c;
+    }
+    IPC_LAUNCH(K_DENSE, st, k_asm_emit, n_sm * 8, 128, 0, A, d_offs, keys, vals, idx);
+    need = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys_sorted, idx, perm, n_items, 0, 64, st));
+    ensure_cub(need);
+    CK(cub::DeviceRadixSort::SortPairs(cub_tmp, need, keys, keys_sorted, idx, perm, n_items, 0, 64, st));
+    IPC_LAUNCH(K_DENSE, st, k_asm_heads, n_sm * 8, 256, 0, n_items, keys_sorted, heads);
+    need = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, need, heads, uidx, n_items, st));
+    ensure_cub(need);
+    CK(cub::DeviceScan::ExclusiveSum(cub_tmp, need, heads, uidx, n_items, st));
+    CK(cudaMemcpyAsync(h_ll, uidx + n_items - 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_count, heads + n_items - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    long long n_unique = h_ll[0] + *h_count;
+    IPC_LAUNCH(K_DENSE, st, k_asm_starts, n_sm * 8, 256, 0, n_items, heads, uidx, seg_start);
+    CK(cudaMemsetAsync(row_cnt, 0, sizeof(int) * pcg.n_node, st));
+    CK(cudaMemsetAsync(g_asm, 0, sizeof(double) * W.n_dof, st));
+    IPC_LAUNCH(K_DENSE, st, k_asm_reduce, n_sm * 8, 128, 0, n_items, n_unique, keys_sorted, seg_start, perm, vals,
+               g_asm, bcol, bval, row_cnt, bpos);
+    IPC_LAUNCH(K_DENSE, st, k_bsr_rowfirst, n_sm * 8, 256, 0, n_unique, keys_sorted, seg_start, row_first);
+    // PCG
+    pcg.row_first = row_first;
+    pcg.row_cnt = row_cnt;
+    pcg.bcol = bcol;
+    pcg.bval = bval;
+    pcg.env_on = S.newton_active;
+    double rtol2 = pcg_rtol * pcg_rtol;
+    IPC_LAUNCH(K_DENSE, st, k_pcg_setup, n_sm * 8, 128, 0, pcg, g_asm);
+    IPC_LAUNCH(K_DENSE, st, k_pcg_partial, std::max(pcg.n_chunk, 1), 256, 0, pcg, 0);
+    IPC_LAUNCH(K_DENSE, st, k_pcg_env, nblk(n_env, 128), 128, 0, pcg, n_env, 0, rtol2);
+    const int BATCH = 25;
+    for (int it = 0; it < pcg_max_iters; it += BATCH) {
+      for (int b = 0; b < BATCH; ++b) {
+        IPC_LAUNCH(K_DENSE, st, k_pcg_spmv, n_sm * 8, 128, 0, pcg);
+        IPC_LAUNCH(K_DENSE, st, k_pcg_partial, std::max(pcg.n_chunk, 1), 256, 0, pcg, 1);
+        IPC_LAUNCH(K_DENSE, st, k_pcg_env, nblk(n_env, 128), 128, 0, pcg, n_env, 1, rtol2);
+        IPC_LAUNCH(K_DENSE, st, k_pcg_update, n_sm * 8, 128, 0, pcg);
+        IPC_LAUNCH(K_DENSE, st, k_pcg_partial, std::max(pcg.n_chunk, 1), 256, 0, pcg, 2);
+        IPC_LAUNCH(K_DENSE, st, k_pcg_env, nblk(n_env, 128), 128, 0, pcg, n_env, 2, rtol2);
+        IPC_LAUNCH(K_DENSE, st, k_pcg_dir, n_sm * 8, 128, 0, pcg);
+        IPC_LAUNCH(K_DENSE, st, k_pcg_roll, nblk(n_env, 128), 128, 0, pcg, n_env);
+      }
+      if (count(pcg.env_live) == 0) break;
+    }
+    IPC_LAUNCH(K_DENSE, st, k_pcg_finish, n_env, 256, 0, W, S, pcg, g_asm, W.p, W.grad);
+    CK(cudaGetLastError());
   }
 
   Derivs D_with(const PairBufs& pb) {
@@ -705,10 +878,13 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
         throw std::runtime_error("more than 64 collision bodies in one environment");
     }
     const int DENSE_MAX = 160;
-    if (w->max_env_dof > DENSE_MAX)
-      throw std::runtime_error("environment exceeds the dense-solve DoF limit (sparse PCG path not built)");
-    size_t smem = (size_t)(w->max_env_dof * w->max_env_dof + 2 * w->max_env_dof) * sizeof(double);
-    CK(cudaFuncSetAttribute(k_dense_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    w->sparse = w->max_env_dof > DENSE_MAX;
+    if (!w->sparse) {
+      size_t smem = (size_t)(w->max_env_dof * w->max_env_dof + 2 * w->max_env_dof) * sizeof(double);
+      CK(cudaFuncSetAttribute(k_dense_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    } else {
+      w->setup_sparse(d);
+    }
     // env scalar state
     EnvState& S = w->S;
     S.e0 = P.alloc<double>(ne); S.e_new = P.alloc<double>(ne); S.alpha = P.alloc<double>(ne);

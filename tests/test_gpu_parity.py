@@ -140,3 +140,37 @@ def test_grasp_trial_flags_match_reference(golden):
     np.testing.assert_allclose(np.array(tr.forces), z["forces"], rtol=1e-5, atol=1e-5)
     x = sc.state.gather()
     assert np.abs(x - z["x_final"]).max() <= 1e-5 * np.abs(z["x_final"]).max()
+
+
+def test_config0_soft_drop_sparse_path_matches_oracle():
+    """Config 0 (~1.3k tets, 1029 DoFs): BSR assembly + PCG path, per step
+    against the oracle (splu direct solve)."""
+    from paper_2311_05945_b200 import workloads as WL
+
+    a, b = WL.soft_drop(divisions=6), WL.soft_drop(divisions=6)
+    lay = S.Layout(b)
+    cfg = SolverConfig()
+    for k in range(25):
+        _, rep = step(a, cfg)
+        r = S.step(b, S.Config(), lay)
+        xa, xb = a.state.gather(), b.state.gather()
+        assert rep.newton_iters == r.newton_iters, k
+        assert np.abs(xa - xb).max() <= REL * np.abs(xb).max(), k
+        assert rep.min_dist_after > 0.0
+    assert a.barrier.kappa == b.barrier.kappa
+
+
+def test_soft_cube_grasp_trial_matches_reference(golden):
+    z = golden("traj_grasp_soft.npz")
+    g = Gripper(parse_urdf(data_path("pj_gripper.urdf")))
+    obj = SoftBody(box_tet(0.05, 2, center=(0.0, CUBE_Y, 0.0)),
+                   Material(youngs_modulus=1e5, poisson_ratio=0.3, density=500.0))
+    pose = top_down_pose((0.0, CUBE_Y, 0.0))
+    sc = build_grasp_scene(obj, g, pose, [0.0, 0.0], mu=float(z["mu"]))
+    tr = GraspTrial(pose, np.zeros(2))
+    autograsp(sc, g, tr)
+    lift_and_shake(sc, g, obj, tr)
+    assert tr.outcome == str(z["outcome"]) and tr.steps == int(z["steps"])
+    np.testing.assert_allclose(np.array(tr.forces), z["forces"], rtol=1e-4, atol=1e-4)
+    x = sc.state.gather()
+    assert np.abs(x - z["x_final"]).max() <= 1e-5 * np.abs(z["x_final"]).max()
