@@ -38,6 +38,23 @@ def _dist():
     return ws, rank, lr
 
 
+def shard_seed(seed: int, rank: int) -> int:
+    """Each rank owns a disjoint, reproducible slice of environments (weak scaling)."""
+    return seed + 1000 * rank
+
+
+def gather_timing(total_ms: float, newton: float, device=None):
+    """Max time / summed work over ranks (torch.distributed must be initialised;
+    NCCL on GPUs, gloo in the CPU tests). Only the timings cross ranks."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([total_ms, float(newton)], dtype=torch.float64, device=device)
+    g = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(g, t)
+    return max(float(x[0]) for x in g), sum(float(x[1]) for x in g)
+
+
 def _cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -200,7 +217,7 @@ def main():
         dist.init_process_group("nccl")
     cfg = SolverConfig()
     E = args.envs
-    seed = args.seed + 1000 * rank
+    seed = shard_seed(args.seed, rank)
     scenes, grippers, half, poses = WL.grasp_batch(E, seed=seed)
     sched = WL.schedule(grippers, half, poses, W + K)
     world = GpuWorld(scenes)
@@ -236,14 +253,7 @@ def main():
     total_ms = float(np.sum(t_ms))
     final_err = sum(r.error + r.line_search_failed for r in reps)
     if ws > 1:
-        import torch
-        import torch.distributed as dist
-
-        tt = torch.tensor([total_ms, float(newton)], device=f"cuda:{lr}", dtype=torch.float64)
-        g = [torch.zeros_like(tt) for _ in range(ws)]
-        dist.all_gather(g, tt)
-        total_ms = max(float(x[0]) for x in g)
-        newton = sum(float(x[1]) for x in g)
+        total_ms, newton = gather_timing(total_ms, newton, device=f"cuda:{lr}")
     value = E * ws * K / (total_ms * 1e-3)
 
     # end-to-end through the public API: host targets in, state out, every step
@@ -258,10 +268,7 @@ def main():
         x, v = w2.get_state()
     e2e_s = time.perf_counter() - t0
     if ws > 1:
-        tt = torch.tensor([e2e_s], device=f"cuda:{lr}", dtype=torch.float64)
-        g = [torch.zeros_like(tt) for _ in range(ws)]
-        dist.all_gather(g, tt)
-        e2e_s = max(float(x[0]) for x in g)
+        e2e_s, _ = gather_timing(e2e_s, 0.0, device=f"cuda:{lr}")
     e2e = E * ws * K / e2e_s
     h2d = 12 * 8 * world.n_cons
     d2h = 2 * 8 * world.n_dof
