@@ -235,11 +235,12 @@ def main():
                   f"{1e3 * ms / max(c, 1):9.1f} us/launch", file=sys.stderr)
 
     # timed region: device-resident inputs, L2 flushed between steps
-    world.profile(True, kernels=[dom])
+    world.profile(True, kernels=None if os.environ.get("BENCH_PROFILE") == "2" else [dom])
     t_ms, newton = [], 0
     with Clocks(lr) as clk:
         for k in range(W, W + K):
             world.flush_l2()
+            st0 = world.stats()
             world.mark(0)
             reps = world.step_scheduled(cfg, k)
             world.mark(1)
@@ -247,9 +248,16 @@ def main():
             newton += sum(r.newton_iters for r in reps)
             if os.environ.get("BENCH_PROFILE"):
                 it = [r.newton_iters for r in reps]
+                st1 = world.stats()
+                d = {kk: st1[kk] - st0[kk] for kk in st1}
                 print(f"[step {k}] {t_ms[-1]:8.2f} ms newton mean {np.mean(it):.2f} max {max(it)} "
-                      f"al max {max(r.al_outer for r in reps)}", file=sys.stderr)
+                      f"al max {max(r.al_outer for r in reps)} batched {d}", file=sys.stderr)
     prof, launches = world.profile_read()
+    if os.environ.get("BENCH_PROFILE") == "2":
+        for n, (ms, c) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
+            print(f"[timed profile] {n:14s} {ms:9.2f} ms {c:6d} launches "
+                  f"{1e3 * ms / max(c, 1):9.1f} us/launch", file=sys.stderr)
+        dom = max(prof, key=lambda n: prof[n][0])
     total_ms = float(np.sum(t_ms))
     final_err = sum(r.error + r.line_search_failed for r in reps)
     if ws > 1:

@@ -141,6 +141,9 @@ int ipc_set_device(int device);
 int ipc_world_profile(ipc_world *w, int on, uint32_t kernel_mask);
 int ipc_world_profile_read(ipc_world *w, double *ms, int64_t *count, int64_t *launches);
 int ipc_world_flush_l2(ipc_world *w, int64_t bytes);
+/* Cumulative host-loop counters: batched Newton iterations, line-search
+ * rounds, host synchronisations (out: 3). */
+int ipc_world_stats(ipc_world *w, int64_t *out);
 int ipc_world_mark(ipc_world *w, int slot);
 int ipc_world_elapsed(ipc_world *w, int a, int b, double *ms);
 int ipc_world_sync(ipc_world *w);

@@ -54,8 +54,13 @@ enum Kid {
   K_BROAD_DCD = 0, K_BROAD_SWEEP, K_PAIRS_D, K_PAIRS_V, K_TET, K_BODY, K_GROUND, K_FRICTION, K_ENERGY,
   K_DENSE, K_CCD, K_LAGS, K_WORLD, K_SENSE, K_MISC, NKID
 };
+struct OverflowRetry : std::exception {
+  const char* what() const noexcept override { return "candidate capacity overflow"; }
+};
+
 struct Prof {
   bool on = false;
+  bool capturing = false;
   unsigned mask = ~0u;
   long long launches = 0;
   struct Rec {
@@ -65,6 +70,7 @@ struct Prof {
   std::vector<cudaEvent_t> pool;
   std::vector<Rec> pending;
   Rec cur{};
+  std::vector<Rec> capture_list;  // event pairs baked into a graph being captured
   double ms[NKID] = {};
   long long cnt[NKID] = {};
   cudaEvent_t ev() {
@@ -101,7 +107,8 @@ static inline void prof_begin(int kid, cudaStream_t s) {
   if (p->on && ((p->mask >> kid) & 1u)) {
     p->cur.kid = kid;
     p->cur.a = p->ev();
-    CK(cudaEventRecord(p->cur.a, s));
+    if (p->capturing) CK(cudaEventRecordWithFlags(p->cur.a, s, cudaEventRecordExternal));
+    else CK(cudaEventRecord(p->cur.a, s));
   } else {
     p->cur.kid = -1;
   }
@@ -110,8 +117,10 @@ static inline void prof_end(int kid, cudaStream_t s) {
   Prof* p = g_prof;
   if (!p || p->cur.kid < 0) return;
   p->cur.b = p->ev();
-  CK(cudaEventRecord(p->cur.b, s));
-  p->pending.push_back(p->cur);
+  if (p->capturing) CK(cudaEventRecordWithFlags(p->cur.b, s, cudaEventRecordExternal));
+  else CK(cudaEventRecord(p->cur.b, s));
+  if (p->capturing) p->capture_list.push_back(p->cur);
+  else p->pending.push_back(p->cur);
   p->cur.kid = -1;
 }
 #define IPC_LAUNCH(kid, stream, kern, grid, block, smem, ...) \
@@ -152,6 +161,34 @@ __global__ void k_start_check(World W, EnvState S, Cands C, const double* ptv, c
     ok[e] = !bad;
     S.err[e] = bad;
   }
+}
+__global__ void k_status(int n_env, const int* newton, const int* ls, const int* ov1, const int* ov2, int* out) {
+  __shared__ int a, b;
+  if (threadIdx.x == 0) a = b = 0;
+  __syncthreads();
+  int ca = 0, cb = 0;
+  for (int e = threadIdx.x; e < n_env; e += blockDim.x) {
+    ca += newton[e] != 0;
+    cb += ls[e] != 0;
+  }
+  atomicAdd(&a, ca);
+  atomicAdd(&b, cb);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
+    out[2] = *ov1 | *ov2;
+  }
+}
+// dxw = xw(x + p) - xw(x); sweep boxes over [xw, xw + dxw] (ref broadphase.py:206)
+__global__ void k_sweep_box2(int n, const double* xwt, const double* xw, double* dxw, double* lo, double* hi) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * n) return;
+  double d = __dsub_rn(xwt[i], xw[i]);
+  dxw[i] = d;
+  double a = xw[i], b = __dadd_rn(xw[i], d);
+  lo[i] = fmin(a, b);
+  hi[i] = fmax(a, b);
 }
 __global__ void k_copy_int(int n, const int* a, int* b) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -332,6 +369,10 @@ struct ipc_world {
   cudaStream_t st = 0;
   Prof prof;
   int n_sm = 148;
+  long long stat_iters = 0, stat_ls_rounds = 0, stat_syncs = 0;
+  int max_slots = 0;
+  int* d_status = nullptr;
+  int* h_status = nullptr;
   long long* work[2] = {nullptr, nullptr};
   int* work_env[2] = {nullptr, nullptr};
   int* work_n = nullptr;
@@ -341,7 +382,9 @@ struct ipc_world {
   std::vector<cudaEvent_t> marks;
 
   ~ipc_world() {
+    drop_graphs();
     if (h_count) cudaFreeHost(h_count);
+    if (h_status) cudaFreeHost(h_status);
   }
 
   int count(const int* flag) {
@@ -447,6 +490,17 @@ struct ipc_world {
     D.fr_h = pool.alloc<double>(PK * tot);
   }
 
+  // broad phase without a host round trip; overflow stays sticky in the
+  // store's flag and is handled by replaying the step (see ipc_world_step)
+  void broad_nosync(CandStore& cs, const double* lo, const double* hi, const int* env_mask) {
+    for (int kind = 0; kind < 3; ++kind)
+      IPC_LAUNCH((&cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD), st, k_broad, n_env, BP_THREADS, 0, W, lo, hi, cs.c,
+                 kind, env_mask);
+    IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_pt, env_mask, cs.c.pre_pt);
+    IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_ee, env_mask, cs.c.pre_ee);
+    IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_gnd, env_mask, cs.c.pre_gnd);
+  }
+
   // run broad phase; grow capacities and retry on overflow
   void broad(CandStore& cs, PairBufs& pb, bool derivs, const double* lo, const double* hi,
              const int* env_mask) {
@@ -522,51 +576,197 @@ struct ipc_world {
     IPC_LAUNCH(K_ENERGY, st, k_env_energy, n_env, RED_THREADS, 0, W, x, W.xhat, T, cs.c, L, flag, out);
   }
 
-  void newton_solve(const ipc_step_config& cfg) {
-    double h = cfg.h;
-    IPC_LAUNCH(K_MISC, st, k_newton_begin, nblk(n_env, 128), 128, 0, n_env, S, al_flag);
-    size_t smem = (size_t)(max_env_dof * max_env_dof + 2 * max_env_dof) * sizeof(double);
-    for (int it = 0; it < cfg.max_newton_iters; ++it) {
-      if (count(S.newton_active) == 0) break;
-      world_pos(W.x, W.xw);
-      broad(dcd, pb_dcd, true, W.xw, W.xw, S.newton_active);
-      IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.min_s, INFINITY, S.newton_active);
-      terms(W.x, W.xw, dcd, pb_dcd, true, h, S.newton_active, S.min_s);
-      energy(W.x, dcd, pb_dcd, S.newton_active, S.e0);
-      if (sparse)
-        sparse_solve(cfg);
-      else
-        IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, smem, W, S, D_with(pb_dcd), dcd.c, L, W.x,
-                   W.xhat, W.p, W.grad);
-      CK(cudaGetLastError());
-      IPC_LAUNCH(K_MISC, st, k_newton_check, nblk(n_env, 128), 128, 0, n_env, S, h, cfg.newton_tol);
-      if (count(S.ls_active) == 0) continue;
-      // CCD bound along p (ref solver.py:333-343)
-      IPC_LAUNCH(K_MISC, st, k_axpy_env, nblk(W.n_dof, 256), 256, 0, W, W.x, W.p, nullptr, S.ls_active, W.xt);
-      world_pos(W.xt, xwt);
-      IPC_LAUNCH(K_MISC, st, k_sub, nblk(3 * W.n_slot, 256), 256, 0, 3 * W.n_slot, xwt, W.xw, W.dxw);
-      IPC_LAUNCH(K_MISC, st, k_sweep_box, nblk(3 * W.n_slot, 256), 256, 0, W.n_slot, W.xw, W.dxw, xlo, xhi);
-      broad(sweep, pb_sweep, false, xlo, xhi, S.ls_active);
-      IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.alpha_max, 1.0, S.ls_active);
-      for (int kind = 0; kind < 2; ++kind)
-        if (kind == 0 ? sweep.pt_total : sweep.ee_total)
-          IPC_LAUNCH(K_CCD, st, k_ccd_pairs, n_sm * 8, 64, 0, W, W.xw, W.dxw, sweep.c, kind,
-                     cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
-      int max_slots = 0;
-      for (int e = 0; e < n_env; ++e) max_slots = std::max(max_slots, h_env_slot[e + 1] - h_env_slot[e]);
-      IPC_LAUNCH(K_CCD, st, k_ccd_ground, dim3(nblk(max_slots, 128), n_env), 128, 0, W, W.xw, W.dxw, sweep.c,
-                                                                      cfg.ccd_conservative_factor, S.ls_active,
-                                                                      S.alpha_max);
-      IPC_LAUNCH(K_MISC, st, k_ls_begin, nblk(n_env, 128), 128, 0, n_env, S, ls_count);
-      for (int ls = 0; ls < cfg.max_line_search_halvings + 1; ++ls) {
-        if (count(S.ls_active) == 0) break;
-        IPC_LAUNCH(K_MISC, st, k_axpy_env, nblk(W.n_dof, 256), 256, 0, W, W.x, W.p, S.alpha, S.ls_active, W.xt);
+  // ---- one Newton iteration = three fixed launch sequences ----------------
+  // head: DCD broad phase, derivative pass of every term, E0, solve, check
+  void seq_head(const ipc_step_config& cfg) {
+    world_pos(W.x, W.xw);
+    broad_nosync(dcd, W.xw, W.xw, S.newton_active);
+    IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.min_s, INFINITY, S.newton_active);
+    terms(W.x, W.xw, dcd, pb_dcd, true, cfg.h, S.newton_active, S.min_s);
+    energy(W.x, dcd, pb_dcd, S.newton_active, S.e0);
+    if (sparse) {
+      sparse_solve(cfg);
+    } else {
+      size_t smem = (size_t)(max_env_dof * max_env_dof + 2 * max_env_dof) * sizeof(double);
+      IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, smem, W, S, D_with(pb_dcd), dcd.c, L, W.x,
+                 W.xhat, W.p, W.grad);
+    }
+    IPC_LAUNCH(K_MISC, st, k_newton_check, nblk(n_env, 128), 128, 0, n_env, S, cfg.h, cfg.newton_tol);
+  }
+  // CCD bound along p (ref solver.py:333-343)
+  void seq_ccd(const ipc_step_config& cfg) {
+    IPC_LAUNCH(K_MISC, st, k_axpy_env, nblk(W.n_dof, 256), 256, 0, W, W.x, W.p, nullptr, 1.0, S.ls_active, W.xt);
+    world_pos(W.xt, xwt);
+    IPC_LAUNCH(K_MISC, st, k_sweep_box2, nblk(3 * W.n_slot, 256), 256, 0, W.n_slot, xwt, W.xw, W.dxw, xlo, xhi);
+    broad_nosync(sweep, xlo, xhi, S.ls_active);
+    IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.alpha_max, 1.0, S.ls_active);
+    for (int kind = 0; kind < 2; ++kind)
+      if (kind == 0 ? sweep.pt_total : sweep.ee_total)
+        IPC_LAUNCH(K_CCD, st, k_ccd_pairs, n_sm * 8, 64, 0, W, W.xw, W.dxw, sweep.c, kind,
+                   cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
+    IPC_LAUNCH(K_CCD, st, k_ccd_ground, dim3(nblk(max_slots, 128), n_env), 128, 0, W, W.xw, W.dxw, sweep.c,
+               cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
+    IPC_LAUNCH(K_MISC, st, k_ls_begin, nblk(n_env, 128), 128, 0, n_env, S, ls_count);
+  }
+  // one backtracking round (ref solver.py:257): M speculative halvings
+  void seq_ls_round(const ipc_step_config& cfg, int M) {
+    if (!sparse) {
+      IPC_LAUNCH(K_ENERGY, st, k_ls_value, dim3(n_env, M), RED_THREADS, (size_t)3 * max_slots * sizeof(double), W, S,
+                 sweep.c, L, W.x, W.p, W.xhat, cfg.h * cfg.h, cfg.h, e_multi);
+    } else {
+      double scale = 1.0;
+      for (int m = 0; m < M; ++m, scale *= 0.5) {
+        IPC_LAUNCH(K_MISC, st, k_axpy_env, nblk(W.n_dof, 256), 256, 0, W, W.x, W.p, S.alpha, scale, S.ls_active, W.xt);
         world_pos(W.xt, xwt);
-        terms(W.xt, xwt, sweep, pb_sweep, false, h, S.ls_active, nullptr);
-        energy(W.xt, sweep, pb_sweep, S.ls_active, S.e_new);
-        IPC_LAUNCH(K_MISC, st, k_ls_check, nblk(n_env, 128), 128, 0, W, S, ls_count, cfg.max_line_search_halvings, accepted);
-        IPC_LAUNCH(K_MISC, st, k_copy_env, nblk(W.n_dof, 256), 256, 0, W, W.xt, W.x, accepted);
+        terms(W.xt, xwt, sweep, pb_sweep, false, cfg.h, S.ls_active, nullptr);
+        energy(W.xt, sweep, pb_sweep, S.ls_active, e_multi + (size_t)m * n_env);
       }
+    }
+    IPC_LAUNCH(K_MISC, st, k_ls_check_multi, nblk(n_env, 128), 128, 0, W, S, ls_count,
+               cfg.max_line_search_halvings, M, e_multi, accepted);
+    IPC_LAUNCH(K_MISC, st, k_axpy_env, nblk(W.n_dof, 256), 256, 0, W, W.x, W.p, S.alpha, 1.0, accepted, W.x);
+  }
+  void seq_ls(const ipc_step_config& cfg) { seq_ls_round(cfg, 1); }
+
+  // M speculative halvings in one round (follow-up rounds only)
+  static constexpr int LS_M = 8;
+  double* e_multi = nullptr;
+  void seq_ls_multi(const ipc_step_config& cfg) { seq_ls_round(cfg, LS_M); }
+
+  // ---- CUDA graphs of the sequences (dense worlds) ------------------------
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    long long kernels = 0;
+    std::vector<Prof::Rec> timed;  // event pairs recorded inside the graph
+  };
+  Graph g_iter, g_ls;
+  bool graphs_valid = false;
+  bool use_graphs = true;
+  ipc_step_config graph_cfg{};
+
+  void grow_overflowed() {
+    CK(cudaStreamSynchronize(st));
+    for (CandStore* cs : {&dcd, &sweep}) {
+      std::vector<int> np(n_env), ne(n_env);
+      CK(cudaMemcpy(np.data(), cs->c.n_pt, 4 * n_env, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ne.data(), cs->c.n_ee, 4 * n_env, cudaMemcpyDeviceToHost));
+      std::vector<long long> ptc = cs->pt_cap, eec = cs->ee_cap;
+      bool grew = false;
+      for (int e = 0; e < n_env; ++e) {
+        long long nv = h_env_slot[e + 1] - h_env_slot[e], nt = h_env_tri[e + 1] - h_env_tri[e];
+        long long nE = h_env_edge[e + 1] - h_env_edge[e];
+        if (np[e] >= ptc[e] && ptc[e] < nv * nt) { ptc[e] = std::min(nv * nt, 4 * std::max(ptc[e], 1LL)); grew = true; }
+        if (ne[e] >= eec[e] && eec[e] < nE * nE) { eec[e] = std::min(nE * nE, 4 * std::max(eec[e], 1LL)); grew = true; }
+      }
+      if (!grew) continue;
+      alloc_cands(*cs, ptc, eec);
+      alloc_pairbufs(cs == &dcd ? pb_dcd : pb_sweep, *cs, cs == &dcd);
+      if (cs == &dcd) lags_stale = true;
+    }
+    drop_graphs();
+  }
+
+  void drop_graphs() {
+    for (Graph* g : {&g_iter, &g_ls}) {
+      if (g->exec) cudaGraphExecDestroy(g->exec);
+      g->exec = nullptr;
+      for (auto& r : g->timed) { prof.pool.push_back(r.a); prof.pool.push_back(r.b); }
+      g->timed.clear();
+    }
+    graphs_valid = false;
+  }
+
+  template <typename F>
+  void capture(Graph& g, F body) {
+    long long l0 = prof.launches;
+    prof.capturing = true;
+    prof.capture_list.clear();
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    body();
+    cudaGraph_t graph;
+    CK(cudaStreamEndCapture(st, &graph));
+    prof.capturing = false;
+    CK(cudaGraphInstantiate(&g.exec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    g.kernels = prof.launches - l0;
+    prof.launches = l0;
+    g.timed = prof.capture_list;
+    prof.capture_list.clear();
+  }
+
+  static bool same_cfg(const ipc_step_config& a, const ipc_step_config& b) {
+    return a.h == b.h && a.newton_tol == b.newton_tol && a.max_line_search_halvings == b.max_line_search_halvings &&
+           a.ccd_conservative_factor == b.ccd_conservative_factor;
+  }
+
+  void ensure_graphs(const ipc_step_config& cfg) {
+    if (graphs_valid && same_cfg(cfg, graph_cfg) && graph_prof_on == prof.on && graph_prof_mask == prof.mask)
+      return;
+    drop_graphs();
+    capture(g_iter, [&] {
+      seq_head(cfg);
+      seq_ccd(cfg);
+      seq_ls(cfg);
+    });
+    capture(g_ls, [&] { seq_ls_multi(cfg); });
+    graph_cfg = cfg;
+    graph_prof_on = prof.on;
+    graph_prof_mask = prof.mask;
+    graphs_valid = true;
+  }
+  bool graph_prof_on = false;
+  unsigned graph_prof_mask = 0;
+
+  void run(Graph& g) {
+    CK(cudaGraphLaunch(g.exec, st));
+    prof.launches += g.kernels;
+    if (!g.timed.empty()) graph_timed.push_back(&g);
+  }
+  std::vector<Graph*> graph_timed;  // graphs whose event pairs await a sync
+
+  // device status after a sync: active counts + sticky overflow
+  struct Status {
+    int newton, ls, overflow;
+  };
+  Status status() {
+    IPC_LAUNCH(K_MISC, st, k_status, 1, 256, 0, n_env, S.newton_active, S.ls_active, dcd.c.overflow,
+               sweep.c.overflow, d_status);
+    CK(cudaMemcpyAsync(h_status, d_status, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ++stat_syncs;
+    for (Graph* g : graph_timed)
+      for (auto& r : g->timed) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, r.a, r.b));
+        prof.ms[r.kid] += t;
+        prof.cnt[r.kid] += 1;
+      }
+    graph_timed.clear();
+    if (h_status[2]) throw OverflowRetry();
+    return Status{h_status[0], h_status[1], h_status[2]};
+  }
+
+  void newton_solve(const ipc_step_config& cfg) {
+    IPC_LAUNCH(K_MISC, st, k_newton_begin, nblk(n_env, 128), 128, 0, n_env, S, al_flag);
+    bool graphs = use_graphs && !sparse;
+    if (graphs) ensure_graphs(cfg);
+    for (int it = 0; it < cfg.max_newton_iters; ++it) {
+      if (graphs) {
+        run(g_iter);
+      } else {
+        seq_head(cfg);
+        seq_ccd(cfg);
+        seq_ls(cfg);
+      }
+      ++stat_iters;
+      ++stat_ls_rounds;
+      Status s = status();
+      for (int ls = 1; s.ls && ls < cfg.max_line_search_halvings + 1; ls += LS_M) {
+        if (graphs) run(g_ls); else seq_ls_multi(cfg);
+        ++stat_ls_rounds;
+        s = status();
+      }
+      if (s.newton == 0) break;
     }
     // envs still active after the iteration cap did not converge
     IPC_LAUNCH(K_MISC, st, k_mark_unconverged, nblk(n_env, 128), 128, 0, n_env, S);
@@ -866,12 +1066,16 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     w->xlo = P.alloc<double>(3 * (size_t)d->n_slot);
     w->xhi = P.alloc<double>(3 * (size_t)d->n_slot);
     w->slot_force = P.alloc<double>(3 * (size_t)d->n_slot);
+    w->d_status = P.alloc<int>(4);
+    w->e_multi = P.alloc<double>((size_t)ipc_world::LS_M * ne);
+    CK(cudaMallocHost(&w->h_status, 4 * sizeof(int)));
     w->d_targets = P.alloc<double>(12 * (size_t)d->n_cons);
     w->h_env_slot.assign(d->env_slot, d->env_slot + ne + 1);
     w->h_env_dof.assign(d->env_dof, d->env_dof + ne + 1);
     w->h_env_tri.assign(d->env_tri, d->env_tri + ne + 1);
     w->h_env_edge.assign(d->env_edge, d->env_edge + ne + 1);
     w->h_env_cbody.assign(d->env_cbody, d->env_cbody + ne + 1);
+    for (int e = 0; e < ne; ++e) w->max_slots = std::max(w->max_slots, d->env_slot[e + 1] - d->env_slot[e]);
     for (int e = 0; e < ne; ++e) {
       w->max_env_dof = std::max(w->max_env_dof, d->env_dof[e + 1] - d->env_dof[e]);
       if (d->env_cbody[e + 1] - d->env_cbody[e] > 64)
@@ -966,9 +1170,9 @@ int ipc_world_step_scheduled(ipc_world* w, const ipc_step_config* cfg, int k, co
   return step_impl(w, cfg, nullptr, k, enable, rep);
 }
 
-static int step_impl(ipc_world* w, const ipc_step_config* cfg, const double* targets, int sched_k,
-                     const uint8_t* enable, ipc_step_report* rep) {
-  GUARD({
+static void step_core(ipc_world* w, const ipc_step_config* cfg, const double* targets, int sched_k,
+                      const uint8_t* enable, ipc_step_report* rep) {
+  {
     g_prof = &w->prof;
     World& W = w->W;
     EnvState& S = w->S;
@@ -1078,6 +1282,26 @@ static int step_impl(ipc_world* w, const ipc_step_config* cfg, const double* tar
     } else {
       CK(cudaStreamSynchronize(st));
     }
+  }
+}
+
+static int step_impl(ipc_world* w, const ipc_step_config* cfg, const double* targets, int sched_k,
+                     const uint8_t* enable, ipc_step_report* rep) {
+  GUARD({
+    g_prof = &w->prof;
+    for (int attempt = 0;; ++attempt) {
+      try {
+        CK(cudaMemsetAsync(w->dcd.c.overflow, 0, sizeof(int), w->st));
+        CK(cudaMemsetAsync(w->sweep.c.overflow, 0, sizeof(int), w->st));
+        step_core(w, cfg, targets, sched_k, enable, rep);
+        break;
+      } catch (const OverflowRetry&) {
+        if (attempt >= 6) throw std::runtime_error("candidate capacity overflow persists");
+        // replay the step from x_prev with larger candidate capacities
+        CK(cudaMemcpyAsync(w->W.x, w->W.x_prev, sizeof(double) * w->W.n_dof, cudaMemcpyDeviceToDevice, w->st));
+        w->grow_overflowed();
+      }
+    }
   })
 }
 
@@ -1106,6 +1330,13 @@ int ipc_world_profile_read(ipc_world* w, double* ms, int64_t* count, int64_t* la
     }
     if (launches) *launches = w->prof.launches;
   })
+}
+
+int ipc_world_stats(ipc_world* w, int64_t* out) {
+  out[0] = w->stat_iters;
+  out[1] = w->stat_ls_rounds;
+  out[2] = w->stat_syncs;
+  return 0;
 }
 
 int ipc_world_flush_l2(ipc_world* w, int64_t bytes) {

@@ -590,6 +590,59 @@ IPC_HD void psd_project(double* A, int ld) {
     }
 }
 
+// PSD projection of a 3NS x 3NS stencil Hessian that annihilates rigid
+// translations (every contact/friction stencil energy depends on vertex
+// differences only). With Q = Q0 ⊗ I3, Q0 the orthonormal NS x (NS-1)
+// Helmert basis of the complement of (1,…,1), A = Q (QᵀAQ) Qᵀ exactly, and
+// since Q has orthonormal columns the eigenvalue clamp commutes:
+// A⁺ = Q (QᵀAQ)⁺ Qᵀ. Same operator as the full clamp (ref spd.py:6), on a
+// 3(NS-1) core: 9x9 instead of 12x12, 6x6 instead of 9x9, 3x3 instead of 6x6.
+template <int NS>
+IPC_HD void psd_project_tf(double* A, int ld) {
+  constexpr int N = 3 * NS, R = 3 * (NS - 1);
+  double q0[NS][NS - 1];
+  for (int j = 0; j < NS - 1; ++j) {
+    double nrm = rsqrt((double)((j + 1) * (j + 2)));
+    for (int a = 0; a < NS; ++a) q0[a][j] = a <= j ? nrm : (a == j + 1 ? -(j + 1) * nrm : 0.0);
+  }
+  for (int i = 0; i < N; ++i)
+    for (int j = i + 1; j < N; ++j) {
+      double s = 0.5 * (A[i * ld + j] + A[j * ld + i]);
+      A[i * ld + j] = A[j * ld + i] = s;
+    }
+  double T[N * R];  // T = A Q
+  for (int r = 0; r < N; ++r)
+    for (int J = 0; J < NS - 1; ++J)
+      for (int c = 0; c < 3; ++c) {
+        double s = 0.0;
+        for (int b = 0; b < NS; ++b) s += A[r * ld + 3 * b + c] * q0[b][J];
+        T[r * R + 3 * J + c] = s;
+      }
+  double M[R * R];  // M = Qᵀ A Q
+  for (int I = 0; I < NS - 1; ++I)
+    for (int rr = 0; rr < 3; ++rr)
+      for (int k = 0; k < R; ++k) {
+        double s = 0.0;
+        for (int a = 0; a < NS; ++a) s += q0[a][I] * T[(3 * a + rr) * R + k];
+        M[(3 * I + rr) * R + k] = s;
+      }
+  psd_project<R>(M, R);
+  for (int r = 0; r < N; ++r)  // T = Q M
+    for (int k = 0; k < R; ++k) {
+      int a = r / 3, rr = r % 3;
+      double s = 0.0;
+      for (int I = 0; I < NS - 1; ++I) s += q0[a][I] * M[(3 * I + rr) * R + k];
+      T[r * R + k] = s;
+    }
+  for (int r = 0; r < N; ++r)  // A = T Qᵀ
+    for (int c = r; c < N; ++c) {
+      int b = c / 3, cc = c % 3;
+      double s = 0.0;
+      for (int J = 0; J < NS - 1; ++J) s += T[r * R + 3 * J + cc] * q0[b][J];
+      A[r * ld + c] = A[c * ld + r] = s;
+    }
+}
+
 // Project only the rows/columns of a 12x12 stencil Hessian whose slots are
 // active (mask bit per 3-row slot); inactive rows are identically zero, and
 // zero rows/columns carry eigenvalue 0, so this equals the full projection.
@@ -600,14 +653,14 @@ IPC_HD void psd_project_masked12(double* H, int mask) {
     if (mask & (1 << s))
       for (int c = 0; c < 3; ++c) idx[k++] = 3 * s + c;
   if (k == 12) {
-    psd_project<12>(H, 12);
+    psd_project_tf<4>(H, 12);
     return;
   }
   double sub[81];
   for (int i = 0; i < k; ++i)
     for (int j = 0; j < k; ++j) sub[i * k + j] = H[idx[i] * 12 + idx[j]];
-  if (k == 6) psd_project<6>(sub, 6);
-  else psd_project<9>(sub, 9);
+  if (k == 6) psd_project_tf<2>(sub, 6);
+  else psd_project_tf<3>(sub, 9);
   for (int i = 0; i < k; ++i)
     for (int j = 0; j < k; ++j) H[idx[i] * 12 + idx[j]] = sub[i * k + j];
 }
@@ -727,6 +780,62 @@ IPC_HD void polar(const M3& f, M3& R, M3& S) {
       double s = 0.0;
       for (int k = 0; k < 3; ++k) s += V.m[i * 3 + k] * sig[k] * V.m[j * 3 + k];
       S.m[i * 3 + j] = s;
+    }
+}
+
+// PSD projection of the orthogonality Hessian ∂²/∂A² of c‖AAᵀ−I‖²_F (ref
+// terms.py:234-247, projected at :269) in closed form. The energy is
+// isotropic in A's singular values, E = c Σ(σᵢ²−1)², so its 9x9 Hessian has
+// the eigensystem (signed SVD A = U Σ Vᵀ, U, V proper):
+//   scaling  vec(uᵢvᵢᵀ)                 λ = c(12σᵢ² − 4)
+//   twist    vec(uᵢvⱼᵀ − uⱼvᵢᵀ)/√2      λ = 4c(σᵢ² − σᵢσⱼ + σⱼ² − 1)
+//   flip     vec(uᵢvⱼᵀ + uⱼvᵢᵀ)/√2      λ = 4c(σᵢ² + σᵢσⱼ + σⱼ² − 1)
+// (polynomial eigenvalues: no divided differences, stable at σᵢ = σⱼ).
+// out = Σ max(λ, 0) q qᵀ equals the eigenvalue clamp of the explicit Hessian
+// to ~1e-14 relative (checked in tests), at ~1/20 of the cost.
+IPC_HD void ortho_hess_psd(const M3& A, double c, double* h9) {
+  M3 ata = m3_tmul(A, A);
+  double w[3];
+  M3 V;
+  sym3_eig(ata, w, V);
+  if (m3_det(V) < 0) {
+    V.m[2] = -V.m[2]; V.m[5] = -V.m[5]; V.m[8] = -V.m[8];
+  }
+  double s[3];
+  for (int i = 0; i < 3; ++i) s[i] = sqrt(fmax(w[i], 0.0));
+  auto av = [&](int k) {
+    return v3(A.m[0] * V.m[k] + A.m[1] * V.m[3 + k] + A.m[2] * V.m[6 + k],
+              A.m[3] * V.m[k] + A.m[4] * V.m[3 + k] + A.m[5] * V.m[6 + k],
+              A.m[6] * V.m[k] + A.m[7] * V.m[3 + k] + A.m[8] * V.m[6 + k]);
+  };
+  V3 u[3];
+  u[0] = (1.0 / fmax(s[0], 1e-300)) * av(0);
+  u[1] = (1.0 / fmax(s[1], 1e-300)) * av(1);
+  u[2] = cross(u[0], u[1]);
+  s[2] = dot(av(2), u[2]);
+  V3 v[3] = {v3(V.m[0], V.m[3], V.m[6]), v3(V.m[1], V.m[4], V.m[7]), v3(V.m[2], V.m[5], V.m[8])};
+  for (int i = 0; i < 81; ++i) h9[i] = 0.0;
+  double q[9];
+  auto add = [&](double lam) {
+    if (!(lam > 0.0)) return;
+    for (int a = 0; a < 9; ++a)
+      for (int b = 0; b < 9; ++b) h9[9 * a + b] += lam * q[a] * q[b];
+  };
+  for (int i = 0; i < 3; ++i) {
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) q[3 * a + b] = at(u[i], a) * at(v[i], b);
+    add(c * (12.0 * s[i] * s[i] - 4.0));
+  }
+  const double r2 = 0.70710678118654752440;
+  for (int i = 0; i < 3; ++i)
+    for (int j = i + 1; j < 3; ++j) {
+      double base = s[i] * s[i] + s[j] * s[j] - 1.0, cross_ = s[i] * s[j];
+      for (int sgn = -1; sgn <= 1; sgn += 2) {
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b)
+            q[3 * a + b] = r2 * (at(u[i], a) * at(v[j], b) + sgn * at(u[j], a) * at(v[i], b));
+        add(4.0 * c * (base + sgn * cross_));
+      }
     }
 }
 

@@ -40,13 +40,15 @@ __global__ void k_world(World W, const double* __restrict__ x, double* __restric
   }
 }
 
-// out = a + alpha_e * b over DoFs of envs with flag set (others copy a)
-__global__ void k_axpy_env(World W, const double* a, const double* b, const double* alpha,
+
+// out = a + (scale * alpha_e) * b over DoFs of flagged envs (others copy a);
+// scale is a power of two, so scale * alpha equals repeated halving exactly
+__global__ void k_axpy_env(World W, const double* a, const double* b, const double* alpha, double scale,
                            const int* flag, double* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= W.n_dof) return;
   int e = W.dof_env[i];
-  out[i] = (flag == nullptr || flag[e]) ? __dadd_rn(a[i], __dmul_rn(alpha ? alpha[e] : 1.0, b[i])) : a[i];
+  out[i] = (flag == nullptr || flag[e]) ? __dadd_rn(a[i], __dmul_rn(alpha ? alpha[e] * scale : 1.0, b[i])) : a[i];
 }
 
 __global__ void k_sub(int n, const double* a, const double* b, double* out) {
@@ -375,18 +377,8 @@ __global__ void k_body(World W, const double* __restrict__ x, const double* __re
   if (deriv) {
     M3 MA = m3_mul(Mm, A);
     for (int i = 0; i < 9; ++i) g[3 + i] += h2 * 4.0 * c * MA.m[i];
-    M3 ata = m3_tmul(A, A);
     double h9[81];
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j)
-        for (int k = 0; k < 3; ++k)
-          for (int l = 0; l < 3; ++l) {
-            double t = A.m[3 * i + l] * A.m[3 * k + j];
-            if (i == k) t += ata.m[3 * l + j];
-            if (j == l) t += Mm.m[3 * i + k];
-            h9[(3 * i + j) * 9 + 3 * k + l] = 4.0 * c * t;
-          }
-    psd_project<9>(h9, 9);
+    ortho_hess_psd(A, c, h9);
     for (int i = 0; i < 144; ++i) H[i] = M[i];
     for (int i = 0; i < 9; ++i)
       for (int j = 0; j < 9; ++j) H[(3 + i) * 12 + 3 + j] += h2 * h9[9 * i + j];

@@ -70,6 +70,182 @@ __global__ void __launch_bounds__(RED_THREADS) k_env_energy(World W, const doubl
   if (tid == 0) out[e] = s;
 }
 
+// ---------------------------------------------------------------------------
+// Fused line-search energy: one CTA per (env, trial m) evaluates
+// E(x + α 2^-m p) — trial world positions staged in shared memory, then
+// inertia, h²-scaled elasticity and orthogonality, kinematic targets, barrier
+// over the swept candidates, ground, lagged friction — and reduces it in a
+// fixed order. Per-element formulas and operation order are those of the
+// element kernels (k_body, k_tet, k_pair_dist, k_ground, k_friction), so the
+// values are the same bits; a whole M-trial backtracking round is one launch.
+// ---------------------------------------------------------------------------
+__device__ double body_value(const World& W, int b, int e, const double* q, const double* xh, double h2) {
+  const double* M = W.aff_M + 144 * b;
+  double d[12];
+  for (int i = 0; i < 12; ++i) d[i] = q[i] - xh[i];
+  double v = 0.0;
+  for (int i = 0; i < 12; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < 12; ++j) s += M[12 * i + j] * d[j];
+    v += d[i] * s;
+  }
+  v *= 0.5;
+  double c = W.aff_ortho[b];
+  M3 A;
+  for (int i = 0; i < 9; ++i) A.m[i] = q[3 + i];
+  M3 Mm = m3_mul(A, m3_T(A));
+  m3_add_diag(Mm, -1.0);
+  double ov = 0.0;
+  for (int i = 0; i < 9; ++i) ov += Mm.m[i] * Mm.m[i];
+  v += h2 * c * ov;
+  for (int k = W.env_cons[e]; k < W.env_cons[e + 1]; ++k) {
+    if (W.cons_aff[k] != b) continue;
+    double kap = W.cons_kappa[k], sm = sqrt(W.cons_mass[k]);
+    const double* tg = W.cons_target + 12 * k;
+    const double* lam = W.cons_lam + 12 * k;
+    double dd = 0.0, ld = 0.0;
+    for (int i = 0; i < 12; ++i) {
+      double di = q[i] - tg[i];
+      dd += di * di;
+      ld += lam[i] * di;
+    }
+    v += 0.5 * kap * dd - sm * ld;
+  }
+  return v;
+}
+
+__device__ __forceinline__ double axpy_rn(double x, double a, double p) { return __dadd_rn(x, __dmul_rn(a, p)); }
+
+__global__ void __launch_bounds__(RED_THREADS) k_ls_value(World W, EnvState S, Cands C, Lags L,
+                                                           const double* __restrict__ x,
+                                                           const double* __restrict__ p,
+                                                           const double* __restrict__ xhat, double h2, double h,
+                                                           double* e_multi) {
+  extern __shared__ double sxw[];
+  __shared__ double sh[RED_THREADS / 32];
+  int e = blockIdx.x, m = blockIdx.y;
+  if (!S.ls_active[e]) return;
+  double a = S.alpha[e] * ldexp(1.0, -m);
+  int tid = threadIdx.x;
+  int s0 = W.env_slot[e], s1 = W.env_slot[e + 1];
+  for (int s = s0 + tid; s < s1; s += blockDim.x) {
+    int d = W.slot_dof[s];
+    double* o = sxw + 3 * (s - s0);
+    if (!W.slot_aff[s]) {
+      for (int c = 0; c < 3; ++c) o[c] = axpy_rn(x[d + c], a, p[d + c]);
+    } else {
+      const double* r = W.slot_rest + 3 * s;
+      for (int i = 0; i < 3; ++i) {
+        double a0 = axpy_rn(x[d + 3 + 3 * i], a, p[d + 3 + 3 * i]);
+        double a1 = axpy_rn(x[d + 4 + 3 * i], a, p[d + 4 + 3 * i]);
+        double a2 = axpy_rn(x[d + 5 + 3 * i], a, p[d + 5 + 3 * i]);
+        double mm = __dadd_rn(__dadd_rn(__dmul_rn(a0, r[0]), __dmul_rn(a1, r[1])), __dmul_rn(a2, r[2]));
+        o[i] = __dadd_rn(axpy_rn(x[d + i], a, p[d + i]), mm);
+      }
+    }
+  }
+  __syncthreads();
+  auto XW = [&](int s) { return ld3(sxw + 3 * (s - s0)); };
+  double acc = 0.0;
+  for (int v = W.env_vert[e] + tid; v < W.env_vert[e + 1]; v += blockDim.x) {
+    int d = W.vert_dof[v];
+    double mass = W.vert_mass[v], sv = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      double dd = axpy_rn(x[d + c], a, p[d + c]) - xhat[d + c];
+      sv += dd * mass * dd;
+    }
+    acc += 0.5 * sv;
+  }
+  for (int b = W.env_aff[e] + tid; b < W.env_aff[e + 1]; b += blockDim.x) {
+    int o = W.aff_dof[b];
+    double q[12];
+    for (int i = 0; i < 12; ++i) q[i] = axpy_rn(x[o + i], a, p[o + i]);
+    acc += body_value(W, b, e, q, xhat + o, h2);
+  }
+  for (int t = W.env_tet[e] + tid; t < W.env_tet[e + 1]; t += blockDim.x) {
+    int4 td = W.tet_dof[t];
+    int dv[4] = {td.x, td.y, td.z, td.w};
+    V3 X[4];
+    for (int k = 0; k < 4; ++k)
+      X[k] = v3(axpy_rn(x[dv[k]], a, p[dv[k]]), axpy_rn(x[dv[k] + 1], a, p[dv[k] + 1]),
+                axpy_rn(x[dv[k] + 2], a, p[dv[k] + 2]));
+    V3 e1 = X[1] - X[0], e2 = X[2] - X[0], e3 = X[3] - X[0];
+    M3 Ds;
+    Ds.m[0] = e1.x; Ds.m[1] = e2.x; Ds.m[2] = e3.x;
+    Ds.m[3] = e1.y; Ds.m[4] = e2.y; Ds.m[5] = e3.y;
+    Ds.m[6] = e1.z; Ds.m[7] = e2.z; Ds.m[8] = e3.z;
+    M3 Dmi;
+    for (int i = 0; i < 9; ++i) Dmi.m[i] = W.tet_Dminv[9 * t + i];
+    M3 F = m3_mul(Ds, Dmi);
+    double psi = psi_value(W.tet_model[t], F, W.tet_mu[t], W.tet_lam[t]);
+    acc += isinf(psi) ? INFINITY : (h2 * W.tet_vol[t]) * psi;
+  }
+  double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
+  for (int kind = 0; kind < 2; ++kind) {
+    int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
+    long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
+    for (int k = tid; k < n; k += blockDim.x) {
+      int2 pr = kind == 0 ? C.pt[off + k] : C.ee[off + k];
+      int sl[4];
+      pair_slots(W, kind, pr, sl);
+      V3 X[4];
+      for (int i = 0; i < 4; ++i) X[i] = XW(sl[i]);
+      double d2;
+      if (kind == 0) d2 = pt_dist2(pt_region(X[0], X[1], X[2], X[3]), X[0], X[1], X[2], X[3]);
+      else d2 = ee_dist2(ee_region(X[0], X[1], X[2], X[3], nullptr), X[0], X[1], X[2], X[3]);
+      if (!(d2 < shat)) continue;
+      if (d2 <= 0.0) {
+        acc += INFINITY;
+        continue;
+      }
+      double bv = barrier_val(d2, shat);
+      if (kind == 0) {
+        acc += kappa * bv;
+      } else {
+        double mo = mollifier_val(cross2(X[1] - X[0], X[3] - X[2]), 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y]);
+        acc += kappa * (mo * bv);
+      }
+    }
+  }
+  if (W.env_has_ground[e]) {
+    double gy = W.env_ground_y[e];
+    for (int k = tid; k < C.n_gnd[e]; k += blockDim.x) {
+      int s = C.gnd[C.gnd_off[e] + k];
+      double d = sxw[3 * (s - s0) + 1] - gy;
+      if (d <= 0.0) {
+        acc += INFINITY;
+        continue;
+      }
+      double ss = d * d;
+      if (ss < shat) acc += kappa * barrier_val(ss, shat);
+    }
+  }
+  double eh = W.env_epsv[e] * h, mu = W.env_mu[e];
+  for (int k = tid; k < L.n[e]; k += blockDim.x) {
+    long long q = L.off[e] + k;
+    int4 s4 = L.slots[q];
+    int sl[4] = {s4.x, s4.y, s4.z, s4.w};
+    const double* gam = L.gamma + 4 * q;
+    const double* T = L.tangent + 6 * q;
+    double u3[3] = {0, 0, 0};
+    for (int i = 0; i < 4; ++i)
+      for (int c = 0; c < 3; ++c) u3[c] += gam[i] * (sxw[3 * (sl[i] - s0) + c] - W.xw0[3 * sl[i] + c]);
+    double u0 = T[0] * u3[0] + T[2] * u3[1] + T[4] * u3[2];
+    double u1 = T[1] * u3[0] + T[3] * u3[1] + T[5] * u3[2];
+    double hu[4];
+    acc += smooth_norm(u0, u1, mu * L.lam[q], eh, nullptr, hu);
+  }
+  for (int k = tid; k < L.g_n[e]; k += blockDim.x) {
+    int q = W.env_slot[e] + k;
+    int s = L.g_slot[q];
+    double u0 = sxw[3 * (s - s0)] - W.xw0[3 * s], u1 = sxw[3 * (s - s0) + 2] - W.xw0[3 * s + 2];
+    double hu[4];
+    acc += smooth_norm(u0, u1, mu * L.g_lam[q], eh, nullptr, hu);
+  }
+  double tot = block_sum(acc, sh);
+  if (tid == 0) e_multi[(long long)m * W.n_env + e] = tot;
+}
+
 // Derivative buffers of one assembly.
 struct Derivs {
   double *body_g, *body_h;           // 12, 144 per affine body
@@ -88,19 +264,31 @@ struct Derivs {
 template <typename HGet>
 __device__ void add_stencil(const World& W, int d0, int n, double* H, double* g, int ns, const int* sl,
                             const double* gs, HGet hget) {
+  // stage the stencil (slot kinds, lever arms, 12x12 block, gradient) in
+  // shared memory: the lift below reads each value many times
+  __shared__ double sH[144], sg[12], srest[12];
+  __shared__ int saff[4];
+  int tid = threadIdx.x;
+  int N = 3 * ns;
+  for (int i = tid; i < N * N; i += blockDim.x) sH[i] = hget(i / N, i % N);
+  for (int i = tid; i < N; i += blockDim.x) sg[i] = gs[i];
+  if (tid < ns) {
+    int s = sl[tid];
+    saff[tid] = W.slot_aff[s];
+    for (int c = 0; c < 3; ++c) srest[3 * tid + c] = W.slot_rest[3 * s + c];
+  }
+  __syncthreads();
   int key[4], wid[4], grp[4], gstart[5];
   int ng = 0;
   for (int a = 0; a < ns; ++a) {
-    int s = sl[a];
-    int k = W.slot_dof[s] - d0;
-    bool aff = W.slot_aff[s];
+    int k = W.slot_dof[sl[a]] - d0;
     int gi = -1;
     for (int q = 0; q < ng; ++q)
       if (key[q] == k) gi = q;
     if (gi < 0) {
       gi = ng++;
       key[gi] = k;
-      wid[gi] = aff ? 12 : 3;
+      wid[gi] = saff[a] ? 12 : 3;
     }
     grp[a] = gi;
   }
@@ -109,15 +297,14 @@ __device__ void add_stencil(const World& W, int d0, int n, double* H, double* g,
   int tot = gstart[ng];
   // row index R within group q: (component i, weight w) of J_a[:, R]
   auto sel = [&](int a, int R, int* i) -> double {
-    int s = sl[a];
-    if (!W.slot_aff[s] || R < 3) {
+    if (!saff[a] || R < 3) {
       *i = R;
       return 1.0;
     }
     *i = (R - 3) / 3;
-    return W.slot_rest[3 * s + (R - 3) % 3];
+    return srest[3 * a + (R - 3) % 3];
   };
-  for (int idx = threadIdx.x; idx < tot * tot; idx += blockDim.x) {
+  for (int idx = tid; idx < tot * tot; idx += blockDim.x) {
     int r = idx / tot, c = idx - r * tot;
     int qr = 0, qc = 0;
     while (r >= gstart[qr + 1]) ++qr;
@@ -132,12 +319,12 @@ __device__ void add_stencil(const World& W, int d0, int n, double* H, double* g,
         if (grp[b] != qc) continue;
         int ib;
         double wb = sel(b, Cc, &ib);
-        acc += wa * wb * hget(3 * a + ia, 3 * b + ib);
+        acc += wa * wb * sH[(3 * a + ia) * N + 3 * b + ib];
       }
     }
     H[(key[qr] + R) * n + key[qc] + Cc] += acc;
   }
-  for (int r = threadIdx.x; r < tot; r += blockDim.x) {
+  for (int r = tid; r < tot; r += blockDim.x) {
     int qr = 0;
     while (r >= gstart[qr + 1]) ++qr;
     int R = r - gstart[qr];
@@ -146,7 +333,7 @@ __device__ void add_stencil(const World& W, int d0, int n, double* H, double* g,
       if (grp[a] != qr) continue;
       int ia;
       double wa = sel(a, R, &ia);
-      acc += wa * gs[3 * a + ia];
+      acc += wa * sg[3 * a + ia];
     }
     g[key[qr] + R] += acc;
   }
@@ -209,9 +396,35 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState
     const unsigned char* act = kind == 0 ? D.pt_act : D.ee_act;
     const double* gg = kind == 0 ? D.pt_g : D.ee_g;
     const double* hh = kind == 0 ? D.pt_h : D.ee_h;
-    for (int k = 0; k < nn; ++k) {
-      long long q = off + k;
-      if (!act[q]) continue;
+    // ordered compaction of the active candidates, one chunk at a time, so
+    // the serial assembly loop only visits stencils that contribute
+    __shared__ long long alist[DENSE_THREADS];
+    __shared__ int wtot[DENSE_THREADS / 32];
+    __shared__ int atot;
+    for (int k0 = 0; k0 < nn; k0 += DENSE_THREADS) {
+      int kk = k0 + tid;
+      bool on = kk < nn && act[off + kk];
+      {
+        int lane = tid & 31, wid = tid >> 5;
+        unsigned m = __ballot_sync(0xffffffffu, on);
+        if (lane == 0) wtot[wid] = __popc(m);
+        __syncthreads();
+        if (tid == 0) {
+          int acc = 0;
+          for (int w = 0; w < DENSE_THREADS / 32; ++w) {
+            int t = wtot[w];
+            wtot[w] = acc;
+            acc += t;
+          }
+          atot = acc;
+        }
+        __syncthreads();
+        if (on) alist[wtot[wid] + __popc(m & ((1u << lane) - 1u))] = off + kk;
+        __syncthreads();
+      }
+      int na = atot;
+    for (int ai = 0; ai < na; ++ai) {
+      long long q = alist[ai];
       int2 pr = kind == 0 ? C.pt[q] : C.ee[q];
       int sl[4];
       if (kind == 0) {
@@ -223,6 +436,8 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState
       }
       const double* hp = hh + PK * q;
       add_stencil(W, d0, n, H, g, 4, sl, gg + 12 * q, [&](int i, int j) { return pk_get(hp, i, j); });
+    }
+      __syncthreads();
     }
   }
   // ground barrier (y only)
@@ -381,6 +596,44 @@ __global__ void k_ls_check(World W, EnvState S, int* ls_count, int max_halvings,
   int c = ls_count[e] + 1;
   ls_count[e] = c;
   S.alpha[e] = a;
+  if (c >= max_halvings || a < 1e-12) {
+    S.ls_active[e] = 0;
+    S.ls_failed[e] = 1;
+    S.converged[e] = 0;
+    S.newton_active[e] = 0;
+  }
+}
+
+// speculative backtracking: trials m = 0..M-1 evaluated E(x + α 2^-m p) into
+// e_multi[m * n_env + e]; take the first trial the sequential search would
+// have accepted (same floor / halving-count rules, ref solver.py:257-272)
+__global__ void k_ls_check_multi(World W, EnvState S, int* ls_count, int max_halvings, int M,
+                                 const double* e_multi, int* accepted) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= W.n_env) return;
+  accepted[e] = 0;
+  if (!S.ls_active[e]) return;
+  double a = S.alpha[e];
+  int c = ls_count[e];
+  for (int m = 0; m < M; ++m) {
+    if (c >= max_halvings || a < 1e-12) {
+      S.ls_active[e] = 0;
+      S.ls_failed[e] = 1;
+      S.converged[e] = 0;
+      S.newton_active[e] = 0;
+      return;
+    }
+    if (e_multi[(long long)m * W.n_env + e] <= S.e0[e]) {
+      S.alpha[e] = a;
+      accepted[e] = 1;
+      S.ls_active[e] = 0;
+      return;
+    }
+    a *= 0.5;
+    ++c;
+  }
+  S.alpha[e] = a;
+  ls_count[e] = c;
   if (c >= max_halvings || a < 1e-12) {
     S.ls_active[e] = 0;
     S.ls_failed[e] = 1;
