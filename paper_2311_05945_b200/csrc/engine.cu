@@ -493,12 +493,9 @@ struct ipc_world {
   // broad phase without a host round trip; overflow stays sticky in the
   // store's flag and is handled by replaying the step (see ipc_world_step)
   void broad_nosync(CandStore& cs, const double* lo, const double* hi, const int* env_mask) {
-    for (int kind = 0; kind < 3; ++kind)
-      IPC_LAUNCH((&cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD), st, k_broad, n_env, BP_THREADS, 0, W, lo, hi, cs.c,
-                 kind, env_mask);
-    IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_pt, env_mask, cs.c.pre_pt);
-    IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_ee, env_mask, cs.c.pre_ee);
-    IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_gnd, env_mask, cs.c.pre_gnd);
+    IPC_LAUNCH((&cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD), st, k_broad, dim3(n_env, 3), BP_THREADS, 0, W, lo, hi,
+               cs.c, -1, env_mask);
+    IPC_LAUNCH(K_MISC, st, k_prefix3, 3, 1024, 0, n_env, cs.c, env_mask);
   }
 
   // run broad phase; grow capacities and retry on overflow
@@ -506,16 +503,15 @@ struct ipc_world {
              const int* env_mask) {
     for (int attempt = 0; attempt < 8; ++attempt) {
       CK(cudaMemsetAsync(cs.c.overflow, 0, sizeof(int), st));
-      for (int kind = 0; kind < 3; ++kind) IPC_LAUNCH((&cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD), st, k_broad, n_env, BP_THREADS, 0, W, lo, hi, cs.c, kind, env_mask);
+      IPC_LAUNCH((&cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD), st, k_broad, dim3(n_env, 3), BP_THREADS, 0, W, lo, hi,
+                 cs.c, -1, env_mask);
       CK(cudaGetLastError());
       int ov = 0;
       CK(cudaMemcpyAsync(h_count, cs.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       ov = *h_count;
       if (!ov) {
-        IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_pt, env_mask, cs.c.pre_pt);
-        IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_ee, env_mask, cs.c.pre_ee);
-        IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, n_env, cs.c.n_gnd, env_mask, cs.c.pre_gnd);
+        IPC_LAUNCH(K_MISC, st, k_prefix3, 3, 1024, 0, n_env, cs.c, env_mask);
         return;
       }
       // grow: read counts are clipped, so grow every env capacity 4x
@@ -537,17 +533,19 @@ struct ipc_world {
   // the envs flagged at the last broad phase, then (deriv) the heavy
   // derivative pass over the compacted active list
   void pairs(const double* xw, CandStore& cs, PairBufs& pb, int deriv, double* min_s, int kid) {
-    for (int kind = 0; kind < 2; ++kind) {
-      long long cap = kind == 0 ? cs.pt_total : cs.ee_total;
-      if (!cap) continue;
-      if (deriv) CK(cudaMemsetAsync(work_n + kind, 0, sizeof(int), st));
-      IPC_LAUNCH(kid, st, k_pair_dist, n_sm * 8, 128, 0, W, xw, cs.c, kind, deriv, kind == 0 ? pb.pt_val : pb.ee_val,
-                 kind == 0 ? pb.pt_act : pb.ee_act, min_s, work[kind], work_env[kind], work_n + kind);
-      if (deriv)
-        IPC_LAUNCH(kid == K_SENSE ? K_SENSE : K_PAIRS_D, st, k_pair_hess, n_sm * 4, 64, 0, W, xw, cs.c, kind,
-                   work[kind], work_env[kind], work_n + kind, kind == 0 ? pb.pt_g : pb.ee_g,
-                   kind == 0 ? pb.pt_h : pb.ee_h, kind == 0 ? pb.pt_act : pb.ee_act);
-    }
+    if (!cs.pt_total && !cs.ee_total) return;
+    PairIO io{};
+    io.val[0] = pb.pt_val; io.val[1] = pb.ee_val;
+    io.act[0] = pb.pt_act; io.act[1] = pb.ee_act;
+    io.g[0] = pb.pt_g; io.g[1] = pb.ee_g;
+    io.h[0] = pb.pt_h; io.h[1] = pb.ee_h;
+    io.work[0] = work[0]; io.work[1] = work[1];
+    io.work_env[0] = work_env[0]; io.work_env[1] = work_env[1];
+    io.work_n = work_n;
+    if (deriv) CK(cudaMemsetAsync(work_n, 0, 2 * sizeof(int), st));
+    IPC_LAUNCH(kid, st, k_pair_dist, dim3(n_sm * 8, 2), 128, 0, W, xw, cs.c, deriv, io, min_s);
+    if (deriv)
+      IPC_LAUNCH(kid == K_SENSE ? K_SENSE : K_PAIRS_D, st, k_pair_hess, dim3(n_sm * 4, 2), 64, 0, W, xw, cs.c, io);
   }
 
   void world_pos(const double* x, double* xw) {
@@ -600,10 +598,9 @@ struct ipc_world {
     IPC_LAUNCH(K_MISC, st, k_sweep_box2, nblk(3 * W.n_slot, 256), 256, 0, W.n_slot, xwt, W.xw, W.dxw, xlo, xhi);
     broad_nosync(sweep, xlo, xhi, S.ls_active);
     IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.alpha_max, 1.0, S.ls_active);
-    for (int kind = 0; kind < 2; ++kind)
-      if (kind == 0 ? sweep.pt_total : sweep.ee_total)
-        IPC_LAUNCH(K_CCD, st, k_ccd_pairs, n_sm * 8, 64, 0, W, W.xw, W.dxw, sweep.c, kind,
-                   cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
+    if (sweep.pt_total || sweep.ee_total)
+      IPC_LAUNCH(K_CCD, st, k_ccd_pairs, dim3(n_sm * 8, 2), 64, 0, W, W.xw, W.dxw, sweep.c,
+                 cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
     IPC_LAUNCH(K_CCD, st, k_ccd_ground, dim3(nblk(max_slots, 128), n_env), 128, 0, W, W.xw, W.dxw, sweep.c,
                cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
     IPC_LAUNCH(K_MISC, st, k_ls_begin, nblk(n_env, 128), 128, 0, n_env, S, ls_count);

@@ -119,6 +119,7 @@ __device__ __forceinline__ bool cull_item(const World& W, int cb0, int rb, int B
 __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __restrict__ lo,
                                                        const double* __restrict__ hi, Cands C,
                                                        int kind, const int* env_mask) {
+  if (kind < 0) kind = blockIdx.y;  // all three kinds in one launch
   __shared__ int warp_tot[BP_THREADS / 32];
   __shared__ int total;
   __shared__ double blo[3 * MAX_BODIES], bhi[3 * MAX_BODIES];
@@ -248,17 +249,27 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
         n_hit += hit;
       }
     }
-    // exclusive scan of per-item counts (item order = output order)
-    cnt[threadIdx.x] = n_hit;
-    __syncthreads();
-    for (int o = 1; o < BP_THREADS; o <<= 1) {
-      int v = threadIdx.x >= o ? cnt[threadIdx.x - o] : 0;
-      __syncthreads();
-      cnt[threadIdx.x] += v;
-      __syncthreads();
+    // exclusive scan of per-item counts (item order = output order):
+    // warp-shuffle inclusive scan, then one pass over the warp totals
+    int incl = n_hit;
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    long long dst = base + cnt[threadIdx.x] - n_hit;
-    long long chunk_total = cnt[BP_THREADS - 1];
+    if (lane == 31) cnt[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int w = 0; w < BP_THREADS / 32; ++w) {
+        int t = cnt[w];
+        cnt[w] = acc;
+        acc += t;
+      }
+      cnt[BP_THREADS / 32] = acc;
+    }
+    __syncthreads();
+    long long dst = base + cnt[wid] + incl - n_hit;
+    long long chunk_total = cnt[BP_THREADS / 32];
     __syncthreads();
     // pass 2: write
     if (n_hit) {
@@ -307,6 +318,32 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
 // per-env exclusive prefix of candidate counts over flagged envs (one CTA);
 // pre has n_env + 1 entries, pre[n_env] = total
 __global__ void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
+  __shared__ int part[1024];
+  int tid = threadIdx.x, nt = blockDim.x;
+  int per = (n_env + nt - 1) / nt;
+  int a = tid * per, b = min(n_env, a + per);
+  int s = 0;
+  for (int e = a; e < b; ++e) s += (flag == nullptr || flag[e]) ? cnt[e] : 0;
+  part[tid] = s;
+  __syncthreads();
+  for (int o = 1; o < nt; o <<= 1) {
+    int v = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  int run = part[tid] - s;
+  for (int e = a; e < b; ++e) {
+    pre[e] = run;
+    run += (flag == nullptr || flag[e]) ? cnt[e] : 0;
+  }
+  if (tid == nt - 1) pre[n_env] = part[nt - 1];
+}
+
+// the three candidate-count prefixes (PT, EE, ground) in one launch
+__global__ void k_prefix3(int n_env, Cands C, const int* flag) {
+  const int* cnt = blockIdx.x == 0 ? C.n_pt : (blockIdx.x == 1 ? C.n_ee : C.n_gnd);
+  int* pre = blockIdx.x == 0 ? C.pre_pt : (blockIdx.x == 1 ? C.pre_ee : C.pre_gnd);
   __shared__ int part[1024];
   int tid = threadIdx.x, nt = blockDim.x;
   int per = (n_env + nt - 1) / nt;
@@ -483,9 +520,24 @@ __device__ __forceinline__ void pair_slots(const World& W, int kind, int2 pr, in
   }
 }
 
-__global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int kind, int deriv,
-                            double* val, unsigned char* active, double* env_min_s, long long* work,
-                            int* work_env, int* work_n) {
+struct PairIO {  // per-kind (0 PT, 1 EE) buffers; kind = blockIdx.y
+  double* val[2];
+  unsigned char* act[2];
+  double* g[2];
+  double* h[2];
+  long long* work[2];
+  int* work_env[2];
+  int* work_n;
+};
+
+__global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int deriv, PairIO io,
+                            double* env_min_s) {
+  const int kind = blockIdx.y;
+  double* val = io.val[kind];
+  unsigned char* active = io.act[kind];
+  long long* work = io.work[kind];
+  int* work_env = io.work_env[kind];
+  int* work_n = io.work_n + kind;
   const int* pre = kind == 0 ? C.pre_pt : C.pre_ee;
   int total = pre[W.n_env];
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
@@ -532,10 +584,14 @@ __global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int
 // derivatives, barrier chain rule, mollifier product rule, PSD projection.
 // Values were written by pass 1; the value term is recomputed from the same
 // formulas here for the derivative distance s (ref contact.py:505-556).
-__global__ void __launch_bounds__(64) k_pair_hess(World W, const double* __restrict__ xw, Cands C, int kind,
-                                                  const long long* work, const int* work_env, const int* work_n,
-                                                  double* g12, double* hp, unsigned char* active) {
-  int total = *work_n;
+__global__ void __launch_bounds__(64) k_pair_hess(World W, const double* __restrict__ xw, Cands C, PairIO io) {
+  const int kind = blockIdx.y;
+  const long long* work = io.work[kind];
+  const int* work_env = io.work_env[kind];
+  double* g12 = io.g[kind];
+  double* hp = io.h[kind];
+  unsigned char* active = io.act[kind];
+  int total = io.work_n[kind];
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < total; w += gridDim.x * blockDim.x) {
     long long k = work[w];
     int e = work_env[w];
@@ -876,8 +932,8 @@ __device__ double pair_ccd_alpha(int kind, const V3* X, const V3* D, double cons
 }
 
 __global__ void k_ccd_pairs(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
-                            Cands C, int kind, double conservative, const int* env_flag,
-                            double* env_alpha) {
+                            Cands C, double conservative, const int* env_flag, double* env_alpha) {
+  const int kind = blockIdx.y;
   const int* pre = kind == 0 ? C.pre_pt : C.pre_ee;
   int total = pre[W.n_env];
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {

@@ -264,10 +264,16 @@ struct Derivs {
 template <typename HGet>
 __device__ void add_stencil(const World& W, int d0, int n, double* H, double* g, int ns, const int* sl,
                             const double* gs, HGet hget) {
-  // stage the stencil (slot kinds, lever arms, 12x12 block, gradient) in
-  // shared memory: the lift below reads each value many times
+  // Stage the stencil in shared memory, then build a row table: lifted row r
+  // (a DoF of one of the stencil's merged groups) is Σ over the group's slots
+  // a of w_a(r) · (slot-space row 3a + i_a(r)). Entry (r, c) of the lifted
+  // block is Σ_p Σ_q w_p w_q H_s[idx_p, idx_q] over the ≤3 terms of row r and
+  // column c; every thread owns distinct output entries (no atomics).
   __shared__ double sH[144], sg[12], srest[12];
-  __shared__ int saff[4];
+  __shared__ int saff[4], skey[4];
+  __shared__ int rt_n[48], rt_idx[48][3], rt_dof[48];
+  __shared__ double rt_w[48][3];
+  __shared__ int s_tot;
   int tid = threadIdx.x;
   int N = 3 * ns;
   for (int i = tid; i < N * N; i += blockDim.x) sH[i] = hget(i / N, i % N);
@@ -275,67 +281,69 @@ __device__ void add_stencil(const World& W, int d0, int n, double* H, double* g,
   if (tid < ns) {
     int s = sl[tid];
     saff[tid] = W.slot_aff[s];
+    skey[tid] = W.slot_dof[s] - d0;
     for (int c = 0; c < 3; ++c) srest[3 * tid + c] = W.slot_rest[3 * s + c];
   }
   __syncthreads();
-  int key[4], wid[4], grp[4], gstart[5];
-  int ng = 0;
-  for (int a = 0; a < ns; ++a) {
-    int k = W.slot_dof[sl[a]] - d0;
-    int gi = -1;
-    for (int q = 0; q < ng; ++q)
-      if (key[q] == k) gi = q;
-    if (gi < 0) {
-      gi = ng++;
-      key[gi] = k;
-      wid[gi] = saff[a] ? 12 : 3;
+  if (tid < 32) {  // one warp builds the row table
+    int key[4], wid[4], grp[4], gstart[5];
+    int ng = 0;
+    for (int a = 0; a < ns; ++a) {
+      int gi = -1;
+      for (int q = 0; q < ng; ++q)
+        if (key[q] == skey[a]) gi = q;
+      if (gi < 0) {
+        gi = ng++;
+        key[gi] = skey[a];
+        wid[gi] = saff[a] ? 12 : 3;
+      }
+      grp[a] = gi;
     }
-    grp[a] = gi;
+    gstart[0] = 0;
+    for (int q = 0; q < ng; ++q) gstart[q + 1] = gstart[q] + wid[q];
+    int tot = gstart[ng];
+    for (int r = tid; r < tot; r += 32) {
+      int q = 0;
+      while (r >= gstart[q + 1]) ++q;
+      int R = r - gstart[q];
+      int cnt = 0;
+      for (int a = 0; a < ns; ++a) {
+        if (grp[a] != q) continue;
+        int ia;
+        double wa;
+        if (!saff[a] || R < 3) {
+          ia = R;
+          wa = 1.0;
+        } else {
+          ia = (R - 3) / 3;
+          wa = srest[3 * a + (R - 3) % 3];
+        }
+        rt_idx[r][cnt] = 3 * a + ia;
+        rt_w[r][cnt] = wa;
+        ++cnt;
+      }
+      rt_n[r] = cnt;
+      rt_dof[r] = key[q] + R;
+    }
+    if (tid == 0) s_tot = tot;
   }
-  gstart[0] = 0;
-  for (int q = 0; q < ng; ++q) gstart[q + 1] = gstart[q] + wid[q];
-  int tot = gstart[ng];
-  // row index R within group q: (component i, weight w) of J_a[:, R]
-  auto sel = [&](int a, int R, int* i) -> double {
-    if (!saff[a] || R < 3) {
-      *i = R;
-      return 1.0;
-    }
-    *i = (R - 3) / 3;
-    return srest[3 * a + (R - 3) % 3];
-  };
+  __syncthreads();
+  int tot = s_tot;
   for (int idx = tid; idx < tot * tot; idx += blockDim.x) {
     int r = idx / tot, c = idx - r * tot;
-    int qr = 0, qc = 0;
-    while (r >= gstart[qr + 1]) ++qr;
-    while (c >= gstart[qc + 1]) ++qc;
-    int R = r - gstart[qr], Cc = c - gstart[qc];
     double acc = 0.0;
-    for (int a = 0; a < ns; ++a) {
-      if (grp[a] != qr) continue;
-      int ia;
-      double wa = sel(a, R, &ia);
-      for (int b = 0; b < ns; ++b) {
-        if (grp[b] != qc) continue;
-        int ib;
-        double wb = sel(b, Cc, &ib);
-        acc += wa * wb * sH[(3 * a + ia) * N + 3 * b + ib];
-      }
+    for (int p = 0; p < rt_n[r]; ++p) {
+      const double* hr = sH + rt_idx[r][p] * N;
+      double sub = 0.0;
+      for (int q = 0; q < rt_n[c]; ++q) sub += rt_w[c][q] * hr[rt_idx[c][q]];
+      acc += rt_w[r][p] * sub;
     }
-    H[(key[qr] + R) * n + key[qc] + Cc] += acc;
+    H[rt_dof[r] * n + rt_dof[c]] += acc;
   }
   for (int r = tid; r < tot; r += blockDim.x) {
-    int qr = 0;
-    while (r >= gstart[qr + 1]) ++qr;
-    int R = r - gstart[qr];
     double acc = 0.0;
-    for (int a = 0; a < ns; ++a) {
-      if (grp[a] != qr) continue;
-      int ia;
-      double wa = sel(a, R, &ia);
-      acc += wa * sg[3 * a + ia];
-    }
-    g[key[qr] + R] += acc;
+    for (int p = 0; p < rt_n[r]; ++p) acc += rt_w[r][p] * sg[rt_idx[r][p]];
+    g[rt_dof[r]] += acc;
   }
   __syncthreads();
 }
@@ -473,36 +481,38 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState
   double gn = block_max(gmax, red);
   if (tid == 0) S.gnorm[e] = gn;
   __syncthreads();
-  // Cholesky H = L Lᵀ (lower, in place)
+  // LDLᵀ without scaling (one block sync per column): after step k the
+  // lower column c_k = H[k+1:, k] and pivot a_k = H[k][k] give
+  // H = Σ c_k c_kᵀ / a_k, i.e. L' = c / a (unit lower), D = diag(a). Same
+  // factorization as Cholesky (SPD input), no sqrt/divide on the hot path.
   for (int k = 0; k < n; ++k) {
-    if (tid == 0) {
-      double akk = H[k * n + k];
-      if (!(akk > 0.0)) fail = 1;
-      H[k * n + k] = sqrt(fmax(akk, 1e-300));
-    }
-    __syncthreads();
-    double lkk = H[k * n + k];
-    for (int i = k + 1 + tid; i < n; i += blockDim.x) H[i * n + k] /= lkk;
-    __syncthreads();
+    double akk = H[k * n + k];
+    if (tid == 0 && !(akk > 0.0)) fail = 1;
+    double inv = 1.0 / akk;
     int m = n - k - 1;
-    for (int idx = tid; idx < m * m; idx += blockDim.x) {
-      int i = k + 1 + idx / m, j = k + 1 + idx % m;
-      if (j <= i) H[i * n + j] -= H[i * n + k] * H[j * n + k];
+    // trailing update H[i][j] -= c_i c_j / a_k for k < j <= i, 2D thread map
+    for (int ii = tid >> 4; ii < m; ii += blockDim.x >> 4) {
+      int i = k + 1 + ii;
+      double ci = H[i * n + k] * inv;
+      for (int jj = tid & 15; jj <= ii; jj += 16) {
+        int j = k + 1 + jj;
+        H[i * n + j] -= ci * H[j * n + k];
+      }
     }
     __syncthreads();
   }
-  // forward: L z = -g
+  // forward: L' u = -g  (y holds -g)
   for (int k = 0; k < n; ++k) {
-    if (tid == 0) y[k] /= H[k * n + k];
-    __syncthreads();
-    for (int i = k + 1 + tid; i < n; i += blockDim.x) y[i] -= H[i * n + k] * y[k];
+    double uk = y[k], inv = 1.0 / H[k * n + k];
+    for (int i = k + 1 + tid; i < n; i += blockDim.x) y[i] -= (H[i * n + k] * inv) * uk;
     __syncthreads();
   }
-  // backward: Lᵀ p = z
+  for (int i = tid; i < n; i += blockDim.x) y[i] /= H[i * n + i];
+  __syncthreads();
+  // backward: L'ᵀ p = D⁻¹ u
   for (int k = n - 1; k >= 0; --k) {
-    if (tid == 0) y[k] /= H[k * n + k];
-    __syncthreads();
-    for (int i = tid; i < k; i += blockDim.x) y[i] -= H[k * n + i] * y[k];
+    double xk = y[k];
+    for (int i = tid; i < k; i += blockDim.x) y[i] -= (H[k * n + i] / H[i * n + i]) * xk;
     __syncthreads();
   }
   double pg = 0.0;
