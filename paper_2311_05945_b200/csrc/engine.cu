@@ -544,8 +544,10 @@ struct ipc_world {
     io.work_n = work_n;
     if (deriv) CK(cudaMemsetAsync(work_n, 0, 2 * sizeof(int), st));
     IPC_LAUNCH(kid, st, k_pair_dist, dim3(n_sm * 8, 2), 128, 0, W, xw, cs.c, deriv, io, min_s);
-    if (deriv)
-      IPC_LAUNCH(kid == K_SENSE ? K_SENSE : K_PAIRS_D, st, k_pair_hess, dim3(n_sm * 4, 2), 64, 0, W, xw, cs.c, io);
+    if (deriv) {
+      IPC_LAUNCH(kid == K_SENSE ? K_SENSE : K_PAIRS_D, st, k_pair_hess<0>, n_sm * 8, 64, 0, W, xw, cs.c, io);
+      IPC_LAUNCH(kid == K_SENSE ? K_SENSE : K_PAIRS_D, st, k_pair_hess<1>, n_sm * 8, 64, 0, W, xw, cs.c, io);
+    }
   }
 
   void world_pos(const double* x, double* xw) {

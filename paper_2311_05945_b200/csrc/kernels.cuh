@@ -584,8 +584,10 @@ __global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int
 // derivatives, barrier chain rule, mollifier product rule, PSD projection.
 // Values were written by pass 1; the value term is recomputed from the same
 // formulas here for the derivative distance s (ref contact.py:505-556).
+// one instantiation per pair kind keeps each kernel's code (and register
+// demand) small: the combined kernel was instruction-cache bound
+template <int kind>
 __global__ void __launch_bounds__(64) k_pair_hess(World W, const double* __restrict__ xw, Cands C, PairIO io) {
-  const int kind = blockIdx.y;
   const long long* work = io.work[kind];
   const int* work_env = io.work_env[kind];
   double* g12 = io.g[kind];

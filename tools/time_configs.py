@@ -31,7 +31,7 @@ def run(name, scene, n_steps, drive=None):
                       "n_dof": scene.state.n_dof}), flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "prof2" not in sys.argv:
     which = sys.argv[1:] or ["0", "1", "2"]
     if "0" in which:
         run("config0 soft cube drop (1296 tets)", WL.soft_drop(6), 40)
@@ -52,3 +52,30 @@ if __name__ == "__main__":
         print("tets", len(cube.mesh.tets), flush=True)
         run(f"config2 soft cube grasp ({len(cube.mesh.tets)} tets)", sc, 30,
             lambda k: g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, 0.0262)))
+
+
+def profile_config2(div=12, n=8):
+    """Per-kernel event timing of config 2 after a few warm-up steps."""
+    sc, g, cube = WL.soft_grasp(div)
+    cfg = SolverConfig()
+    for k in range(4):
+        g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, 0.0262))
+        step(sc, cfg)
+    w = sc.engine
+    w.profile(True)
+    st0 = w.stats()
+    t0 = time.perf_counter()
+    for k in range(n):
+        g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, 0.0262))
+        step(sc, cfg)
+    dt = time.perf_counter() - t0
+    prof, launches = w.profile_read()
+    st1 = w.stats()
+    print(f"config2 {n} steps {1e3 * dt / n:.1f} ms/step, launches {launches}, "
+          f"{ {k: st1[k] - st0[k] for k in st1} }")
+    for name, (ms, c) in sorted(prof.items(), key=lambda kv: -kv[1][0])[:12]:
+        print(f"  {name:14s} {ms:9.2f} ms {c:6d} launches {1e3 * ms / max(c, 1):9.1f} us/launch")
+
+
+if __name__ == "__main__" and "prof2" in sys.argv:
+    profile_config2()
