@@ -142,7 +142,7 @@ int ipc_world_profile(ipc_world *w, int on, uint32_t kernel_mask);
 int ipc_world_profile_read(ipc_world *w, double *ms, int64_t *count, int64_t *launches);
 int ipc_world_flush_l2(ipc_world *w, int64_t bytes);
 /* Cumulative host-loop counters: batched Newton iterations, line-search
- * rounds, host synchronisations (out: 3). */
+ * rounds, host synchronisations, sparse-path PCG iterations (out: 4). */
 int ipc_world_stats(ipc_world *w, int64_t *out);
 int ipc_world_mark(ipc_world *w, int slot);
 int ipc_world_elapsed(ipc_world *w, int a, int b, double *ms);

@@ -99,7 +99,7 @@ SIGNATURES = {
 
 KERNEL_IDS = ("broad_dcd", "broad_ccd", "pairs_deriv", "pairs_value", "tet", "body", "ground",
               "friction", "energy_reduce", "dense_solve", "ccd", "lags", "world_pos", "sensing",
-              "misc")
+              "misc", "pcg", "assembly")
 
 _lib = None
 

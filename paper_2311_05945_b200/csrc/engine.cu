@@ -52,7 +52,7 @@ static inline int nblk(long long n, int t) { return (int)std::max<long long>(1, 
 // ---------------------------------------------------------------------------
 enum Kid {
   K_BROAD_DCD = 0, K_BROAD_SWEEP, K_PAIRS_D, K_PAIRS_V, K_TET, K_BODY, K_GROUND, K_FRICTION, K_ENERGY,
-  K_DENSE, K_CCD, K_LAGS, K_WORLD, K_SENSE, K_MISC, NKID
+  K_DENSE, K_CCD, K_LAGS, K_WORLD, K_SENSE, K_MISC, K_PCG, K_ASM, NKID
 };
 struct OverflowRetry : std::exception {
   const char* what() const noexcept override { return "candidate capacity overflow"; }
@@ -492,9 +492,23 @@ struct ipc_world {
 
   // broad phase without a host round trip; overflow stays sticky in the
   // store's flag and is handled by replaying the step (see ipc_world_step)
+  // broad phase over [lo, hi]: chunk boxes, then one CTA per env (bp_z == 1)
+  // or bp_z CTAs per env in a count pass and a write pass
+  static constexpr long long BROAD_ITEMS = 8192;
+  int bp_z = 1;
+  int* bp_cnt = nullptr;
+  void launch_broad(CandStore& cs, const double* lo, const double* hi, const int* env_mask) {
+    int kid = &cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD;
+    IPC_LAUNCH(kid, st, k_chunk_boxes, nblk(W.n_tchunk + W.n_echunk, 128), 128, 0, W, lo, hi);
+    if (bp_z == 1) {
+      IPC_LAUNCH(kid, st, k_broad, dim3(n_env, 3), BP_THREADS, 0, W, lo, hi, cs.c, -1, env_mask, -1, nullptr);
+    } else {
+      IPC_LAUNCH(kid, st, k_broad, dim3(n_env, 3, bp_z), BP_THREADS, 0, W, lo, hi, cs.c, -1, env_mask, 0, bp_cnt);
+      IPC_LAUNCH(kid, st, k_broad, dim3(n_env, 2, bp_z), BP_THREADS, 0, W, lo, hi, cs.c, -1, env_mask, 1, bp_cnt);
+    }
+  }
   void broad_nosync(CandStore& cs, const double* lo, const double* hi, const int* env_mask) {
-    IPC_LAUNCH((&cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD), st, k_broad, dim3(n_env, 3), BP_THREADS, 0, W, lo, hi,
-               cs.c, -1, env_mask);
+    launch_broad(cs, lo, hi, env_mask);
     IPC_LAUNCH(K_MISC, st, k_prefix3, 3, 1024, 0, n_env, cs.c, env_mask);
   }
 
@@ -503,8 +517,7 @@ struct ipc_world {
              const int* env_mask) {
     for (int attempt = 0; attempt < 8; ++attempt) {
       CK(cudaMemsetAsync(cs.c.overflow, 0, sizeof(int), st));
-      IPC_LAUNCH((&cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD), st, k_broad, dim3(n_env, 3), BP_THREADS, 0, W, lo, hi,
-                 cs.c, -1, env_mask);
+      launch_broad(cs, lo, hi, env_mask);
       CK(cudaGetLastError());
       int ov = 0;
       CK(cudaMemcpyAsync(h_count, cs.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -790,12 +803,19 @@ struct ipc_world {
   double* g_asm = nullptr;
   int pcg_max_iters = 20000;
   double pcg_rtol = 1e-12;
+  int coop_blocks = 0;
+  int* d_nlive = nullptr;
+  double* d_beta = nullptr;
+  double* d_part1 = nullptr;
+  double* d_part2 = nullptr;
   long long* h_ll = nullptr;  // pinned scalars
 
   void setup_sparse(const ipc_world_desc* d) {
     int nn = d->n_dof / 3;
     std::vector<int> node_env(nn), chunk_env, c0, c1, env_chunk(n_env + 1, 0);
-    const int CH = 256;
+    // env-aligned reduction chunks: small enough that the PCG spreads over
+    // the SMs even for a single large env, at most 256 nodes
+    int CH = std::max(32, std::min(256, ((nn + 2 * n_sm - 1) / (2 * n_sm) + 31) / 32 * 32));
     for (int e = 0; e < n_env; ++e) {
       int a = d->env_dof[e] / 3, b = d->env_dof[e + 1] / 3;
       for (int i = a; i < b; ++i) node_env[i] = e;
@@ -831,6 +851,11 @@ struct ipc_world {
     row_first = pool.alloc<int>(nn);
     g_asm = pool.alloc<double>(d->n_dof);
     CK(cudaMallocHost(&h_ll, 4 * sizeof(long long)));
+    d_nlive = pool.alloc<int>(3);
+    CK(cudaMemset(d_nlive, 0, 3 * sizeof(int)));
+    d_part2 = pool.alloc<double>(2 * (size_t)std::max(pcg.n_chunk, 1));
+    d_beta = pool.alloc<double>(n_env);
+    d_part1 = pool.alloc<double>(2 * (size_t)std::max(pcg.n_chunk, 1));
   }
 
   template <typename T>
@@ -861,7 +886,7 @@ struct ipc_world {
       n_el_cap = n_el;
     }
     AsmIn A{W, S, D_with(pb_dcd), dcd.c, L, W.x, W.xhat, sp};
-    IPC_LAUNCH(K_DENSE, st, k_asm_count, n_sm * 8, 128, 0, A, d_counts);
+    IPC_LAUNCH(K_ASM, st, k_asm_count, n_sm * 8, 128, 0, A, d_counts);
     size_t need = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, need, d_counts, d_offs, n_el, st));
     ensure_cub(need);
@@ -890,12 +915,12 @@ struct ipc_world {
       bpos = pool.alloc<int>(c);
       items_cap = c;
     }
-    IPC_LAUNCH(K_DENSE, st, k_asm_emit, n_sm * 8, 128, 0, A, d_offs, keys, vals, idx);
+    IPC_LAUNCH(K_ASM, st, k_asm_emit, n_sm * 8, 128, 0, A, d_offs, keys, vals, idx);
     need = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys_sorted, idx, perm, n_items, 0, 64, st));
     ensure_cub(need);
     CK(cub::DeviceRadixSort::SortPairs(cub_tmp, need, keys, keys_sorted, idx, perm, n_items, 0, 64, st));
-    IPC_LAUNCH(K_DENSE, st, k_asm_heads, n_sm * 8, 256, 0, n_items, keys_sorted, heads);
+    IPC_LAUNCH(K_ASM, st, k_asm_heads, n_sm * 8, 256, 0, n_items, keys_sorted, heads);
     need = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, need, heads, uidx, n_items, st));
     ensure_cub(need);
@@ -904,12 +929,12 @@ struct ipc_world {
     CK(cudaMemcpyAsync(h_count, heads + n_items - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     long long n_unique = h_ll[0] + *h_count;
-    IPC_LAUNCH(K_DENSE, st, k_asm_starts, n_sm * 8, 256, 0, n_items, heads, uidx, seg_start);
+    IPC_LAUNCH(K_ASM, st, k_asm_starts, n_sm * 8, 256, 0, n_items, heads, uidx, seg_start);
     CK(cudaMemsetAsync(row_cnt, 0, sizeof(int) * pcg.n_node, st));
     CK(cudaMemsetAsync(g_asm, 0, sizeof(double) * W.n_dof, st));
-    IPC_LAUNCH(K_DENSE, st, k_asm_reduce, n_sm * 8, 128, 0, n_items, n_unique, keys_sorted, seg_start, perm, vals,
+    IPC_LAUNCH(K_ASM, st, k_asm_reduce, n_sm * 8, 128, 0, n_items, n_unique, keys_sorted, seg_start, perm, vals,
                g_asm, bcol, bval, row_cnt, bpos);
-    IPC_LAUNCH(K_DENSE, st, k_bsr_rowfirst, n_sm * 8, 256, 0, n_unique, keys_sorted, seg_start, row_first);
+    IPC_LAUNCH(K_ASM, st, k_bsr_rowfirst, n_sm * 8, 256, 0, n_unique, keys_sorted, seg_start, row_first);
     // PCG
     pcg.row_first = row_first;
     pcg.row_cnt = row_cnt;
@@ -920,19 +945,20 @@ struct ipc_world {
     IPC_LAUNCH(K_DENSE, st, k_pcg_setup, n_sm * 8, 128, 0, pcg, g_asm);
     IPC_LAUNCH(K_DENSE, st, k_pcg_partial, std::max(pcg.n_chunk, 1), 256, 0, pcg, 0);
     IPC_LAUNCH(K_DENSE, st, k_pcg_env, nblk(n_env, 128), 128, 0, pcg, n_env, 0, rtol2);
-    const int BATCH = 25;
-    for (int it = 0; it < pcg_max_iters; it += BATCH) {
-      for (int b = 0; b < BATCH; ++b) {
-        IPC_LAUNCH(K_DENSE, st, k_pcg_spmv, n_sm * 8, 128, 0, pcg);
-        IPC_LAUNCH(K_DENSE, st, k_pcg_partial, std::max(pcg.n_chunk, 1), 256, 0, pcg, 1);
-        IPC_LAUNCH(K_DENSE, st, k_pcg_env, nblk(n_env, 128), 128, 0, pcg, n_env, 1, rtol2);
-        IPC_LAUNCH(K_DENSE, st, k_pcg_update, n_sm * 8, 128, 0, pcg);
-        IPC_LAUNCH(K_DENSE, st, k_pcg_partial, std::max(pcg.n_chunk, 1), 256, 0, pcg, 2);
-        IPC_LAUNCH(K_DENSE, st, k_pcg_env, nblk(n_env, 128), 128, 0, pcg, n_env, 2, rtol2);
-        IPC_LAUNCH(K_DENSE, st, k_pcg_dir, n_sm * 8, 128, 0, pcg);
-        IPC_LAUNCH(K_DENSE, st, k_pcg_roll, nblk(n_env, 128), 128, 0, pcg, n_env);
+    {
+      // persistent cooperative PCG: all iterations in one launch
+      if (!coop_blocks) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_coop, 256, 0));
+        // one block per reduction chunk: idle blocks would only lengthen every grid barrier
+        coop_blocks = std::max(1, std::min(std::min(per_sm, 4) * n_sm, pcg.n_chunk));
       }
-      if (count(pcg.env_live) == 0) break;
+      CK(cudaMemsetAsync(d_nlive, 0, 2 * sizeof(int), st));
+      int iters = pcg_max_iters;
+      void* args[] = {(void*)&pcg, (void*)&n_env, (void*)&rtol2, (void*)&iters, (void*)&d_nlive, (void*)&d_part1, (void*)&d_part2};
+      prof_begin(K_PCG, st);
+      CK(cudaLaunchCooperativeKernel((void*)k_pcg_coop, dim3(coop_blocks), dim3(256), args, 0, st));
+      prof_end(K_PCG, st);
     }
     IPC_LAUNCH(K_DENSE, st, k_pcg_finish, n_env, 256, 0, W, S, pcg, g_asm, W.p, W.grad);
     CK(cudaGetLastError());
@@ -1047,6 +1073,27 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
       W.cbody_slot = ranges(d->slot_cbody, d->n_slot);
       W.cbody_tri = ranges(d->tri_cbody, d->n_tri);
       W.cbody_edge = ranges(d->edge_cbody, d->n_edge);
+      // chunk tables: each body's primitive range split into runs of 32
+      auto chunks = [&](const int32_t* owner, int n, int* n_chunk, const int** p0, const int** cb) {
+        std::vector<int> cnt(d->n_cbody + 1, 0);
+        for (int i = 0; i < n; ++i) cnt[owner[i] + 1]++;
+        std::vector<int> first(d->n_cbody + 1, 0);
+        for (int b = 0; b < d->n_cbody; ++b) first[b + 1] = first[b] + cnt[b + 1];
+        std::vector<int> starts, cbc(d->n_cbody + 1, 0);
+        for (int b = 0; b < d->n_cbody; ++b) {
+          cbc[b] = (int)starts.size();
+          for (int s = first[b]; s < first[b + 1]; s += 32) starts.push_back(s);
+        }
+        cbc[d->n_cbody] = (int)starts.size();
+        starts.push_back(n);
+        *n_chunk = (int)starts.size() - 1;
+        *p0 = P.upload(starts.data(), starts.size());
+        *cb = P.upload(cbc.data(), cbc.size());
+      };
+      chunks(d->tri_cbody, d->n_tri, &W.n_tchunk, &W.tchunk_p0, &W.cbody_tchunk);
+      chunks(d->edge_cbody, d->n_edge, &W.n_echunk, &W.echunk_p0, &W.cbody_echunk);
+      W.tchunk_box = P.alloc<double>(6 * (size_t)std::max(W.n_tchunk, 1));
+      W.echunk_box = P.alloc<double>(6 * (size_t)std::max(W.n_echunk, 1));
       int dev = 0;
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&w->n_sm, cudaDevAttrMultiProcessorCount, dev));
@@ -1075,6 +1122,19 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     w->h_env_edge.assign(d->env_edge, d->env_edge + ne + 1);
     w->h_env_cbody.assign(d->env_cbody, d->env_cbody + ne + 1);
     for (int e = 0; e < ne; ++e) w->max_slots = std::max(w->max_slots, d->env_slot[e + 1] - d->env_slot[e]);
+    {
+      // CTAs per env in the broad phase: ~BROAD_ITEMS items each
+      long long mx = 0;
+      for (int e = 0; e < ne; ++e) {
+        long long nb = d->env_cbody[e + 1] - d->env_cbody[e];
+        long long rows = std::max(d->env_slot[e + 1] - d->env_slot[e], d->env_edge[e + 1] - d->env_edge[e]);
+        mx = std::max(mx, rows * nb);
+      }
+      const char* ez = getenv("IPC_BROAD_ITEMS");
+      long long per = ez ? std::max(64LL, atoll(ez)) : ipc_world::BROAD_ITEMS;
+      w->bp_z = (int)std::min(64LL, std::max(1LL, (mx + per - 1) / per));
+      if (w->bp_z > 1) w->bp_cnt = P.alloc<int>((size_t)ne * 2 * w->bp_z);
+    }
     for (int e = 0; e < ne; ++e) {
       w->max_env_dof = std::max(w->max_env_dof, d->env_dof[e + 1] - d->env_dof[e]);
       if (d->env_cbody[e + 1] - d->env_cbody[e] > 64)
@@ -1332,10 +1392,17 @@ int ipc_world_profile_read(ipc_world* w, double* ms, int64_t* count, int64_t* la
 }
 
 int ipc_world_stats(ipc_world* w, int64_t* out) {
-  out[0] = w->stat_iters;
-  out[1] = w->stat_ls_rounds;
-  out[2] = w->stat_syncs;
-  return 0;
+  GUARD({
+    out[0] = w->stat_iters;
+    out[1] = w->stat_ls_rounds;
+    out[2] = w->stat_syncs;
+    int pit[3] = {0, 0, 0};
+    if (w->d_nlive) {
+      CK(cudaStreamSynchronize(w->st));
+      CK(cudaMemcpy(pit, w->d_nlive, sizeof(pit), cudaMemcpyDeviceToHost));
+    }
+    out[3] = pit[2];
+  })
 }
 
 int ipc_world_flush_l2(ipc_world* w, int64_t bytes) {

@@ -8,7 +8,7 @@
 //    formulas (the reference autodiffs them: geometry/distgrad.py:237-257);
 //  * the log barrier on squared distance (energy/barrier.py:51) and the
 //    edge-edge mollifier (energy/contact.py:414-449);
-//  * eigenvalue-clamping PSD projection (energy/spd.py:6) by cyclic Jacobi,
+//  * eigenvalue-clamping PSD projection (energy/spd.py:6) by Householder tridiagonalisation + implicit QL (tred2/tql2),
 //    with a Cholesky fast path for blocks that are already positive definite;
 //  * NeoHookean / StVK / FixedCorotated densities, PK1 and F-space Hessians
 //    (energy/elastic.py:23-167).

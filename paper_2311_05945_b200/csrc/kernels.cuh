@@ -116,10 +116,95 @@ __device__ __forceinline__ bool cull_item(const World& W, int cb0, int rb, int B
   return !box_hit(qlo, qhi, blo + 3 * B, bhi + 3 * B, margin);
 }
 
+// primitive test of one (row, primitive) pair: inflated box overlap and the
+// topological filter (shared vertex); the body-level filters ran already
+__device__ __forceinline__ bool prim_hit(const World& W, int kind, int row, int2 er, int t, const double* qlo,
+                                         const double* qhi, const double* __restrict__ lo,
+                                         const double* __restrict__ hi, double margin) {
+  double plo[3], phi[3];
+  if (kind == 0) {
+    int3 tv = W.tri_v[t];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      plo[c] = fmin(fmin(lo[3 * tv.x + c], lo[3 * tv.y + c]), lo[3 * tv.z + c]);
+      phi[c] = fmax(fmax(hi[3 * tv.x + c], hi[3 * tv.y + c]), hi[3 * tv.z + c]);
+    }
+    return box_hit(qlo, qhi, plo, phi, margin) && !(tv.x == row || tv.y == row || tv.z == row);
+  }
+  int2 ej = W.edge_v[t];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    plo[c] = fmin(lo[3 * ej.x + c], lo[3 * ej.y + c]);
+    phi[c] = fmax(hi[3 * ej.x + c], hi[3 * ej.y + c]);
+  }
+  return box_hit(qlo, qhi, plo, phi, margin) && !(er.x == ej.x || er.x == ej.y || er.y == ej.x || er.y == ej.y);
+}
+
+// visit, in increasing index order, the primitives of body gb in [c0, c1)
+// that hit the row's query box; 32-primitive chunks whose inflated AABB
+// misses the query box are skipped whole (exact: each primitive's inflated
+// box lies inside its chunk's)
+template <typename F>
+__device__ __forceinline__ void for_item_prims(const World& W, int kind, int row, int2 er, const double* qlo,
+                                               const double* qhi, const double* __restrict__ lo,
+                                               const double* __restrict__ hi, double margin, int gb, int c0,
+                                               int c1, F f) {
+  const int* cp0 = kind == 0 ? W.tchunk_p0 : W.echunk_p0;
+  const double* cbox = kind == 0 ? W.tchunk_box : W.echunk_box;
+  int ch0 = kind == 0 ? W.cbody_tchunk[gb] : W.cbody_echunk[gb];
+  int ch1 = kind == 0 ? W.cbody_tchunk[gb + 1] : W.cbody_echunk[gb + 1];
+  for (int ch = ch0; ch < ch1; ++ch) {
+    int p0 = max(cp0[ch], c0), p1 = min(cp0[ch + 1], c1);
+    if (p0 >= p1) continue;
+    if (!box_hit(qlo, qhi, cbox + 6 * ch, cbox + 6 * ch + 3, margin)) continue;
+    for (int t = p0; t < p1; ++t)
+      if (prim_hit(W, kind, row, er, t, qlo, qhi, lo, hi, margin)) f(t);
+  }
+}
+
+// AABBs of the 32-primitive chunks (triangles then edges) at [lo, hi]
+__global__ void k_chunk_boxes(World W, const double* __restrict__ lo, const double* __restrict__ hi) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  int nt = W.n_tchunk, ne = W.n_echunk;
+  if (c >= nt + ne) return;
+  bool tri = c < nt;
+  int ch = tri ? c : c - nt;
+  const int* cp0 = tri ? W.tchunk_p0 : W.echunk_p0;
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int t = cp0[ch]; t < cp0[ch + 1]; ++t) {
+    int vs[3];
+    int nv = 2;
+    if (tri) {
+      int3 tv = W.tri_v[t];
+      vs[0] = tv.x; vs[1] = tv.y; vs[2] = tv.z;
+      nv = 3;
+    } else {
+      int2 ev = W.edge_v[t];
+      vs[0] = ev.x; vs[1] = ev.y;
+    }
+    for (int k = 0; k < nv; ++k)
+      for (int d = 0; d < 3; ++d) {
+        mn[d] = fmin(mn[d], lo[3 * vs[k] + d]);
+        mx[d] = fmax(mx[d], hi[3 * vs[k] + d]);
+      }
+  }
+  double* box = (tri ? W.tchunk_box : W.echunk_box) + 6 * ch;
+  for (int d = 0; d < 3; ++d) {
+    box[d] = mn[d];
+    box[3 + d] = mx[d];
+  }
+}
+
+// Multi-CTA split (gridDim.z = Z > 1, large envs): the env's item list is cut
+// into Z contiguous ranges; pass 0 counts each range's hits into blk_cnt,
+// pass 1 writes at the range's exclusive offset, so the output order is the
+// same as with one CTA. pass -1: single CTA per env, count + write.
 __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __restrict__ lo,
                                                        const double* __restrict__ hi, Cands C,
-                                                       int kind, const int* env_mask) {
+                                                       int kind, const int* env_mask, int pass,
+                                                       int* blk_cnt) {
   if (kind < 0) kind = blockIdx.y;  // all three kinds in one launch
+  const int Z = gridDim.z, z = blockIdx.z;
   __shared__ int warp_tot[BP_THREADS / 32];
   __shared__ int total;
   __shared__ double blo[3 * MAX_BODIES], bhi[3 * MAX_BODIES];
@@ -130,6 +215,7 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
   int s0 = W.env_slot[e], s1 = W.env_slot[e + 1];
   int cb0 = W.env_cbody[e], nb = W.env_cbody[e + 1] - cb0;
   if (kind == 2) {
+    if (z != 0 || pass == 1) return;
     int base = 0;
     if (!W.env_has_ground[e]) {
       if (threadIdx.x == 0) C.n_gnd[e] = 0;
@@ -149,11 +235,12 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
     return;
   }
   if (!W.env_pairs[e]) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && z == 0 && pass != 1) {
       if (kind == 0) C.n_pt[e] = 0; else C.n_ee[e] = 0;
     }
     return;
   }
+  int* bc = blk_cnt ? blk_cnt + ((long long)e * 2 + kind) * Z : nullptr;
   // body boxes: one warp per body
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int B = wid; B < nb; B += BP_THREADS / 32) {
@@ -190,15 +277,62 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
     cap = C.ee_off[e + 1] - off;
   }
   long long n_items = (long long)nrow * nb;
+  long long per = ((n_items + Z - 1) / Z + BP_THREADS - 1) / BP_THREADS * BP_THREADS;
+  long long i_begin = min(n_items, z * per), i_end = min(n_items, i_begin + per);
   long long base = 0;
-  for (long long i0 = 0; i0 < n_items; i0 += BP_THREADS) {
+  if (pass == 0) {  // count only
+    __shared__ int tot;
+    if (threadIdx.x == 0) tot = 0;
+    __syncthreads();
+    int mine = 0;
+    for (long long it = i_begin + threadIdx.x; it < i_end; it += BP_THREADS) {
+      int row = 0, B = 0, c0 = 0, c1 = 0, rb = 0;
+      double qlo[3], qhi[3];
+      int2 er = make_int2(0, 0);
+      row = r0 + (int)(it / nb);
+      B = (int)(it % nb);
+      if (kind == 0) {
+        rb = W.slot_cbody[row];
+        for (int c = 0; c < 3; ++c) {
+          qlo[c] = lo[3 * row + c];
+          qhi[c] = hi[3 * row + c];
+        }
+        c0 = W.cbody_tri[cb0 + B];
+        c1 = W.cbody_tri[cb0 + B + 1];
+      } else {
+        rb = W.edge_cbody[row];
+        er = W.edge_v[row];
+        for (int c = 0; c < 3; ++c) {
+          qlo[c] = fmin(lo[3 * er.x + c], lo[3 * er.y + c]);
+          qhi[c] = fmax(hi[3 * er.x + c], hi[3 * er.y + c]);
+        }
+        c0 = max(W.cbody_edge[cb0 + B], row + 1);
+        c1 = W.cbody_edge[cb0 + B + 1];
+      }
+      if (c0 < c1 && !cull_item(W, cb0, rb, B, qlo, qhi, blo, bhi, margin))
+        for_item_prims(W, kind, row, er, qlo, qhi, lo, hi, margin, B + cb0, c0, c1, [&](int) { ++mine; });
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0 && mine) atomicAdd(&tot, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) bc[z] = tot;
+    return;
+  }
+  long long grand = 0;
+  if (pass == 1) {
+    for (int k = 0; k < Z; ++k) {
+      if (k < z) base += bc[k];
+      grand += bc[k];
+    }
+  }
+  for (long long i0 = i_begin; i0 < i_end; i0 += BP_THREADS) {
     long long it = i0 + threadIdx.x;
     int row = 0, B = 0, c0 = 0, c1 = 0;
     double qlo[3], qhi[3];
     int rb = 0;
     int2 er = make_int2(0, 0);
     bool live = false;
-    if (it < n_items) {
+    if (it < i_end) {
       row = r0 + (int)(it / nb);
       B = (int)(it % nb);
       if (kind == 0) {
@@ -221,34 +355,9 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
       }
       live = c0 < c1 && !cull_item(W, cb0, rb, B, qlo, qhi, blo, bhi, margin);
     }
-    // pass 1: count hits of this item
+    // pass 1: count hits of this item (chunk-culled primitive loop)
     int n_hit = 0;
-    if (live) {
-      for (int t = c0; t < c1; ++t) {
-        bool hit;
-        if (kind == 0) {
-          int3 tv = W.tri_v[t];
-          double plo[3], phi[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            plo[c] = fmin(fmin(lo[3 * tv.x + c], lo[3 * tv.y + c]), lo[3 * tv.z + c]);
-            phi[c] = fmax(fmax(hi[3 * tv.x + c], hi[3 * tv.y + c]), hi[3 * tv.z + c]);
-          }
-          hit = box_hit(qlo, qhi, plo, phi, margin) && !(tv.x == row || tv.y == row || tv.z == row);
-        } else {
-          int2 ej = W.edge_v[t];
-          double plo[3], phi[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            plo[c] = fmin(lo[3 * ej.x + c], lo[3 * ej.y + c]);
-            phi[c] = fmax(hi[3 * ej.x + c], hi[3 * ej.y + c]);
-          }
-          hit = box_hit(qlo, qhi, plo, phi, margin) &&
-                !(er.x == ej.x || er.x == ej.y || er.y == ej.x || er.y == ej.y);
-        }
-        n_hit += hit;
-      }
-    }
+    if (live) for_item_prims(W, kind, row, er, qlo, qhi, lo, hi, margin, B + cb0, c0, c1, [&](int) { ++n_hit; });
     // exclusive scan of per-item counts (item order = output order):
     // warp-shuffle inclusive scan, then one pass over the warp totals
     int incl = n_hit;
@@ -273,38 +382,19 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
     __syncthreads();
     // pass 2: write
     if (n_hit) {
-      for (int t = c0; t < c1; ++t) {
-        bool hit;
-        if (kind == 0) {
-          int3 tv = W.tri_v[t];
-          double plo[3], phi[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            plo[c] = fmin(fmin(lo[3 * tv.x + c], lo[3 * tv.y + c]), lo[3 * tv.z + c]);
-            phi[c] = fmax(fmax(hi[3 * tv.x + c], hi[3 * tv.y + c]), hi[3 * tv.z + c]);
-          }
-          hit = box_hit(qlo, qhi, plo, phi, margin) && !(tv.x == row || tv.y == row || tv.z == row);
-        } else {
-          int2 ej = W.edge_v[t];
-          double plo[3], phi[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            plo[c] = fmin(lo[3 * ej.x + c], lo[3 * ej.y + c]);
-            phi[c] = fmax(hi[3 * ej.x + c], hi[3 * ej.y + c]);
-          }
-          hit = box_hit(qlo, qhi, plo, phi, margin) &&
-                !(er.x == ej.x || er.x == ej.y || er.y == ej.x || er.y == ej.y);
+      for_item_prims(W, kind, row, er, qlo, qhi, lo, hi, margin, B + cb0, c0, c1, [&](int t) {
+        if (dst < cap) {
+          if (kind == 0) C.pt[off + dst] = make_int2(row, t);
+          else C.ee[off + dst] = make_int2(row, t);
         }
-        if (hit) {
-          if (dst < cap) {
-            if (kind == 0) C.pt[off + dst] = make_int2(row, t);
-            else C.ee[off + dst] = make_int2(row, t);
-          }
-          ++dst;
-        }
-      }
+        ++dst;
+      });
     }
     base += chunk_total;
+  }
+  if (pass == 1) {
+    if (z != 0) return;
+    base = grand;
   }
   if (threadIdx.x == 0) {
     if (base > cap) {

@@ -486,3 +486,215 @@ __global__ void k_pcg_finish(World W, EnvState S, Pcg P, const double* g, double
 }
 
 }  // namespace ipc
+
+#include <cooperative_groups.h>
+
+namespace ipc {
+namespace cg = cooperative_groups;
+
+// The whole block-Jacobi PCG loop as one cooperative persistent kernel:
+// phases separated by grid-wide barriers, per-env scalars updated by one
+// thread per env, chunk partial sums reduced per block in a fixed order
+// (same arithmetic as the per-phase kernels above, no host round trips).
+__device__ __forceinline__ void coop_partial(const Pcg& P, int which, double* sh) {
+  for (int c = blockIdx.x; c < P.n_chunk; c += gridDim.x) {
+    int e = P.chunk_env[c];
+    bool on = P.env_on[e] && P.env_live[e];
+    double a = 0.0, b = 0.0;
+    if (on)
+      for (int nd = P.chunk_n0[c] + threadIdx.x; nd < P.chunk_n1[c]; nd += blockDim.x)
+        for (int k = 0; k < 3; ++k) {
+          int i = 3 * nd + k;
+          if (which == 1) a += P.p[i] * P.Ap[i];
+          else {
+            a += P.r[i] * P.z[i];
+            b += P.r[i] * P.r[i];
+          }
+        }
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_down_sync(0xffffffffu, a, o);
+      b += __shfl_down_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+      sh[w] = a;
+      sh[32 + w] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && on) {
+      double sa = 0.0, sb = 0.0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+        sa += sh[k];
+        sb += sh[32 + k];
+      }
+      P.part[2 * c] = sa;
+      P.part[2 * c + 1] = sb;
+    }
+    __syncthreads();
+  }
+}
+
+// chunk-aligned block pass: block owns chunk c (all of its nodes), so the
+// node update and the chunk's partial dot products need no extra barrier
+__device__ __forceinline__ void chunk_reduce(double a, double b, double* sh, double* out2) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) {
+    sh[w] = a;
+    sh[32 + w] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      sa += sh[k];
+      sb += sh[32 + k];
+    }
+    out2[0] = sa;
+    out2[1] = sb;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void env_sums(const Pcg& P, int e, const double* part, double* a, double* b) {
+  double sa = 0.0, sb = 0.0;
+  for (int c = P.env_chunk[e]; c < P.env_chunk[e + 1]; ++c) {
+    sa += part[2 * c];
+    sb += part[2 * c + 1];
+  }
+  *a = sa;
+  *b = sb;
+}
+
+// (Σa, Σb) over env e's chunk partials, computed by warp 0 with a fixed
+// lane/shuffle tree (bitwise identical in every block) and broadcast via smem
+__device__ __forceinline__ void block_env_sums(const Pcg& P, int e, const double* part, double* out2) {
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double a = 0.0, b = 0.0;
+    for (int c = P.env_chunk[e] + threadIdx.x; c < P.env_chunk[e + 1]; c += 32) {
+      a += part[2 * c];
+      b += part[2 * c + 1];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (threadIdx.x == 0) {
+      out2[0] = a;
+      out2[1] = b;
+    }
+  }
+  __syncthreads();
+}
+
+// Persistent PCG over all envs, three grid barriers per iteration. Per-chunk
+// partials: part1 = p·Ap; (r·z, r·r) double-buffered in bufs[0] (= P.part,
+// written by the setup pass) and bufs[1]; every block derives an env's
+// liveness, α and β from the same partials, so no per-env scalar pass is
+// needed. cnt[0..1]: live-env counters (alternating), cnt[2]: cumulative
+// iteration count (stats).
+__global__ void k_pcg_coop(Pcg P, int n_env, double rtol2, int max_iters, int* cnt, double* part1, double* part2) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[64];
+  __shared__ double es[6];  // env sums: cur (rz, rr), part1 (pAp, -), nxt (rz, rr)
+  (void)n_env;
+  for (int it = 0; it < max_iters; ++it) {
+    const double* cur = (it & 1) ? part2 : P.part;
+    double* nxt = (it & 1) ? P.part : part2;
+    // phase A: Ap = H p on the block's chunks (one warp per row, lanes over
+    // the row's 3x3 blocks) + chunk partial p·Ap
+    for (int c = blockIdx.x; c < P.n_chunk; c += gridDim.x) {
+      int e = P.chunk_env[c];
+      if (!P.env_on[e] || !P.env_live[e]) continue;
+      block_env_sums(P, e, cur, es);
+      if (!(es[1] > rtol2 * P.env_bb[e])) continue;
+      int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      double a = 0.0;
+      for (int nd = P.chunk_n0[c] + wid; nd < P.chunk_n1[c]; nd += nw) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        int f = P.row_first[nd], rc = P.row_cnt[nd];
+        for (int j = lane; j < rc; j += 32) {
+          const double* B = P.bval + 9 * (long long)(f + j);
+          const double* pv = P.p + 3 * (long long)P.bcol[f + j];
+          double p0 = pv[0], p1 = pv[1], p2 = pv[2];
+          s0 += B[0] * p0 + B[1] * p1 + B[2] * p2;
+          s1 += B[3] * p0 + B[4] * p1 + B[5] * p2;
+          s2 += B[6] * p0 + B[7] * p1 + B[8] * p2;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if (lane == 0) {
+          P.Ap[3 * nd] = s0;
+          P.Ap[3 * nd + 1] = s1;
+          P.Ap[3 * nd + 2] = s2;
+          a += P.p[3 * nd] * s0 + P.p[3 * nd + 1] * s1 + P.p[3 * nd + 2] * s2;
+        }
+      }
+      chunk_reduce(a, 0.0, sh, part1 + 2 * c);
+    }
+    grid.sync();
+    // phase B: α = rz / pAp; x, r, z update + next (r·z, r·r) partials
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[(it + 1) & 1] = 0;
+    for (int c = blockIdx.x; c < P.n_chunk; c += gridDim.x) {
+      int e = P.chunk_env[c];
+      bool live = P.env_on[e] && P.env_live[e];
+      if (live) {
+        block_env_sums(P, e, cur, es);
+        live = es[1] > rtol2 * P.env_bb[e];
+      }
+      if (!live) {
+        if (threadIdx.x == 0) {  // keep both buffers equal for finished envs
+          nxt[2 * c] = cur[2 * c];
+          nxt[2 * c + 1] = cur[2 * c + 1];
+        }
+        continue;
+      }
+      block_env_sums(P, e, part1, es + 2);
+      double al = es[0] / es[2];
+      double a = 0.0, b = 0.0;
+      for (int nd = P.chunk_n0[c] + threadIdx.x; nd < P.chunk_n1[c]; nd += blockDim.x) {
+        for (int k = 0; k < 3; ++k) {
+          int i = 3 * nd + k;
+          P.x[i] += al * P.p[i];
+          P.r[i] -= al * P.Ap[i];
+        }
+        const double* M = P.Minv + 9 * nd;
+        for (int k = 0; k < 3; ++k) {
+          double z = M[3 * k] * P.r[3 * nd] + M[3 * k + 1] * P.r[3 * nd + 1] + M[3 * k + 2] * P.r[3 * nd + 2];
+          P.z[3 * nd + k] = z;
+          a += P.r[3 * nd + k] * z;
+          b += P.r[3 * nd + k] * P.r[3 * nd + k];
+        }
+      }
+      chunk_reduce(a, b, sh, nxt + 2 * c);
+    }
+    grid.sync();
+    // phase C: convergence test and p = z + β p
+    for (int c = blockIdx.x; c < P.n_chunk; c += gridDim.x) {
+      int e = P.chunk_env[c];
+      if (!P.env_on[e] || !P.env_live[e]) continue;
+      block_env_sums(P, e, cur, es);
+      if (!(es[1] > rtol2 * P.env_bb[e])) continue;
+      block_env_sums(P, e, nxt, es + 4);
+      if (!(es[5] > rtol2 * P.env_bb[e])) continue;  // converged this iteration
+      double be = es[4] / es[0];
+      for (int nd = P.chunk_n0[c] + threadIdx.x; nd < P.chunk_n1[c]; nd += blockDim.x)
+        for (int k = 0; k < 3; ++k) P.p[3 * nd + k] = P.z[3 * nd + k] + be * P.p[3 * nd + k];
+      if (c == P.env_chunk[e] && threadIdx.x == 0) atomicAdd(cnt + (it & 1), 1);
+    }
+    grid.sync();
+    if (cnt[it & 1] == 0 || it + 1 == max_iters) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) cnt[2] += it + 1;
+      break;
+    }
+  }
+}
+
+}  // namespace ipc

@@ -83,6 +83,11 @@ struct World {
   const unsigned char *cbody_rigid, *cbody_kin;
   const unsigned long long* cbody_excl;
   const int *cbody_slot, *cbody_tri, *cbody_edge;  // [n_cbody+1] contiguous primitive ranges
+  // 32-primitive chunks per body (second culling level of the broad phase)
+  int n_tchunk, n_echunk;
+  const int *tchunk_p0, *echunk_p0;        // [n_chunk+1] first primitive of each chunk
+  const int *cbody_tchunk, *cbody_echunk;  // [n_cbody+1] chunk ranges of each body
+  double *tchunk_box, *echunk_box;         // 6 per chunk (lo, hi), refreshed per broad phase
   // constraints
   const int* cons_aff;
   double *cons_target, *cons_lam, *cons_kappa, *cons_kappa0, *cons_mass, *cons_lastres;

@@ -310,9 +310,10 @@ class GpuWorld:
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(N.KERNEL_IDS)}, launches.value
 
     def stats(self):
-        out = np.zeros(3, np.int64)
+        out = np.zeros(4, np.int64)
         N.check(self.lib.ipc_world_stats(self.handle, N.ptr(out, N._i64p)))
-        return {"newton_iters": int(out[0]), "ls_rounds": int(out[1]), "syncs": int(out[2])}
+        return {"newton_iters": int(out[0]), "ls_rounds": int(out[1]), "syncs": int(out[2]),
+                "pcg_iters": int(out[3])}
 
     def flush_l2(self, nbytes=256 << 20):
         N.check(self.lib.ipc_world_flush_l2(self.handle, int(nbytes)))
