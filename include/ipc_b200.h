@@ -144,6 +144,10 @@ int ipc_world_flush_l2(ipc_world *w, int64_t bytes);
 /* Cumulative host-loop counters: batched Newton iterations, line-search
  * rounds, host synchronisations, sparse-path PCG iterations (out: 4). */
 int ipc_world_stats(ipc_world *w, int64_t *out);
+/* Per-phase SM-cycle totals of the fused per-environment step (world, DCD
+ * broad phase, terms, energy, dense solve, CCD prep, CCD broad phase, CCD,
+ * line search, other); zeros unless built with -DIPC_FUSED_TIMERS. */
+int ipc_world_fused_timers(ipc_world *w, int64_t *out, int n);
 int ipc_world_mark(ipc_world *w, int slot);
 int ipc_world_elapsed(ipc_world *w, int a, int b, double *ms);
 int ipc_world_sync(ipc_world *w);

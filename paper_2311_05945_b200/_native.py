@@ -12,7 +12,7 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libipc_b200.so")
+LIB_PATH = os.environ.get("IPC_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libipc_b200.so")
 
 _i32p = C.POINTER(C.c_int32)
 _u8p = C.POINTER(C.c_uint8)
@@ -86,6 +86,7 @@ SIGNATURES = {
     "ipc_world_profile": (C.c_int, [C.c_void_p, C.c_int, C.c_uint32]),
     "ipc_world_profile_read": (C.c_int, [C.c_void_p, _f64p, _i64p, _i64p]),
     "ipc_world_stats": (C.c_int, [C.c_void_p, _i64p]),
+    "ipc_world_fused_timers": (C.c_int, [C.c_void_p, _i64p, C.c_int]),
     "ipc_world_flush_l2": (C.c_int, [C.c_void_p, C.c_int64]),
     "ipc_world_mark": (C.c_int, [C.c_void_p, C.c_int]),
     "ipc_world_elapsed": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _f64p]),
@@ -99,7 +100,7 @@ SIGNATURES = {
 
 KERNEL_IDS = ("broad_dcd", "broad_ccd", "pairs_deriv", "pairs_value", "tet", "body", "ground",
               "friction", "energy_reduce", "dense_solve", "ccd", "lags", "world_pos", "sensing",
-              "misc", "pcg", "assembly")
+              "misc", "pcg", "assembly", "fused_step")
 
 _lib = None
 

@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include "sparse.cuh"
+#include "fused.cuh"
 
 using namespace ipc;
 
@@ -52,7 +53,7 @@ static inline int nblk(long long n, int t) { return (int)std::max<long long>(1, 
 // ---------------------------------------------------------------------------
 enum Kid {
   K_BROAD_DCD = 0, K_BROAD_SWEEP, K_PAIRS_D, K_PAIRS_V, K_TET, K_BODY, K_GROUND, K_FRICTION, K_ENERGY,
-  K_DENSE, K_CCD, K_LAGS, K_WORLD, K_SENSE, K_MISC, K_PCG, K_ASM, NKID
+  K_DENSE, K_CCD, K_LAGS, K_WORLD, K_SENSE, K_MISC, K_PCG, K_ASM, K_FUSED, NKID
 };
 struct OverflowRetry : std::exception {
   const char* what() const noexcept override { return "candidate capacity overflow"; }
@@ -784,6 +785,76 @@ struct ipc_world {
     IPC_LAUNCH(K_MISC, st, k_mark_unconverged, nblk(n_env, 128), 128, 0, n_env, S);
   }
 
+  // ---------------- fused per-env step (dense worlds) ----------------
+  bool fused_on = true;     // IPC_FUSED=0 selects the batched launch sequence
+  int fused_max_dof = 128;  // dense LDLᵀ in shared memory: n² doubles
+  int* fq = nullptr;
+  long long* d_fstat = nullptr;
+  double *v_save = nullptr, *kappa_save = nullptr;
+  int fused_blocks = 0;
+  size_t fused_smem = 0;
+  bool use_fused() const { return fused_on && !sparse && max_env_dof <= fused_max_dof; }
+
+  void step_fused(const ipc_step_config& cfg) {
+    if (lags_stale) {
+      alloc_lags();
+      lags_stale = false;
+    }
+    if (!fq) {
+      fq = pool.alloc<int>(1);
+      d_fstat = pool.alloc<long long>(2 + FT_N);
+      v_save = pool.alloc<double>(W.n_dof);
+      kappa_save = pool.alloc<double>(n_env);
+    }
+    if (!fused_blocks) {
+      fused_smem = sizeof(double) * (size_t)std::max(max_env_dof * max_env_dof + 2 * max_env_dof, 3 * max_slots);
+      CK(cudaFuncSetAttribute(k_env_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_env_step, 256, fused_smem));
+      fused_blocks = std::max(1, std::min(n_env, std::max(per_sm, 1) * n_sm));
+    }
+    // the step commits v and κ in place: keep copies for an overflow replay
+    CK(cudaMemcpyAsync(v_save, W.v, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(kappa_save, W.env_kappa, sizeof(double) * n_env, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(fq, 0, sizeof(int), st));
+    FusedArgs A{};
+    A.W = W;
+    A.S = S;
+    A.dc = dcd.c;
+    A.sw = sweep.c;
+    A.L = L;
+    A.D = D_with(pb_dcd);
+    A.T = Terms{body_val, tet_val, pb_dcd.pt_val, pb_dcd.ee_val, pb_dcd.gnd_val, fr_val, frg_val, nullptr};
+    A.xwt = xwt;
+    A.xlo = xlo;
+    A.xhi = xhi;
+    A.enable = enable;
+    A.ok = ok;
+    A.accepted = accepted;
+    A.ls_count = ls_count;
+    A.targets = d_targets;
+    A.queue = fq;
+    A.stat = d_fstat;
+    A.timers = d_fstat + 2;
+    A.h = cfg.h;
+    A.newton_tol = cfg.newton_tol;
+    A.ccd_cons = cfg.ccd_conservative_factor;
+    A.max_newton = cfg.max_newton_iters;
+    A.max_halvings = cfg.max_line_search_halvings;
+    A.fp_iters = std::max(cfg.friction_fixed_point_iters, 1);
+    A.al_max_outer = cfg.al_max_outer;
+    IPC_LAUNCH(K_FUSED, st, k_env_step, fused_blocks, 256, fused_smem, A);
+    CK(cudaMemcpyAsync(h_status, dcd.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_status + 1, sweep.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ++stat_syncs;
+    if (h_status[0] || h_status[1]) {
+      CK(cudaMemcpyAsync(W.v, v_save, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(W.env_kappa, kappa_save, sizeof(double) * n_env, cudaMemcpyDeviceToDevice, st));
+      throw OverflowRetry();
+    }
+  }
+
   // ---------------- sparse path (large environments) ----------------
   bool sparse = false;
   Pcg pcg{};
@@ -1130,6 +1201,8 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
         long long rows = std::max(d->env_slot[e + 1] - d->env_slot[e], d->env_edge[e + 1] - d->env_edge[e]);
         mx = std::max(mx, rows * nb);
       }
+      const char* fz = getenv("IPC_FUSED");
+      if (fz && fz[0] == '0') w->fused_on = false;
       const char* ez = getenv("IPC_BROAD_ITEMS");
       long long per = ez ? std::max(64LL, atoll(ez)) : ipc_world::BROAD_ITEMS;
       w->bp_z = (int)std::min(64LL, std::max(1LL, (mx + per - 1) / per));
@@ -1257,6 +1330,9 @@ static void step_core(ipc_world* w, const ipc_step_config* cfg, const double* ta
     } else {
       IPC_LAUNCH(K_MISC, st, k_fill_int, nblk(ne, 128), 128, 0, ne, w->enable, 1);
     }
+    if (w->use_fused()) {
+      w->step_fused(*cfg);
+    } else {
     IPC_LAUNCH(K_MISC, st, k_copy_int, nblk(ne, 128), 128, 0, ne, w->enable, w->ok);
     w->broad(w->dcd, w->pb_dcd, true, W.xw0, W.xw0, w->ok);
     // feasibility of the incoming state (ref solver.py:372-385)
@@ -1311,6 +1387,7 @@ static void step_core(ipc_world* w, const ipc_step_config* cfg, const double* ta
                                                              nullptr, nullptr, S.min_s);
     IPC_LAUNCH(K_MISC, st, k_kappa_adapt, nblk(ne, 128), 128, 0, W, S, w->ok);
     IPC_LAUNCH(K_MISC, st, k_finalize, nblk(W.n_dof, 256), 256, 0, W, h, w->ok);
+    }
     CK(cudaGetLastError());
     if (rep) {
       std::vector<int> it(ne), cc(ne), cv(ne), lf(ne), ao(ne), er(ne);
@@ -1402,6 +1479,22 @@ int ipc_world_stats(ipc_world* w, int64_t* out) {
       CK(cudaMemcpy(pit, w->d_nlive, sizeof(pit), cudaMemcpyDeviceToHost));
     }
     out[3] = pit[2];
+    if (w->d_fstat) {
+      long long fs[2];
+      CK(cudaMemcpy(fs, w->d_fstat, sizeof(fs), cudaMemcpyDeviceToHost));
+      out[0] += fs[0];
+      out[1] += fs[1];
+    }
+  })
+}
+
+int ipc_world_fused_timers(ipc_world* w, int64_t* out, int n) {
+  GUARD({
+    for (int k = 0; k < n; ++k) out[k] = 0;
+    if (w->d_fstat) {
+      CK(cudaStreamSynchronize(w->st));
+      CK(cudaMemcpy(out, w->d_fstat + 2, sizeof(long long) * std::min(n, (int)FT_N), cudaMemcpyDeviceToHost));
+    }
   })
 }
 

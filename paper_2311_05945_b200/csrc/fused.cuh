@@ -1,0 +1,361 @@
+// Fused per-environment time step for dense worlds: one 256-thread CTA runs
+// the whole of ref solver.py:355-454 for one environment — feasibility check,
+// predictor, lagged-friction fixed point, augmented-Lagrangian outer loop,
+// Newton iterations (DCD broad phase, every energy term, dense LDLᵀ solve,
+// CCD sweep + conservative advancement, backtracking line search), post-step
+// distance and κ adaptation — with block barriers between phases and no host
+// round trip. CTAs pull environments from an atomic queue, so a long
+// contact-onset solve in one env overlaps with the rest of the batch instead
+// of serialising the launch sequence of the batched path.
+//
+// Every per-element formula is the batched path's own item function
+// (kernels.cuh / solve.cuh), so both paths produce the same values; only
+// the schedule differs (sequential line-search trials instead of speculative
+// ones, which accept the same α).
+#pragma once
+#include "solve.cuh"
+
+namespace ipc {
+
+// optional phase timers (build with -DIPC_FUSED_TIMERS): SM cycles per phase,
+// summed over envs into FusedArgs::timers
+enum { FT_WORLD, FT_BROAD_DCD, FT_TERMS, FT_ENERGY, FT_DENSE, FT_CCD_PREP, FT_BROAD_CCD, FT_CCD, FT_LS, FT_OTHER,
+       FT_N };
+#ifdef IPC_FUSED_TIMERS
+#define FT_MARK(A, k)                                                   \
+  do {                                                                  \
+    __syncthreads();                                                    \
+    if (threadIdx.x == 0) {                                             \
+      long long now = clock64();                                        \
+      atomicAdd((unsigned long long*)(A).timers + (k), now - ft_t0);    \
+      ft_t0 = now;                                                      \
+    }                                                                   \
+  } while (0)
+#define FT_START long long ft_t0 = clock64()
+#else
+#define FT_MARK(A, k) do { } while (0)
+#define FT_START do { } while (0)
+#endif
+
+struct FusedArgs {
+  World W;
+  EnvState S;
+  Cands dc, sw;  // DCD / CCD-sweep candidate stores
+  Lags L;
+  Derivs D;      // derivative buffers of the DCD store
+  Terms T;       // value buffers of the DCD store
+  double *xwt, *xlo, *xhi;
+  const int* enable;
+  int *ok, *accepted, *ls_count;
+  const double* targets;
+  int* queue;        // [0]: next env
+  long long* stat;   // [0] Newton iterations, [1] line-search trials
+  long long* timers; // [FT_N] (IPC_FUSED_TIMERS builds)
+  double h, newton_tol, ccd_cons;
+  int max_newton, max_halvings, fp_iters, al_max_outer;
+};
+
+__device__ __noinline__ void fused_pair_hess0(const World& W, const double* xw, const Cands& C, long long q, int e,
+                                              const Derivs& D) {
+  pair_hess_item<0>(W, xw, C, q, e, D.pt_g, D.pt_h, D.pt_act);
+}
+__device__ __noinline__ void fused_pair_hess1(const World& W, const double* xw, const Cands& C, long long q, int e,
+                                              const Derivs& D) {
+  pair_hess_item<1>(W, xw, C, q, e, D.ee_g, D.ee_h, D.ee_act);
+}
+__device__ __noinline__ void fused_body(const World& W, const double* x, const double* xhat, double h2, int deriv,
+                                        int b, double* val, double* g, double* hh) {
+  body_item(W, x, xhat, h2, deriv, b, val, g, hh);
+}
+__device__ __noinline__ void fused_tet(const World& W, const double* x, double h2, int deriv, int t, double* val,
+                                       double* g, double* hp) {
+  tet_item(W, x, h2, deriv, t, val, g, hp);
+}
+
+__device__ __forceinline__ void env_world(const World& W, const double* x, double* xw, int e) {
+  for (int s = W.env_slot[e] + threadIdx.x; s < W.env_slot[e + 1]; s += blockDim.x) world_slot(W, x, xw, s);
+  __syncthreads();
+}
+
+// broad phase of env e over [lo, hi] into C; returns false on capacity
+// overflow (sticky flag: the host replays the whole step with more room)
+__device__ bool env_broad(const World& W, const double* lo, const double* hi, const Cands& C, int e) {
+  __shared__ int s_ov;
+  int b0 = W.env_cbody[e], b1 = W.env_cbody[e + 1];
+  int t0 = W.cbody_tchunk[b0], t1 = W.cbody_tchunk[b1];
+  int q0 = W.cbody_echunk[b0], q1 = W.cbody_echunk[b1];
+  for (int c = t0 + threadIdx.x; c < t1; c += blockDim.x) chunk_box(W, lo, hi, c);
+  for (int c = q0 + threadIdx.x; c < q1; c += blockDim.x) chunk_box(W, lo, hi, W.n_tchunk + c);
+  __syncthreads();
+  for (int kind = 0; kind < 3; ++kind) {
+    broad_env(W, lo, hi, C, kind, e, 0, 1, -1, nullptr);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) s_ov = *(volatile int*)C.overflow;
+  __syncthreads();
+  return !s_ov;
+}
+
+// element values (deriv = 0) or values + derivatives of every term at x / xw;
+// returns the env's minimum squared distance over candidates and ground
+__device__ double env_terms(const FusedArgs& A, const double* x, const double* xw, int deriv, int e) {
+  const World& W = A.W;
+  __shared__ double s_min;
+  if (threadIdx.x == 0) s_min = INFINITY;
+  __syncthreads();
+  double h2 = A.h * A.h;
+  if (deriv) {
+    for (int b = W.env_aff[e] + threadIdx.x; b < W.env_aff[e + 1]; b += blockDim.x)
+      fused_body(W, x, W.xhat, h2, 1, b, A.T.body_val, A.D.body_g, A.D.body_h);
+    for (int t = W.env_tet[e] + threadIdx.x; t < W.env_tet[e + 1]; t += blockDim.x)
+      fused_tet(W, x, h2, 1, t, A.T.tet_val, A.D.tet_g, A.D.tet_h);
+  }
+  const Cands& C = A.dc;
+  for (int kind = 0; kind < 2; ++kind) {
+    int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
+    long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
+    double* val = kind == 0 ? A.T.pt_val : A.T.ee_val;
+    unsigned char* act = kind == 0 ? A.D.pt_act : A.D.ee_act;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      bool on = pair_value_item(W, xw, C, kind, off + k, e, val, act, &s_min);
+      if (on && deriv) {
+        if (kind == 0) fused_pair_hess0(W, xw, C, off + k, e, A.D);
+        else fused_pair_hess1(W, xw, C, off + k, e, A.D);
+      }
+    }
+  }
+  for (int k = threadIdx.x; k < C.n_gnd[e]; k += blockDim.x)
+    ground_item(W, xw, C, deriv, C.gnd_off[e] + k, e, A.T.gnd_val, A.D.gnd_gy, A.D.gnd_hyy, &s_min);
+  if (deriv) {
+    const Lags& L = A.L;
+    for (int k = threadIdx.x; k < L.n[e]; k += blockDim.x)
+      friction_item(W, xw, W.xw0, L, A.h, 1, L.off[e] + k, e, A.T.fr_val, A.D.fr_g, A.D.fr_h);
+    for (int k = threadIdx.x; k < L.g_n[e]; k += blockDim.x)
+      friction_gnd_item(W, xw, W.xw0, L, A.h, 1, W.env_slot[e] + k, e, A.T.frg_val, A.D.frg_g, A.D.frg_h);
+  }
+  __syncthreads();
+  double m = s_min;
+  __syncthreads();
+  return m;
+}
+
+// any non-finite candidate value of the incoming state (k_start_check)
+__device__ bool env_infeasible(const FusedArgs& A, int e) {
+  const Cands& C = A.dc;
+  int bad = 0;
+  for (int k = threadIdx.x; k < C.n_pt[e]; k += blockDim.x) bad |= isinf(A.T.pt_val[C.pt_off[e] + k]);
+  for (int k = threadIdx.x; k < C.n_ee[e]; k += blockDim.x) bad |= isinf(A.T.ee_val[C.ee_off[e] + k]);
+  for (int k = threadIdx.x; k < C.n_gnd[e]; k += blockDim.x) bad |= isinf(A.T.gnd_val[C.gnd_off[e] + k]);
+  return __syncthreads_or(bad);
+}
+
+__device__ __forceinline__ int env_flag_read(const int* f, int e) {
+  __shared__ int s_f;
+  __syncthreads();
+  if (threadIdx.x == 0) s_f = f[e];
+  __syncthreads();
+  return s_f;
+}
+
+// Newton loop of one env (ref solver.py:295-352); false on overflow
+__device__ bool env_newton(const FusedArgs& A, int e, double* sm) {
+  const World& W = A.W;
+  const EnvState& S = A.S;
+  __shared__ double s_amin;
+  int d0 = W.env_dof[e], d1 = W.env_dof[e + 1];
+  int s0 = W.env_slot[e], s1 = W.env_slot[e + 1];
+  if (threadIdx.x == 0) newton_begin_env(S, S.al_active, e);
+  FT_START;
+  for (int it = 0; it < A.max_newton; ++it) {
+    if (!env_flag_read(S.newton_active, e)) break;
+    // head: DCD candidates at x, derivatives, E0, Newton direction
+    FT_MARK(A, FT_OTHER);
+    env_world(W, W.x, W.xw, e);
+    FT_MARK(A, FT_WORLD);
+    if (!env_broad(W, W.xw, W.xw, A.dc, e)) return false;
+    FT_MARK(A, FT_BROAD_DCD);
+    double ms = env_terms(A, W.x, W.xw, 1, e);
+    FT_MARK(A, FT_TERMS);
+    double e0 = env_energy_block(W, W.x, W.xhat, A.T, A.dc, A.L, e);
+    if (threadIdx.x == 0) {
+      S.min_s[e] = ms;
+      S.e0[e] = e0;
+    }
+    FT_MARK(A, FT_ENERGY);
+    dense_solve_block(W, S, A.D, A.dc, A.L, W.x, W.xhat, W.p, W.grad, e, sm);
+    FT_MARK(A, FT_DENSE);
+    if (threadIdx.x == 0) {
+      newton_check_env(S, A.h, A.newton_tol, e);
+      atomicAdd((unsigned long long*)A.stat, 1ull);
+    }
+    if (!env_flag_read(S.ls_active, e)) continue;  // converged (newton_active cleared)
+    // CCD bound along p: sweep boxes of x -> x + p
+    for (int i = d0 + threadIdx.x; i < d1; i += blockDim.x) W.xt[i] = __dadd_rn(W.x[i], __dmul_rn(1.0, W.p[i]));
+    __syncthreads();
+    env_world(W, W.xt, A.xwt, e);
+    for (int i = 3 * s0 + threadIdx.x; i < 3 * s1; i += blockDim.x) {
+      double dd = __dsub_rn(A.xwt[i], W.xw[i]);
+      W.dxw[i] = dd;
+      double a = W.xw[i], b = __dadd_rn(W.xw[i], dd);
+      A.xlo[i] = fmin(a, b);
+      A.xhi[i] = fmax(a, b);
+    }
+    FT_MARK(A, FT_CCD_PREP);
+    if (!env_broad(W, A.xlo, A.xhi, A.sw, e)) return false;
+    FT_MARK(A, FT_BROAD_CCD);
+    if (threadIdx.x == 0) s_amin = 1.0;
+    __syncthreads();
+    {
+      const Cands& C = A.sw;
+      for (int kind = 0; kind < 2; ++kind) {
+        int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
+        long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+          double a = ccd_pair_item(W, W.xw, W.dxw, C, kind, off + k, A.ccd_cons);
+          if (a < 1.0) atomic_min_pos(&s_amin, a);
+        }
+      }
+      for (int k = threadIdx.x; k < C.n_gnd[e]; k += blockDim.x) {
+        double a = ccd_ground_item(W, W.xw, W.dxw, C, C.gnd_off[e] + k, e, A.ccd_cons);
+        if (a <= 1.0) atomic_min_pos(&s_amin, a);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      S.alpha_max[e] = s_amin;
+      ls_begin_env(S, A.ls_count, e);
+      A.accepted[e] = 0;
+    }
+    FT_MARK(A, FT_CCD);
+    // backtracking (ref solver.py:257): E(x + α p) <= E0, α halved
+    while (env_flag_read(S.ls_active, e)) {
+      double a = S.alpha[e];
+      double en = ls_value_block(W, A.sw, A.L, W.x, W.p, W.xhat, A.h * A.h, A.h, a, e, sm);
+      if (threadIdx.x == 0) {
+        S.e_new[e] = en;
+        ls_check_env(S, A.ls_count, A.max_halvings, A.accepted, e);
+        atomicAdd((unsigned long long*)A.stat + 1, 1ull);
+      }
+    }
+    FT_MARK(A, FT_LS);
+    if (env_flag_read(A.accepted, e)) {
+      double a = S.alpha[e];
+      for (int i = d0 + threadIdx.x; i < d1; i += blockDim.x) W.x[i] = __dadd_rn(W.x[i], __dmul_rn(a, W.p[i]));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && S.newton_active[e]) {  // iteration cap: not converged
+    S.converged[e] = 0;
+    S.newton_active[e] = 0;
+  }
+  __syncthreads();
+  return true;
+}
+
+// whole step of env e; false when a candidate store overflowed
+__device__ bool env_step(const FusedArgs& A, int e, double* sm) {
+  const World& W = A.W;
+  const EnvState& S = A.S;
+  int tid = threadIdx.x;
+  int d0 = W.env_dof[e], d1 = W.env_dof[e + 1];
+  if (tid == 0) {
+    S.newton_iters[e] = 0; S.ccd_calls[e] = 0; S.al_outer[e] = 0; S.ls_failed[e] = 0;
+    S.converged[e] = 1; S.err[e] = 0; S.min_s_before[e] = INFINITY; S.gnorm[e] = 0.0;
+    A.ok[e] = A.enable[e] ? 1 : 0;
+  }
+  env_world(W, W.x, W.xw0, e);
+  bool ok = env_flag_read(A.ok, e);
+  if (ok) {
+    // feasibility of the incoming state (ref solver.py:372-385)
+    if (!env_broad(W, W.xw0, W.xw0, A.dc, e)) return false;
+    env_terms(A, W.x, W.xw0, 0, e);
+    if (env_infeasible(A, e)) {
+      ok = false;
+      if (tid == 0) {
+        A.ok[e] = 0;
+        S.err[e] = 1;
+      }
+    }
+  }
+  // predictor x̂ = x + h v + h² a_g (ref bodies.py:292)
+  double h = A.h, hh = h * h;
+  for (int i = d0 + tid; i < d1; i += blockDim.x) W.xhat[i] = W.x[i] + h * W.v[i];
+  __syncthreads();
+  for (int v = W.env_vert[e] + tid; v < W.env_vert[e + 1]; v += blockDim.x) {
+    int d = W.vert_dof[v];
+    const double* g = W.env_gravity + 3 * e;
+    for (int c = 0; c < 3; ++c) W.xhat[d + c] += hh * g[c];
+  }
+  for (int b = W.env_aff[e] + tid; b < W.env_aff[e + 1]; b += blockDim.x) {
+    int o = W.aff_dof[b];
+    for (int c = 0; c < 12; ++c) W.xhat[o + c] += hh * W.aff_acc[12 * b + c];
+  }
+  // fresh AL cycle (ref solver.py:394-400)
+  for (int k = W.env_cons[e] + tid; k < W.env_cons[e + 1]; k += blockDim.x) {
+    for (int i = 0; i < 12; ++i) {
+      W.cons_lam[12 * k + i] = 0.0;
+      W.cons_target[12 * k + i] = A.targets[12 * k + i];
+    }
+    W.cons_kappa[k] = W.cons_kappa0[k];
+    W.cons_lastres[k] = INFINITY;
+  }
+  __syncthreads();
+  for (int fp = 0; fp < A.fp_iters; ++fp) {
+    if (ok) {
+      if (fp == 0) {
+        lags_env(W, W.xw0, A.dc, A.L, e);
+      } else {
+        env_world(W, W.x, W.xw, e);
+        if (!env_broad(W, W.xw, W.xw, A.dc, e)) return false;
+        lags_env(W, W.xw, A.dc, A.L, e);
+      }
+    }
+    if (tid == 0) S.al_active[e] = ok ? 1 : 0;
+    __syncthreads();
+    for (int outer = 0; outer < A.al_max_outer; ++outer) {
+      if (!env_flag_read(S.al_active, e)) break;
+      if (!env_newton(A, e, sm)) return false;
+      if (tid == 0) al_update_env(W, S, outer, e);
+    }
+    if (tid == 0 && S.ls_failed[e]) A.ok[e] = 0;
+    ok = env_flag_read(A.ok, e);
+  }
+  // post-step distance and barrier adaptation (ref solver.py:440-450)
+  ok = A.enable[e] && !env_flag_read(S.err, e);
+  if (tid == 0) {
+    A.ok[e] = ok ? 1 : 0;
+    S.min_s[e] = INFINITY;
+  }
+  __syncthreads();
+  if (ok) {
+    env_world(W, W.x, W.xw, e);
+    if (!env_broad(W, W.xw, W.xw, A.dc, e)) return false;
+    double ms = env_terms(A, W.x, W.xw, 0, e);
+    if (tid == 0) {
+      S.min_s[e] = ms;
+      kappa_adapt_env(W, S, e);
+    }
+  }
+  for (int i = d0 + tid; i < d1; i += blockDim.x) {
+    if (!ok) W.x[i] = W.x_prev[i];
+    else W.v[i] = (W.x[i] - W.x_prev[i]) / h;
+  }
+  __syncthreads();
+  return true;
+}
+
+__global__ void __launch_bounds__(256, 1) k_env_step(FusedArgs A) {
+  extern __shared__ double sm[];
+  __shared__ int s_e;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_e = *(volatile int*)A.dc.overflow || *(volatile int*)A.sw.overflow
+                                    ? A.W.n_env : atomicAdd(A.queue, 1);
+    __syncthreads();
+    int e = s_e;
+    if (e >= A.W.n_env) return;
+    env_step(A, e, sm);
+  }
+}
+
+}  // namespace ipc

@@ -21,9 +21,8 @@ IPC_HD void atomic_min_pos(double* addr, double v) {
 // world-space slot positions: soft slots copy their DoF, affine slots
 // p + A x0 with numpy's operation order (ref contact.py:296)
 // ---------------------------------------------------------------------------
-__global__ void k_world(World W, const double* __restrict__ x, double* __restrict__ xw) {
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= W.n_slot) return;
+__device__ __forceinline__ void world_slot(const World& W, const double* __restrict__ x, double* __restrict__ xw,
+                                           int s) {
   int d = W.slot_dof[s];
   if (!W.slot_aff[s]) {
     xw[3 * s] = x[d];
@@ -38,6 +37,11 @@ __global__ void k_world(World W, const double* __restrict__ x, double* __restric
     double m = __dadd_rn(__dadd_rn(__dmul_rn(a[0], r[0]), __dmul_rn(a[1], r[1])), __dmul_rn(a[2], r[2]));
     xw[3 * s + i] = __dadd_rn(x[d + i], m);
   }
+}
+
+__global__ void k_world(World W, const double* __restrict__ x, double* __restrict__ xw) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < W.n_slot) world_slot(W, x, xw, s);
 }
 
 
@@ -163,10 +167,10 @@ __device__ __forceinline__ void for_item_prims(const World& W, int kind, int row
 }
 
 // AABBs of the 32-primitive chunks (triangles then edges) at [lo, hi]
-__global__ void k_chunk_boxes(World W, const double* __restrict__ lo, const double* __restrict__ hi) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  int nt = W.n_tchunk, ne = W.n_echunk;
-  if (c >= nt + ne) return;
+// c indexes triangle chunks then edge chunks
+__device__ __forceinline__ void chunk_box(const World& W, const double* __restrict__ lo,
+                                          const double* __restrict__ hi, int c) {
+  int nt = W.n_tchunk;
   bool tri = c < nt;
   int ch = tri ? c : c - nt;
   const int* cp0 = tri ? W.tchunk_p0 : W.echunk_p0;
@@ -195,22 +199,22 @@ __global__ void k_chunk_boxes(World W, const double* __restrict__ lo, const doub
   }
 }
 
+__global__ void k_chunk_boxes(World W, const double* __restrict__ lo, const double* __restrict__ hi) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < W.n_tchunk + W.n_echunk) chunk_box(W, lo, hi, c);
+}
+
 // Multi-CTA split (gridDim.z = Z > 1, large envs): the env's item list is cut
 // into Z contiguous ranges; pass 0 counts each range's hits into blk_cnt,
 // pass 1 writes at the range's exclusive offset, so the output order is the
 // same as with one CTA. pass -1: single CTA per env, count + write.
-__global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __restrict__ lo,
-                                                       const double* __restrict__ hi, Cands C,
-                                                       int kind, const int* env_mask, int pass,
-                                                       int* blk_cnt) {
-  if (kind < 0) kind = blockIdx.y;  // all three kinds in one launch
-  const int Z = gridDim.z, z = blockIdx.z;
+// block function (blockDim.x == BP_THREADS): range z of Z of env e's items
+__device__ void broad_env(const World& W, const double* __restrict__ lo, const double* __restrict__ hi,
+                          const Cands& C, int kind, int e, int z, int Z, int pass, int* blk_cnt) {
   __shared__ int warp_tot[BP_THREADS / 32];
   __shared__ int total;
   __shared__ double blo[3 * MAX_BODIES], bhi[3 * MAX_BODIES];
   __shared__ int cnt[BP_THREADS];
-  int e = blockIdx.x;
-  if (env_mask && !env_mask[e]) return;
   double margin = W.env_dhat[e];
   int s0 = W.env_slot[e], s1 = W.env_slot[e + 1];
   int cb0 = W.env_cbody[e], nb = W.env_cbody[e + 1] - cb0;
@@ -405,6 +409,16 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
   }
 }
 
+__global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __restrict__ lo,
+                                                       const double* __restrict__ hi, Cands C,
+                                                       int kind, const int* env_mask, int pass,
+                                                       int* blk_cnt) {
+  if (kind < 0) kind = blockIdx.y;  // all three kinds in one launch
+  int e = blockIdx.x;
+  if (env_mask && !env_mask[e]) return;
+  broad_env(W, lo, hi, C, kind, e, blockIdx.z, gridDim.z, pass, blk_cnt);
+}
+
 // per-env exclusive prefix of candidate counts over flagged envs (one CTA);
 // pre has n_env + 1 entries, pre[n_env] = total
 __global__ void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
@@ -471,13 +485,10 @@ __device__ __forceinline__ int find_env(const int* __restrict__ pre, int n_env, 
 // ---------------------------------------------------------------------------
 
 // per affine body: inertia + h² orthogonality (projected) + kinematic target
-__global__ void k_body(World W, const double* __restrict__ x, const double* __restrict__ xhat,
-                       double h2, int deriv, const int* env_flag, double* val, double* g12,
-                       double* h144) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= W.n_aff) return;
+__device__ __forceinline__ void body_item(const World& W, const double* __restrict__ x,
+                                          const double* __restrict__ xhat, double h2, int deriv, int b,
+                                          double* val, double* g12, double* h144) {
   int e = W.aff_env[b];
-  if (env_flag && !env_flag[e]) return;
   int o = W.aff_dof[b];
   const double* M = W.aff_M + 144 * b;
   double d[12];
@@ -535,12 +546,18 @@ __global__ void k_body(World W, const double* __restrict__ x, const double* __re
   }
 }
 
+__global__ void k_body(World W, const double* __restrict__ x, const double* __restrict__ xhat,
+                       double h2, int deriv, const int* env_flag, double* val, double* g12,
+                       double* h144) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= W.n_aff) return;
+  if (env_flag && !env_flag[W.aff_env[b]]) return;
+  body_item(W, x, xhat, h2, deriv, b, val, g12, h144);
+}
+
 // per tet: h² V ψ(F), gradient, PSD-projected stencil Hessian (ref elastic.py:204)
-__global__ void k_tet(World W, const double* __restrict__ x, double h2, int deriv,
-                      const int* env_flag, double* val, double* g12, double* hp) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= W.n_tet) return;
-  if (env_flag && !env_flag[W.tet_env[t]]) return;
+__device__ __forceinline__ void tet_item(const World& W, const double* __restrict__ x, double h2, int deriv,
+                                         int t, double* val, double* g12, double* hp) {
   int4 d = W.tet_dof[t];
   V3 x0 = ld3(x + d.x), x1 = ld3(x + d.y), x2 = ld3(x + d.z), x3 = ld3(x + d.w);
   V3 e1 = x1 - x0, e2 = x2 - x0, e3 = x3 - x0;
@@ -594,6 +611,14 @@ __global__ void k_tet(World W, const double* __restrict__ x, double h2, int deri
   }
 }
 
+__global__ void k_tet(World W, const double* __restrict__ x, double h2, int deriv,
+                      const int* env_flag, double* val, double* g12, double* hp) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= W.n_tet) return;
+  if (env_flag && !env_flag[W.tet_env[t]]) return;
+  tet_item(W, x, h2, deriv, t, val, g12, hp);
+}
+
 // Contact pairs, pass 1 (light, every candidate of every flagged env):
 // region + squared distance, value κ b (× mollifier) for active pairs, 0
 // otherwise, INF when an active pair has non-positive distance
@@ -620,19 +645,11 @@ struct PairIO {  // per-kind (0 PT, 1 EE) buffers; kind = blockIdx.y
   int* work_n;
 };
 
-__global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int deriv, PairIO io,
-                            double* env_min_s) {
-  const int kind = blockIdx.y;
-  double* val = io.val[kind];
-  unsigned char* active = io.act[kind];
-  long long* work = io.work[kind];
-  int* work_env = io.work_env[kind];
-  int* work_n = io.work_n + kind;
-  const int* pre = kind == 0 ? C.pre_pt : C.pre_ee;
-  int total = pre[W.n_env];
-  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
-    int e = find_env(pre, W.n_env, g);
-    long long q = (kind == 0 ? C.pt_off[e] : C.ee_off[e]) + (g - pre[e]);
+// value of candidate q of env e; returns true when the pair is active
+// (0 < d² < ŝ: its derivatives are needed)
+__device__ __forceinline__ bool pair_value_item(const World& W, const double* __restrict__ xw, const Cands& C,
+                                                int kind, long long q, int e, double* val,
+                                                unsigned char* active, double* env_min_s) {
     int2 pr = kind == 0 ? C.pt[q] : C.ee[q];
     int sl[4];
     pair_slots(W, kind, pr, sl);
@@ -646,26 +663,39 @@ __global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int
       int r = ee_region(X[0], X[1], X[2], X[3], nullptr);
       d2 = ee_dist2(r, X[0], X[1], X[2], X[3]);
     }
-    if (env_min_s) atomic_min_pos(env_min_s + e, d2);
+    if (env_min_s) atomic_min_pos(env_min_s, d2);
     double dhat = W.env_dhat[e], shat = dhat * dhat;
     if (active) active[q] = 0;
     if (!(d2 < shat)) {
       val[q] = 0.0;
-      continue;
+      return false;
     }
     if (d2 <= 0.0) {
       val[q] = INFINITY;
-      continue;
+      return false;
     }
     double kappa = W.env_kappa[e];
     double b = barrier_val(d2, shat);
     double m = 1.0;
     if (kind == 1) m = mollifier_val(cross2(X[1] - X[0], X[3] - X[2]), 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y]);
     val[q] = kind == 1 ? kappa * (m * b) : kappa * b;
-    if (deriv) {
-      int slot = atomicAdd(work_n, 1);
-      work[slot] = q;
-      work_env[slot] = e;
+    return true;
+}
+
+__global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int deriv, PairIO io,
+                            double* env_min_s) {
+  const int kind = blockIdx.y;
+  const int* pre = kind == 0 ? C.pre_pt : C.pre_ee;
+  int total = pre[W.n_env];
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    int e = find_env(pre, W.n_env, g);
+    long long q = (kind == 0 ? C.pt_off[e] : C.ee_off[e]) + (g - pre[e]);
+    bool act = pair_value_item(W, xw, C, kind, q, e, io.val[kind], io.act[kind],
+                               env_min_s ? env_min_s + e : nullptr);
+    if (act && deriv) {
+      int slot = atomicAdd(io.work_n + kind, 1);
+      io.work[kind][slot] = q;
+      io.work_env[kind][slot] = e;
     }
   }
 }
@@ -677,16 +707,9 @@ __global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int
 // one instantiation per pair kind keeps each kernel's code (and register
 // demand) small: the combined kernel was instruction-cache bound
 template <int kind>
-__global__ void __launch_bounds__(64) k_pair_hess(World W, const double* __restrict__ xw, Cands C, PairIO io) {
-  const long long* work = io.work[kind];
-  const int* work_env = io.work_env[kind];
-  double* g12 = io.g[kind];
-  double* hp = io.h[kind];
-  unsigned char* active = io.act[kind];
-  int total = io.work_n[kind];
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < total; w += gridDim.x * blockDim.x) {
-    long long k = work[w];
-    int e = work_env[w];
+__device__ __forceinline__ void pair_hess_item(const World& W, const double* __restrict__ xw, const Cands& C,
+                                               long long k, int e, double* g12, double* hp,
+                                               unsigned char* active) {
     int2 pr = kind == 0 ? C.pt[k] : C.ee[k];
     int sl[4];
     pair_slots(W, kind, pr, sl);
@@ -729,33 +752,37 @@ __global__ void __launch_bounds__(64) k_pair_hess(World W, const double* __restr
                                    (em * db) * H[i * 12 + j]);
       if (t < 1.0) mask = 0xF;
     }
+#ifndef IPC_NO_PSD
     psd_project_masked12(H, mask);
+#endif
     for (int i = 0; i < 12; ++i) g12[12 * k + i] = gout[i];
     for (int i = 0; i < 12; ++i)
       for (int j = i; j < 12; ++j) hp[PK * k + pk(i, j)] = H[i * 12 + j];
     active[k] = (unsigned char)0xF;
-  }
+}
+
+template <int kind>
+__global__ void __launch_bounds__(64) k_pair_hess(World W, const double* __restrict__ xw, Cands C, PairIO io) {
+  int total = io.work_n[kind];
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < total; w += gridDim.x * blockDim.x)
+    pair_hess_item<kind>(W, xw, C, io.work[kind][w], io.work_env[kind][w], io.g[kind], io.h[kind], io.act[kind]);
 }
 
 // ground candidates (ref contact.py:564): value, y-gradient, clamped y-curvature
-__global__ void k_ground(World W, const double* __restrict__ xw, Cands C, int deriv,
-                         const int* env_flag, double* val, double* gy, double* hyy,
-                         double* env_min_s) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  int e = blockIdx.y;
-  if (k >= C.n_gnd[e]) return;
-  if (env_flag && !env_flag[e]) return;
-  k += C.gnd_off[e];
+// ground candidate k (global index) of env e; min_s: the env's minimum
+__device__ __forceinline__ void ground_item(const World& W, const double* __restrict__ xw, const Cands& C,
+                                            int deriv, int k, int e, double* val, double* gy, double* hyy,
+                                            double* min_s) {
   int s = C.gnd[k];
   double d = xw[3 * s + 1] - W.env_ground_y[e];
   double dhat = W.env_dhat[e], shat = dhat * dhat;
   if (d <= 0.0) {
     val[k] = INFINITY;
-    if (env_min_s) atomic_min_pos(env_min_s + e, 0.0);
+    if (min_s) atomic_min_pos(min_s, 0.0);
     return;
   }
   double ss = d * d;
-  if (env_min_s) atomic_min_pos(env_min_s + e, ss);
+  if (min_s) atomic_min_pos(min_s, ss);
   if (!(ss < shat)) {
     val[k] = 0.0;
     if (deriv) { gy[k] = 0.0; hyy[k] = 0.0; }
@@ -769,6 +796,16 @@ __global__ void k_ground(World W, const double* __restrict__ xw, Cands C, int de
     gy[k] = kappa * db * 2.0 * d;
     hyy[k] = fmax(kappa * (d2b * 4.0 * d * d + db * 2.0), 0.0);
   }
+}
+
+__global__ void k_ground(World W, const double* __restrict__ xw, Cands C, int deriv,
+                         const int* env_flag, double* val, double* gy, double* hyy,
+                         double* env_min_s) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.y;
+  if (k >= C.n_gnd[e]) return;
+  if (env_flag && !env_flag[e]) return;
+  ground_item(W, xw, C, deriv, k + C.gnd_off[e], e, val, gy, hyy, env_min_s ? env_min_s + e : nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -787,11 +824,9 @@ IPC_HD void tangent_basis(V3 n, double* T /*3x2 row-major*/) {
 
 // lag one candidate pair if active and λ > 0; lags are appended per env in
 // candidate order (PT list then EE list) — one CTA per env for ordering.
-__global__ void k_lags(World W, const double* __restrict__ xw, Cands C, Lags L, const int* env_flag) {
+__device__ void lags_env(const World& W, const double* __restrict__ xw, const Cands& C, const Lags& L, int e) {
   __shared__ int warp_tot[BP_THREADS / 32];
   __shared__ int total;
-  int e = blockIdx.x;
-  if (env_flag && !env_flag[e]) return;
   double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
   long long lo = L.off[e];
   int base = 0;
@@ -901,6 +936,12 @@ __global__ void k_lags(World W, const double* __restrict__ xw, Cands C, Lags L, 
   if (threadIdx.x == 0) L.g_n[e] = gbase;
 }
 
+__global__ void k_lags(World W, const double* __restrict__ xw, Cands C, Lags L, const int* env_flag) {
+  int e = blockIdx.x;
+  if (env_flag && !env_flag[e]) return;
+  lags_env(W, xw, C, L, e);
+}
+
 IPC_HD double f0s(double y, double eh) {
   return y < eh ? y * y / eh - y * y * y / (3.0 * eh * eh) + eh / 3.0 : y;
 }
@@ -926,15 +967,9 @@ IPC_HD double smooth_norm(double u0, double u1, double ml, double eh, double* gu
   return v;
 }
 
-__global__ void k_friction(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
-                           Lags L, double h, int deriv, const int* env_flag, double* val,
-                           double* g12, double* hp) {
-  int total = L.pre[W.n_env];
-  for (int gi = blockIdx.x * blockDim.x + threadIdx.x; gi < total; gi += gridDim.x * blockDim.x) {
-  int e = find_env(L.pre, W.n_env, gi);
-  if (env_flag && !env_flag[e]) continue;
-  int k = gi - L.pre[e];
-  long long q = L.off[e] + k;
+__device__ __forceinline__ void friction_item(const World& W, const double* __restrict__ xw,
+                                              const double* __restrict__ xw0, const Lags& L, double h, int deriv,
+                                              long long q, int e, double* val, double* g12, double* hp) {
   int4 s4 = L.slots[q];
   int sl[4] = {s4.x, s4.y, s4.z, s4.w};
   const double* gam = L.gamma + 4 * q;
@@ -948,7 +983,7 @@ __global__ void k_friction(World W, const double* __restrict__ xw, const double*
   double eh = W.env_epsv[e] * h;
   double gu[2], hu[4];
   val[q] = smooth_norm(u0, u1, ml, eh, deriv ? gu : nullptr, hu);
-  if (!deriv) continue;
+  if (!deriv) return;
   double g3[3], h3[9];
   for (int a = 0; a < 3; ++a) {
     g3[a] = T[2 * a] * gu[0] + T[2 * a + 1] * gu[1];
@@ -960,18 +995,23 @@ __global__ void k_friction(World W, const double* __restrict__ xw, const double*
     for (int a = 0; a < 3; ++a) g12[12 * q + 3 * i + a] = gam[i] * g3[a];
   for (int r = 0; r < 12; ++r)
     for (int c = r; c < 12; ++c) hp[PK * q + pk(r, c)] = gam[r / 3] * gam[c / 3] * h3[3 * (r % 3) + c % 3];
+}
+
+__global__ void k_friction(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
+                           Lags L, double h, int deriv, const int* env_flag, double* val,
+                           double* g12, double* hp) {
+  int total = L.pre[W.n_env];
+  for (int gi = blockIdx.x * blockDim.x + threadIdx.x; gi < total; gi += gridDim.x * blockDim.x) {
+    int e = find_env(L.pre, W.n_env, gi);
+    if (env_flag && !env_flag[e]) continue;
+    friction_item(W, xw, xw0, L, h, deriv, L.off[e] + (gi - L.pre[e]), e, val, g12, hp);
   }
 }
 
 // ground friction: tangent frame (x, z)
-__global__ void k_friction_gnd(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
-                               Lags L, double h, int deriv, const int* env_flag, double* val,
-                               double* g3, double* h3) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  int e = blockIdx.y;
-  if (k >= L.g_n[e]) return;
-  if (env_flag && !env_flag[e]) return;
-  int q = W.env_slot[e] + k;
+__device__ __forceinline__ void friction_gnd_item(const World& W, const double* __restrict__ xw,
+                                                  const double* __restrict__ xw0, const Lags& L, double h,
+                                                  int deriv, int q, int e, double* val, double* g3, double* h3) {
   int s = L.g_slot[q];
   double u0 = xw[3 * s] - xw0[3 * s], u1 = xw[3 * s + 2] - xw0[3 * s + 2];
   double ml = W.env_mu[e] * L.g_lam[q];
@@ -983,6 +1023,16 @@ __global__ void k_friction_gnd(World W, const double* __restrict__ xw, const dou
   h3[9 * q + 0] = hu[0]; h3[9 * q + 1] = 0.0; h3[9 * q + 2] = hu[1];
   h3[9 * q + 3] = 0.0; h3[9 * q + 4] = 0.0; h3[9 * q + 5] = 0.0;
   h3[9 * q + 6] = hu[2]; h3[9 * q + 7] = 0.0; h3[9 * q + 8] = hu[3];
+}
+
+__global__ void k_friction_gnd(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
+                               Lags L, double h, int deriv, const int* env_flag, double* val,
+                               double* g3, double* h3) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.y;
+  if (k >= L.g_n[e]) return;
+  if (env_flag && !env_flag[e]) return;
+  friction_gnd_item(W, xw, xw0, L, h, deriv, W.env_slot[e] + k, e, val, g3, h3);
 }
 
 // ---------------------------------------------------------------------------
@@ -1023,6 +1073,32 @@ __device__ double pair_ccd_alpha(int kind, const V3* X, const V3* D, double cons
   return fmin(1.0, fmax(conservative * t, 1e-12));
 }
 
+__device__ __forceinline__ double ccd_pair_item(const World& W, const double* __restrict__ xw,
+                                                const double* __restrict__ dxw, const Cands& C, int kind,
+                                                long long q, double conservative) {
+  int2 pr = kind == 0 ? C.pt[q] : C.ee[q];
+  int sl[4];
+  pair_slots(W, kind, pr, sl);
+  V3 X[4], D[4];
+  for (int i = 0; i < 4; ++i) {
+    X[i] = ld3(xw + 3 * sl[i]);
+    D[i] = ld3(dxw + 3 * sl[i]);
+  }
+  return pair_ccd_alpha(kind, X, D, conservative);
+}
+
+// ground crossing time of ground candidate k (global index) of env e, or 2 (none)
+__device__ __forceinline__ double ccd_ground_item(const World& W, const double* __restrict__ xw,
+                                                  const double* __restrict__ dxw, const Cands& C, int k, int e,
+                                                  double conservative) {
+  int s = C.gnd[k];
+  double y = xw[3 * s + 1], dy = dxw[3 * s + 1];
+  if (!(dy < 0.0)) return 2.0;
+  double t = (y - W.env_ground_y[e]) / -dy;
+  if (!(t <= 1.0)) return 2.0;
+  return fmin(1.0, conservative * t);
+}
+
 __global__ void k_ccd_pairs(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
                             Cands C, double conservative, const int* env_flag, double* env_alpha) {
   const int kind = blockIdx.y;
@@ -1032,15 +1108,7 @@ __global__ void k_ccd_pairs(World W, const double* __restrict__ xw, const double
     int e = find_env(pre, W.n_env, g);
     if (env_flag && !env_flag[e]) continue;
     long long q = (kind == 0 ? C.pt_off[e] : C.ee_off[e]) + (g - pre[e]);
-    int2 pr = kind == 0 ? C.pt[q] : C.ee[q];
-    int sl[4];
-    pair_slots(W, kind, pr, sl);
-    V3 X[4], D[4];
-    for (int i = 0; i < 4; ++i) {
-      X[i] = ld3(xw + 3 * sl[i]);
-      D[i] = ld3(dxw + 3 * sl[i]);
-    }
-    double a = pair_ccd_alpha(kind, X, D, conservative);
+    double a = ccd_pair_item(W, xw, dxw, C, kind, q, conservative);
     if (a < 1.0) atomic_min_pos(env_alpha + e, a);
   }
 }
@@ -1051,12 +1119,8 @@ __global__ void k_ccd_ground(World W, const double* __restrict__ xw, const doubl
   int e = blockIdx.y;
   if (k >= C.n_gnd[e]) return;
   if (env_flag && !env_flag[e]) return;
-  int s = C.gnd[C.gnd_off[e] + k];
-  double y = xw[3 * s + 1], dy = dxw[3 * s + 1];
-  if (!(dy < 0.0)) return;
-  double t = (y - W.env_ground_y[e]) / -dy;
-  if (!(t <= 1.0)) return;
-  atomic_min_pos(env_alpha + e, fmin(1.0, conservative * t));
+  double a = ccd_ground_item(W, xw, dxw, C, C.gnd_off[e] + k, e, conservative);
+  if (a <= 1.0) atomic_min_pos(env_alpha + e, a);
 }
 
 }  // namespace ipc

@@ -41,13 +41,10 @@ struct Terms {
 };
 
 // E(x) per env = ½(x−x̂)ᵀM(x−x̂) [soft part here, affine in body_val] + Σ element values
-__global__ void __launch_bounds__(RED_THREADS) k_env_energy(World W, const double* __restrict__ x,
-                                                             const double* __restrict__ xhat, Terms T,
-                                                             Cands C, Lags L, const int* env_flag,
-                                                             double* out) {
+// block function: env e's energy, valid on thread 0
+__device__ double env_energy_block(const World& W, const double* __restrict__ x, const double* __restrict__ xhat,
+                                   const Terms& T, const Cands& C, const Lags& L, int e) {
   __shared__ double sh[RED_THREADS / 32];
-  int e = blockIdx.x;
-  if (env_flag && !env_flag[e]) return;
   double acc = 0.0;
   int tid = threadIdx.x;
   for (int v = W.env_vert[e] + tid; v < W.env_vert[e + 1]; v += RED_THREADS) {
@@ -66,8 +63,17 @@ __global__ void __launch_bounds__(RED_THREADS) k_env_energy(World W, const doubl
   for (int k = tid; k < C.n_gnd[e]; k += RED_THREADS) acc += T.gnd_val[C.gnd_off[e] + k];
   for (int k = tid; k < L.n[e]; k += RED_THREADS) acc += T.fr_val[L.off[e] + k];
   for (int k = tid; k < L.g_n[e]; k += RED_THREADS) acc += T.frg_val[W.env_slot[e] + k];
-  double s = block_sum(acc, sh);
-  if (tid == 0) out[e] = s;
+  return block_sum(acc, sh);
+}
+
+__global__ void __launch_bounds__(RED_THREADS) k_env_energy(World W, const double* __restrict__ x,
+                                                             const double* __restrict__ xhat, Terms T,
+                                                             Cands C, Lags L, const int* env_flag,
+                                                             double* out) {
+  int e = blockIdx.x;
+  if (env_flag && !env_flag[e]) return;
+  double s = env_energy_block(W, x, xhat, T, C, L, e);
+  if (threadIdx.x == 0) out[e] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -116,16 +122,12 @@ __device__ double body_value(const World& W, int b, int e, const double* q, cons
 
 __device__ __forceinline__ double axpy_rn(double x, double a, double p) { return __dadd_rn(x, __dmul_rn(a, p)); }
 
-__global__ void __launch_bounds__(RED_THREADS) k_ls_value(World W, EnvState S, Cands C, Lags L,
-                                                           const double* __restrict__ x,
-                                                           const double* __restrict__ p,
-                                                           const double* __restrict__ xhat, double h2, double h,
-                                                           double* e_multi) {
-  extern __shared__ double sxw[];
+// block function: E(x + a p) of env e (valid on thread 0); sxw: 3 doubles
+// per env slot of shared scratch
+__device__ double ls_value_block(const World& W, const Cands& C, const Lags& L, const double* __restrict__ x,
+                                 const double* __restrict__ p, const double* __restrict__ xhat, double h2, double h,
+                                 double a, int e, double* sxw) {
   __shared__ double sh[RED_THREADS / 32];
-  int e = blockIdx.x, m = blockIdx.y;
-  if (!S.ls_active[e]) return;
-  double a = S.alpha[e] * ldexp(1.0, -m);
   int tid = threadIdx.x;
   int s0 = W.env_slot[e], s1 = W.env_slot[e + 1];
   for (int s = s0 + tid; s < s1; s += blockDim.x) {
@@ -243,7 +245,21 @@ __global__ void __launch_bounds__(RED_THREADS) k_ls_value(World W, EnvState S, C
     acc += smooth_norm(u0, u1, mu * L.g_lam[q], eh, nullptr, hu);
   }
   double tot = block_sum(acc, sh);
-  if (tid == 0) e_multi[(long long)m * W.n_env + e] = tot;
+  __syncthreads();  // sxw is reused by the caller
+  return tot;
+}
+
+__global__ void __launch_bounds__(RED_THREADS) k_ls_value(World W, EnvState S, Cands C, Lags L,
+                                                           const double* __restrict__ x,
+                                                           const double* __restrict__ p,
+                                                           const double* __restrict__ xhat, double h2, double h,
+                                                           double* e_multi) {
+  extern __shared__ double sxw[];
+  int e = blockIdx.x, m = blockIdx.y;
+  if (!S.ls_active[e]) return;
+  double a = S.alpha[e] * ldexp(1.0, -m);
+  double tot = ls_value_block(W, C, L, x, p, xhat, h2, h, a, e, sxw);
+  if (threadIdx.x == 0) e_multi[(long long)m * W.n_env + e] = tot;
 }
 
 // Derivative buffers of one assembly.
@@ -352,15 +368,12 @@ constexpr int DENSE_THREADS = 256;
 
 // Assemble the env's dense Hessian/gradient, Cholesky-solve H p = −g with the
 // gradient fallback of ref solver.py:241, write p, ‖p‖∞, ‖g‖∞.
-__global__ void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState S, Derivs D, Cands C,
-                                                                Lags L, const double* __restrict__ x,
-                                                                const double* __restrict__ xhat,
-                                                                double* p_out, double* g_out) {
-  extern __shared__ double sm[];
+// block function: assemble + solve env e; sm holds n² + 2n doubles
+__device__ void dense_solve_block(const World& W, const EnvState& S, const Derivs& D, const Cands& C,
+                                  const Lags& L, const double* __restrict__ x, const double* __restrict__ xhat,
+                                  double* p_out, double* g_out, int e, double* sm) {
   __shared__ double red[DENSE_THREADS / 32];
   __shared__ int fail;
-  int e = blockIdx.x;
-  if (!S.newton_active[e]) return;
   int d0 = W.env_dof[e], n = W.env_dof[e + 1] - d0;
   double* H = sm;
   double* g = sm + n * n;
@@ -540,12 +553,20 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState
   if (tid == 0) S.pnorm[e] = pn;
 }
 
+__global__ void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState S, Derivs D, Cands C,
+                                                                Lags L, const double* __restrict__ x,
+                                                                const double* __restrict__ xhat,
+                                                                double* p_out, double* g_out) {
+  extern __shared__ double sm[];
+  int e = blockIdx.x;
+  if (!S.newton_active[e]) return;
+  dense_solve_block(W, S, D, C, L, x, xhat, p_out, g_out, e, sm);
+}
+
 // ---------------------------------------------------------------------------
 // bookkeeping kernels (one thread per env)
 // ---------------------------------------------------------------------------
-__global__ void k_newton_begin(int n_env, EnvState S, const int* flag) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n_env) return;
+__device__ __forceinline__ void newton_begin_env(const EnvState& S, const int* flag, int e) {
   int on = flag[e] ? 1 : 0;
   S.newton_active[e] = on;
   if (on) {
@@ -553,12 +574,15 @@ __global__ void k_newton_begin(int n_env, EnvState S, const int* flag) {
     S.prev_pnorm[e] = INFINITY;
   }
 }
+__global__ void k_newton_begin(int n_env, EnvState S, const int* flag) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n_env) newton_begin_env(S, flag, e);
+}
 
 // two-consecutive-small-steps rule of ref solver.py:326-332
-__global__ void k_newton_check(int n_env, EnvState S, double h, double tol) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n_env || !S.newton_active[e]) {
-    if (e < n_env) S.ls_active[e] = 0;
+__device__ __forceinline__ void newton_check_env(const EnvState& S, double h, double tol, int e) {
+  if (!S.newton_active[e]) {
+    S.ls_active[e] = 0;
     return;
   }
   S.newton_iters[e] += 1;
@@ -576,10 +600,13 @@ __global__ void k_newton_check(int n_env, EnvState S, double h, double tol) {
   S.ls_active[e] = 1;
   S.alpha_max[e] = 1.0;
 }
-
-__global__ void k_ls_begin(int n_env, EnvState S, int* ls_count) {
+__global__ void k_newton_check(int n_env, EnvState S, double h, double tol) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n_env || !S.ls_active[e]) return;
+  if (e < n_env) newton_check_env(S, h, tol, e);
+}
+
+__device__ __forceinline__ void ls_begin_env(const EnvState& S, int* ls_count, int e) {
+  if (!S.ls_active[e]) return;
   S.ccd_calls[e] += 1;
   S.alpha[e] = S.alpha_max[e];
   ls_count[e] = 0;
@@ -590,11 +617,14 @@ __global__ void k_ls_begin(int n_env, EnvState S, int* ls_count) {
     S.newton_active[e] = 0;
   }
 }
+__global__ void k_ls_begin(int n_env, EnvState S, int* ls_count) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n_env) ls_begin_env(S, ls_count, e);
+}
 
 // Armijo with c = 0 (ref solver.py:257); accepted envs copy xt -> x
-__global__ void k_ls_check(World W, EnvState S, int* ls_count, int max_halvings, int* accepted) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= W.n_env) return;
+__device__ __forceinline__ void ls_check_env(const EnvState& S, int* ls_count, int max_halvings, int* accepted,
+                                             int e) {
   accepted[e] = 0;
   if (!S.ls_active[e]) return;
   if (S.e_new[e] <= S.e0[e]) {
@@ -612,6 +642,10 @@ __global__ void k_ls_check(World W, EnvState S, int* ls_count, int max_halvings,
     S.converged[e] = 0;
     S.newton_active[e] = 0;
   }
+}
+__global__ void k_ls_check(World W, EnvState S, int* ls_count, int max_halvings, int* accepted) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < W.n_env) ls_check_env(S, ls_count, max_halvings, accepted, e);
 }
 
 // speculative backtracking: trials m = 0..M-1 evaluated E(x + α 2^-m p) into
@@ -659,9 +693,8 @@ __global__ void k_copy_env(World W, const double* src, double* dst, const int* f
 }
 
 // multiplier update after each inner solve (ref constraints.py:215, solver.py:414-434)
-__global__ void k_al_update(World W, EnvState S, int outer) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= W.n_env || !S.al_active[e]) return;
+__device__ __forceinline__ void al_update_env(const World& W, const EnvState& S, int outer, int e) {
+  if (!S.al_active[e]) return;
   double res = 0.0;
   for (int k = W.env_cons[e]; k < W.env_cons[e + 1]; ++k) {
     int o = W.aff_dof[W.cons_aff[k]];
@@ -682,6 +715,10 @@ __global__ void k_al_update(World W, EnvState S, int outer) {
   S.al_outer[e] = max(S.al_outer[e], outer + 1);
   bool has = W.env_cons[e + 1] > W.env_cons[e];
   if (!has || res <= 1e-6 || S.ls_failed[e]) S.al_active[e] = 0;
+}
+__global__ void k_al_update(World W, EnvState S, int outer) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < W.n_env) al_update_env(W, S, outer, e);
 }
 
 __global__ void k_cons_reset(World W, const double* targets) {
@@ -726,13 +763,15 @@ __global__ void k_finalize(World W, double h, const int* ok) {
 }
 
 // post-step: min distance + κ doubling (ref barrier.py:85, solver.py:440-450)
-__global__ void k_kappa_adapt(World W, EnvState S, const int* ok) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= W.n_env || !ok[e]) return;
+__device__ __forceinline__ void kappa_adapt_env(const World& W, const EnvState& S, int e) {
   double md = isinf(S.min_s[e]) ? INFINITY : sqrt(S.min_s[e]);
   S.min_s[e] = md;  // now a distance
   double k = W.env_kappa[e], k0 = W.env_kappa0[e], dhat = W.env_dhat[e];
   if (md < 1e-4 * dhat && k < 1e8 * k0) W.env_kappa[e] = fmin(2.0 * k, 1e8 * k0);
+}
+__global__ void k_kappa_adapt(World W, EnvState S, const int* ok) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < W.n_env && ok[e]) kappa_adapt_env(W, S, e);
 }
 
 __global__ void k_fill(int n, double* a, double v) {

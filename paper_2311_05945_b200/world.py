@@ -315,6 +315,15 @@ class GpuWorld:
         return {"newton_iters": int(out[0]), "ls_rounds": int(out[1]), "syncs": int(out[2]),
                 "pcg_iters": int(out[3])}
 
+    FUSED_PHASES = ("world", "broad_dcd", "terms", "energy", "dense", "ccd_prep", "broad_ccd", "ccd",
+                    "line_search", "other")
+
+    def fused_timers(self):
+        """SM cycles per phase of the fused step (zeros unless built with -DIPC_FUSED_TIMERS)."""
+        out = np.zeros(len(self.FUSED_PHASES), np.int64)
+        N.check(self.lib.ipc_world_fused_timers(self.handle, N.ptr(out, N._i64p), len(out)))
+        return dict(zip(self.FUSED_PHASES, (int(v) for v in out)))
+
     def flush_l2(self, nbytes=256 << 20):
         N.check(self.lib.ipc_world_flush_l2(self.handle, int(nbytes)))
 
