@@ -144,6 +144,12 @@ int ipc_world_flush_l2(ipc_world *w, int64_t bytes);
 /* Cumulative host-loop counters: batched Newton iterations, line-search
  * rounds, host synchronisations, sparse-path PCG iterations (out: 4). */
 int ipc_world_stats(ipc_world *w, int64_t *out);
+/* Select the step schedule of a dense world: 1 = fused per-environment step
+ * (one CTA runs a whole env step), 0 = batched launch sequence (default),
+ * which hands the Newton loops of the last few active envs to per-env CTAs.
+ * All schedules compute the same step; worlds whose env systems exceed
+ * shared memory always use the batched sequence. */
+int ipc_world_set_fused(ipc_world *w, int on);
 /* Per-phase SM-cycle totals of the fused per-environment step (world, DCD
  * broad phase, terms, energy, dense solve, CCD prep, CCD broad phase, CCD,
  * line search, other); zeros unless built with -DIPC_FUSED_TIMERS. */

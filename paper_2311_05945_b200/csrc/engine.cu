@@ -128,6 +128,7 @@ static inline void prof_end(int kid, cudaStream_t s) {
   do {                                                        \
     prof_begin((kid), (stream));                              \
     kern<<<grid, block, smem, stream>>>(__VA_ARGS__);         \
+    CK(cudaPeekAtLastError());                                \
     prof_end((kid), (stream));                                \
   } while (0)
 
@@ -601,8 +602,7 @@ struct ipc_world {
     if (sparse) {
       sparse_solve(cfg);
     } else {
-      size_t smem = (size_t)(max_env_dof * max_env_dof + 2 * max_env_dof) * sizeof(double);
-      IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, smem, W, S, D_with(pb_dcd), dcd.c, L, W.x,
+      IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, dense_smem, W, S, D_with(pb_dcd), dcd.c, L, W.x,
                  W.xhat, W.p, W.grad);
     }
     IPC_LAUNCH(K_MISC, st, k_newton_check, nblk(n_env, 128), 128, 0, n_env, S, cfg.h, cfg.newton_tol);
@@ -780,26 +780,35 @@ struct ipc_world {
         s = status();
       }
       if (s.newton == 0) break;
+      // few envs left: finish their Newton loops in per-env CTAs
+      if (graphs && tail_envs > 0 && s.newton <= tail_envs && it + 1 < cfg.max_newton_iters && fused_setup()) {
+        CK(cudaMemsetAsync(fq, 0, sizeof(int), st));
+        FusedArgs A = fused_args(cfg);
+        IPC_LAUNCH(K_FUSED, st, k_env_newton_rest, std::min(s.newton, fused_blocks), 256, fused_smem, A, it + 1);
+        status();
+        break;
+      }
     }
     // envs still active after the iteration cap did not converge
     IPC_LAUNCH(K_MISC, st, k_mark_unconverged, nblk(n_env, 128), 128, 0, n_env, S);
   }
 
   // ---------------- fused per-env step (dense worlds) ----------------
-  bool fused_on = true;     // IPC_FUSED=0 selects the batched launch sequence
+  bool fused_on = false;    // IPC_FUSED=1: whole step in the fused per-env kernel
+  int tail_envs = 148;      // batched schedule: hand off to per-env CTAs at <= this many active envs
   int fused_max_dof = 128;  // dense LDLᵀ in shared memory: n² doubles
   int* fq = nullptr;
   long long* d_fstat = nullptr;
   double *v_save = nullptr, *kappa_save = nullptr;
   int fused_blocks = 0;
   size_t fused_smem = 0;
+  size_t dense_smem = 0;
+  int max_env_prims = 0;  // max over envs of slots + tris + edges + chunks
+  int max_env_groups = 0;  // max over envs of soft vertices + affine bodies
   bool use_fused() const { return fused_on && !sparse && max_env_dof <= fused_max_dof; }
 
-  void step_fused(const ipc_step_config& cfg) {
-    if (lags_stale) {
-      alloc_lags();
-      lags_stale = false;
-    }
+  // shared setup of the fused kernels; false when the env systems do not fit
+  bool fused_setup() {
     if (!fq) {
       fq = pool.alloc<int>(1);
       d_fstat = pool.alloc<long long>(2 + FT_N);
@@ -807,16 +816,32 @@ struct ipc_world {
       kappa_save = pool.alloc<double>(n_env);
     }
     if (!fused_blocks) {
-      fused_smem = sizeof(double) * (size_t)std::max(max_env_dof * max_env_dof + 2 * max_env_dof, 3 * max_slots);
+      // time-shared scratch: dense system, line-search positions, staged
+      // broad-phase boxes (6 doubles per slot / primitive / chunk)
+      size_t need = std::max(max_env_dof * max_env_dof + 2 * max_env_dof, 3 * max_slots);
+      need = std::max(need, (size_t)6 * max_env_prims);
+      int dev = 0, optin = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      cudaFuncAttributes fa;
+      CK(cudaFuncGetAttributes(&fa, k_env_step));
+      size_t avail = (size_t)optin - fa.sharedSizeBytes;
+      size_t base = sizeof(double) * (size_t)(max_env_dof * max_env_dof + 2 * max_env_dof);
+      fused_smem = std::min(avail, sizeof(double) * need);
+      if (fused_smem < base) {  // cannot hold the dense system: batched path
+        fused_on = false;
+        return false;
+      }
       CK(cudaFuncSetAttribute(k_env_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_env_step, 256, fused_smem));
       fused_blocks = std::max(1, std::min(n_env, std::max(per_sm, 1) * n_sm));
+      CK(cudaFuncSetAttribute(k_env_newton_rest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
     }
-    // the step commits v and κ in place: keep copies for an overflow replay
-    CK(cudaMemcpyAsync(v_save, W.v, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(kappa_save, W.env_kappa, sizeof(double) * n_env, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemsetAsync(fq, 0, sizeof(int), st));
+    return true;
+  }
+
+  FusedArgs fused_args(const ipc_step_config& cfg) {
     FusedArgs A{};
     A.W = W;
     A.S = S;
@@ -843,6 +868,21 @@ struct ipc_world {
     A.max_halvings = cfg.max_line_search_halvings;
     A.fp_iters = std::max(cfg.friction_fixed_point_iters, 1);
     A.al_max_outer = cfg.al_max_outer;
+    A.smem_doubles = (int)(fused_smem / sizeof(double));
+    return A;
+  }
+
+  bool step_fused(const ipc_step_config& cfg) {
+    if (lags_stale) {
+      alloc_lags();
+      lags_stale = false;
+    }
+    if (!fused_setup()) return false;
+    // the step commits v and κ in place: keep copies for an overflow replay
+    CK(cudaMemcpyAsync(v_save, W.v, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(kappa_save, W.env_kappa, sizeof(double) * n_env, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(fq, 0, sizeof(int), st));
+    FusedArgs A = fused_args(cfg);
     IPC_LAUNCH(K_FUSED, st, k_env_step, fused_blocks, 256, fused_smem, A);
     CK(cudaMemcpyAsync(h_status, dcd.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_status + 1, sweep.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -853,6 +893,7 @@ struct ipc_world {
       CK(cudaMemcpyAsync(W.env_kappa, kappa_save, sizeof(double) * n_env, cudaMemcpyDeviceToDevice, st));
       throw OverflowRetry();
     }
+    return true;
   }
 
   // ---------------- sparse path (large environments) ----------------
@@ -1202,7 +1243,10 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
         mx = std::max(mx, rows * nb);
       }
       const char* fz = getenv("IPC_FUSED");
-      if (fz && fz[0] == '0') w->fused_on = false;
+      if (fz) w->fused_on = fz[0] == '1';
+      w->tail_envs = w->n_sm;
+      const char* tz = getenv("IPC_TAIL");
+      if (tz) w->tail_envs = atoi(tz);
       const char* ez = getenv("IPC_BROAD_ITEMS");
       long long per = ez ? std::max(64LL, atoll(ez)) : ipc_world::BROAD_ITEMS;
       w->bp_z = (int)std::min(64LL, std::max(1LL, (mx + per - 1) / per));
@@ -1210,14 +1254,31 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     }
     for (int e = 0; e < ne; ++e) {
       w->max_env_dof = std::max(w->max_env_dof, d->env_dof[e + 1] - d->env_dof[e]);
+      {
+        int nt = d->env_tri[e + 1] - d->env_tri[e], nE = d->env_edge[e + 1] - d->env_edge[e];
+        int nbod = d->env_cbody[e + 1] - d->env_cbody[e];
+        int chunks_ub = (nt + nE) / 32 + 2 * nbod + 2;
+        w->max_env_prims = std::max(w->max_env_prims, d->env_slot[e + 1] - d->env_slot[e] + nt + nE + chunks_ub);
+        w->max_env_groups = std::max(w->max_env_groups, d->env_vert[e + 1] - d->env_vert[e] + d->env_aff[e + 1] - d->env_aff[e]);
+      }
       if (d->env_cbody[e + 1] - d->env_cbody[e] > 64)
         throw std::runtime_error("more than 64 collision bodies in one environment");
     }
     const int DENSE_MAX = 160;
     w->sparse = w->max_env_dof > DENSE_MAX;
     if (!w->sparse) {
-      size_t smem = (size_t)(w->max_env_dof * w->max_env_dof + 2 * w->max_env_dof) * sizeof(double);
-      CK(cudaFuncSetAttribute(k_dense_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      // dense system n² + 2n, plus the slot lever arms of the parallel
+      // assembly when they fit next to the kernel's static shared memory
+      int optin = 0, cur = 0;
+      CK(cudaGetDevice(&cur));
+      CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cur));
+      cudaFuncAttributes fa;
+      CK(cudaFuncGetAttributes(&fa, k_dense_solve));
+      size_t avail = (size_t)optin - fa.sharedSizeBytes;
+      size_t base = (size_t)(w->max_env_dof * w->max_env_dof + 2 * w->max_env_dof) * sizeof(double);
+      if (base > avail) throw std::runtime_error("dense environment system exceeds shared memory");
+      w->dense_smem = base;
+      CK(cudaFuncSetAttribute(k_dense_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->dense_smem));
     } else {
       w->setup_sparse(d);
     }
@@ -1330,9 +1391,7 @@ static void step_core(ipc_world* w, const ipc_step_config* cfg, const double* ta
     } else {
       IPC_LAUNCH(K_MISC, st, k_fill_int, nblk(ne, 128), 128, 0, ne, w->enable, 1);
     }
-    if (w->use_fused()) {
-      w->step_fused(*cfg);
-    } else {
+    if (!(w->use_fused() && w->step_fused(*cfg))) {
     IPC_LAUNCH(K_MISC, st, k_copy_int, nblk(ne, 128), 128, 0, ne, w->enable, w->ok);
     w->broad(w->dcd, w->pb_dcd, true, W.xw0, W.xw0, w->ok);
     // feasibility of the incoming state (ref solver.py:372-385)
@@ -1485,6 +1544,13 @@ int ipc_world_stats(ipc_world* w, int64_t* out) {
       out[0] += fs[0];
       out[1] += fs[1];
     }
+  })
+}
+
+int ipc_world_set_fused(ipc_world* w, int on) {
+  GUARD({
+    w->fused_on = on != 0;
+    w->fused_blocks = 0;
   })
 }
 

@@ -53,6 +53,7 @@ struct FusedArgs {
   long long* timers; // [FT_N] (IPC_FUSED_TIMERS builds)
   double h, newton_tol, ccd_cons;
   int max_newton, max_halvings, fp_iters, al_max_outer;
+  int smem_doubles;  // dynamic shared memory per CTA (time-shared scratch)
 };
 
 __device__ __noinline__ void fused_pair_hess0(const World& W, const double* xw, const Cands& C, long long q, int e,
@@ -96,37 +97,288 @@ __device__ bool env_broad(const World& W, const double* lo, const double* hi, co
   return !s_ov;
 }
 
+// Broad phase of env e with every box staged in shared memory (buf, cap
+// doubles): slot boxes, triangle / edge boxes, 32-primitive chunk boxes, body
+// boxes. Same tests, same box arithmetic and the same (row, primitive)
+// output order as broad_env; the global-memory version runs when the env's
+// boxes do not fit. Returns false on capacity overflow.
+__device__ bool env_broad_sm(const World& W, const double* __restrict__ lo, const double* __restrict__ hi,
+                             const Cands& C, int e, double* buf, int cap_d) {
+  __shared__ double blo[3 * MAX_BODIES], bhi[3 * MAX_BODIES];
+  __shared__ int surv[BP_WIN], soff[BP_WIN];
+  __shared__ int wtot[BP_THREADS / 32];
+  __shared__ int s_ov, s_total;
+  int s0 = W.env_slot[e], s1 = W.env_slot[e + 1], ns = s1 - s0;
+  int t0 = W.env_tri[e], nt = W.env_tri[e + 1] - t0;
+  int e0 = W.env_edge[e], ne = W.env_edge[e + 1] - e0;
+  int cb0 = W.env_cbody[e], nb = W.env_cbody[e + 1] - cb0;
+  int tc0 = W.cbody_tchunk[cb0], ntc = W.cbody_tchunk[cb0 + nb] - tc0;
+  int ec0 = W.cbody_echunk[cb0], nec = W.cbody_echunk[cb0 + nb] - ec0;
+  if (6 * (ns + nt + ne + ntc + nec) > cap_d) return env_broad(W, lo, hi, C, e);
+  double* sb = buf;            // slot boxes (lo xyz, hi xyz)
+  double* tb = sb + 6 * ns;    // triangle boxes
+  double* eb = tb + 6 * nt;    // edge boxes
+  double* tcb = eb + 6 * ne;   // triangle chunk boxes
+  double* ecb = tcb + 6 * ntc; // edge chunk boxes
+  int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int i = tid; i < 3 * ns; i += blockDim.x) {
+    int s = i / 3, c = i - 3 * s;
+    sb[6 * s + c] = lo[3 * (s0 + s) + c];
+    sb[6 * s + 3 + c] = hi[3 * (s0 + s) + c];
+  }
+  __syncthreads();
+  for (int t = tid; t < nt; t += blockDim.x) {
+    int3 v = W.tri_v[t0 + t];
+    const double *a = sb + 6 * (v.x - s0), *b = sb + 6 * (v.y - s0), *c = sb + 6 * (v.z - s0);
+    for (int k = 0; k < 3; ++k) {
+      tb[6 * t + k] = fmin(fmin(a[k], b[k]), c[k]);
+      tb[6 * t + 3 + k] = fmax(fmax(a[3 + k], b[3 + k]), c[3 + k]);
+    }
+  }
+  for (int t = tid; t < ne; t += blockDim.x) {
+    int2 v = W.edge_v[e0 + t];
+    const double *a = sb + 6 * (v.x - s0), *b = sb + 6 * (v.y - s0);
+    for (int k = 0; k < 3; ++k) {
+      eb[6 * t + k] = fmin(a[k], b[k]);
+      eb[6 * t + 3 + k] = fmax(a[3 + k], b[3 + k]);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < ntc + nec; i += blockDim.x) {
+    bool tri = i < ntc;
+    int ch = tri ? tc0 + i : ec0 + (i - ntc);
+    const int* cp0 = tri ? W.tchunk_p0 : W.echunk_p0;
+    const double* pb = tri ? tb - 6 * t0 : eb - 6 * e0;  // indexed by global primitive id below
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int q = cp0[ch]; q < cp0[ch + 1]; ++q)
+      for (int k = 0; k < 3; ++k) {
+        mn[k] = fmin(mn[k], pb[6 * q + k]);
+        mx[k] = fmax(mx[k], pb[6 * q + 3 + k]);
+      }
+    double* o = (tri ? tcb : ecb) + 6 * (tri ? i : i - ntc);
+    for (int k = 0; k < 3; ++k) {
+      o[k] = mn[k];
+      o[3 + k] = mx[k];
+    }
+  }
+  for (int B = wid; B < nb; B += BP_THREADS / 32) {  // body boxes, one warp per body
+    int a0 = W.cbody_slot[cb0 + B] - s0, a1 = W.cbody_slot[cb0 + B + 1] - s0;
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int v = a0 + lane; v < a1; v += 32)
+      for (int c = 0; c < 3; ++c) {
+        mn[c] = fmin(mn[c], sb[6 * v + c]);
+        mx[c] = fmax(mx[c], sb[6 * v + 3 + c]);
+      }
+    for (int o = 16; o > 0; o >>= 1)
+      for (int c = 0; c < 3; ++c) {
+        mn[c] = fmin(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+        mx[c] = fmax(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+      }
+    if (lane == 0)
+      for (int c = 0; c < 3; ++c) {
+        blo[3 * B + c] = mn[c];
+        bhi[3 * B + c] = mx[c];
+      }
+  }
+  __syncthreads();
+  double margin = W.env_dhat[e];
+  // ground candidates (kind 2)
+  if (!W.env_has_ground[e]) {
+    if (tid == 0) C.n_gnd[e] = 0;
+  } else {
+    double lim = __dadd_rn(W.env_ground_y[e], margin);
+    int off = C.gnd_off[e], base = 0;
+    for (int v0 = 0; v0 < ns; v0 += BP_THREADS) {
+      int v = v0 + tid;
+      bool hit = v < ns && sb[6 * v + 1] < lim && !W.cbody_kin[W.slot_cbody[s0 + v]];
+      int o = block_ordered_offset<BP_THREADS>(hit, wtot, &s_total);
+      if (hit) C.gnd[off + base + o] = s0 + v;
+      base += s_total;
+      __syncthreads();
+    }
+    if (tid == 0) C.n_gnd[e] = base;
+  }
+  for (int kind = 0; kind < 2; ++kind) {
+    if (!W.env_pairs[e]) {
+      if (tid == 0) {
+        if (kind == 0) C.n_pt[e] = 0; else C.n_ee[e] = 0;
+      }
+      continue;
+    }
+    int r0 = kind == 0 ? s0 : e0, nrow = kind == 0 ? ns : ne;
+    long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
+    long long cap = (kind == 0 ? C.pt_off[e + 1] : C.ee_off[e + 1]) - off;
+    int n_items = nrow * nb;
+    // query box of row r (local index): slot box or edge box
+    const double* qb = kind == 0 ? sb : eb;
+    const int* cp0 = kind == 0 ? W.tchunk_p0 : W.echunk_p0;
+    const int* cbc = kind == 0 ? W.cbody_tchunk : W.cbody_echunk;
+    const double* chb = kind == 0 ? tcb : ecb;
+    int chbase = kind == 0 ? tc0 : ec0;
+    const double* pbx = kind == 0 ? tb : eb;
+    int pbase = kind == 0 ? t0 : e0;
+    auto range = [&](int it, int& row, int& B, int& c0, int& c1) {
+      row = it / nb;
+      B = it - row * nb;
+      if (kind == 0) {
+        c0 = W.cbody_tri[cb0 + B];
+        c1 = W.cbody_tri[cb0 + B + 1];
+      } else {
+        c0 = max(W.cbody_edge[cb0 + B], r0 + row + 1);
+        c1 = W.cbody_edge[cb0 + B + 1];
+      }
+    };
+    // visit the hits of item (row, B) in primitive order
+    auto visit = [&](int row, int B, int c0, int c1, auto f) {
+      const double* q = qb + 6 * row;
+      int grow = r0 + row;
+      int2 er = kind == 1 ? W.edge_v[grow] : make_int2(0, 0);
+      for (int ch = cbc[cb0 + B]; ch < cbc[cb0 + B + 1]; ++ch) {
+        int p0 = max(cp0[ch], c0), p1 = min(cp0[ch + 1], c1);
+        if (p0 >= p1) continue;
+        const double* cb = chb + 6 * (ch - chbase);
+        if (!box_hit(q, q + 3, cb, cb + 3, margin)) continue;
+        for (int t = p0; t < p1; ++t) {
+          const double* pb = pbx + 6 * (t - pbase);
+          if (!box_hit(q, q + 3, pb, pb + 3, margin)) continue;
+          if (kind == 0) {
+            int3 tv = W.tri_v[t];
+            if (tv.x == grow || tv.y == grow || tv.z == grow) continue;
+          } else {
+            int2 ej = W.edge_v[t];
+            if (er.x == ej.x || er.x == ej.y || er.y == ej.x || er.y == ej.y) continue;
+          }
+          f(t);
+        }
+      }
+    };
+    constexpr int SEG = BP_WIN / (BP_THREADS / 32);
+    long long base = 0;
+    for (int win = 0; win < n_items; win += BP_WIN) {
+      int nsv = 0;
+      int seg0 = win + wid * SEG;
+      for (int j = 0; j < SEG; j += 32) {
+        int it = seg0 + j + lane;
+        bool live = false;
+        if (it < n_items) {
+          int row, B, c0, c1;
+          range(it, row, B, c0, c1);
+          int rb = kind == 0 ? W.slot_cbody[r0 + row] : W.edge_cbody[r0 + row];
+          const double* q = qb + 6 * row;
+          live = c0 < c1 && !cull_item(W, cb0, rb, B, q, q + 3, blo, bhi, margin);
+        }
+        unsigned m = __ballot_sync(0xffffffffu, live);
+        if (live) surv[wid * SEG + nsv + __popc(m & ((1u << lane) - 1u))] = it - win;
+        nsv += __popc(m);
+      }
+      __syncwarp();
+      int run = 0;
+      for (int j0 = 0; j0 < nsv; j0 += 32) {
+        int j = j0 + lane, n_hit = 0;
+        if (j < nsv) {
+          int row, B, c0, c1;
+          range(win + surv[wid * SEG + j], row, B, c0, c1);
+          visit(row, B, c0, c1, [&](int) { ++n_hit; });
+        }
+        int incl = n_hit;
+        for (int o = 1; o < 32; o <<= 1) {
+          int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        if (j < nsv) soff[wid * SEG + j] = run + incl - n_hit;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) wtot[wid] = run;
+      __syncthreads();
+      long long wbase = base, wsum = 0;
+      for (int w = 0; w < BP_THREADS / 32; ++w) {
+        if (w < wid) wbase += wtot[w];
+        wsum += wtot[w];
+      }
+      for (int j = lane; j < nsv; j += 32) {
+        int row, B, c0, c1;
+        range(win + surv[wid * SEG + j], row, B, c0, c1);
+        long long dst = wbase + soff[wid * SEG + j];
+        int grow = r0 + row;
+        visit(row, B, c0, c1, [&](int t) {
+          if (dst < cap) {
+            if (kind == 0) C.pt[off + dst] = make_int2(grow, t);
+            else C.ee[off + dst] = make_int2(grow, t);
+          }
+          ++dst;
+        });
+      }
+      base += wsum;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      if (base > cap) {
+        atomicExch(C.overflow, 1);
+        base = cap;
+      }
+      if (kind == 0) C.n_pt[e] = (int)base; else C.n_ee[e] = (int)base;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) s_ov = *(volatile int*)C.overflow;
+  __syncthreads();
+  return !s_ov;
+}
+
 // element values (deriv = 0) or values + derivatives of every term at x / xw;
-// returns the env's minimum squared distance over candidates and ground
+// returns the env's minimum squared distance over candidates and ground.
+// Derivative pass: one value sweep over all candidates (PT and EE together)
+// appends the active pairs to a shared work list, then bodies, tets and the
+// active pairs are spread over the block in one round, so the latency is one
+// pair Hessian rather than one per kind.
+constexpr int FUSED_WORK = 1024;
 __device__ double env_terms(const FusedArgs& A, const double* x, const double* xw, int deriv, int e) {
   const World& W = A.W;
   __shared__ double s_min;
-  if (threadIdx.x == 0) s_min = INFINITY;
+  __shared__ int s_nw;
+  __shared__ int s_work[FUSED_WORK];  // kind << 30 | local candidate index
+  if (threadIdx.x == 0) {
+    s_min = INFINITY;
+    s_nw = 0;
+  }
   __syncthreads();
   double h2 = A.h * A.h;
-  if (deriv) {
-    for (int b = W.env_aff[e] + threadIdx.x; b < W.env_aff[e + 1]; b += blockDim.x)
-      fused_body(W, x, W.xhat, h2, 1, b, A.T.body_val, A.D.body_g, A.D.body_h);
-    for (int t = W.env_tet[e] + threadIdx.x; t < W.env_tet[e + 1]; t += blockDim.x)
-      fused_tet(W, x, h2, 1, t, A.T.tet_val, A.D.tet_g, A.D.tet_h);
-  }
   const Cands& C = A.dc;
-  for (int kind = 0; kind < 2; ++kind) {
-    int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
-    long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
-    double* val = kind == 0 ? A.T.pt_val : A.T.ee_val;
-    unsigned char* act = kind == 0 ? A.D.pt_act : A.D.ee_act;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-      bool on = pair_value_item(W, xw, C, kind, off + k, e, val, act, &s_min);
-      if (on && deriv) {
-        if (kind == 0) fused_pair_hess0(W, xw, C, off + k, e, A.D);
-        else fused_pair_hess1(W, xw, C, off + k, e, A.D);
-      }
+  int n_pt = C.n_pt[e], n_ee = C.n_ee[e];
+  long long pt_off = C.pt_off[e], ee_off = C.ee_off[e];
+  for (int k = threadIdx.x; k < n_pt + n_ee; k += blockDim.x) {
+    int kind = k < n_pt ? 0 : 1;
+    int j = kind == 0 ? k : k - n_pt;
+    long long q = (kind == 0 ? pt_off : ee_off) + j;
+    bool on = pair_value_item(W, xw, C, kind, q, e, kind == 0 ? A.T.pt_val : A.T.ee_val,
+                              kind == 0 ? A.D.pt_act : A.D.ee_act, &s_min);
+    if (on && deriv) {
+      int slot = atomicAdd(&s_nw, 1);
+      if (slot < FUSED_WORK) s_work[slot] = (kind << 30) | j;
+      else if (kind == 0) fused_pair_hess0(W, xw, C, q, e, A.D);
+      else fused_pair_hess1(W, xw, C, q, e, A.D);
     }
   }
   for (int k = threadIdx.x; k < C.n_gnd[e]; k += blockDim.x)
     ground_item(W, xw, C, deriv, C.gnd_off[e] + k, e, A.T.gnd_val, A.D.gnd_gy, A.D.gnd_hyy, &s_min);
   if (deriv) {
+    __syncthreads();
+    int nw = min(s_nw, FUSED_WORK);
+    int b0 = W.env_aff[e], nbody = W.env_aff[e + 1] - b0;
+    int t0 = W.env_tet[e], ntet = W.env_tet[e + 1] - t0;
+    int total = nbody + ntet + nw;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      if (i < nbody) {
+        fused_body(W, x, W.xhat, h2, 1, b0 + i, A.T.body_val, A.D.body_g, A.D.body_h);
+      } else if (i < nbody + ntet) {
+        fused_tet(W, x, h2, 1, t0 + (i - nbody), A.T.tet_val, A.D.tet_g, A.D.tet_h);
+      } else {
+        int w = s_work[i - nbody - ntet];
+        int kind = w >> 30, j = w & ((1 << 30) - 1);
+        if (kind == 0) fused_pair_hess0(W, xw, C, pt_off + j, e, A.D);
+        else fused_pair_hess1(W, xw, C, ee_off + j, e, A.D);
+      }
+    }
     const Lags& L = A.L;
     for (int k = threadIdx.x; k < L.n[e]; k += blockDim.x)
       friction_item(W, xw, W.xw0, L, A.h, 1, L.off[e] + k, e, A.T.fr_val, A.D.fr_g, A.D.fr_h);
@@ -157,22 +409,23 @@ __device__ __forceinline__ int env_flag_read(const int* f, int e) {
   return s_f;
 }
 
-// Newton loop of one env (ref solver.py:295-352); false on overflow
-__device__ bool env_newton(const FusedArgs& A, int e, double* sm) {
+// Newton loop of one env (ref solver.py:295-352) from iteration it0 (begin:
+// fresh loop state); false on overflow
+__device__ bool env_newton(const FusedArgs& A, int e, double* sm, bool begin = true, int it0 = 0) {
   const World& W = A.W;
   const EnvState& S = A.S;
   __shared__ double s_amin;
   int d0 = W.env_dof[e], d1 = W.env_dof[e + 1];
   int s0 = W.env_slot[e], s1 = W.env_slot[e + 1];
-  if (threadIdx.x == 0) newton_begin_env(S, S.al_active, e);
+  if (threadIdx.x == 0 && begin) newton_begin_env(S, S.al_active, e);
   FT_START;
-  for (int it = 0; it < A.max_newton; ++it) {
+  for (int it = it0; it < A.max_newton; ++it) {
     if (!env_flag_read(S.newton_active, e)) break;
     // head: DCD candidates at x, derivatives, E0, Newton direction
     FT_MARK(A, FT_OTHER);
     env_world(W, W.x, W.xw, e);
     FT_MARK(A, FT_WORLD);
-    if (!env_broad(W, W.xw, W.xw, A.dc, e)) return false;
+    if (!env_broad_sm(W, W.xw, W.xw, A.dc, e, sm, A.smem_doubles)) return false;
     FT_MARK(A, FT_BROAD_DCD);
     double ms = env_terms(A, W.x, W.xw, 1, e);
     FT_MARK(A, FT_TERMS);
@@ -201,7 +454,7 @@ __device__ bool env_newton(const FusedArgs& A, int e, double* sm) {
       A.xhi[i] = fmax(a, b);
     }
     FT_MARK(A, FT_CCD_PREP);
-    if (!env_broad(W, A.xlo, A.xhi, A.sw, e)) return false;
+    if (!env_broad_sm(W, A.xlo, A.xhi, A.sw, e, sm, A.smem_doubles)) return false;
     FT_MARK(A, FT_BROAD_CCD);
     if (threadIdx.x == 0) s_amin = 1.0;
     __syncthreads();
@@ -267,7 +520,7 @@ __device__ bool env_step(const FusedArgs& A, int e, double* sm) {
   bool ok = env_flag_read(A.ok, e);
   if (ok) {
     // feasibility of the incoming state (ref solver.py:372-385)
-    if (!env_broad(W, W.xw0, W.xw0, A.dc, e)) return false;
+    if (!env_broad_sm(W, W.xw0, W.xw0, A.dc, e, sm, A.smem_doubles)) return false;
     env_terms(A, W.x, W.xw0, 0, e);
     if (env_infeasible(A, e)) {
       ok = false;
@@ -306,7 +559,7 @@ __device__ bool env_step(const FusedArgs& A, int e, double* sm) {
         lags_env(W, W.xw0, A.dc, A.L, e);
       } else {
         env_world(W, W.x, W.xw, e);
-        if (!env_broad(W, W.xw, W.xw, A.dc, e)) return false;
+        if (!env_broad_sm(W, W.xw, W.xw, A.dc, e, sm, A.smem_doubles)) return false;
         lags_env(W, W.xw, A.dc, A.L, e);
       }
     }
@@ -329,7 +582,7 @@ __device__ bool env_step(const FusedArgs& A, int e, double* sm) {
   __syncthreads();
   if (ok) {
     env_world(W, W.x, W.xw, e);
-    if (!env_broad(W, W.xw, W.xw, A.dc, e)) return false;
+    if (!env_broad_sm(W, W.xw, W.xw, A.dc, e, sm, A.smem_doubles)) return false;
     double ms = env_terms(A, W.x, W.xw, 0, e);
     if (tid == 0) {
       S.min_s[e] = ms;
@@ -342,6 +595,29 @@ __device__ bool env_step(const FusedArgs& A, int e, double* sm) {
   }
   __syncthreads();
   return true;
+}
+
+// Hand-off from the batched schedule: once few envs are still iterating, each
+// continues its Newton loop from iteration it0 in its own CTA (same state in
+// EnvState / World, same item functions), without per-iteration launches.
+__global__ void __launch_bounds__(256, 1) k_env_newton_rest(FusedArgs A, int it0) {
+  extern __shared__ double sm[];
+  __shared__ int s_e;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int e = A.W.n_env;
+      if (!*(volatile int*)A.dc.overflow && !*(volatile int*)A.sw.overflow)
+        do {
+          e = atomicAdd(A.queue, 1);
+        } while (e < A.W.n_env && !A.S.newton_active[e]);
+      s_e = e;
+    }
+    __syncthreads();
+    int e = s_e;
+    if (e >= A.W.n_env) return;
+    env_newton(A, e, sm, false, it0);
+  }
 }
 
 __global__ void __launch_bounds__(256, 1) k_env_step(FusedArgs A) {

@@ -101,6 +101,7 @@ __device__ __forceinline__ bool excluded(const World& W, int cb0, int b1, int b2
 }
 
 constexpr int BP_THREADS = 256;
+constexpr int BP_WIN = 1024;  // broad-phase items per window (multiple of BP_THREADS)
 
 // kind 0: PT, 1: EE, 2: ground. One CTA per environment. Work items are
 // (row primitive, collision body) pairs in lexicographic order; an item is
@@ -214,7 +215,6 @@ __device__ void broad_env(const World& W, const double* __restrict__ lo, const d
   __shared__ int warp_tot[BP_THREADS / 32];
   __shared__ int total;
   __shared__ double blo[3 * MAX_BODIES], bhi[3 * MAX_BODIES];
-  __shared__ int cnt[BP_THREADS];
   double margin = W.env_dhat[e];
   int s0 = W.env_slot[e], s1 = W.env_slot[e + 1];
   int cb0 = W.env_cbody[e], nb = W.env_cbody[e + 1] - cb0;
@@ -283,118 +283,112 @@ __device__ void broad_env(const World& W, const double* __restrict__ lo, const d
   long long n_items = (long long)nrow * nb;
   long long per = ((n_items + Z - 1) / Z + BP_THREADS - 1) / BP_THREADS * BP_THREADS;
   long long i_begin = min(n_items, z * per), i_end = min(n_items, i_begin + per);
-  long long base = 0;
-  if (pass == 0) {  // count only
-    __shared__ int tot;
-    if (threadIdx.x == 0) tot = 0;
-    __syncthreads();
-    int mine = 0;
-    for (long long it = i_begin + threadIdx.x; it < i_end; it += BP_THREADS) {
-      int row = 0, B = 0, c0 = 0, c1 = 0, rb = 0;
-      double qlo[3], qhi[3];
-      int2 er = make_int2(0, 0);
-      row = r0 + (int)(it / nb);
-      B = (int)(it % nb);
-      if (kind == 0) {
-        rb = W.slot_cbody[row];
-        for (int c = 0; c < 3; ++c) {
-          qlo[c] = lo[3 * row + c];
-          qhi[c] = hi[3 * row + c];
-        }
-        c0 = W.cbody_tri[cb0 + B];
-        c1 = W.cbody_tri[cb0 + B + 1];
-      } else {
-        rb = W.edge_cbody[row];
-        er = W.edge_v[row];
-        for (int c = 0; c < 3; ++c) {
-          qlo[c] = fmin(lo[3 * er.x + c], lo[3 * er.y + c]);
-          qhi[c] = fmax(hi[3 * er.x + c], hi[3 * er.y + c]);
-        }
-        c0 = max(W.cbody_edge[cb0 + B], row + 1);
-        c1 = W.cbody_edge[cb0 + B + 1];
-      }
-      if (c0 < c1 && !cull_item(W, cb0, rb, B, qlo, qhi, blo, bhi, margin))
-        for_item_prims(W, kind, row, er, qlo, qhi, lo, hi, margin, B + cb0, c0, c1, [&](int) { ++mine; });
-    }
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-    if (lane == 0 && mine) atomicAdd(&tot, mine);
-    __syncthreads();
-    if (threadIdx.x == 0) bc[z] = tot;
-    return;
-  }
-  long long grand = 0;
+  long long base = 0, grand = 0;
   if (pass == 1) {
     for (int k = 0; k < Z; ++k) {
       if (k < z) base += bc[k];
       grand += bc[k];
     }
   }
-  for (long long i0 = i_begin; i0 < i_end; i0 += BP_THREADS) {
-    long long it = i0 + threadIdx.x;
-    int row = 0, B = 0, c0 = 0, c1 = 0;
-    double qlo[3], qhi[3];
-    int rb = 0;
-    int2 er = make_int2(0, 0);
-    bool live = false;
-    if (it < i_end) {
-      row = r0 + (int)(it / nb);
-      B = (int)(it % nb);
-      if (kind == 0) {
-        rb = W.slot_cbody[row];
-        for (int c = 0; c < 3; ++c) {
-          qlo[c] = lo[3 * row + c];
-          qhi[c] = hi[3 * row + c];
-        }
-        c0 = W.cbody_tri[cb0 + B];
-        c1 = W.cbody_tri[cb0 + B + 1];
-      } else {
-        rb = W.edge_cbody[row];
-        er = W.edge_v[row];
-        for (int c = 0; c < 3; ++c) {
-          qlo[c] = fmin(lo[3 * er.x + c], lo[3 * er.y + c]);
-          qhi[c] = fmax(hi[3 * er.x + c], hi[3 * er.y + c]);
-        }
-        c0 = max(W.cbody_edge[cb0 + B], row + 1);
-        c1 = W.cbody_edge[cb0 + B + 1];
+  // Windows of BP_WIN items; warp w owns the contiguous segment
+  // [win + w·SEG, win + (w+1)·SEG). Stage A: body-level culling, ordered
+  // warp-local compaction of the surviving items (ballots, no block barrier).
+  // Stage B: each survivor's hit count (chunk-culled primitive loop) and a
+  // warp-local exclusive scan. One block barrier publishes the warp totals;
+  // the write pass re-traverses the survivors. Output order = item order.
+  __shared__ int surv[BP_WIN], soff[BP_WIN];
+  __shared__ int wtot[BP_THREADS / 32];
+  constexpr int SEG = BP_WIN / (BP_THREADS / 32);
+  auto item = [&](long long it, int& row, int& B, int& c0, int& c1, int& rb, int2& er, double* qlo,
+                  double* qhi) {
+    row = r0 + (int)(it / nb);
+    B = (int)(it % nb);
+    if (kind == 0) {
+      rb = W.slot_cbody[row];
+      for (int c = 0; c < 3; ++c) {
+        qlo[c] = lo[3 * row + c];
+        qhi[c] = hi[3 * row + c];
       }
-      live = c0 < c1 && !cull_item(W, cb0, rb, B, qlo, qhi, blo, bhi, margin);
-    }
-    // pass 1: count hits of this item (chunk-culled primitive loop)
-    int n_hit = 0;
-    if (live) for_item_prims(W, kind, row, er, qlo, qhi, lo, hi, margin, B + cb0, c0, c1, [&](int) { ++n_hit; });
-    // exclusive scan of per-item counts (item order = output order):
-    // warp-shuffle inclusive scan, then one pass over the warp totals
-    int incl = n_hit;
-    for (int o = 1; o < 32; o <<= 1) {
-      int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    if (lane == 31) cnt[wid] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int acc = 0;
-      for (int w = 0; w < BP_THREADS / 32; ++w) {
-        int t = cnt[w];
-        cnt[w] = acc;
-        acc += t;
+      c0 = W.cbody_tri[cb0 + B];
+      c1 = W.cbody_tri[cb0 + B + 1];
+    } else {
+      rb = W.edge_cbody[row];
+      er = W.edge_v[row];
+      for (int c = 0; c < 3; ++c) {
+        qlo[c] = fmin(lo[3 * er.x + c], lo[3 * er.y + c]);
+        qhi[c] = fmax(hi[3 * er.x + c], hi[3 * er.y + c]);
       }
-      cnt[BP_THREADS / 32] = acc;
+      c0 = max(W.cbody_edge[cb0 + B], row + 1);
+      c1 = W.cbody_edge[cb0 + B + 1];
     }
-    __syncthreads();
-    long long dst = base + cnt[wid] + incl - n_hit;
-    long long chunk_total = cnt[BP_THREADS / 32];
-    __syncthreads();
-    // pass 2: write
-    if (n_hit) {
-      for_item_prims(W, kind, row, er, qlo, qhi, lo, hi, margin, B + cb0, c0, c1, [&](int t) {
-        if (dst < cap) {
-          if (kind == 0) C.pt[off + dst] = make_int2(row, t);
-          else C.ee[off + dst] = make_int2(row, t);
-        }
-        ++dst;
-      });
+  };
+  for (long long win = i_begin; win < i_end; win += BP_WIN) {
+    // stage A
+    int ns = 0;
+    long long seg0 = win + (long long)wid * SEG;
+    for (int j = 0; j < SEG; j += 32) {
+      long long it = seg0 + j + lane;
+      bool live = false;
+      if (it < i_end) {
+        int row, B, c0, c1, rb;
+        int2 er = make_int2(0, 0);
+        double qlo[3], qhi[3];
+        item(it, row, B, c0, c1, rb, er, qlo, qhi);
+        live = c0 < c1 && !cull_item(W, cb0, rb, B, qlo, qhi, blo, bhi, margin);
+      }
+      unsigned m = __ballot_sync(0xffffffffu, live);
+      if (live) surv[wid * SEG + ns + __popc(m & ((1u << lane) - 1u))] = (int)(it - win);
+      ns += __popc(m);
     }
-    base += chunk_total;
+    __syncwarp();
+    // stage B: counts + warp-local exclusive scan (survivor order)
+    int run = 0;
+    for (int j0 = 0; j0 < ns; j0 += 32) {
+      int j = j0 + lane, n_hit = 0;
+      if (j < ns) {
+        int row, B, c0, c1, rb;
+        int2 er = make_int2(0, 0);
+        double qlo[3], qhi[3];
+        item(win + surv[wid * SEG + j], row, B, c0, c1, rb, er, qlo, qhi);
+        for_item_prims(W, kind, row, er, qlo, qhi, lo, hi, margin, B + cb0, c0, c1, [&](int) { ++n_hit; });
+      }
+      int incl = n_hit;
+      for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (j < ns) soff[wid * SEG + j] = run + incl - n_hit;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) wtot[wid] = run;
+    __syncthreads();
+    long long wbase = base, wsum = 0;
+    for (int w = 0; w < BP_THREADS / 32; ++w) {
+      if (w < wid) wbase += wtot[w];
+      wsum += wtot[w];
+    }
+    if (pass != 0) {
+      for (int j = lane; j < ns; j += 32) {
+        int row, B, c0, c1, rb;
+        int2 er = make_int2(0, 0);
+        double qlo[3], qhi[3];
+        item(win + surv[wid * SEG + j], row, B, c0, c1, rb, er, qlo, qhi);
+        long long dst = wbase + soff[wid * SEG + j];
+        for_item_prims(W, kind, row, er, qlo, qhi, lo, hi, margin, B + cb0, c0, c1, [&](int t) {
+          if (dst < cap) {
+            if (kind == 0) C.pt[off + dst] = make_int2(row, t);
+            else C.ee[off + dst] = make_int2(row, t);
+          }
+          ++dst;
+        });
+      }
+    }
+    base += wsum;
+    __syncthreads();
+  }
+  if (pass == 0) {  // count only: this range's total
+    if (threadIdx.x == 0) bc[z] = (int)base;
+    return;
   }
   if (pass == 1) {
     if (z != 0) return;

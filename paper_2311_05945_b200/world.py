@@ -315,6 +315,11 @@ class GpuWorld:
         return {"newton_iters": int(out[0]), "ls_rounds": int(out[1]), "syncs": int(out[2]),
                 "pcg_iters": int(out[3])}
 
+    def set_fused(self, on: bool):
+        """Fused per-environment step (True) or batched launch sequence with the
+        per-env tail hand-off (False, default)."""
+        N.check(self.lib.ipc_world_set_fused(self.handle, 1 if on else 0))
+
     FUSED_PHASES = ("world", "broad_dcd", "terms", "energy", "dense", "ccd_prep", "broad_ccd", "ccd",
                     "line_search", "other")
 

@@ -27,3 +27,25 @@ def golden():
         return cache[name]
 
     return load
+
+
+# Every GPU test runs under the three step schedules of dense worlds: the
+# fused per-environment kernel, the batched launch sequence, and the hybrid
+# (batched, then per-env CTAs once few envs are still iterating). The native
+# library reads IPC_FUSED / IPC_TAIL when a world is created.
+SCHEDULES = {"fused": {"IPC_FUSED": "1"}, "batched": {"IPC_FUSED": "0", "IPC_TAIL": "0"},
+             "hybrid": {"IPC_FUSED": "0", "IPC_TAIL": "1000000"}}
+
+
+@pytest.fixture(autouse=True)
+def ipc_schedule(request, monkeypatch):
+    mode = getattr(request, "param", None)
+    if mode is not None:
+        for k, v in SCHEDULES[mode].items():
+            monkeypatch.setenv(k, v)
+    yield mode
+
+
+def pytest_generate_tests(metafunc):
+    if metafunc.definition.get_closest_marker("gpu") and "ipc_schedule" in metafunc.fixturenames:
+        metafunc.parametrize("ipc_schedule", list(SCHEDULES), indirect=True)
