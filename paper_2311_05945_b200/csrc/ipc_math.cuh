@@ -443,18 +443,26 @@ IPC_HD bool chol_pd(const double* A, int ld) {
 // cyclic Jacobi at N = 12.
 template <int N>
 IPC_HD void sym_eigen(double* V, double* d, double* e) {
+  // Every loop is unrolled and every array index is a compile-time constant
+  // (the data-dependent QL bounds l..m become predicates), so V, d, e can be
+  // register-allocated instead of living in local memory.
+#pragma unroll
   for (int j = 0; j < N; ++j) d[j] = V[(N - 1) * N + j];
+#pragma unroll
   for (int i = N - 1; i > 0; --i) {
     double scale = 0.0, h = 0.0;
+#pragma unroll
     for (int k = 0; k < i; ++k) scale += fabs(d[k]);
     if (scale == 0.0) {
       e[i] = d[i - 1];
+#pragma unroll
       for (int j = 0; j < i; ++j) {
         d[j] = V[(i - 1) * N + j];
         V[i * N + j] = 0.0;
         V[j * N + i] = 0.0;
       }
     } else {
+#pragma unroll
       for (int k = 0; k < i; ++k) {
         d[k] /= scale;
         h += d[k] * d[k];
@@ -465,11 +473,14 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
       e[i] = scale * g;
       h -= f * g;
       d[i - 1] = f - g;
+#pragma unroll
       for (int j = 0; j < i; ++j) e[j] = 0.0;
+#pragma unroll
       for (int j = 0; j < i; ++j) {
         f = d[j];
         V[j * N + i] = f;
         g = e[j] + V[j * N + j] * f;
+#pragma unroll
         for (int k = j + 1; k <= i - 1; ++k) {
           g += V[k * N + j] * d[k];
           e[k] += V[k * N + j] * f;
@@ -477,15 +488,19 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
         e[j] = g;
       }
       f = 0.0;
+#pragma unroll
       for (int j = 0; j < i; ++j) {
         e[j] /= h;
         f += e[j] * d[j];
       }
       double hh = f / (h + h);
+#pragma unroll
       for (int j = 0; j < i; ++j) e[j] -= hh * d[j];
+#pragma unroll
       for (int j = 0; j < i; ++j) {
         f = d[j];
         g = e[j];
+#pragma unroll
         for (int k = j; k <= i - 1; ++k) V[k * N + j] -= (f * e[k] + g * d[k]);
         d[j] = V[(i - 1) * N + j];
         V[i * N + j] = 0.0;
@@ -493,20 +508,27 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
     }
     d[i] = h;
   }
+#pragma unroll
   for (int i = 0; i < N - 1; ++i) {
     V[(N - 1) * N + i] = V[i * N + i];
     V[i * N + i] = 1.0;
     double h = d[i + 1];
     if (h != 0.0) {
+#pragma unroll
       for (int k = 0; k <= i; ++k) d[k] = V[k * N + i + 1] / h;
+#pragma unroll
       for (int j = 0; j <= i; ++j) {
         double g = 0.0;
+#pragma unroll
         for (int k = 0; k <= i; ++k) g += V[k * N + i + 1] * V[k * N + j];
+#pragma unroll
         for (int k = 0; k <= i; ++k) V[k * N + j] -= g * d[k];
       }
     }
+#pragma unroll
     for (int k = 0; k <= i; ++k) V[k * N + i + 1] = 0.0;
   }
+#pragma unroll
   for (int j = 0; j < N; ++j) {
     d[j] = V[(N - 1) * N + j];
     V[(N - 1) * N + j] = 0.0;
@@ -514,18 +536,20 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
   V[(N - 1) * N + N - 1] = 1.0;
   e[0] = 0.0;
   // implicit QL
+#pragma unroll
   for (int i = 1; i < N; ++i) e[i - 1] = e[i];
   e[N - 1] = 0.0;
   double f = 0.0, tst1 = 0.0;
   const double eps = 2.220446049250313e-16;
+#pragma unroll
   for (int l = 0; l < N; ++l) {
     tst1 = fmax(tst1, fabs(d[l]) + fabs(e[l]));
-    int m = l;
-    while (m < N - 1) {
-      if (fabs(e[m]) <= eps * tst1) break;
-      ++m;
-    }
-    if (m > l) {
+    // m = first index >= l with a negligible off-diagonal (predicated search)
+    int m = N - 1;
+#pragma unroll
+    for (int k = N - 2; k >= l; --k)
+      if (fabs(e[k]) <= eps * tst1) m = k;
+    if (l < N - 1 && m > l) {
       for (int iter = 0; iter < 60; ++iter) {
         double g = d[l];
         double p = (d[l + 1] - g) / (2.0 * e[l]);
@@ -535,26 +559,34 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
         d[l + 1] = e[l] * (p + r);
         double dl1 = d[l + 1];
         double h = g - d[l];
+#pragma unroll
         for (int i = l + 2; i < N; ++i) d[i] -= h;
         f += h;
-        p = d[m];
-        double c = 1.0, c2 = 1.0, c3 = 1.0, el1 = e[l + 1], s = 0.0, s2 = 0.0;
-        for (int i = m - 1; i >= l; --i) {
-          c3 = c2;
-          c2 = c;
-          s2 = s;
-          g = c * e[i];
-          h = c * p;
-          r = hypot(p, e[i]);
-          e[i + 1] = s * r;
-          s = e[i] / r;
-          c = p / r;
-          p = c * d[i] - s * g;
-          d[i + 1] = h + s * (c * g + s * d[i]);
-          for (int k = 0; k < N; ++k) {
-            h = V[k * N + i + 1];
-            V[k * N + i + 1] = s * V[k * N + i] + c * h;
-            V[k * N + i] = c * V[k * N + i] - s * h;
+        p = 0.0;
+#pragma unroll
+        for (int k = l; k < N; ++k)
+          if (k == m) p = d[k];
+        double c = 1.0, c2 = 1.0, c3 = 1.0, el1 = e[l + 1 < N ? l + 1 : N - 1], s = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int i = N - 2; i >= l; --i) {
+          if (i < m) {
+            c3 = c2;
+            c2 = c;
+            s2 = s;
+            g = c * e[i];
+            h = c * p;
+            r = hypot(p, e[i]);
+            e[i + 1] = s * r;
+            s = e[i] / r;
+            c = p / r;
+            p = c * d[i] - s * g;
+            d[i + 1] = h + s * (c * g + s * d[i]);
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              h = V[k * N + i + 1];
+              V[k * N + i + 1] = s * V[k * N + i] + c * h;
+              V[k * N + i] = c * V[k * N + i] - s * h;
+            }
           }
         }
         p = -s * s2 * c3 * el1 * e[l] / dl1;
