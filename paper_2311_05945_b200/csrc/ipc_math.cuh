@@ -418,8 +418,10 @@ IPC_HD double cross2_derivs(const V3* x, double* Gc, double* Hc) {
 template <int N>
 IPC_HD bool chol_pd(const double* A, int ld) {
   double L[N * (N + 1) / 2];
+#pragma unroll
   for (int j = 0; j < N; ++j) {
     double d = A[j * ld + j];
+#pragma unroll
     for (int k = 0; k < j; ++k) {
       double l = L[j * (j + 1) / 2 + k];
       d -= l * l;
@@ -427,8 +429,10 @@ IPC_HD bool chol_pd(const double* A, int ld) {
     if (!(d > 1e-14 * fabs(A[j * ld + j]) && d > 0.0)) return false;
     double dj = sqrt(d);
     L[j * (j + 1) / 2 + j] = dj;
+#pragma unroll
     for (int i = j + 1; i < N; ++i) {
       double s = A[i * ld + j];
+#pragma unroll
       for (int k = 0; k < j; ++k) s -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
       L[i * (i + 1) / 2 + j] = s / dj;
     }
@@ -603,20 +607,28 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
 // In-place: A <- V max(Λ,0) Vᵀ. Symmetrizes first (ref spd.py:8).
 template <int N>
 IPC_HD void psd_project(double* A, int ld) {
+#pragma unroll
   for (int i = 0; i < N; ++i)
+#pragma unroll
     for (int j = i + 1; j < N; ++j) {
       double s = 0.5 * (A[i * ld + j] + A[j * ld + i]);
       A[i * ld + j] = A[j * ld + i] = s;
     }
   if (chol_pd<N>(A, ld)) return;  // already positive definite: projection is the identity
   double V[N * N], d[N], e[N];
+#pragma unroll
   for (int i = 0; i < N; ++i)
+#pragma unroll
     for (int j = 0; j < N; ++j) V[i * N + j] = A[i * ld + j];
   sym_eigen<N>(V, d, e);
+#pragma unroll
   for (int i = 0; i < N; ++i) d[i] = fmax(d[i], 0.0);
+#pragma unroll
   for (int i = 0; i < N; ++i)
+#pragma unroll
     for (int j = i; j < N; ++j) {
       double s = 0.0;
+#pragma unroll
       for (int k = 0; k < N; ++k) s += V[i * N + k] * d[k] * V[j * N + k];
       A[i * ld + j] = A[j * ld + i] = s;
     }
@@ -633,46 +645,68 @@ template <int NS>
 IPC_HD void psd_project_tf(double* A, int ld) {
   constexpr int N = 3 * NS, R = 3 * (NS - 1);
   double q0[NS][NS - 1];
+#pragma unroll
   for (int j = 0; j < NS - 1; ++j) {
     double nrm = rsqrt((double)((j + 1) * (j + 2)));
+#pragma unroll
     for (int a = 0; a < NS; ++a) q0[a][j] = a <= j ? nrm : (a == j + 1 ? -(j + 1) * nrm : 0.0);
   }
+#pragma unroll
   for (int i = 0; i < N; ++i)
+#pragma unroll
     for (int j = i + 1; j < N; ++j) {
       double s = 0.5 * (A[i * ld + j] + A[j * ld + i]);
       A[i * ld + j] = A[j * ld + i] = s;
     }
-  double T[N * R];  // T = A Q
-  for (int r = 0; r < N; ++r)
-    for (int J = 0; J < NS - 1; ++J)
-      for (int c = 0; c < 3; ++c) {
-        double s = 0.0;
-        for (int b = 0; b < NS; ++b) s += A[r * ld + 3 * b + c] * q0[b][J];
-        T[r * R + 3 * J + c] = s;
-      }
-  double M[R * R];  // M = Qᵀ A Q
+  // M = Qᵀ A Q, block (I, J) = Σ_ab q0[a][I] q0[b][J] A_ab (3x3 blocks)
+  double M[R * R];
+#pragma unroll
   for (int I = 0; I < NS - 1; ++I)
-    for (int rr = 0; rr < 3; ++rr)
-      for (int k = 0; k < R; ++k) {
-        double s = 0.0;
-        for (int a = 0; a < NS; ++a) s += q0[a][I] * T[(3 * a + rr) * R + k];
-        M[(3 * I + rr) * R + k] = s;
-      }
+#pragma unroll
+    for (int J = 0; J < NS - 1; ++J)
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < NS; ++a) {
+            if (a > I + 1) continue;  // q0[a][I] == 0
+            double t = 0.0;
+#pragma unroll
+            for (int b = 0; b < NS; ++b) {
+              if (b > J + 1) continue;
+              t += q0[b][J] * A[(3 * a + r) * ld + 3 * b + c];
+            }
+            s += q0[a][I] * t;
+          }
+          M[(3 * I + r) * R + 3 * J + c] = s;
+        }
   psd_project<R>(M, R);
-  for (int r = 0; r < N; ++r)  // T = Q M
-    for (int k = 0; k < R; ++k) {
-      int a = r / 3, rr = r % 3;
-      double s = 0.0;
-      for (int I = 0; I < NS - 1; ++I) s += q0[a][I] * M[(3 * I + rr) * R + k];
-      T[r * R + k] = s;
-    }
-  for (int r = 0; r < N; ++r)  // A = T Qᵀ
-    for (int c = r; c < N; ++c) {
-      int b = c / 3, cc = c % 3;
-      double s = 0.0;
-      for (int J = 0; J < NS - 1; ++J) s += T[r * R + 3 * J + cc] * q0[b][J];
-      A[r * ld + c] = A[c * ld + r] = s;
-    }
+  // A = Q M Qᵀ
+#pragma unroll
+  for (int a = 0; a < NS; ++a)
+#pragma unroll
+    for (int b = a; b < NS; ++b)
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (b == a && c < r) continue;
+          double s = 0.0;
+#pragma unroll
+          for (int I = 0; I < NS - 1; ++I) {
+            if (a > I + 1) continue;
+            double t = 0.0;
+#pragma unroll
+            for (int J = 0; J < NS - 1; ++J) {
+              if (b > J + 1) continue;
+              t += M[(3 * I + r) * R + 3 * J + c] * q0[b][J];
+            }
+            s += q0[a][I] * t;
+          }
+          A[(3 * a + r) * ld + 3 * b + c] = A[(3 * b + c) * ld + 3 * a + r] = s;
+        }
 }
 
 // Project only the rows/columns of a 12x12 stencil Hessian whose slots are
