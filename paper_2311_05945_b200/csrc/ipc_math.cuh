@@ -412,6 +412,45 @@ IPC_HD double cross2_derivs(const V3* x, double* Gc, double* Hc) {
   return cross2(u, v);
 }
 
+// gradient of c = |u x v|² into Gc; when H is given, hscale · ∇²c is
+// accumulated into H (no separate 12x12 array)
+IPC_HD double cross2_grad_acc(const V3* x, double* Gc, double* H, double hscale) {
+  V3 u = x[1] - x[0], v = x[3] - x[2];
+  double uu = dot(u, u), vv = dot(v, v), uv = dot(u, v);
+  V3 gv[2] = {2.0 * (vv * u - uv * v), 2.0 * (uu * v - uv * u)};
+  const signed char cm[2][4] = {{-1, 1, 0, 0}, {0, 0, -1, 1}};
+  const int sl[4] = {0, 1, 2, 3};
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+      if (cm[i][a]) add_vec(Gc, sl[a], (double)cm[i][a], gv[i]);
+  if (H) {
+    M3 huu = m3_outer(v, v);
+    for (int i = 0; i < 9; ++i) huu.m[i] *= -2.0;
+    m3_add_diag(huu, 2.0 * vv);
+    M3 hvv = m3_outer(u, u);
+    for (int i = 0; i < 9; ++i) hvv.m[i] *= -2.0;
+    m3_add_diag(hvv, 2.0 * uu);
+    M3 huv = m3_outer(u, v), t2 = m3_outer(v, u);
+    for (int i = 0; i < 9; ++i) huv.m[i] = 4.0 * huv.m[i] - 2.0 * t2.m[i];
+    m3_add_diag(huv, -2.0 * uv);
+    M3 hv[2][2] = {{huu, huv}, {m3_T(huv), hvv}};
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            int c = cm[i][a] * cm[j][b];
+            if (c) add_blk(H, sl[a], sl[b], hscale * (double)c, hv[i][j]);
+          }
+  }
+  return cross2(u, v);
+}
+
 // ---------------------------------------------------------------------------
 // PSD projection of a symmetric NxN block (row-major, stride LD)
 // ---------------------------------------------------------------------------

@@ -724,12 +724,11 @@ __device__ __forceinline__ void pair_hess_item(const World& W, const double* __r
       for (int i = 0; i < 12; ++i)
         for (int j = 0; j < 12; ++j) H[i * 12 + j] = kappa * (d2b * G[i] * G[j] + db * H[i * 12 + j]);
     } else {
+      // mollified EE (ref contact.py:414-449): H = κ[(d2e b) ∇c∇cᵀ + (de b) ∇²c
+      //   + (de db)(∇c∇sᵀ + ∇s∇cᵀ) + (em d2b) ∇s∇sᵀ + (em db) ∇²s]; the ∇²c
+      // term is accumulated in place and skipped when the mollifier is flat
       double eps = 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y];
-      double Gc[12], Hc[144];
-      for (int i = 0; i < 12; ++i) Gc[i] = 0.0;
-      for (int i = 0; i < 144; ++i) Hc[i] = 0.0;
-      double c = cross2_derivs(X, Gc, Hc);
-      double t = c / eps;
+      double t = cross2(X[1] - X[0], X[3] - X[2]) / eps;
       double em, de, d2e;
       if (t < 1.0) {
         em = t * (2.0 - t);
@@ -738,13 +737,20 @@ __device__ __forceinline__ void pair_hess_item(const World& W, const double* __r
       } else {
         em = 1.0; de = 0.0; d2e = 0.0;
       }
-      for (int i = 0; i < 12; ++i) gout[i] = kappa * ((de * b) * Gc[i] + (em * db) * G[i]);
       for (int i = 0; i < 12; ++i)
-        for (int j = 0; j < 12; ++j)
-          H[i * 12 + j] = kappa * ((d2e * b) * Gc[i] * Gc[j] + (de * b) * Hc[i * 12 + j] +
-                                   (de * db) * (Gc[i] * G[j] + G[i] * Gc[j]) + (em * d2b) * G[i] * G[j] +
-                                   (em * db) * H[i * 12 + j]);
-      if (t < 1.0) mask = 0xF;
+        for (int j = 0; j < 12; ++j) H[i * 12 + j] = kappa * ((em * d2b) * G[i] * G[j] + (em * db) * H[i * 12 + j]);
+      if (t < 1.0) {
+        double Gc[12];
+        for (int i = 0; i < 12; ++i) Gc[i] = 0.0;
+        cross2_grad_acc(X, Gc, H, kappa * (de * b));
+        for (int i = 0; i < 12; ++i)
+          for (int j = 0; j < 12; ++j)
+            H[i * 12 + j] += kappa * ((d2e * b) * Gc[i] * Gc[j] + (de * db) * (Gc[i] * G[j] + G[i] * Gc[j]));
+        for (int i = 0; i < 12; ++i) gout[i] = kappa * ((de * b) * Gc[i] + (em * db) * G[i]);
+        mask = 0xF;
+      } else {
+        for (int i = 0; i < 12; ++i) gout[i] = kappa * ((em * db) * G[i]);
+      }
     }
 #ifndef IPC_NO_PSD
     psd_project_masked12(H, mask);
