@@ -174,8 +174,8 @@ def main():
     ap.add_argument("--envs", type=int, default=1024, help="environments per GPU")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--cpu-sample", type=int, default=0, help="envs in the CPU sample (0 = 2x cores)")
-    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="envs in the CPU sample (0 = one per core)")
+    ap.add_argument("--cpu-steps", type=int, default=0, help="timed CPU steps (0 = the GPU's K)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     ws, rank, lr = _dist()
@@ -185,8 +185,8 @@ def main():
         if rank != 0:
             return
         cores = _cores()
-        sample = args.cpu_sample or 2 * cores
-        ksteps = min(K, args.cpu_steps)
+        sample = args.cpu_sample or cores
+        ksteps = args.cpu_steps or K
         v, t, newton, used = cpu_arm(sample, args.seed, W, ksteps, cores)
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": ksteps, "warmup": W, "ms_per_step": 1e3 * t / ksteps,
@@ -237,6 +237,7 @@ def main():
     # timed region: device-resident inputs, L2 flushed between steps
     world.profile(True, kernels=None if os.environ.get("BENCH_PROFILE") == "2" else [dom])
     t_ms, newton = [], 0
+    stats0 = world.stats()
     with Clocks(lr) as clk:
         for k in range(W, W + K):
             world.flush_l2()
@@ -253,6 +254,8 @@ def main():
                 print(f"[step {k}] {t_ms[-1]:8.2f} ms newton mean {np.mean(it):.2f} max {max(it)} "
                       f"al max {max(r.al_outer for r in reps)} batched {d}", file=sys.stderr)
     prof, launches = world.profile_read()
+    stats1 = world.stats()
+    fused_iters = stats1["fused_env_iters"] - stats0["fused_env_iters"]
     if os.environ.get("BENCH_PROFILE") == "2":
         for n, (ms, c) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
             print(f"[timed profile] {n:14s} {ms:9.2f} ms {c:6d} launches "
@@ -284,7 +287,7 @@ def main():
     # roofline of the dominant kernel: algorithmic bytes / measured launch time
     ms_dom, cnt_dom = prof[dom]
     peak, peak_kind = _peaks()
-    algo = _algo_bytes(dom, world)
+    algo = _algo_bytes(dom, world, fused_iters / max(prof[dom][1], 1))
     avg_s = (ms_dom / max(cnt_dom, 1)) * 1e-3
     achieved = algo / avg_s / 1e9 if avg_s > 0 else 0.0
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
@@ -303,11 +306,12 @@ def main():
             "gpu_launches": launches, "clocks": clk.summary(), "failed_envs_last_step": final_err}
     if rank == 0 and ws == 1 and not args.no_cpu:
         cores = _cores()
-        sample = args.cpu_sample or 2 * cores
-        v, t, _, used = cpu_arm(sample, args.seed, W, min(K, args.cpu_steps), cores)
+        sample = args.cpu_sample or cores
+        ksteps = args.cpu_steps or K
+        v, t, _, used = cpu_arm(sample, args.seed, W, ksteps, cores)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": used, "kind": "port",
-                                "sample": f"first {sample} envs, {min(K, args.cpu_steps)} steps "
-                                          f"after {W} warm-up steps, oracle/ numpy port"}
+                                "sample": f"first {sample} envs of the same batch, the same {ksteps} timed "
+                                          f"steps after {W} warm-up steps, oracle/ numpy port, one env per core"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -315,11 +319,16 @@ def main():
         dist.destroy_process_group()
 
 
-def _algo_bytes(kernel, world):
+def _algo_bytes(kernel, world, fused_env_iters_per_launch=0.0):
     """Algorithmic DRAM bytes of one launch of `kernel` over the whole batch
     (DESIGN.md §Roofline): the minimum each launch must move."""
     p = world.packed
     ns, nt, ne, nd = p.n("slot"), p.n("tri"), p.n("edge"), p.n("dof")
+    if kernel == "fused_step":
+        # per env Newton iteration: x, p, grad, x̂ (read/write) and the env's
+        # slot positions twice (DCD + sweep) — mean env of the batch
+        per_env = (6 * nd * 8 + 2 * ns * 24) / max(world.n_env, 1)
+        return fused_env_iters_per_launch * per_env
     if kernel.startswith("broad"):
         # slot boxes (lo, hi) + primitive index lists, read once
         return ns * 48 + nt * 16 + ne * 12

@@ -141,8 +141,9 @@ int ipc_set_device(int device);
 int ipc_world_profile(ipc_world *w, int on, uint32_t kernel_mask);
 int ipc_world_profile_read(ipc_world *w, double *ms, int64_t *count, int64_t *launches);
 int ipc_world_flush_l2(ipc_world *w, int64_t bytes);
-/* Cumulative host-loop counters: batched Newton iterations, line-search
- * rounds, host synchronisations, sparse-path PCG iterations (out: 4). */
+/* Cumulative counters: batched Newton iterations, line-search rounds, host
+ * synchronisations, sparse-path PCG iterations, per-env Newton iterations and
+ * line-search trials run inside the fused per-env kernels (out: 6). */
 int ipc_world_stats(ipc_world *w, int64_t *out);
 /* Select the step schedule of a dense world: 1 = fused per-environment step
  * (one CTA runs a whole env step), 0 = batched launch sequence (default),

@@ -1538,12 +1538,10 @@ int ipc_world_stats(ipc_world* w, int64_t* out) {
       CK(cudaMemcpy(pit, w->d_nlive, sizeof(pit), cudaMemcpyDeviceToHost));
     }
     out[3] = pit[2];
-    if (w->d_fstat) {
-      long long fs[2];
-      CK(cudaMemcpy(fs, w->d_fstat, sizeof(fs), cudaMemcpyDeviceToHost));
-      out[0] += fs[0];
-      out[1] += fs[1];
-    }
+    long long fs[2] = {0, 0};
+    if (w->d_fstat) CK(cudaMemcpy(fs, w->d_fstat, sizeof(fs), cudaMemcpyDeviceToHost));
+    out[4] = fs[0];
+    out[5] = fs[1];
   })
 }
 

@@ -310,10 +310,10 @@ class GpuWorld:
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(N.KERNEL_IDS)}, launches.value
 
     def stats(self):
-        out = np.zeros(4, np.int64)
+        out = np.zeros(6, np.int64)
         N.check(self.lib.ipc_world_stats(self.handle, N.ptr(out, N._i64p)))
         return {"newton_iters": int(out[0]), "ls_rounds": int(out[1]), "syncs": int(out[2]),
-                "pcg_iters": int(out[3])}
+                "pcg_iters": int(out[3]), "fused_env_iters": int(out[4]), "fused_ls_trials": int(out[5])}
 
     def set_fused(self, on: bool):
         """Fused per-environment step (True) or batched launch sequence with the
