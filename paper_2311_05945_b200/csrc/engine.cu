@@ -499,8 +499,14 @@ struct ipc_world {
   static constexpr long long BROAD_ITEMS = 8192;
   int bp_z = 1;
   int* bp_cnt = nullptr;
+  size_t broad_smem = 0;  // k_broad_sm: staged boxes of the largest env (0: unused)
   void launch_broad(CandStore& cs, const double* lo, const double* hi, const int* env_mask) {
     int kid = &cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD;
+    if (broad_smem && bp_z == 1) {
+      IPC_LAUNCH(kid, st, k_broad_sm, n_env, BP_THREADS, broad_smem, W, lo, hi, cs.c, env_mask,
+                 (int)(broad_smem / sizeof(double)));
+      return;
+    }
     IPC_LAUNCH(kid, st, k_chunk_boxes, nblk(W.n_tchunk + W.n_echunk, 128), 128, 0, W, lo, hi);
     if (bp_z == 1) {
       IPC_LAUNCH(kid, st, k_broad, dim3(n_env, 3), BP_THREADS, 0, W, lo, hi, cs.c, -1, env_mask, -1, nullptr);
@@ -1263,6 +1269,17 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
       }
       if (d->env_cbody[e + 1] - d->env_cbody[e] > 64)
         throw std::runtime_error("more than 64 collision bodies in one environment");
+    }
+    {
+      // batched broad phase with the env's boxes staged in shared memory when
+      // they fit comfortably (several CTAs per SM); else the global version
+      size_t bsm = sizeof(double) * 6 * (size_t)w->max_env_prims;
+      const char* bz = getenv("IPC_BROAD_SM");
+      bool on = !(bz && bz[0] == '0');
+      if (on && bsm <= 64 * 1024 && w->bp_z == 1) {
+        w->broad_smem = std::max(bsm, (size_t)1024);
+        CK(cudaFuncSetAttribute(k_broad_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->broad_smem));
+      }
     }
     const int DENSE_MAX = 160;
     w->sparse = w->max_env_dof > DENSE_MAX;

@@ -325,6 +325,17 @@ __device__ bool env_broad_sm(const World& W, const double* __restrict__ lo, cons
   return !s_ov;
 }
 
+// Batched schedule: the shared-memory broad phase, one CTA per flagged env
+// (all three kinds; chunk boxes built in shared memory).
+__global__ void __launch_bounds__(BP_THREADS) k_broad_sm(World W, const double* __restrict__ lo,
+                                                          const double* __restrict__ hi, Cands C,
+                                                          const int* env_mask, int cap_d) {
+  extern __shared__ double bsm[];
+  int e = blockIdx.x;
+  if (env_mask && !env_mask[e]) return;
+  env_broad_sm(W, lo, hi, C, e, bsm, cap_d);
+}
+
 // element values (deriv = 0) or values + derivatives of every term at x / xw;
 // returns the env's minimum squared distance over candidates and ground.
 // Derivative pass: one value sweep over all candidates (PT and EE together)
