@@ -385,6 +385,10 @@ struct ipc_world {
 
   ~ipc_world() {
     drop_graphs();
+    for (auto s2 : side)
+      if (s2) cudaStreamDestroy(s2);
+    for (auto e2 : fj)
+      if (e2) cudaEventDestroy(e2);
     if (h_count) cudaFreeHost(h_count);
     if (h_status) cudaFreeHost(h_status);
   }
@@ -565,9 +569,11 @@ struct ipc_world {
     io.work_n = work_n;
     if (deriv) CK(cudaMemsetAsync(work_n, 0, 2 * sizeof(int), st));
     IPC_LAUNCH(kid, st, k_pair_dist, dim3(n_sm * 8, 2), 128, 0, W, xw, cs.c, deriv, io, min_s);
-    if (deriv) {
+    if (deriv) {  // the two kinds' derivative passes run as parallel branches
+      fork_to(side[2], fj[3]);
+      IPC_LAUNCH(kid == K_SENSE ? K_SENSE : K_PAIRS_D, side[2], k_pair_hess<1>, n_sm * 8, 64, 0, W, xw, cs.c, io);
       IPC_LAUNCH(kid == K_SENSE ? K_SENSE : K_PAIRS_D, st, k_pair_hess<0>, n_sm * 8, 64, 0, W, xw, cs.c, io);
-      IPC_LAUNCH(kid == K_SENSE ? K_SENSE : K_PAIRS_D, st, k_pair_hess<1>, n_sm * 8, 64, 0, W, xw, cs.c, io);
+      join_from(side[2], fj[3]);
     }
   }
 
@@ -576,19 +582,40 @@ struct ipc_world {
   }
 
   // derivative or value pass of every term over (cands, lags)
+  // side streams: independent element kernels run as parallel branches
+  // (parallel graph branches when captured); fj: fork/join events
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fj[4] = {nullptr, nullptr, nullptr, nullptr};
+  void fork_to(cudaStream_t s2, cudaEvent_t ev) {
+    CK(cudaEventRecord(ev, st));
+    CK(cudaStreamWaitEvent(s2, ev, 0));
+  }
+  void join_from(cudaStream_t s2, cudaEvent_t ev) {
+    CK(cudaEventRecord(ev, s2));
+    CK(cudaStreamWaitEvent(st, ev, 0));
+  }
+
   void terms(const double* x, const double* xw, CandStore& cs, PairBufs& pb, bool deriv, double h,
              const int* flag, double* min_s) {
     double h2 = h * h;
-    IPC_LAUNCH(K_BODY, st, k_body, nblk(W.n_aff, 64), 64, 0, W, x, W.xhat, h2, deriv, flag, body_val, D.body_g, D.body_h);
-    if (W.n_tet) IPC_LAUNCH(K_TET, st, k_tet, nblk(W.n_tet, 64), 64, 0, W, x, h2, deriv, flag, tet_val, D.tet_g, D.tet_h);
-    pairs(xw, cs, pb, deriv, min_s, K_PAIRS_V);
     int max_slots = 0;
     for (int e = 0; e < n_env; ++e) max_slots = std::max(max_slots, h_env_slot[e + 1] - h_env_slot[e]);
-    IPC_LAUNCH(K_GROUND, st, k_ground, dim3(nblk(max_slots, 128), n_env), 128, 0, W, xw, cs.c, deriv, flag, pb.gnd_val,
-                                                                pb.gnd_gy, pb.gnd_hyy, min_s);
-    IPC_LAUNCH(K_FRICTION, st, k_friction, n_sm * 4, 128, 0, W, xw, W.xw0, L, h, deriv, flag, fr_val, D.fr_g, D.fr_h);
-    IPC_LAUNCH(K_FRICTION, st, k_friction_gnd, dim3(nblk(max_slots, 128), n_env), 128, 0, W, xw, W.xw0, L, h, deriv, flag,
-                                                                      frg_val, D.frg_g, D.frg_h);
+    // branch 1: affine bodies + tets; branch 2: ground + friction; main: pairs
+    fork_to(side[0], fj[0]);
+    CK(cudaStreamWaitEvent(side[1], fj[0], 0));
+    IPC_LAUNCH(K_BODY, side[0], k_body, nblk(W.n_aff, 64), 64, 0, W, x, W.xhat, h2, deriv, flag, body_val, D.body_g,
+               D.body_h);
+    if (W.n_tet)
+      IPC_LAUNCH(K_TET, side[0], k_tet, nblk(W.n_tet, 64), 64, 0, W, x, h2, deriv, flag, tet_val, D.tet_g, D.tet_h);
+    IPC_LAUNCH(K_GROUND, side[1], k_ground, dim3(nblk(max_slots, 128), n_env), 128, 0, W, xw, cs.c, deriv, flag,
+               pb.gnd_val, pb.gnd_gy, pb.gnd_hyy, min_s);
+    IPC_LAUNCH(K_FRICTION, side[1], k_friction, n_sm * 4, 128, 0, W, xw, W.xw0, L, h, deriv, flag, fr_val, D.fr_g,
+               D.fr_h);
+    IPC_LAUNCH(K_FRICTION, side[1], k_friction_gnd, dim3(nblk(max_slots, 128), n_env), 128, 0, W, xw, W.xw0, L, h,
+               deriv, flag, frg_val, D.frg_g, D.frg_h);
+    pairs(xw, cs, pb, deriv, min_s, K_PAIRS_V);
+    join_from(side[0], fj[1]);
+    join_from(side[1], fj[2]);
     CK(cudaGetLastError());
   }
 
@@ -1334,6 +1361,8 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     w->D.tet_g = P.alloc<double>(12 * (size_t)d->n_tet);
     w->D.tet_h = P.alloc<double>(PK * (size_t)d->n_tet);
     CK(cudaStreamCreateWithFlags(&w->st, cudaStreamNonBlocking));
+    for (int i = 0; i < 3; ++i) CK(cudaStreamCreateWithFlags(&w->side[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&w->fj[i], cudaEventDisableTiming));
     CK(cudaDeviceSynchronize());
     *out = w;
     return 0;
