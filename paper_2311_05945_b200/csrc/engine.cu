@@ -631,12 +631,17 @@ struct ipc_world {
     broad_nosync(dcd, W.xw, W.xw, S.newton_active);
     IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.min_s, INFINITY, S.newton_active);
     terms(W.x, W.xw, dcd, pb_dcd, true, cfg.h, S.newton_active, S.min_s);
-    energy(W.x, dcd, pb_dcd, S.newton_active, S.e0);
     if (sparse) {
+      energy(W.x, dcd, pb_dcd, S.newton_active, S.e0);
       sparse_solve(cfg);
-    } else {
+    } else {  // E0 reduction as a parallel branch of the dense solve
+      fork_to(side[0], fj[0]);
+      Terms T{body_val, tet_val, pb_dcd.pt_val, pb_dcd.ee_val, pb_dcd.gnd_val, fr_val, frg_val, nullptr};
+      IPC_LAUNCH(K_ENERGY, side[0], k_env_energy, n_env, RED_THREADS, 0, W, W.x, W.xhat, T, dcd.c, L, S.newton_active,
+                 S.e0);
       IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, dense_smem, W, S, D_with(pb_dcd), dcd.c, L, W.x,
                  W.xhat, W.p, W.grad);
+      join_from(side[0], fj[1]);
     }
     IPC_LAUNCH(K_MISC, st, k_newton_check, nblk(n_env, 128), 128, 0, n_env, S, cfg.h, cfg.newton_tol);
   }
@@ -647,11 +652,13 @@ struct ipc_world {
     IPC_LAUNCH(K_MISC, st, k_sweep_box2, nblk(3 * W.n_slot, 256), 256, 0, W.n_slot, xwt, W.xw, W.dxw, xlo, xhi);
     broad_nosync(sweep, xlo, xhi, S.ls_active);
     IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.alpha_max, 1.0, S.ls_active);
+    fork_to(side[0], fj[0]);  // ground crossings as a parallel branch
+    IPC_LAUNCH(K_CCD, side[0], k_ccd_ground, dim3(nblk(max_slots, 128), n_env), 128, 0, W, W.xw, W.dxw, sweep.c,
+               cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
     if (sweep.pt_total || sweep.ee_total)
       IPC_LAUNCH(K_CCD, st, k_ccd_pairs, dim3(n_sm * 8, 2), 64, 0, W, W.xw, W.dxw, sweep.c,
                  cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
-    IPC_LAUNCH(K_CCD, st, k_ccd_ground, dim3(nblk(max_slots, 128), n_env), 128, 0, W, W.xw, W.dxw, sweep.c,
-               cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
+    join_from(side[0], fj[1]);
     IPC_LAUNCH(K_MISC, st, k_ls_begin, nblk(n_env, 128), 128, 0, n_env, S, ls_count);
   }
   // one backtracking round (ref solver.py:257): M speculative halvings

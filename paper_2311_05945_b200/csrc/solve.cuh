@@ -345,8 +345,11 @@ __device__ void add_stencil(const World& W, int d0, int n, double* H, double* g,
   }
   __syncthreads();
   int tot = s_tot;
+  // lower triangle only (rt_dof[c] <= rt_dof[r]): the LDLᵀ below never
+  // reads the upper part
   for (int idx = tid; idx < tot * tot; idx += blockDim.x) {
     int r = idx / tot, c = idx - r * tot;
+    if (rt_dof[c] > rt_dof[r]) continue;
     double acc = 0.0;
     for (int p = 0; p < rt_n[r]; ++p) {
       const double* hr = sH + rt_idx[r][p] * N;
@@ -405,7 +408,8 @@ __device__ void dense_solve_block(const World& W, const EnvState& S, const Deriv
     const double* hp = D.tet_h + PK * t;
     for (int i = tid; i < 144; i += blockDim.x) {
       int r = i / 12, c = i % 12;
-      H[(dv[r / 3] + r % 3) * n + dv[c / 3] + c % 3] += pk_get(hp, r, c);
+      int rr = dv[r / 3] + r % 3, cc = dv[c / 3] + c % 3;
+      if (cc <= rr) H[rr * n + cc] += pk_get(hp, r, c);
     }
     for (int i = tid; i < 12; i += blockDim.x) g[dv[i / 3] + i % 3] += D.tet_g[12 * t + i];
     __syncthreads();
