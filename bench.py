@@ -290,6 +290,14 @@ def main():
     algo = _algo_bytes(dom, world, fused_iters / max(prof[dom][1], 1))
     avg_s = (ms_dom / max(cnt_dom, 1)) * 1e-3
     achieved = algo / avg_s / 1e9 if avg_s > 0 else 0.0
+    traffic = None  # dram bytes per launch of the dominant kernel from a committed ncu --set full capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1c_fused_traffic.json")) as fh:
+            tj = json.load(fh)
+        if tj.get("kernel") == dom:
+            traffic = float(tj["dram_bytes_read"] + tj["dram_bytes_write"])
+    except (OSError, KeyError, ValueError):
+        pass
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
             "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -300,7 +308,8 @@ def main():
             "newton_iters_per_s": newton / (total_ms * 1e-3),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "launches": cnt_dom, "avg_launch_us": avg_s * 1e6,
+                         "traffic": traffic, "algo_bytes_per_launch": algo, "launches": cnt_dom,
+                         "avg_launch_us": avg_s * 1e6,
                          "share_of_step": ms_dom / total_ms if total_ms else None},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "clocks": clk.summary(), "failed_envs_last_step": final_err}
