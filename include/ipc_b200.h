@@ -145,6 +145,14 @@ int ipc_world_flush_l2(ipc_world *w, int64_t bytes);
  * synchronisations, sparse-path PCG iterations, per-env Newton iterations and
  * line-search trials run inside the fused per-env kernels (out: 6). */
 int ipc_world_stats(ipc_world *w, int64_t *out);
+/* Advance every environment through steps [k0, k1) of the uploaded command
+ * stream asynchronously: each env runs its own steps back to back in one CTA
+ * (per-env step order preserved; envs never interact), so one env's long
+ * contact-onset solve overlaps with the others' later steps. Same per-env
+ * results as stepping k0..k1-1 with the fused schedule. Dense worlds only.
+ * rep (optional): each env's report of its last step. Replaces a host loop
+ * over ref solver.py:360 `step`. */
+int ipc_world_run_scheduled(ipc_world *w, const ipc_step_config *cfg, int k0, int k1, ipc_step_report *rep);
 /* Select the step schedule of a dense world: 1 = fused per-environment step
  * (one CTA runs a whole env step), 0 = batched launch sequence (default),
  * which hands the Newton loops of the last few active envs to per-env CTAs.

@@ -88,6 +88,7 @@ SIGNATURES = {
     "ipc_world_stats": (C.c_int, [C.c_void_p, _i64p]),
     "ipc_world_fused_timers": (C.c_int, [C.c_void_p, _i64p, C.c_int]),
     "ipc_world_set_fused": (C.c_int, [C.c_void_p, C.c_int]),
+    "ipc_world_run_scheduled": (C.c_int, [C.c_void_p, C.POINTER(StepConfig), C.c_int, C.c_int, C.c_void_p]),
     "ipc_world_flush_l2": (C.c_int, [C.c_void_p, C.c_int64]),
     "ipc_world_mark": (C.c_int, [C.c_void_p, C.c_int]),
     "ipc_world_elapsed": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _f64p]),

@@ -847,6 +847,8 @@ struct ipc_world {
   int max_env_groups = 0;  // max over envs of soft vertices + affine bodies
   bool use_fused() const { return fused_on && !sparse && max_env_dof <= fused_max_dof; }
 
+  void read_reports(ipc_step_report* rep);
+
   // shared setup of the fused kernels; false when the env systems do not fit
   bool fused_setup() {
     if (!fq) {
@@ -877,6 +879,7 @@ struct ipc_world {
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_env_step, 256, fused_smem));
       fused_blocks = std::max(1, std::min(n_env, std::max(per_sm, 1) * n_sm));
       CK(cudaFuncSetAttribute(k_env_newton_rest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+      CK(cudaFuncSetAttribute(k_env_steps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
     }
     return true;
   }
@@ -1502,6 +1505,17 @@ static void step_core(ipc_world* w, const ipc_step_config* cfg, const double* ta
     }
     CK(cudaGetLastError());
     if (rep) {
+      w->read_reports(rep);
+    } else {
+      CK(cudaStreamSynchronize(st));
+    }
+  }
+}
+
+void ipc_world::read_reports(ipc_step_report* rep) {
+  {
+    {
+      int ne = n_env;
       std::vector<int> it(ne), cc(ne), cv(ne), lf(ne), ao(ne), er(ne);
       std::vector<double> gn(ne), mb(ne), ma(ne), kp(ne);
       CK(cudaMemcpyAsync(it.data(), S.newton_iters, 4 * ne, cudaMemcpyDeviceToHost, st));
@@ -1527,8 +1541,6 @@ static void step_core(ipc_world* w, const ipc_step_config* cfg, const double* ta
         rep[e].min_dist_after = ma[e];
         rep[e].kappa = kp[e];
       }
-    } else {
-      CK(cudaStreamSynchronize(st));
     }
   }
 }
@@ -1550,6 +1562,45 @@ static int step_impl(ipc_world* w, const ipc_step_config* cfg, const double* tar
         w->grow_overflowed();
       }
     }
+  })
+}
+
+int ipc_world_run_scheduled(ipc_world* w, const ipc_step_config* cfg, int k0, int k1, ipc_step_report* rep) {
+  GUARD({
+    g_prof = &w->prof;
+    if (!w->sched || k0 < 0 || k1 > w->sched_steps || k0 > k1)
+      throw std::runtime_error("run_scheduled: steps outside the uploaded schedule");
+    if (w->sparse || !w->fused_setup()) throw std::runtime_error("run_scheduled: needs a dense world");
+    World& W = w->W;
+    int ne = w->n_env;
+    double* x0 = w->pool.alloc<double>(W.n_dof);
+    CK(cudaMemcpyAsync(x0, W.x, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, w->st));
+    for (int attempt = 0;; ++attempt) {
+      if (w->lags_stale) {
+        w->alloc_lags();
+        w->lags_stale = false;
+      }
+      CK(cudaMemsetAsync(w->dcd.c.overflow, 0, sizeof(int), w->st));
+      CK(cudaMemsetAsync(w->sweep.c.overflow, 0, sizeof(int), w->st));
+      CK(cudaMemcpyAsync(w->v_save, W.v, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, w->st));
+      CK(cudaMemcpyAsync(w->kappa_save, W.env_kappa, sizeof(double) * ne, cudaMemcpyDeviceToDevice, w->st));
+      IPC_LAUNCH(K_MISC, w->st, k_fill_int, nblk(ne, 128), 128, 0, ne, w->enable, 1);
+      CK(cudaMemsetAsync(w->fq, 0, sizeof(int), w->st));
+      FusedArgs A = w->fused_args(*cfg);
+      IPC_LAUNCH(K_FUSED, w->st, k_env_steps, w->fused_blocks, 256, w->fused_smem, A, w->sched, W.n_cons, k0, k1);
+      CK(cudaMemcpyAsync(w->h_status, w->dcd.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, w->st));
+      CK(cudaMemcpyAsync(w->h_status + 1, w->sweep.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, w->st));
+      CK(cudaStreamSynchronize(w->st));
+      if (!w->h_status[0] && !w->h_status[1]) break;
+      if (attempt >= 6) throw std::runtime_error("candidate capacity overflow persists");
+      // replay the whole range from its start with larger capacities
+      CK(cudaMemcpyAsync(W.x, x0, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, w->st));
+      CK(cudaMemcpyAsync(W.v, w->v_save, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, w->st));
+      CK(cudaMemcpyAsync(W.env_kappa, w->kappa_save, sizeof(double) * ne, cudaMemcpyDeviceToDevice, w->st));
+      w->grow_overflowed();
+    }
+    w->pool.free_one(x0);
+    if (rep) w->read_reports(rep);
   })
 }
 

@@ -631,6 +631,30 @@ __global__ void __launch_bounds__(256, 1) k_env_newton_rest(FusedArgs A, int it0
   }
 }
 
+// Asynchronous range: each env runs its own steps k0..k1-1 of the
+// device-resident command stream back to back in one CTA (envs never
+// interact, so only the per-env step order matters); a contact-onset solve
+// in one env overlaps with the other envs' later steps.
+__global__ void __launch_bounds__(256, 1) k_env_steps(FusedArgs A, const double* sched, int n_cons, int k0, int k1) {
+  extern __shared__ double sm[];
+  __shared__ int s_e;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_e = *(volatile int*)A.dc.overflow || *(volatile int*)A.sw.overflow
+                                    ? A.W.n_env : atomicAdd(A.queue, 1);
+    __syncthreads();
+    int e = s_e;
+    if (e >= A.W.n_env) return;
+    for (int k = k0; k < k1; ++k) {
+      FusedArgs Ak = A;
+      Ak.targets = sched + 12 * (size_t)n_cons * k;
+      for (int i = A.W.env_dof[e] + threadIdx.x; i < A.W.env_dof[e + 1]; i += blockDim.x) A.W.x_prev[i] = A.W.x[i];
+      __syncthreads();
+      if (!env_step(Ak, e, sm)) break;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256, 1) k_env_step(FusedArgs A) {
   extern __shared__ double sm[];
   __shared__ int s_e;

@@ -244,6 +244,16 @@ class GpuWorld:
         N.check(self.lib.ipc_world_step_scheduled(self.handle, C.byref(c), int(k), en, reps))
         return reps
 
+    def run_scheduled(self, cfg, k0, k1, want_reports=True):
+        """Steps k0..k1-1 of the uploaded command stream, each env asynchronously
+        in its own CTA (ipc_world_run_scheduled); reports of each env's last step."""
+        c = N.StepConfig(cfg.h, cfg.newton_tol, cfg.max_newton_iters, cfg.max_line_search_halvings,
+                         cfg.ccd_conservative_factor, cfg.friction_fixed_point_iters,
+                         cfg.al_max_outer)
+        reps = (N.StepReportC * self.n_env)() if want_reports else None
+        N.check(self.lib.ipc_world_run_scheduled(self.handle, C.byref(c), int(k0), int(k1), reps))
+        return reps
+
     # -- queries -----------------------------------------------------------
     def candidates(self, env=0, which=0):
         cap = 1 << 22

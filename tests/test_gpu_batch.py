@@ -73,3 +73,41 @@ def test_batch_grasp_outcomes_match_oracle():
         assert out[e] == tr.outcome, (e, out[e], tr.outcome)
         assert bg.steps[e] == tr.steps, (e, bg.steps[e], tr.steps)
         np.testing.assert_allclose(np.array(bg.forces[e]), np.array(tr.forces), rtol=1e-3, atol=1e-4)
+
+
+def test_run_scheduled_matches_per_step_fused():
+    """Asynchronous range (each env runs its own steps back to back) gives the
+    per-step fused schedule's states bit for bit, and the default (hybrid)
+    per-step schedule's to 1e-9, including the contact-onset steps."""
+    import os
+
+    from paper_2311_05945_b200 import workloads as WL
+    from paper_2311_05945_b200.solver import SolverConfig
+    from paper_2311_05945_b200.world import GpuWorld
+
+    E, K = 12, 10
+    cfg = SolverConfig()
+
+    def fresh():
+        scenes, grippers, half, poses = WL.grasp_batch(E, seed=5)
+        w = GpuWorld(scenes)
+        w.upload_schedule(WL.schedule(grippers, half, poses, K))
+        return w
+
+    wa = fresh()
+    reps_a = wa.run_scheduled(cfg, 0, K)
+    xa, va = wa.get_state()
+    wf = fresh()
+    wf.set_fused(True)
+    for k in range(K):
+        reps_f = wf.step_scheduled(cfg, k)
+    xf, vf = wf.get_state()
+    assert np.array_equal(xa, xf) and np.array_equal(va, vf)
+    assert [r.newton_iters for r in reps_a] == [r.newton_iters for r in reps_f]
+    if os.environ.get("IPC_FUSED") != "1":
+        wh = fresh()
+        wh.set_fused(False)
+        for k in range(K):
+            wh.step_scheduled(cfg, k)
+        xh, _ = wh.get_state()
+        assert np.abs(xa - xh).max() <= 1e-9 * np.abs(xh).max()
