@@ -174,3 +174,37 @@ def test_soft_cube_grasp_trial_matches_reference(golden):
     np.testing.assert_allclose(np.array(tr.forces), z["forces"], rtol=1e-4, atol=1e-4)
     x = sc.state.gather()
     assert np.abs(x - z["x_final"]).max() <= 1e-5 * np.abs(z["x_final"]).max()
+
+
+@pytest.mark.parametrize("items", [None, "256"])
+def test_broad_phase_variants_identical(monkeypatch, items):
+    """The shared-memory broad phase (one CTA per env, staged boxes), the
+    global-memory one, and the multi-CTA split (count + write passes) give
+    bit-identical, identically ordered candidate lists on a grasp batch."""
+    from paper_2311_05945_b200 import workloads as WL
+    from paper_2311_05945_b200.solver import SolverConfig
+    from paper_2311_05945_b200.world import GpuWorld
+
+    E, K = 8, 6
+    cfg = SolverConfig()
+
+    def run(env):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        scenes, grippers, half, poses = WL.grasp_batch(E, seed=11)
+        w = GpuWorld(scenes)
+        w.upload_schedule(WL.schedule(grippers, half, poses, K))
+        for k in range(K):
+            w.step_scheduled(cfg, k, want_reports=False)
+        return [[w.candidates(e, which) for which in (0, 1, 2)] for e in range(E)], w.get_state()[0]
+
+    base = {"IPC_BROAD_SM": "1"}
+    alt = {"IPC_BROAD_SM": "0"}
+    if items:
+        alt["IPC_BROAD_ITEMS"] = items  # force several CTAs per env in the global version
+    ca, xa = run(base)
+    cb, xb = run(alt)
+    for e in range(E):
+        for which in range(3):
+            assert np.array_equal(ca[e][which], cb[e][which]), (e, which)
+    assert np.array_equal(xa, xb)
