@@ -430,6 +430,8 @@ struct ipc_world {
       cs.c.pre_pt = pool.alloc<int>(n_env + 1);
       cs.c.pre_ee = pool.alloc<int>(n_env + 1);
       cs.c.pre_gnd = pool.alloc<int>(n_env + 1);
+      cs.c.need_pt = pool.alloc<int>(n_env);
+      cs.c.need_ee = pool.alloc<int>(n_env);
     }
     if (&cs == &dcd) {  // derivative work lists track the DCD capacity
       for (int k = 0; k < 2; ++k) {
@@ -539,13 +541,16 @@ struct ipc_world {
         IPC_LAUNCH(K_MISC, st, k_prefix3, 3, 1024, 0, n_env, cs.c, env_mask);
         return;
       }
-      // grow: read counts are clipped, so grow every env capacity 4x
+      // grow the overflowed envs to 1.5x their unclipped counts (at least 4x)
+      std::vector<int> np(n_env), nq(n_env);
+      CK(cudaMemcpy(np.data(), cs.c.need_pt, 4 * n_env, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(nq.data(), cs.c.need_ee, 4 * n_env, cudaMemcpyDeviceToHost));
       std::vector<long long> ptc = cs.pt_cap, eec = cs.ee_cap;
       for (int e = 0; e < n_env; ++e) {
         long long nv = h_env_slot[e + 1] - h_env_slot[e], nt = h_env_tri[e + 1] - h_env_tri[e];
         long long ne = h_env_edge[e + 1] - h_env_edge[e];
-        ptc[e] = std::min(nv * nt, 4 * ptc[e]);
-        eec[e] = std::min(ne * ne, 4 * eec[e]);
+        if (np[e] > ptc[e]) ptc[e] = std::min(nv * nt, std::max(4 * ptc[e], (long long)np[e] * 3 / 2));
+        if (nq[e] > eec[e]) eec[e] = std::min(ne * ne, std::max(4 * eec[e], (long long)nq[e] * 3 / 2));
       }
       alloc_cands(cs, ptc, eec);
       alloc_pairbufs(pb, cs, derivs);
@@ -700,16 +705,24 @@ struct ipc_world {
   void grow_overflowed() {
     CK(cudaStreamSynchronize(st));
     for (CandStore* cs : {&dcd, &sweep}) {
+      // the broad phase records each env's unclipped candidate count: grow
+      // straight to 1.5x that (at least 4x), so one replay suffices
       std::vector<int> np(n_env), ne(n_env);
-      CK(cudaMemcpy(np.data(), cs->c.n_pt, 4 * n_env, cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(ne.data(), cs->c.n_ee, 4 * n_env, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(np.data(), cs->c.need_pt, 4 * n_env, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ne.data(), cs->c.need_ee, 4 * n_env, cudaMemcpyDeviceToHost));
       std::vector<long long> ptc = cs->pt_cap, eec = cs->ee_cap;
       bool grew = false;
       for (int e = 0; e < n_env; ++e) {
         long long nv = h_env_slot[e + 1] - h_env_slot[e], nt = h_env_tri[e + 1] - h_env_tri[e];
         long long nE = h_env_edge[e + 1] - h_env_edge[e];
-        if (np[e] >= ptc[e] && ptc[e] < nv * nt) { ptc[e] = std::min(nv * nt, 4 * std::max(ptc[e], 1LL)); grew = true; }
-        if (ne[e] >= eec[e] && eec[e] < nE * nE) { eec[e] = std::min(nE * nE, 4 * std::max(eec[e], 1LL)); grew = true; }
+        if (np[e] > ptc[e] && ptc[e] < nv * nt) {
+          ptc[e] = std::min(nv * nt, std::max(4 * std::max(ptc[e], 1LL), (long long)np[e] * 3 / 2));
+          grew = true;
+        }
+        if (ne[e] > eec[e] && eec[e] < nE * nE) {
+          eec[e] = std::min(nE * nE, std::max(4 * std::max(eec[e], 1LL), (long long)ne[e] * 3 / 2));
+          grew = true;
+        }
       }
       if (!grew) continue;
       alloc_cands(*cs, ptc, eec);

@@ -312,6 +312,8 @@ __device__ bool env_broad_sm(const World& W, const double* __restrict__ lo, cons
       __syncthreads();
     }
     if (tid == 0) {
+      int need = (int)min(base, (long long)INT_MAX);
+      if (kind == 0) C.need_pt[e] = need; else C.need_ee[e] = need;
       if (base > cap) {
         atomicExch(C.overflow, 1);
         base = cap;

@@ -1,5 +1,6 @@
 // Kernels of the batched IPC time step. See DESIGN.md for the data flow.
 #pragma once
+#include <climits>
 #include "ipc_math.cuh"
 #include "world.cuh"
 
@@ -395,6 +396,8 @@ __device__ void broad_env(const World& W, const double* __restrict__ lo, const d
     base = grand;
   }
   if (threadIdx.x == 0) {
+    int need = (int)min(base, (long long)INT_MAX);
+    if (kind == 0) C.need_pt[e] = need; else C.need_ee[e] = need;
     if (base > cap) {
       atomicExch(C.overflow, 1);
       base = cap;

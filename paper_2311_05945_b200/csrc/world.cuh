@@ -31,6 +31,7 @@ struct Cands {
   const int* gnd_off;       // == env_slot
   int* overflow;            // [1] set when a capacity is exceeded
   int *pre_pt, *pre_ee, *pre_gnd;  // [n_env+1] prefix of counts over flagged envs
+  int *need_pt, *need_ee;           // [n_env] unclipped counts of the last broad phase (capacity growth)
 };
 
 struct Lags {  // lagged friction (ref friction.py:35)
