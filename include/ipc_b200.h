@@ -181,6 +181,45 @@ int ipc_psd_project(int dim, int64_t n, double *mats);
 int ipc_elastic_eval(int model, int64_t n, const double *F, double mu, double lam, double *psi,
                      double *P, double *H9);
 
+/* ---- penetrated-grasp repair (ref robot/repair.py, robot/proximity.py) ----
+ * A batch of E repair problems, flattened with per-env prefix arrays.
+ * Hand: env e owns links [env_link[e], env_link[e+1]); link l owns world
+ * vertices [link_vert[l], link_vert[l+1]) of hand_v (placed at probe 0, i.e.
+ * the input pose with the opened joints) and triangles [link_tri[l],
+ * link_tri[l+1]) of hand_t (GLOBAL indices into hand_v). Object of env e:
+ * vertices [env_obj_vert[e], ..) of obj_v, triangles [env_obj_tri[e], ..) of
+ * obj_t (indices LOCAL to the env's object). Probe k translates the hand by
+ * -retraction[k] * normal[e]. */
+typedef struct ipc_repair_desc {
+  int32_t n_env;
+  const int32_t *env_link, *link_vert, *link_tri;
+  const double *hand_v;
+  const int32_t *hand_t;
+  const int32_t *env_obj_vert, *env_obj_tri;
+  const double *obj_v;
+  const int32_t *obj_t;
+  const double *normal;     /* [3E] world palm normal per env */
+  int32_t n_probe;
+  const double *retraction; /* [n_probe] probe distances (m) */
+} ipc_repair_desc;
+
+/* First probe whose placement has no crossing triangles and no containment
+ * either way (ref repair.py:98-113 loop with _hand_object_overlap :49);
+ * probe_index[e] = n_probe when no probe clears (unsalvageable). */
+int ipc_repair_retract(const ipc_repair_desc *d, int32_t *probe_index);
+/* ref proximity.py:254 max_penetration, batched: env e's points
+ * [env_pt[e], env_pt[e+1]) of pts against its object mesh. */
+int ipc_max_penetration(int32_t n_env, const int32_t *env_pt, const double *pts,
+                        const int32_t *env_obj_vert, const int32_t *env_obj_tri,
+                        const double *obj_v, const int32_t *obj_t, double *out);
+/* ref proximity.py:183 winding_numbers */
+int ipc_winding_numbers(int64_t n_pts, const double *pts, int32_t n_verts, const double *verts,
+                        int32_t n_tris, const int32_t *tris, double *out);
+/* ref proximity.py:163 count_mesh_intersections */
+int ipc_count_mesh_intersections(int32_t nva, const double *va, int32_t nta, const int32_t *ta,
+                                 int32_t nvb, const double *vb, int32_t ntb, const int32_t *tb,
+                                 int64_t *count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,6 +56,14 @@ class StepReportC(C.Structure):
                 ("kappa", C.c_double)]
 
 
+class RepairDesc(C.Structure):
+    _fields_ = [("n_env", C.c_int32), ("env_link", _i32p), ("link_vert", _i32p),
+                ("link_tri", _i32p), ("hand_v", _f64p), ("hand_t", _i32p),
+                ("env_obj_vert", _i32p), ("env_obj_tri", _i32p), ("obj_v", _f64p),
+                ("obj_t", _i32p), ("normal", _f64p), ("n_probe", C.c_int32),
+                ("retraction", _f64p)]
+
+
 # symbol -> (restype, argtypes); the authoritative list of C-ABI exports
 SIGNATURES = {
     "ipc_last_error": (C.c_char_p, []),
@@ -98,6 +106,13 @@ SIGNATURES = {
     "ipc_psd_project": (C.c_int, [C.c_int, C.c_int64, _f64p]),
     "ipc_elastic_eval": (C.c_int, [C.c_int, C.c_int64, _f64p, C.c_double, C.c_double, _f64p,
                                    _f64p, _f64p]),
+    "ipc_repair_retract": (C.c_int, [C.POINTER(RepairDesc), _i32p]),
+    "ipc_max_penetration": (C.c_int, [C.c_int32, _i32p, _f64p, _i32p, _i32p, _f64p, _i32p,
+                                      _f64p]),
+    "ipc_winding_numbers": (C.c_int, [C.c_int64, _f64p, C.c_int32, _f64p, C.c_int32, _i32p,
+                                      _f64p]),
+    "ipc_count_mesh_intersections": (C.c_int, [C.c_int32, _f64p, C.c_int32, _i32p, C.c_int32,
+                                               _f64p, C.c_int32, _i32p, _i64p]),
 }
 
 KERNEL_IDS = ("broad_dcd", "broad_ccd", "pairs_deriv", "pairs_value", "tet", "body", "ground",

@@ -31,6 +31,9 @@ static int set_err(const char* fmt, ...) {
   return -1;
 }
 
+// error sink for the other translation units of the library (repair.cu)
+extern "C" int ipc__set_error(const char* msg) { return set_err("%s", msg); }
+
 #define CK(call)                                                                     \
   do {                                                                               \
     cudaError_t e_ = (call);                                                         \

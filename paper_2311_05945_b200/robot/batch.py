@@ -67,14 +67,19 @@ class BatchGrasp:
     """
 
     def __init__(self, model, objects, poses, joints, grasp_cfg=None, solver_cfg=None,
-                 density=2000.0, **scene_kwargs):
+                 density=2000.0, grippers=None, target_poses=None, autograsp_only=False,
+                 **scene_kwargs):
         from ..solver import SolverConfig
 
         self.gc = grasp_cfg or GraspConfig()
         self.sc = solver_cfg or SolverConfig()
         self.E = E = len(objects)
         self.objects = list(objects)
-        self.grippers = [Gripper(model, density=density) for _ in range(E)]
+        self.grippers = (list(grippers) if grippers is not None
+                         else [Gripper(model, density=density) for _ in range(E)])
+        # autograsp_only: stop after AutoGrasp (ref repair.py:129 runs only
+        # that phase); envs that reach the stop force finish with no outcome
+        self.autograsp_only = autograsp_only
         g0 = self.grippers[0]
         self.joint_names, self.finger_names = g0.joint_names, g0.finger_names
         self.lo = np.array([j.lower for j in g0.joints])
@@ -86,6 +91,12 @@ class BatchGrasp:
         self.world = w = GpuWorld(self.scenes)
         self.links = sorted(g0.links)  # == order of Gripper.constraints()
         self.pose = np.array([g.pose for g in self.grippers])
+        if target_poses is not None:
+            # scenes start at `poses`, targets command `target_poses`
+            # (ref repair.py:126 gripper.set_targets(pose=pose))
+            self.pose = np.array(target_poses, dtype=np.float64)
+            for g, tp in zip(self.grippers, self.pose):
+                g.set_targets(pose=tp)
         self.q = np.array([g.joint_values for g in self.grippers])
         self.base = self.pose.copy()
         self.lifted = self.pose.copy()
@@ -142,7 +153,10 @@ class BatchGrasp:
                 self.forces[e].append(f[e].copy())
             reached = auto & np.all(f >= gc.stop_force, axis=1)
             self._finish(auto & ~reached & (self.frames >= gc.budget), GraspOutcome.ABORTED)
-            ph[reached] = LIFT_CHECK
+            if self.autograsp_only:
+                ph[reached] = DONE
+            else:
+                ph[reached] = LIFT_CHECK
             close = (ph == AUTO)
             if close.any():
                 inc = gc.close_rate * phi_vec(f, gc.phi_k, gc.phi_f_star)
@@ -195,6 +209,17 @@ class BatchGrasp:
         self.steps[stepping] += 1
         self.phase = nxt
         return True
+
+    def sync_scenes(self):
+        """Copy the device state back into the scenes' bodies (gripper links,
+        objects) so host-side queries see the final placement."""
+        x, v = self.world.get_state()
+        off = 0
+        for sc in self.scenes:
+            n = len(sc.state.gather())
+            sc.state.scatter(x[off:off + n])
+            sc.state.scatter_velocity(v[off:off + n])
+            off += n
 
     def run(self, max_ticks=100_000):
         while max_ticks > 0 and self.tick():

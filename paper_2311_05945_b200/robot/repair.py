@@ -1,0 +1,224 @@
+"""Penetrated-grasp repair: open, retract, re-grasp under spring targets
+(ref pkg/src/srsim/robot/repair.py).
+
+Same names, arguments and results as the reference: ``repair_grasp`` (:82),
+``RepairResult`` (:40), ``RETRACT_STEP`` / ``RETRACT_MAX`` (:36-37). The
+geometric half (the retraction probe loop, ref :98-113, with the overlap test
+of :49) runs on the GPU as one ``ipc_repair_retract`` call that evaluates
+every crossing-pair and containment test of a window of probes at once; the
+dynamic half is AutoGrasp on the GPU step engine. ``repair_batch`` repairs E
+grasps together (config 4): one retraction launch for all envs, one
+``BatchGrasp`` world for the cleared ones, one batched penetration query.
+
+No CPU fallback: with the library or device missing every call raises.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .. import _native as N
+from .grasp import GraspConfig, GraspOutcome, GraspPhase, GraspTrial, autograsp, build_grasp_scene
+from .proximity import max_penetration_batch, surface_samples
+
+RETRACT_STEP = 1e-3  # m per probe (ref repair.py:36)
+RETRACT_MAX = 0.5    # m; beyond this the grasp is unsalvageable (ref :37)
+
+
+@dataclass
+class RepairResult:
+    """ref repair.py:40"""
+    trial: GraspTrial
+    cleared: bool  # retraction found an intersection-free placement
+    retraction_m: float
+    penetration_before_m: float
+    penetration_after_m: float
+
+
+def retraction_schedule():
+    """Probe distances the reference visits — retraction accumulated by
+    repeated ``+= RETRACT_STEP`` while ``<= RETRACT_MAX`` (ref :103-113) —
+    and the distance it reports when no probe clears."""
+    out, r = [], 0.0
+    while r <= RETRACT_MAX:
+        out.append(r)
+        r += RETRACT_STEP
+    return np.array(out), r
+
+
+def _world_mesh(obj):
+    """(world vertices, triangles) of the object (ref repair.py:65)."""
+    from ..bodies import SoftBody
+
+    if isinstance(obj, SoftBody):
+        return obj.x.copy(), np.asarray(obj.mesh.surface.triangles)
+    return obj.world_vertices(), np.asarray(obj.mesh.triangles)
+
+
+def _hand_points(gripper) -> np.ndarray:
+    """ref repair.py:73"""
+    return np.concatenate([surface_samples(b.world_vertices(), b.mesh.triangles, b.mesh.edges)
+                           for b in gripper.bodies()])
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def retract_batch(grippers, poses, opened, obj_meshes):
+    """The probe loop of ref repair.py:98-113 for E envs in one launch.
+
+    grippers: E Gripper instances (placed here at each env's probe-0 pose
+    with its opened joints and left there); poses (E,4,4); opened (E,J);
+    obj_meshes: E (world verts, tris). Returns (cleared bool[E],
+    retraction_m float[E], probe_index int[E]); retraction_m is the
+    reference's accumulated distance (the past-the-cap value when no probe
+    clears)."""
+    lib = N.load()
+    E = len(grippers)
+    sched, end = retraction_schedule()
+    if E == 0:
+        return np.zeros(0, bool), np.zeros(0), np.zeros(0, np.int32)
+    env_link, link_vert, link_tri = [0], [0], [0]
+    hv, ht, normals = [], [], []
+    for g, p, q in zip(grippers, poses, opened):
+        g.place(p, q)
+        normals.append(g.palm_normal(p))
+        for b in g.bodies():
+            v = b.world_vertices()
+            ht.append(np.asarray(b.mesh.triangles, dtype=np.int64) + link_vert[-1])
+            hv.append(v)
+            link_vert.append(link_vert[-1] + len(v))
+            link_tri.append(link_tri[-1] + len(b.mesh.triangles))
+        env_link.append(len(link_vert) - 1)
+    ov = _f64(np.concatenate([m[0] for m in obj_meshes]))
+    ot = _i32(np.concatenate([np.reshape(m[1], (-1, 3)) for m in obj_meshes]))
+    env_ov = _i32(np.concatenate([[0], np.cumsum([len(m[0]) for m in obj_meshes])]))
+    env_ot = _i32(np.concatenate([[0], np.cumsum([len(np.reshape(m[1], (-1, 3)))
+                                                  for m in obj_meshes])]))
+    arrs = dict(env_link=_i32(env_link), link_vert=_i32(link_vert), link_tri=_i32(link_tri),
+                hand_v=_f64(np.concatenate(hv)), hand_t=_i32(np.concatenate(ht)),
+                env_ov=env_ov, env_ot=env_ot, obj_v=ov, obj_t=ot,
+                normal=_f64(np.array(normals)), retr=_f64(sched))
+    d = N.RepairDesc(E, N.ptr(arrs["env_link"], N._i32p), N.ptr(arrs["link_vert"], N._i32p),
+                     N.ptr(arrs["link_tri"], N._i32p), N.ptr(arrs["hand_v"], N._f64p),
+                     N.ptr(arrs["hand_t"], N._i32p), N.ptr(arrs["env_ov"], N._i32p),
+                     N.ptr(arrs["env_ot"], N._i32p), N.ptr(arrs["obj_v"], N._f64p),
+                     N.ptr(arrs["obj_t"], N._i32p), N.ptr(arrs["normal"], N._f64p),
+                     len(sched), N.ptr(arrs["retr"], N._f64p))
+    idx = np.zeros(E, np.int32)
+    N.check(lib.ipc_repair_retract(N.C.byref(d), N.ptr(idx, N._i32p)))
+    cleared = idx < len(sched)
+    retraction = np.where(cleared, sched[np.minimum(idx, len(sched) - 1)], end)
+    return cleared, retraction, idx
+
+
+def _probe_pose(pose, gripper, r):
+    probe = np.array(pose, dtype=np.float64)
+    probe[:3, 3] -= r * gripper.palm_normal(pose)
+    return probe
+
+
+def repair_grasp(obj, gripper, pose, joint_values, open_offset: float = 0.01,
+                 grasp_cfg: GraspConfig = None, solver_cfg=None, backend=None,
+                 **scene_kwargs) -> RepairResult:
+    """Clear interpenetration, then AutoGrasp with springs to the input pose
+    (ref repair.py:82)."""
+    from ..solver import SolverConfig
+
+    gc = grasp_cfg or GraspConfig()
+    sc = solver_cfg or SolverConfig()
+    pose = np.asarray(pose, dtype=np.float64)
+    joint_values = np.asarray(joint_values, dtype=np.float64)
+    trial = GraspTrial(pose.copy(), joint_values.copy())
+    ov, ot = _world_mesh(obj)
+
+    gripper.place(pose, joint_values)
+    pen_before = float(max_penetration_batch([_hand_points(gripper)], [(ov, ot)])[0])
+
+    opened = gripper.clamp_joints(joint_values - open_offset)
+    cleared, retraction, _ = retract_batch([gripper], [pose], [opened], [(ov, ot)])
+    cleared, retraction = bool(cleared[0]), float(retraction[0])
+    trial.retraction_m = retraction
+    if not cleared:
+        trial.outcome = GraspOutcome.ABORTED
+        trial.advance(GraspPhase.DONE)
+        return RepairResult(trial, False, retraction, pen_before, pen_before)
+
+    probe = _probe_pose(pose, gripper, retraction)
+    gripper.place(probe, opened)
+    scene = build_grasp_scene(obj, gripper, probe, opened, h=sc.h, **scene_kwargs)
+    gripper.set_targets(pose=pose)
+    autograsp(scene, gripper, trial, gc, sc, backend)
+
+    pv, pt = _world_mesh(obj)
+    pen_after = float(max_penetration_batch([_hand_points(gripper)], [(pv, pt)])[0])
+    trial.penetration_m = pen_after
+    if trial.outcome is None:
+        trial.outcome = GraspOutcome.SUCCESS
+        trial.advance(GraspPhase.DONE)
+    return RepairResult(trial, True, retraction, pen_before, pen_after)
+
+
+def repair_batch(model, objects, poses, joint_values, open_offset: float = 0.01,
+                 grasp_cfg: GraspConfig = None, solver_cfg=None, density: float = 2000.0,
+                 max_ticks: int = 100_000, **scene_kwargs):
+    """``repair_grasp`` for E grasps at once (config 4). Returns E RepairResults.
+
+    Geometry: one retraction launch for every env; dynamics: the cleared envs
+    share one BatchGrasp world running AutoGrasp only, with link targets at
+    the input poses; penetration before/after: one batched query each."""
+    from .batch import BatchGrasp
+    from .gripper import Gripper
+
+    E = len(objects)
+    poses = np.asarray(poses, dtype=np.float64).reshape(E, 4, 4)
+    joint_values = np.asarray(joint_values, dtype=np.float64).reshape(E, -1)
+    grippers = [Gripper(model, density=density) for _ in range(E)]
+    meshes = [_world_mesh(o) for o in objects]
+    for g, p, q in zip(grippers, poses, joint_values):
+        g.place(p, q)
+    pen_before = max_penetration_batch([_hand_points(g) for g in grippers], meshes)
+    opened = np.array([g.clamp_joints(q - open_offset) for g, q in zip(grippers, joint_values)])
+    cleared, retraction, _ = retract_batch(grippers, poses, opened, meshes)
+
+    trials = [GraspTrial(p.copy(), q.copy()) for p, q in zip(poses, joint_values)]
+    results = [None] * E
+    for e in np.nonzero(~cleared)[0]:
+        t = trials[e]
+        t.retraction_m = float(retraction[e])
+        t.outcome = GraspOutcome.ABORTED
+        t.advance(GraspPhase.DONE)
+        results[e] = RepairResult(t, False, float(retraction[e]), float(pen_before[e]),
+                                  float(pen_before[e]))
+    live = np.nonzero(cleared)[0]
+    if len(live) == 0:
+        return results
+    probes = np.array([_probe_pose(poses[e], grippers[e], retraction[e]) for e in live])
+    bg = BatchGrasp(model, [objects[e] for e in live], probes, opened[live],
+                    grasp_cfg=grasp_cfg, solver_cfg=solver_cfg,
+                    grippers=[grippers[e] for e in live], target_poses=poses[live],
+                    autograsp_only=True, **scene_kwargs)
+    bg.run(max_ticks)
+    bg.sync_scenes()
+    pen_after = max_penetration_batch([_hand_points(grippers[e]) for e in live],
+                                      [_world_mesh(objects[e]) for e in live])
+    for i, e in enumerate(live):
+        t = trials[e]
+        t.retraction_m = float(retraction[e])
+        t.advance(GraspPhase.AUTOGRASP)
+        t.forces = bg.forces[i]
+        t.increments = bg.increments[i]
+        t.steps = int(bg.steps[i])
+        t.penetration_m = float(pen_after[i])
+        t.outcome = bg.outcome[i] if bg.outcome[i] is not None else GraspOutcome.SUCCESS
+        t.advance(GraspPhase.DONE)
+        results[e] = RepairResult(t, True, float(retraction[e]), float(pen_before[e]),
+                                  float(pen_after[i]))
+    return results

@@ -109,3 +109,30 @@ def soft_grasp(divisions: int = 12, mu: float = 0.5):
                     Material(youngs_modulus=1e5, poisson_ratio=0.3, density=500.0))
     sc = build_grasp_scene(cube, g, top_down_pose((0.0, cy, 0.0)), [0.0, 0.0], mu=mu)
     return sc, g, cube
+
+
+def repair_batch(n_env: int, seed: int = 0):
+    """Config 4: penetrated grasps to repair (ref robot/repair.py:82).
+
+    Each env is the parallel-jaw gripper on one synthetic rigid object (a box
+    or a Fibonacci sphere, ``grasp_object``) with the palm pushed 0-15 mm into
+    the object top and each finger commanded up to 5 mm past contact, so the
+    input placement interpenetrates. Returns (objects, poses (E,4,4),
+    joints (E,2)). The objects are fresh bodies: a caller may build scenes
+    from them.
+    """
+    rng = np.random.default_rng(seed)
+    objs, poses, joints = [], [], []
+    for _ in range(n_env):
+        obj, hw, yaw = grasp_object(rng)
+        top = float(obj.world_vertices()[:, 1].max())
+        depth = float(rng.uniform(0.0, 0.015))
+        # the palm face sits 6 cm above the grasp target of top_down_pose
+        # (ref tests/test_robot.py:534: target 0.06 + 10 mm below the top)
+        pose = top_down_pose((0.0, top - 0.06 - depth, 0.0), yaw=yaw)
+        qc = HALF_APERTURE - hw
+        q = np.clip(qc + rng.uniform(-0.004, 0.005, size=2), 0.0, 0.045)
+        objs.append(obj)
+        poses.append(pose)
+        joints.append(q)
+    return objs, np.array(poses), np.array(joints)
