@@ -177,9 +177,13 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=0, help="envs in the CPU sample (0 = one per core)")
     ap.add_argument("--cpu-steps", type=int, default=0, help="timed CPU steps (0 = the GPU's K)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", choices=("grasp", "repair"), default="grasp",
+                    help="grasp = config 3 (headline); repair = config 4 (penetrated-grasp repair)")
     args = ap.parse_args()
     ws, rank, lr = _dist()
     K, W = args.steps, max(args.warmup, 3)
+    if args.workload == "repair":
+        return repair_main(args, ws, rank, lr, K, W)
 
     if args.impl == "reference":
         if rank != 0:
@@ -344,6 +348,167 @@ def main():
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": used, "kind": "port",
                                 "sample": f"first {sample} envs of the same batch, the same {ksteps} timed "
                                           f"steps after {W} warm-up steps, oracle/ numpy port, one env per core"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# config 4: penetrated-grasp repair (ref robot/repair.py)
+# ---------------------------------------------------------------------------
+
+REPAIR_METRIC = "repaired grasps/sec (retraction probe search, config 4)"
+REPAIR_UNIT = "grasps/s"
+# fp64 work per retraction launch is taken from the committed ncu capture
+# (profiles/r1e_repair_ncu.json: dadd + dmul + 2*dfma thread instructions)
+FP64_PEAK_TFLOPS = 37.0  # B200 nominal non-tensor fp64 (no measured figure in MEASURED_PEAKS.json)
+
+
+def _repair_inputs(E, seed, model=None):
+    from paper_2311_05945_b200 import data_path
+    from paper_2311_05945_b200 import workloads as WL
+    from paper_2311_05945_b200.robot import Gripper, parse_urdf
+    from paper_2311_05945_b200.robot.repair import _world_mesh
+
+    model = model or parse_urdf(data_path("pj_gripper.urdf"))
+    objs, poses, joints = WL.repair_batch(E, seed=seed)
+    grippers = [Gripper(model) for _ in range(E)]
+    opened = np.array([g.clamp_joints(q - 0.01) for g, q in zip(grippers, joints)])
+    return model, objs, poses, joints, grippers, opened, [_world_mesh(o) for o in objs]
+
+
+def _cpu_repair_worker(args):
+    E, worker, n_workers, seed, budget_s = args
+    sys.path.insert(0, ROOT)
+    from oracle import proximity as OP
+
+    _, objs, poses, _, grippers, opened, meshes = _repair_inputs(E, seed)
+    done, t = 0, 0.0
+    for e in range(worker, E, n_workers):
+        t0 = time.perf_counter()
+        OP.retract(grippers[e], poses[e], opened[e], meshes[e][0], meshes[e][1])
+        t += time.perf_counter() - t0
+        done += 1
+        if t > budget_s:
+            break
+    return done, t
+
+
+def repair_cpu_arm(E, seed, cores, budget_s=15.0):
+    import multiprocessing as mp
+
+    n_workers = min(cores, E)
+    jobs = [(E, w, n_workers, seed, budget_s) for w in range(n_workers)]
+    with mp.get_context("spawn").Pool(n_workers) as pool:
+        res = pool.map(_cpu_repair_worker, jobs)
+    done = sum(r[0] for r in res)
+    t = max(r[1] for r in res)
+    return done / t, done, n_workers
+
+
+def repair_main(args, ws, rank, lr, K, W):
+    """Config 4: E penetrated grasps per GPU. One step = the retraction probe
+    search of every grasp (ref repair.py:98-113). `value` = grasps / kernel
+    time (inputs resident); `e2e` = grasps / time of the public call
+    (host packing, H2D, kernel, D2H). The full repair (plus AutoGrasp dynamics
+    to the input pose and the post-repair penetration query) is timed once
+    beside it."""
+    E = args.envs if args.envs != 1024 else 4096
+    seed = shard_seed(args.seed, rank)
+    workload = (f"config4 penetrated-grasp repair: per GPU {E} parallel-jaw grasps on synthetic "
+                "boxes/spheres, palm 0-15 mm inside, fingers up to 5 mm past contact")
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cores = _cores()
+        v, done, used = repair_cpu_arm(E, args.seed, cores)
+        line = {"impl": "reference", "metric": REPAIR_METRIC, "value": v, "unit": REPAIR_UNIT,
+                "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": 1e3 * E / v,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": workload, "envs_per_gpu": E},
+                "cpu_baseline": {"value": v, "unit": REPAIR_UNIT, "cores": used, "kind": "port",
+                                 "sample": f"{done} grasps of the batch (~15 s per core)"},
+                "e2e": {"value": v, "unit": REPAIR_UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    from paper_2311_05945_b200 import _native
+    from paper_2311_05945_b200.robot.repair import repair_batch, retract_batch
+
+    lib = _native.load()
+    _native.check(lib.ipc_set_device(lr))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(lr)
+        dist.init_process_group("nccl")
+    model, objs, poses, joints, grippers, opened, meshes = _repair_inputs(E, seed)
+    for _ in range(W):
+        cleared, r, idx = retract_batch(grippers, poses, opened, meshes)
+    k_ms, e2e_s = [], 0.0
+    ms = np.zeros(1)
+    with Clocks(lr) as clk:
+        for _ in range(K):
+            t0 = time.perf_counter()
+            cleared, r, idx = retract_batch(grippers, poses, opened, meshes)
+            e2e_s += time.perf_counter() - t0
+            _native.check(lib.ipc_repair_last_kernel_ms(_native.ptr(ms, _native._f64p)))
+            k_ms.append(float(ms[0]))
+    total_ms = float(np.sum(k_ms))
+    if ws > 1:
+        total_ms, _ = gather_timing(total_ms, 0.0, device=f"cuda:{lr}")
+        e2e_s, _ = gather_timing(e2e_s, 0.0, device=f"cuda:{lr}")
+    value = E * ws * K / (total_ms * 1e-3)
+    nh = sum(len(g.bodies()) for g in grippers)
+    hv = sum(len(b.world_vertices()) for g in grippers[:1] for b in g.bodies()) * E
+    ht = sum(len(b.mesh.triangles) for g in grippers[:1] for b in g.bodies()) * E
+    ov, ot = sum(len(m[0]) for m in meshes), sum(len(m[1]) for m in meshes)
+    h2d = 24 * (hv + ov) + 12 * (ht + ot) + 4 * (2 * E + 2 * nh + 3) + 24 * E + 8 * 501
+    d2h = 4 * E
+    # full repair once: retraction + AutoGrasp (springs to the input pose) + penetration after
+    full = None
+    if os.environ.get("BENCH_REPAIR_FULL", "1") != "0":
+        t0 = time.perf_counter()
+        res = repair_batch(model, objs, poses, joints)
+        full_s = time.perf_counter() - t0
+        full = {"seconds": full_s, "grasps_per_s": E / full_s,
+                "cleared": int(sum(x.cleared for x in res)),
+                "max_penetration_after_m": max(x.penetration_after_m for x in res),
+                "autograsp_env_steps": int(sum(x.trial.steps for x in res)),
+                "note": "host scene build + retraction + AutoGrasp on the GPU engine + "
+                        "penetration query, wall clock, one run"}
+    flops = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1e_repair_ncu.json")) as fh:
+            nj = json.load(fh)
+        if nj.get("envs") == E and nj.get("seed") == args.seed:
+            flops = float(nj["fp64_flops"])
+    except (OSError, KeyError, ValueError):
+        pass
+    avg_s = total_ms * 1e-3 / K
+    achieved = flops / avg_s / 1e12 if flops else None
+    line = {"metric": REPAIR_METRIC, "value": value, "unit": REPAIR_UNIT, "n_gpus": ws, "steps": K,
+            "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "envs_per_gpu": E, "seed": args.seed,
+                       "l2": "inputs re-uploaded every step (fresh device buffers)"},
+            "roofline": {"bound": "fp64", "kernel": "k_repair_retract", "achieved": achieved,
+                         "peak": FP64_PEAK_TFLOPS, "peak_kind": "nominal", "unit": "TFLOP/s",
+                         "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
+                         "traffic": None, "launches": K, "avg_launch_us": avg_s * 1e6},
+            "e2e": {"value": E * ws * K / e2e_s, "unit": REPAIR_UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": K, "clocks": clk.summary(),
+            "cleared": int(cleared.sum()), "mean_probe": float(idx[cleared].mean()),
+            "full_repair": full}
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        v, done, used = repair_cpu_arm(E, args.seed, _cores())
+        line["cpu_baseline"] = {"value": v, "unit": REPAIR_UNIT, "cores": used, "kind": "port",
+                                "sample": f"{done} grasps of the same batch, oracle/ numpy port "
+                                          "of the probe loop, ~15 s per core"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -207,6 +207,9 @@ typedef struct ipc_repair_desc {
  * either way (ref repair.py:98-113 loop with _hand_object_overlap :49);
  * probe_index[e] = n_probe when no probe clears (unsalvageable). */
 int ipc_repair_retract(const ipc_repair_desc *d, int32_t *probe_index);
+/* device time (ms, CUDA events on the launching stream) of the last
+ * ipc_repair_retract kernel launch; measurement hook, no reference analogue */
+int ipc_repair_last_kernel_ms(double *ms);
 /* ref proximity.py:254 max_penetration, batched: env e's points
  * [env_pt[e], env_pt[e+1]) of pts against its object mesh. */
 int ipc_max_penetration(int32_t n_env, const int32_t *env_pt, const double *pts,

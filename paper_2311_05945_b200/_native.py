@@ -107,6 +107,7 @@ SIGNATURES = {
     "ipc_elastic_eval": (C.c_int, [C.c_int, C.c_int64, _f64p, C.c_double, C.c_double, _f64p,
                                    _f64p, _f64p]),
     "ipc_repair_retract": (C.c_int, [C.POINTER(RepairDesc), _i32p]),
+    "ipc_repair_last_kernel_ms": (C.c_int, [_f64p]),
     "ipc_max_penetration": (C.c_int, [C.c_int32, _i32p, _f64p, _i32p, _i32p, _f64p, _i32p,
                                       _f64p]),
     "ipc_winding_numbers": (C.c_int, [C.c_int64, _f64p, C.c_int32, _f64p, C.c_int32, _i32p,

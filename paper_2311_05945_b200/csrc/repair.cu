@@ -160,54 +160,127 @@ struct RepairDev {
   const double *hand_v, *obj_v, *normal, *retr;
 };
 
-// ref repair.py:103-113 for one env per CTA; out[e] = first clear probe or n_probe
+// Containment shortcut: the winding number of a closed surface is 0 at every
+// point outside the surface's bounding box (it is 0 outside the solid), so a
+// point outside the box (with a 1e-9 m guard against rounding) is decided
+// "not inside" without evaluating it; the reference's thresholded decision
+// (> 0.5) is unchanged.
+constexpr double kBoxGuard = 1e-9;
+
+__device__ __forceinline__ bool outside_box(V3 x, V3 lo, V3 hi) {
+  return x.x < lo.x - kBoxGuard || x.x > hi.x + kBoxGuard || x.y < lo.y - kBoxGuard ||
+         x.y > hi.y + kBoxGuard || x.z < lo.z - kBoxGuard || x.z > hi.z + kBoxGuard;
+}
+
+// block-wide bounding box of vertices [v0, v1) of v (all threads call)
+__device__ void block_box(const double* __restrict__ v, int v0, int v1, V3& lo, V3& hi) {
+  __shared__ double red[6][kThreads / 32];
+  double a[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  for (int i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
+    V3 x = ldv(v, i);
+    a[0] = fmin(a[0], x.x), a[1] = fmin(a[1], x.y), a[2] = fmin(a[2], x.z);
+    a[3] = fmax(a[3], x.x), a[4] = fmax(a[4], x.y), a[5] = fmax(a[5], x.z);
+  }
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    for (int o = 16; o; o >>= 1) {
+      double b = __shfl_xor_sync(0xffffffffu, a[c], o);
+      a[c] = c < 3 ? fmin(a[c], b) : fmax(a[c], b);
+    }
+    if ((threadIdx.x & 31) == 0) red[c][threadIdx.x >> 5] = a[c];
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int c = threadIdx.x;
+    double m = red[c][0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = c < 3 ? fmin(m, red[c][w]) : fmax(m, red[c][w]);
+    red[c][0] = m;
+  }
+  __syncthreads();
+  lo = V3{red[0][0], red[1][0], red[2][0]};
+  hi = V3{red[3][0], red[4][0], red[5][0]};
+  __syncthreads();
+}
+
+constexpr int kMaxLinks = 32;
+// triangle boxes staged in shared memory when an env fits (hand at probe 0,
+// object); larger envs test boxes from the vertices in global memory
+constexpr int kStageHT = 64, kStageOT = 448;
+
+// ref repair.py:103-113 for one env per CTA; out[e] = first clear probe or n_probe.
+// Items of one probe, crossing pairs first (cheap, box-filtered, and the
+// usual reason a probe is rejected — a hit flags the probe and its remaining
+// items, including the winding numbers, are skipped), then hand-vertex
+// containment, then link-swallows-object containment.
 __global__ void __launch_bounds__(kThreads) k_repair_retract(RepairDev D, int32_t* out) {
   const int e = blockIdx.x;
   __shared__ int flag[kMaxWindow];
   __shared__ int s_found;
+  __shared__ double s_lbox[kMaxLinks][6];
+  __shared__ double s_hbox[kStageHT][6];
+  __shared__ double s_obox[kStageOT][6];
   const int l0 = D.env_link[e], l1 = D.env_link[e + 1];
   const int hv0 = D.link_vert[l0], hv1 = D.link_vert[l1];
   const int ht0 = D.link_tri[l0], ht1 = D.link_tri[l1];
-  const int ov0 = D.env_ov[e], ot0 = D.env_ot[e], ot1 = D.env_ot[e + 1];
+  const int ov0 = D.env_ov[e], ov1 = D.env_ov[e + 1], ot0 = D.env_ot[e], ot1 = D.env_ot[e + 1];
   const int HT = ht1 - ht0, HV = hv1 - hv0, NL = l1 - l0, NOT = ot1 - ot0;
   const V3 n = V3{D.normal[3 * e], D.normal[3 * e + 1], D.normal[3 * e + 2]};
-  const long long per_probe = (long long)HT * NOT + HV + NL;
+  const int n_cross = HT * NOT;
+  const int per_probe = n_cross + HV + NL;
+  const bool staged = HT <= kStageHT && NOT <= kStageOT;
+  V3 olo, ohi;
+  block_box(D.obj_v, ov0, ov1, olo, ohi);
+  // probe-0 link boxes (NL <= kMaxLinks: links beyond it are never boxed)
+  for (int l = 0; l < min(NL, kMaxLinks); ++l) {
+    V3 lo, hi;
+    block_box(D.hand_v, D.link_vert[l0 + l], D.link_vert[l0 + l + 1], lo, hi);
+    if (threadIdx.x == 0) {
+      s_lbox[l][0] = lo.x, s_lbox[l][1] = lo.y, s_lbox[l][2] = lo.z;
+      s_lbox[l][3] = hi.x, s_lbox[l][4] = hi.y, s_lbox[l][5] = hi.z;
+    }
+  }
+  if (staged) {
+    // box of a translated triangle == translated box: x -> rn(x - d) is monotone
+    for (int i = threadIdx.x; i < HT + NOT; i += blockDim.x) {
+      V3 t[3];
+      const bool hand = i < HT;
+      const int j = hand ? ht0 + i : ot0 + i - HT;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        t[c] = hand ? ldv(D.hand_v, __ldg(D.hand_t + 3 * j + c))
+                    : ldv(D.obj_v, ov0 + __ldg(D.obj_t + 3 * j + c));
+      V3 lo, hi;
+      tri_box(t, lo, hi);
+      double* b = hand ? s_hbox[i] : s_obox[i - HT];
+      b[0] = lo.x, b[1] = lo.y, b[2] = lo.z, b[3] = hi.x, b[4] = hi.y, b[5] = hi.z;
+    }
+  }
   int k0 = 0, win = 1;
   if (threadIdx.x == 0) s_found = D.n_probe;
   while (k0 < D.n_probe) {
     const int W = min(win, D.n_probe - k0);
     if (threadIdx.x < kMaxWindow) flag[threadIdx.x] = 0;
     __syncthreads();
-    const long long total = per_probe * W;
-    for (long long it = threadIdx.x; it < total; it += blockDim.x) {
-      const int p = (int)(it / per_probe);
+    const int total = per_probe * W;
+    for (int it = threadIdx.x; it < total; it += blockDim.x) {
+      const int p = it / per_probe;
       if (*(volatile int*)&flag[p]) continue;
-      long long r = it - (long long)p * per_probe;
+      const int r = it - p * per_probe;
       const double rr = D.retr[k0 + p];
       bool hit = false;
-      if (r < HV) {
-        // hand vertex contained in the object (ref repair.py:56)
-        V3 x = shifted(ldv(D.hand_v, hv0 + (int)r), rr, n);
-        hit = winding(x, D.obj_v, D.obj_t, ot0, ot1, ov0, V3{0, 0, 0}, false) > 0.5;
-      } else if (r < HV + NL) {
-        // object's first vertex swallowed by a link (ref repair.py:59)
-        const int l = l0 + (int)(r - HV);
-        V3 d = V3{__dmul_rn(rr, n.x), __dmul_rn(rr, n.y), __dmul_rn(rr, n.z)};
-        V3 x = ldv(D.obj_v, ov0);
-        double w = 0.0;
-        for (int j = D.link_tri[l]; j < D.link_tri[l + 1]; ++j) {
-          V3 A = ldv(D.hand_v, __ldg(D.hand_t + 3 * j)), B = ldv(D.hand_v, __ldg(D.hand_t + 3 * j + 1)),
-             C = ldv(D.hand_v, __ldg(D.hand_t + 3 * j + 2));
-          A = V3{__dsub_rn(A.x, d.x), __dsub_rn(A.y, d.y), __dsub_rn(A.z, d.z)};
-          B = V3{__dsub_rn(B.x, d.x), __dsub_rn(B.y, d.y), __dsub_rn(B.z, d.z)};
-          C = V3{__dsub_rn(C.x, d.x), __dsub_rn(C.y, d.y), __dsub_rn(C.z, d.z)};
-          w += solid_angle(x, A, B, C);
-        }
-        hit = w / kTwoPi > 0.5;
-      } else {
+      if (r < n_cross) {
         // crossing triangle pair (ref repair.py:53, proximity.py:163)
-        r -= HV + NL;
-        const int i = ht0 + (int)(r / NOT), j = ot0 + (int)(r % NOT);
+        const int il = r / NOT, jl = r - il * NOT;
+        const int i = ht0 + il, j = ot0 + jl;
+        if (staged) {
+          const double* hb = s_hbox[il];
+          const double* ob = s_obox[jl];
+          const double dx = __dmul_rn(rr, n.x), dy = __dmul_rn(rr, n.y), dz = __dmul_rn(rr, n.z);
+          const bool ov = __dsub_rn(hb[0], dx) <= ob[3] && __dsub_rn(hb[3], dx) >= ob[0] &&
+                          __dsub_rn(hb[1], dy) <= ob[4] && __dsub_rn(hb[4], dy) >= ob[1] &&
+                          __dsub_rn(hb[2], dz) <= ob[5] && __dsub_rn(hb[5], dz) >= ob[2];
+          if (!ov) continue;
+        }
         V3 a[3], b[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -218,6 +291,35 @@ __global__ void __launch_bounds__(kThreads) k_repair_retract(RepairDev D, int32_
         tri_box(a, alo, ahi);
         tri_box(b, blo, bhi);
         hit = boxes_overlap(alo, ahi, blo, bhi) && tri_tri_hit(a, b);
+      } else if (r < n_cross + HV) {
+        // hand vertex contained in the object (ref repair.py:56)
+        V3 x = shifted(ldv(D.hand_v, hv0 + (r - n_cross)), rr, n);
+        hit = !outside_box(x, olo, ohi) &&
+              winding(x, D.obj_v, D.obj_t, ot0, ot1, ov0, V3{0, 0, 0}, false) > 0.5;
+      } else {
+        // object's first vertex swallowed by a link (ref repair.py:59)
+        const int li = r - n_cross - HV, l = l0 + li;
+        V3 d = V3{__dmul_rn(rr, n.x), __dmul_rn(rr, n.y), __dmul_rn(rr, n.z)};
+        V3 x = ldv(D.obj_v, ov0);
+        bool skip = false;
+        if (li < kMaxLinks) {
+          V3 xs = x + d;  // the point in the link's probe-0 frame
+          skip = outside_box(xs, V3{s_lbox[li][0], s_lbox[li][1], s_lbox[li][2]},
+                             V3{s_lbox[li][3], s_lbox[li][4], s_lbox[li][5]});
+        }
+        if (!skip) {
+          double w = 0.0;
+          for (int j = D.link_tri[l]; j < D.link_tri[l + 1]; ++j) {
+            V3 A = ldv(D.hand_v, __ldg(D.hand_t + 3 * j)),
+               B = ldv(D.hand_v, __ldg(D.hand_t + 3 * j + 1)),
+               C = ldv(D.hand_v, __ldg(D.hand_t + 3 * j + 2));
+            A = V3{__dsub_rn(A.x, d.x), __dsub_rn(A.y, d.y), __dsub_rn(A.z, d.z)};
+            B = V3{__dsub_rn(B.x, d.x), __dsub_rn(B.y, d.y), __dsub_rn(B.z, d.z)};
+            C = V3{__dsub_rn(C.x, d.x), __dsub_rn(C.y, d.y), __dsub_rn(C.z, d.z)};
+            w += solid_angle(x, A, B, C);
+          }
+          hit = w / kTwoPi > 0.5;
+        }
       }
       if (hit) flag[p] = 1;
     }
@@ -245,9 +347,12 @@ __global__ void __launch_bounds__(kThreads) k_max_penetration(
     const double* __restrict__ ov, const int32_t* __restrict__ ot, double* out) {
   const int e = blockIdx.x;
   const int p0 = env_pt[e], p1 = env_pt[e + 1], vb = env_ov[e], t0 = env_ot[e], t1 = env_ot[e + 1];
+  V3 olo, ohi;
+  block_box(ov, vb, env_ov[e + 1], olo, ohi);
   double best = 0.0;
   for (int i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
     V3 x = ldv(pts, i);
+    if (outside_box(x, olo, ohi)) continue;
     if (!(winding(x, ov, ot, t0, t1, vb, V3{0, 0, 0}, false) > 0.5)) continue;
     double d2 = INFINITY;
     for (int j = t0; j < t1; ++j) {
@@ -300,6 +405,10 @@ __global__ void k_count_crossings(const double* __restrict__ va, const int32_t* 
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
+// device time of the last retraction-search launch (CUDA events around the
+// kernel on the launching stream; read by bench.py for the roofline)
+double g_retract_ms = 0.0;
+
 int grid_for(int64_t n, int t) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -326,10 +435,26 @@ int ipc_repair_retract(const ipc_repair_desc* d, int32_t* probe_index) {
     DBuf<int32_t> out(E);
     RepairDev D{E, d->n_probe, env_link.p, link_vert.p, link_tri.p, hand_t.p, env_ov.p, env_ot.p,
                 obj_t.p, hand_v.p, obj_v.p, normal.p, retr.p};
+    cudaEvent_t ev[2];
+    RCK(cudaEventCreate(&ev[0]));
+    RCK(cudaEventCreate(&ev[1]));
+    RCK(cudaEventRecord(ev[0], 0));
     k_repair_retract<<<E, kThreads>>>(D, out.p);
     RCK(cudaGetLastError());
+    RCK(cudaEventRecord(ev[1], 0));
     out.get(probe_index);
+    float ms = 0.f;
+    RCK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    g_retract_ms = ms;
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
   })
+}
+
+int ipc_repair_last_kernel_ms(double* ms) {
+  if (!ms) return ipc__set_error("null output");
+  *ms = g_retract_ms;
+  return 0;
 }
 
 int ipc_max_penetration(int32_t n_env, const int32_t* env_pt, const double* pts,

@@ -74,8 +74,9 @@ def _f64(a):
 def retract_batch(grippers, poses, opened, obj_meshes):
     """The probe loop of ref repair.py:98-113 for E envs in one launch.
 
-    grippers: E Gripper instances (placed here at each env's probe-0 pose
-    with its opened joints and left there); poses (E,4,4); opened (E,J);
+    grippers: E Gripper instances (when they do not share one URDF model
+    they are placed at each env's probe-0 pose and left there); poses
+    (E,4,4); opened (E,J) already clamped to the joint limits;
     obj_meshes: E (world verts, tris). Returns (cleared bool[E],
     retraction_m float[E], probe_index int[E]); retraction_m is the
     reference's accumulated distance (the past-the-cap value when no probe
@@ -86,17 +87,48 @@ def retract_batch(grippers, poses, opened, obj_meshes):
     if E == 0:
         return np.zeros(0, bool), np.zeros(0), np.zeros(0, np.int32)
     env_link, link_vert, link_tri = [0], [0], [0]
-    hv, ht, normals = [], [], []
-    for g, p, q in zip(grippers, poses, opened):
-        g.place(p, q)
-        normals.append(g.palm_normal(p))
-        for b in g.bodies():
-            v = b.world_vertices()
-            ht.append(np.asarray(b.mesh.triangles, dtype=np.int64) + link_vert[-1])
-            hv.append(v)
-            link_vert.append(link_vert[-1] + len(v))
-            link_tri.append(link_tri[-1] + len(b.mesh.triangles))
-        env_link.append(len(link_vert) - 1)
+    hv, ht = [], []
+    g0 = grippers[0]
+    if all(g.model is g0.model for g in grippers):
+        # one model: vectorized FK over the batch (batch_fk) and per-link
+        # world vertices x0 @ Aᵀ + p — bit-identical to place() +
+        # world_vertices(); the grippers are left untouched
+        from .batch import batch_fk
+
+        lo = np.array([j.lower for j in g0.joints])
+        hi = np.array([j.upper for j in g0.joints])
+        fk = batch_fk(g0, np.asarray(poses, dtype=np.float64),
+                      np.clip(np.asarray(opened, dtype=np.float64), lo, hi))
+        names = sorted(g0.links)  # == Gripper.bodies() order
+        per = []
+        for ln in names:
+            t = fk[ln]
+            a = t[:, :3, :3].reshape(-1, 9).reshape(-1, 3, 3)
+            per.append(g0.links[ln].mesh.vertices[None] @ np.transpose(a, (0, 2, 1))
+                       + t[:, None, :3, 3])
+        hv = [np.concatenate(per, axis=1).reshape(-1, 3)]
+        nv = [len(g0.links[ln].mesh.vertices) for ln in names]
+        nt = [len(g0.links[ln].mesh.triangles) for ln in names]
+        vo = np.concatenate([[0], np.cumsum(nv)[:-1]])
+        tri_one = np.concatenate([np.asarray(g0.links[ln].mesh.triangles, dtype=np.int64) + o
+                                  for ln, o in zip(names, vo)])
+        per_env = int(np.sum(nv))
+        ht = [(tri_one[None] + per_env * np.arange(E)[:, None, None]).reshape(-1, 3)]
+        L = len(names)
+        link_vert = np.concatenate([[0], np.cumsum(np.tile(nv, E))])
+        link_tri = np.concatenate([[0], np.cumsum(np.tile(nt, E))])
+        env_link = np.arange(E + 1) * L
+    else:
+        for g, p, q in zip(grippers, poses, opened):
+            g.place(p, q)
+            for b in g.bodies():
+                v = b.world_vertices()
+                ht.append(np.asarray(b.mesh.triangles, dtype=np.int64) + link_vert[-1])
+                hv.append(v)
+                link_vert.append(link_vert[-1] + len(v))
+                link_tri.append(link_tri[-1] + len(b.mesh.triangles))
+            env_link.append(len(link_vert) - 1)
+    normals = [g.palm_normal(p) for g, p in zip(grippers, poses)]
     ov = _f64(np.concatenate([m[0] for m in obj_meshes]))
     ot = _i32(np.concatenate([np.reshape(m[1], (-1, 3)) for m in obj_meshes]))
     env_ov = _i32(np.concatenate([[0], np.cumsum([len(m[0]) for m in obj_meshes])]))

@@ -92,16 +92,19 @@ def test_random_crossings_match_oracle():
 def test_retraction_matches_reference_all_scenes(geom):
     """All 37 reference scenes (5 ref-test scenes + 32 config-4 envs) in ONE
     batched launch: cleared flags and retraction distances bit-identical."""
+    from paper_2311_05945_b200.robot import Gripper
     from paper_2311_05945_b200.robot.repair import retract_batch
 
     n = len(geom["cleared"])
-    gs = [_gripper() for _ in range(n)]
     poses = [geom[f"s{k}_pose"] for k in range(n)]
-    opened = [g.clamp_joints(geom[f"s{k}_q"] - 0.01) for k, g in enumerate(gs)]
     meshes = [(geom[f"s{k}_v"], geom[f"s{k}_t"]) for k in range(n)]
-    cleared, r, _ = retract_batch(gs, poses, opened, meshes)
-    np.testing.assert_array_equal(cleared, geom["cleared"])
-    np.testing.assert_array_equal(r, geom["retraction"])
+    g0 = _gripper()
+    # one shared URDF model: vectorized host packing; separate models: per-gripper FK
+    for gs in ([g0] + [Gripper(g0.model) for _ in range(n - 1)], [_gripper() for _ in range(n)]):
+        opened = [g.clamp_joints(geom[f"s{k}_q"] - 0.01) for k, g in enumerate(gs)]
+        cleared, r, _ = retract_batch(gs, poses, opened, meshes)
+        np.testing.assert_array_equal(cleared, geom["cleared"])
+        np.testing.assert_array_equal(r, geom["retraction"])
 
 
 def test_penetration_before_matches_reference(geom):
@@ -147,8 +150,7 @@ def test_repair_batch_is_intersection_free(geom):
     reproduces the reference geometry per env and ends intersection-free."""
     from paper_2311_05945_b200 import data_path
     from paper_2311_05945_b200.robot import parse_urdf
-    from paper_2311_05945_b200.robot.proximity import count_mesh_intersections
-    from paper_2311_05945_b200.robot.repair import _world_mesh, repair_batch
+    from paper_2311_05945_b200.robot.repair import repair_batch
     from paper_2311_05945_b200.workloads import repair_batch as make
 
     objs, poses, joints = make(32, seed=4)

@@ -78,3 +78,15 @@ def test_retraction_schedule(geom):
     assert len(r) == 500 and r[0] == 0.0 and r[-1] <= P.RETRACT_MAX < end
     # the unsalvageable reference case stops at the first distance past the cap
     assert not geom["cleared"][4] and geom["retraction"][4] == end
+
+
+def test_product_schedule_and_constants_match_reference():
+    """The product's probe schedule (host side of ipc_repair_retract) is the
+    reference's accumulated-distance loop, value for value."""
+    from paper_2311_05945_b200.robot import repair as R
+
+    assert (R.RETRACT_STEP, R.RETRACT_MAX) == (P.RETRACT_STEP, P.RETRACT_MAX)
+    a, ea = R.retraction_schedule()
+    b, eb = P.retraction_schedule()
+    np.testing.assert_array_equal(a, b)
+    assert ea == eb
