@@ -324,6 +324,20 @@ def main():
             traffic = float(tj["dram_bytes_read"] + tj["dram_bytes_write"])
     except (OSError, KeyError, ValueError):
         pass
+    fp64 = None  # fp64 view of the same kernel from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1f_fused_fp64.json")) as fh:
+            fj = json.load(fh)
+        if fj.get("kernel") == dom:
+            fl = float(fj["fp64_flops"])
+            fp64 = {"flops_per_launch_ncu": fl,
+                    "achieved_tflops": fl / avg_s / 1e12 if avg_s > 0 else None,
+                    "peak_tflops": FP64_PEAK_TFLOPS, "peak_kind": "nominal",
+                    "pipe_active_pct_ncu": fj["fp64_pipe_active_pct"],
+                    "sm_throughput_pct_ncu": fj["sm_throughput_pct"],
+                    "source": "profiles/r1f_fused_fp64.json"}
+    except (OSError, KeyError, ValueError):
+        pass
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
             "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -336,7 +350,8 @@ def main():
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algo_bytes_per_launch": algo, "launches": cnt_dom,
                          "avg_launch_us": avg_s * 1e6,
-                         "share_of_step": ms_dom / total_ms if total_ms else None},
+                         "share_of_step": ms_dom / total_ms if total_ms else None,
+                         "fp64": fp64},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "clocks": clk.summary(), "failed_envs_last_step": final_err,
             "async": async_line}
@@ -480,12 +495,14 @@ def repair_main(args, ws, rank, lr, K, W):
                 "autograsp_env_steps": int(sum(x.trial.steps for x in res)),
                 "note": "host scene build + retraction + AutoGrasp on the GPU engine + "
                         "penetration query, wall clock, one run"}
-    flops = None
+    flops, traffic, pipe = None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "r1e_repair_ncu.json")) as fh:
             nj = json.load(fh)
         if nj.get("envs") == E and nj.get("seed") == args.seed:
             flops = float(nj["fp64_flops"])
+            traffic = float(nj["dram_bytes_read"] + nj["dram_bytes_write"])
+            pipe = float(nj["fp64_pipe_active_pct"])
     except (OSError, KeyError, ValueError):
         pass
     avg_s = total_ms * 1e-3 / K
@@ -498,7 +515,9 @@ def repair_main(args, ws, rank, lr, K, W):
             "roofline": {"bound": "fp64", "kernel": "k_repair_retract", "achieved": achieved,
                          "peak": FP64_PEAK_TFLOPS, "peak_kind": "nominal", "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
-                         "traffic": None, "launches": K, "avg_launch_us": avg_s * 1e6},
+                         "traffic": traffic, "launches": K, "avg_launch_us": avg_s * 1e6,
+                         "fp64_pipe_active_pct_ncu": pipe,
+                         "flops_source": "profiles/r1e_repair_ncu.json (ncu dadd+dmul+2*dfma)"},
             "e2e": {"value": E * ws * K / e2e_s, "unit": REPAIR_UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": K, "clocks": clk.summary(),

@@ -52,7 +52,10 @@ namespace {
 constexpr double kSegEps = 1e-14;     // ref proximity.py:112
 constexpr double kTwoPi = 6.283185307179586;
 constexpr int kThreads = 256;
-constexpr int kMaxWindow = 32;
+#ifndef RETRACT_WINDOW
+#define RETRACT_WINDOW 1
+#endif
+constexpr int kMaxWindow = RETRACT_WINDOW;  // probes evaluated together after probe 0
 
 // RAII device copy of a host array
 template <class T>
@@ -212,10 +215,14 @@ constexpr int kStageHT = 64, kStageOT = 448;
 // usual reason a probe is rejected — a hit flags the probe and its remaining
 // items, including the winding numbers, are skipped), then hand-vertex
 // containment, then link-swallows-object containment.
-__global__ void __launch_bounds__(kThreads) k_repair_retract(RepairDev D, int32_t* out) {
+#ifndef RETRACT_MIN_BLOCKS
+#define RETRACT_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kThreads, RETRACT_MIN_BLOCKS) k_repair_retract(RepairDev D, int32_t* out) {
   const int e = blockIdx.x;
   __shared__ int flag[kMaxWindow];
   __shared__ int s_found;
+  __shared__ double s_d[kMaxWindow][3];  // rn(r_k * n) of the window's probes
   __shared__ double s_lbox[kMaxLinks][6];
   __shared__ double s_hbox[kStageHT][6];
   __shared__ double s_obox[kStageOT][6];
@@ -259,7 +266,15 @@ __global__ void __launch_bounds__(kThreads) k_repair_retract(RepairDev D, int32_
   if (threadIdx.x == 0) s_found = D.n_probe;
   while (k0 < D.n_probe) {
     const int W = min(win, D.n_probe - k0);
-    if (threadIdx.x < kMaxWindow) flag[threadIdx.x] = 0;
+    if (threadIdx.x < kMaxWindow) {
+      flag[threadIdx.x] = 0;
+      if ((int)threadIdx.x < W) {
+        const double rk = D.retr[k0 + threadIdx.x];
+        s_d[threadIdx.x][0] = __dmul_rn(rk, n.x);
+        s_d[threadIdx.x][1] = __dmul_rn(rk, n.y);
+        s_d[threadIdx.x][2] = __dmul_rn(rk, n.z);
+      }
+    }
     __syncthreads();
     const int total = per_probe * W;
     for (int it = threadIdx.x; it < total; it += blockDim.x) {
@@ -275,7 +290,7 @@ __global__ void __launch_bounds__(kThreads) k_repair_retract(RepairDev D, int32_
         if (staged) {
           const double* hb = s_hbox[il];
           const double* ob = s_obox[jl];
-          const double dx = __dmul_rn(rr, n.x), dy = __dmul_rn(rr, n.y), dz = __dmul_rn(rr, n.z);
+          const double dx = s_d[p][0], dy = s_d[p][1], dz = s_d[p][2];
           const bool ov = __dsub_rn(hb[0], dx) <= ob[3] && __dsub_rn(hb[3], dx) >= ob[0] &&
                           __dsub_rn(hb[1], dy) <= ob[4] && __dsub_rn(hb[4], dy) >= ob[1] &&
                           __dsub_rn(hb[2], dz) <= ob[5] && __dsub_rn(hb[5], dz) >= ob[2];

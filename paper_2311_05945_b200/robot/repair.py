@@ -128,12 +128,17 @@ def retract_batch(grippers, poses, opened, obj_meshes):
                 link_vert.append(link_vert[-1] + len(v))
                 link_tri.append(link_tri[-1] + len(b.mesh.triangles))
             env_link.append(len(link_vert) - 1)
-    normals = [g.palm_normal(p) for g, p in zip(grippers, poses)]
+    locs = np.array([g.palm_normal_local for g in grippers])
+    if (locs == locs[0]).all():
+        normals = np.asarray(poses, dtype=np.float64)[:, :3, :3] @ locs[0]
+    else:
+        normals = [g.palm_normal(p) for g, p in zip(grippers, poses)]
+    tris = [t if getattr(t, "ndim", 0) == 2 else np.reshape(t, (-1, 3))
+            for t in (m[1] for m in obj_meshes)]
     ov = _f64(np.concatenate([m[0] for m in obj_meshes]))
-    ot = _i32(np.concatenate([np.reshape(m[1], (-1, 3)) for m in obj_meshes]))
+    ot = _i32(np.concatenate(tris))
     env_ov = _i32(np.concatenate([[0], np.cumsum([len(m[0]) for m in obj_meshes])]))
-    env_ot = _i32(np.concatenate([[0], np.cumsum([len(np.reshape(m[1], (-1, 3)))
-                                                  for m in obj_meshes])]))
+    env_ot = _i32(np.concatenate([[0], np.cumsum([len(t) for t in tris])]))
     arrs = dict(env_link=_i32(env_link), link_vert=_i32(link_vert), link_tri=_i32(link_tri),
                 hand_v=_f64(np.concatenate(hv)), hand_t=_i32(np.concatenate(ht)),
                 env_ov=env_ov, env_ot=env_ot, obj_v=ov, obj_t=ot,
