@@ -47,7 +47,7 @@ extern "C" int ipc__set_error(const char* msg);  // engine.cu
     return ipc__set_error(ex.what());                 \
   }
 
-namespace {
+namespace ipc_repair {
 
 constexpr double kSegEps = 1e-14;     // ref proximity.py:112
 constexpr double kTwoPi = 6.283185307179586;
@@ -430,7 +430,9 @@ int grid_for(int64_t n, int t) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + t - 1) / t, (int64_t)sms * 8));
 }
 
-}  // namespace
+}  // namespace ipc_repair
+
+using namespace ipc_repair;
 
 extern "C" {
 
