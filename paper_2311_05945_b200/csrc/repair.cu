@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -424,6 +425,25 @@ __global__ void k_count_crossings(const double* __restrict__ va, const int32_t* 
 // kernel on the launching stream; read by bench.py for the roofline)
 double g_retract_ms = 0.0;
 
+// grow-only device arena of the retraction entry point (calls are serialised)
+struct Arena {
+  std::mutex mu;
+  char* p = nullptr;
+  size_t cap = 0;
+  char* reserve(size_t bytes) {
+    if (bytes > cap) {
+      if (p) RCK(cudaFree(p));
+      p = nullptr;
+      cap = 0;
+      size_t want = bytes + bytes / 2;
+      RCK(cudaMalloc(&p, want));
+      cap = want;
+    }
+    return p;
+  }
+};
+Arena g_arena;
+
 int grid_for(int64_t n, int t) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -444,22 +464,47 @@ int ipc_repair_retract(const ipc_repair_desc* d, int32_t* probe_index) {
     const int L = d->env_link[E];
     const int HV = d->link_vert[L], HT = d->link_tri[L];
     const int OV = d->env_obj_vert[E], OT = d->env_obj_tri[E];
-    DBuf<int32_t> env_link(d->env_link, E + 1), link_vert(d->link_vert, L + 1),
-        link_tri(d->link_tri, L + 1), hand_t(d->hand_t, 3 * (size_t)HT),
-        env_ov(d->env_obj_vert, E + 1), env_ot(d->env_obj_tri, E + 1), obj_t(d->obj_t, 3 * (size_t)OT);
-    DBuf<double> hand_v(d->hand_v, 3 * (size_t)HV), obj_v(d->obj_v, 3 * (size_t)OV),
-        normal(d->normal, 3 * (size_t)E), retr(d->retraction, d->n_probe);
-    DBuf<int32_t> out(E);
-    RepairDev D{E, d->n_probe, env_link.p, link_vert.p, link_tri.p, hand_t.p, env_ov.p, env_ot.p,
-                obj_t.p, hand_v.p, obj_v.p, normal.p, retr.p};
+    // one grow-only device arena for every input (no per-call cudaMalloc/cudaFree)
+    std::lock_guard<std::mutex> lock(g_arena.mu);
+    size_t off = 0;
+    auto slot = [&](size_t bytes) {
+      size_t o = off;
+      off += (bytes + 255) & ~size_t(255);
+      return o;
+    };
+    const size_t o_el = slot(4 * (E + 1)), o_lv = slot(4 * (L + 1)), o_lt = slot(4 * (L + 1)),
+                 o_ht = slot(12 * (size_t)HT), o_eov = slot(4 * (E + 1)), o_eot = slot(4 * (E + 1)),
+                 o_ot = slot(12 * (size_t)OT), o_hv = slot(24 * (size_t)HV),
+                 o_ov = slot(24 * (size_t)OV), o_n = slot(24 * (size_t)E),
+                 o_r = slot(8 * (size_t)d->n_probe), o_out = slot(4 * (size_t)E);
+    char* base = g_arena.reserve(off);
+    auto up = [&](size_t o, const void* h, size_t bytes) {
+      if (bytes) RCK(cudaMemcpyAsync(base + o, h, bytes, cudaMemcpyHostToDevice, 0));
+    };
+    up(o_el, d->env_link, 4 * (E + 1));
+    up(o_lv, d->link_vert, 4 * (L + 1));
+    up(o_lt, d->link_tri, 4 * (L + 1));
+    up(o_ht, d->hand_t, 12 * (size_t)HT);
+    up(o_eov, d->env_obj_vert, 4 * (E + 1));
+    up(o_eot, d->env_obj_tri, 4 * (E + 1));
+    up(o_ot, d->obj_t, 12 * (size_t)OT);
+    up(o_hv, d->hand_v, 24 * (size_t)HV);
+    up(o_ov, d->obj_v, 24 * (size_t)OV);
+    up(o_n, d->normal, 24 * (size_t)E);
+    up(o_r, d->retraction, 8 * (size_t)d->n_probe);
+    auto I = [&](size_t o) { return reinterpret_cast<const int32_t*>(base + o); };
+    auto F = [&](size_t o) { return reinterpret_cast<const double*>(base + o); };
+    RepairDev D{E, d->n_probe, I(o_el), I(o_lv), I(o_lt), I(o_ht), I(o_eov), I(o_eot), I(o_ot),
+                F(o_hv), F(o_ov), F(o_n), F(o_r)};
+    int32_t* out_p = reinterpret_cast<int32_t*>(base + o_out);
     cudaEvent_t ev[2];
     RCK(cudaEventCreate(&ev[0]));
     RCK(cudaEventCreate(&ev[1]));
     RCK(cudaEventRecord(ev[0], 0));
-    k_repair_retract<<<E, kThreads>>>(D, out.p);
+    k_repair_retract<<<E, kThreads>>>(D, out_p);
     RCK(cudaGetLastError());
     RCK(cudaEventRecord(ev[1], 0));
-    out.get(probe_index);
+    RCK(cudaMemcpy(probe_index, out_p, 4 * (size_t)E, cudaMemcpyDeviceToHost));
     float ms = 0.f;
     RCK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
     g_retract_ms = ms;
