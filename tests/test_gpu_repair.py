@@ -143,6 +143,13 @@ def test_repair_grasp_matches_reference(golden):
         got_q = np.concatenate([obj.q, np.array([b.q for b in g.bodies()]).ravel()])
         assert np.abs(got_q - ref_q).max() <= 1e-5 * np.abs(ref_q).max(), k
         assert r.penetration_after_m == pytest.approx(pa, abs=1e-9)
+        # north_star: the final state is intersection-free
+        from paper_2311_05945_b200.robot.proximity import count_mesh_intersections
+
+        ov = obj.world_vertices()
+        for b in g.bodies():
+            assert count_mesh_intersections(b.world_vertices(), b.mesh.triangles, ov,
+                                            obj.mesh.triangles) == 0
 
 
 def test_repair_batch_is_intersection_free(geom):
@@ -161,3 +168,13 @@ def test_repair_batch_is_intersection_free(geom):
                                rtol=1e-12, atol=1e-15)
     assert all(r.penetration_after_m == 0.0 for r in res)
     assert all(r.trial.outcome is not None for r in res)
+    # the batch runs each env's program exactly as repair_grasp does alone
+    from paper_2311_05945_b200.robot.repair import repair_grasp
+
+    objs2, poses2, joints2 = make(32, seed=4)
+    for e in (0, 7, 19):
+        r1 = repair_grasp(objs2[e], _gripper(), poses2[e], joints2[e])
+        assert (r1.cleared, r1.retraction_m) == (res[e].cleared, res[e].retraction_m)
+        assert r1.trial.outcome == res[e].trial.outcome and r1.trial.steps == res[e].trial.steps
+        np.testing.assert_allclose(np.array(r1.trial.forces), np.array(res[e].trial.forces),
+                                   rtol=1e-6, atol=1e-9)
