@@ -464,6 +464,14 @@ int ipc_repair_retract(const ipc_repair_desc* d, int32_t* probe_index) {
     const int L = d->env_link[E];
     const int HV = d->link_vert[L], HT = d->link_tri[L];
     const int OV = d->env_obj_vert[E], OT = d->env_obj_tri[E];
+    // per-probe work items are 32-bit: (hand tris x object tris + points) of one env
+    for (int e = 0; e < E; ++e) {
+      const long long ht = d->link_tri[d->env_link[e + 1]] - d->link_tri[d->env_link[e]];
+      const long long hv = d->link_vert[d->env_link[e + 1]] - d->link_vert[d->env_link[e]];
+      const long long ot = d->env_obj_tri[e + 1] - d->env_obj_tri[e];
+      if (ht * ot + hv + (d->env_link[e + 1] - d->env_link[e]) > (1LL << 30))
+        throw std::runtime_error("repair env too large for one CTA's 32-bit probe item space");
+    }
     // one grow-only device arena for every input (no per-call cudaMalloc/cudaFree)
     std::lock_guard<std::mutex> lock(g_arena.mu);
     size_t off = 0;
