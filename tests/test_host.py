@@ -167,3 +167,45 @@ def test_multirank_gather_gloo():
         assert p.exitcode == 0
     assert out[0][:2] == out[1][:2] == (11.0, 300.0)
     assert out[0][2] != out[1][2]  # disjoint env shards
+
+
+def test_repair_packing_vectorized_equals_per_gripper(monkeypatch):
+    """retract_batch's two host packings (one shared URDF model: vectorized
+    FK; separate models: per-gripper place()) hand the C-ABI identical arrays."""
+    from paper_2311_05945_b200 import _native as N
+    from paper_2311_05945_b200 import data_path
+    from paper_2311_05945_b200.robot import Gripper, parse_urdf
+    from paper_2311_05945_b200.robot import repair as R
+    from paper_2311_05945_b200.workloads import repair_batch
+
+    captured = []
+
+    class Fake:
+        def ipc_repair_retract(self, d, idx):
+            d = d._obj
+            E = d.n_env
+            L = d.env_link[E]
+            HV, HT = d.link_vert[L], d.link_tri[L]
+            OV, OT = d.env_obj_vert[E], d.env_obj_tri[E]
+            arr = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy()  # noqa: E731
+            captured.append({"env_link": arr(d.env_link, E + 1), "link_vert": arr(d.link_vert, L + 1),
+                             "link_tri": arr(d.link_tri, L + 1), "hand_v": arr(d.hand_v, 3 * HV),
+                             "hand_t": arr(d.hand_t, 3 * HT), "obj_v": arr(d.obj_v, 3 * OV),
+                             "obj_t": arr(d.obj_t, 3 * OT), "normal": arr(d.normal, 3 * E),
+                             "retr": arr(d.retraction, d.n_probe)})
+            return 0
+
+    monkeypatch.setattr(N, "load", lambda *a, **k: Fake())
+    objs, poses, joints = repair_batch(6, seed=3)
+    meshes = [R._world_mesh(o) for o in objs]
+    model = parse_urdf(data_path("pj_gripper.urdf"))
+    shared = [Gripper(model) for _ in range(6)]
+    separate = [Gripper(parse_urdf(data_path("pj_gripper.urdf"))) for _ in range(6)]
+    opened = np.array([shared[0].clamp_joints(q - 0.01) for q in joints])
+    R.retract_batch(shared, poses, opened, meshes)
+    R.retract_batch(separate, poses, opened, meshes)
+    a, b = captured
+    assert a.keys() == b.keys()
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    np.testing.assert_array_equal(a["retr"], R.retraction_schedule()[0])
