@@ -106,14 +106,14 @@ def retract_batch(grippers, poses, opened, obj_meshes):
             a = t[:, :3, :3].reshape(-1, 9).reshape(-1, 3, 3)
             per.append(g0.links[ln].mesh.vertices[None] @ np.transpose(a, (0, 2, 1))
                        + t[:, None, :3, 3])
-        hv = [np.concatenate(per, axis=1).reshape(-1, 3)]
+        hv = np.concatenate(per, axis=1).reshape(-1, 3)
         nv = [len(g0.links[ln].mesh.vertices) for ln in names]
         nt = [len(g0.links[ln].mesh.triangles) for ln in names]
         vo = np.concatenate([[0], np.cumsum(nv)[:-1]])
-        tri_one = np.concatenate([np.asarray(g0.links[ln].mesh.triangles, dtype=np.int64) + o
-                                  for ln, o in zip(names, vo)])
+        tri_one = np.concatenate([np.asarray(g0.links[ln].mesh.triangles, dtype=np.int32) + o
+                                  for ln, o in zip(names, vo)]).astype(np.int32)
         per_env = int(np.sum(nv))
-        ht = [(tri_one[None] + per_env * np.arange(E)[:, None, None]).reshape(-1, 3)]
+        ht = (tri_one[None] + (per_env * np.arange(E, dtype=np.int32))[:, None, None]).reshape(-1, 3)
         L = len(names)
         link_vert = np.concatenate([[0], np.cumsum(np.tile(nv, E))])
         link_tri = np.concatenate([[0], np.cumsum(np.tile(nt, E))])
@@ -128,19 +128,20 @@ def retract_batch(grippers, poses, opened, obj_meshes):
                 link_vert.append(link_vert[-1] + len(v))
                 link_tri.append(link_tri[-1] + len(b.mesh.triangles))
             env_link.append(len(link_vert) - 1)
-    locs = np.array([g.palm_normal_local for g in grippers])
-    if (locs == locs[0]).all():
-        normals = np.asarray(poses, dtype=np.float64)[:, :3, :3] @ locs[0]
+        hv, ht = np.concatenate(hv), np.concatenate(ht)
+    if len({g.palm_normal_local.tobytes() for g in grippers}) == 1:
+        normals = np.asarray(poses, dtype=np.float64)[:, :3, :3] @ g0.palm_normal_local
     else:
         normals = [g.palm_normal(p) for g, p in zip(grippers, poses)]
-    tris = [t if getattr(t, "ndim", 0) == 2 else np.reshape(t, (-1, 3))
-            for t in (m[1] for m in obj_meshes)]
     ov = _f64(np.concatenate([m[0] for m in obj_meshes]))
-    ot = _i32(np.concatenate(tris))
-    env_ov = _i32(np.concatenate([[0], np.cumsum([len(m[0]) for m in obj_meshes])]))
-    env_ot = _i32(np.concatenate([[0], np.cumsum([len(t) for t in tris])]))
+    ot = np.concatenate([m[1] for m in obj_meshes]).reshape(-1, 3)
+    nov = np.fromiter((len(m[0]) for m in obj_meshes), dtype=np.int64, count=E)
+    env_ov = _i32(np.concatenate([[0], np.cumsum(nov)]))
+    env_ot = _i32(np.concatenate([[0], np.cumsum(np.fromiter(
+        (np.size(m[1]) // 3 for m in obj_meshes), dtype=np.int64, count=E))]))
+    ot = _i32(ot)
     arrs = dict(env_link=_i32(env_link), link_vert=_i32(link_vert), link_tri=_i32(link_tri),
-                hand_v=_f64(np.concatenate(hv)), hand_t=_i32(np.concatenate(ht)),
+                hand_v=_f64(hv), hand_t=_i32(ht),
                 env_ov=env_ov, env_ot=env_ot, obj_v=ov, obj_t=ot,
                 normal=_f64(np.array(normals)), retr=_f64(sched))
     d = N.RepairDesc(E, N.ptr(arrs["env_link"], N._i32p), N.ptr(arrs["link_vert"], N._i32p),
