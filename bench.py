@@ -318,7 +318,7 @@ def main():
     achieved = algo / avg_s / 1e9 if avg_s > 0 else 0.0
     traffic = None  # dram bytes per launch of the dominant kernel from a committed ncu --set full capture
     try:
-        with open(os.path.join(ROOT, "profiles", "r1c_fused_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r1f_fused_fp64.json")) as fh:
             tj = json.load(fh)
         if tj.get("kernel") == dom:
             traffic = float(tj["dram_bytes_read"] + tj["dram_bytes_write"])
