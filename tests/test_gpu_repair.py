@@ -178,3 +178,32 @@ def test_repair_batch_is_intersection_free(geom):
         assert r1.trial.outcome == res[e].trial.outcome and r1.trial.steps == res[e].trial.steps
         np.testing.assert_allclose(np.array(r1.trial.forces), np.array(res[e].trial.forces),
                                    rtol=1e-6, atol=1e-9)
+
+
+def test_repair_soft_object():
+    """Repair with a soft tet object (the reference's SoftBody branch of
+    _world_mesh, repair.py:65): the GPU retraction equals the oracle's probe
+    loop on the same surface, and the two-way coupled AutoGrasp ends with no
+    crossing triangles and no contained hand samples."""
+    from paper_2311_05945_b200.bodies import Material, SoftBody
+    from paper_2311_05945_b200.mesh import box_tet
+    from paper_2311_05945_b200.robot.gripper import top_down_pose
+    from paper_2311_05945_b200.robot.proximity import count_mesh_intersections
+    from paper_2311_05945_b200.robot.repair import _world_mesh, repair_grasp
+
+    cy = 0.02515
+    cube = SoftBody(box_tet(0.05, 3, center=(0.0, cy, 0.0)),
+                    Material(youngs_modulus=1e5, poisson_ratio=0.3, density=500.0))
+    pose = top_down_pose((0.0, 0.05015 - 0.06 - 0.008, 0.0))
+    q = np.array([0.02, 0.02])
+    ov, ot = _world_mesh(cube)
+    g0 = _gripper()
+    oc, orr, _ = P.retract(g0, pose, g0.clamp_joints(q - 0.01), ov, np.asarray(ot))
+    g = _gripper()
+    r = repair_grasp(cube, g, pose, q)
+    assert r.cleared == oc and r.retraction_m == orr and orr > 0
+    assert r.penetration_before_m > 0 and r.penetration_after_m == 0.0
+    assert r.trial.outcome is not None
+    sv, st = _world_mesh(cube)
+    for b in g.bodies():
+        assert count_mesh_intersections(b.world_vertices(), b.mesh.triangles, sv, st) == 0
