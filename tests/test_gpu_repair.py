@@ -76,6 +76,16 @@ def test_empty_inputs():
     v = np.zeros((3, 3))
     assert G.count_mesh_intersections(v, np.zeros((0, 3), np.int64), v, [[0, 1, 2]]) == 0
     assert G.max_penetration_batch([], []).shape == (0,)
+    # an env with no sample points, next to one with points inside
+    from paper_2311_05945_b200.mesh import box_surface
+    from paper_2311_05945_b200.robot.repair import retract_batch
+
+    box = box_surface(0.05)
+    out = G.max_penetration_batch([np.zeros((0, 3)), np.zeros((1, 3))],
+                                  [(box.vertices, box.triangles)] * 2)
+    assert out[0] == 0.0 and out[1] == pytest.approx(0.025, rel=1e-12)
+    cleared, r, idx = retract_batch([], [], [], [])
+    assert len(cleared) == len(r) == len(idx) == 0
 
 
 def test_random_crossings_match_oracle():
