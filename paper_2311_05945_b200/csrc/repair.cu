@@ -227,6 +227,10 @@ __global__ void __launch_bounds__(kThreads, RETRACT_MIN_BLOCKS) k_repair_retract
   __shared__ double s_lbox[kMaxLinks][6];
   __shared__ double s_hbox[kStageHT][6];
   __shared__ double s_obox[kStageOT][6];
+  // one-probe rounds: hand triangles whose translated box meets the object's
+  // box (no other hand triangle can overlap any object triangle box)
+  __shared__ int s_act[kStageHT];
+  __shared__ int s_nact;
   const int l0 = D.env_link[e], l1 = D.env_link[e + 1];
   const int hv0 = D.link_vert[l0], hv1 = D.link_vert[l1];
   const int ht0 = D.link_tri[l0], ht1 = D.link_tri[l1];
@@ -234,7 +238,6 @@ __global__ void __launch_bounds__(kThreads, RETRACT_MIN_BLOCKS) k_repair_retract
   const int HT = ht1 - ht0, HV = hv1 - hv0, NL = l1 - l0, NOT = ot1 - ot0;
   const V3 n = V3{D.normal[3 * e], D.normal[3 * e + 1], D.normal[3 * e + 2]};
   const int n_cross = HT * NOT;
-  const int per_probe = n_cross + HV + NL;
   const bool staged = HT <= kStageHT && NOT <= kStageOT;
   V3 olo, ohi;
   block_box(D.obj_v, ov0, ov1, olo, ohi);
@@ -267,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, RETRACT_MIN_BLOCKS) k_repair_retract
   if (threadIdx.x == 0) s_found = D.n_probe;
   while (k0 < D.n_probe) {
     const int W = min(win, D.n_probe - k0);
+    if (threadIdx.x == 0) s_nact = 0;
     if (threadIdx.x < kMaxWindow) {
       flag[threadIdx.x] = 0;
       if ((int)threadIdx.x < W) {
@@ -277,16 +281,32 @@ __global__ void __launch_bounds__(kThreads, RETRACT_MIN_BLOCKS) k_repair_retract
       }
     }
     __syncthreads();
-    const int total = per_probe * W;
+    constexpr bool kOne = kMaxWindow == 1;
+    const bool compact = kOne && staged;
+    if (compact) {
+      if ((int)threadIdx.x < HT) {
+        const double* hb = s_hbox[threadIdx.x];
+        const double dx = s_d[0][0], dy = s_d[0][1], dz = s_d[0][2];
+        if (__dsub_rn(hb[0], dx) <= ohi.x && __dsub_rn(hb[3], dx) >= olo.x &&
+            __dsub_rn(hb[1], dy) <= ohi.y && __dsub_rn(hb[4], dy) >= olo.y &&
+            __dsub_rn(hb[2], dz) <= ohi.z && __dsub_rn(hb[5], dz) >= olo.z)
+          s_act[atomicAdd(&s_nact, 1)] = threadIdx.x;
+      }
+      __syncthreads();
+    }
+    const int n_cross_k = compact ? s_nact * NOT : n_cross;
+    const int per_probe_k = n_cross_k + HV + NL;
+    const int total = per_probe_k * W;
     for (int it = threadIdx.x; it < total; it += blockDim.x) {
-      const int p = it / per_probe;
+      const int p = it / per_probe_k;
       if (*(volatile int*)&flag[p]) continue;
-      const int r = it - p * per_probe;
+      const int r = it - p * per_probe_k;
       const double rr = D.retr[k0 + p];
       bool hit = false;
-      if (r < n_cross) {
+      if (r < n_cross_k) {
         // crossing triangle pair (ref repair.py:53, proximity.py:163)
-        const int il = r / NOT, jl = r - il * NOT;
+        const int ic = r / NOT, jl = r - ic * NOT;
+        const int il = compact ? s_act[ic] : ic;
         const int i = ht0 + il, j = ot0 + jl;
         if (staged) {
           const double* hb = s_hbox[il];
@@ -307,14 +327,14 @@ __global__ void __launch_bounds__(kThreads, RETRACT_MIN_BLOCKS) k_repair_retract
         tri_box(a, alo, ahi);
         tri_box(b, blo, bhi);
         hit = boxes_overlap(alo, ahi, blo, bhi) && tri_tri_hit(a, b);
-      } else if (r < n_cross + HV) {
+      } else if (r < n_cross_k + HV) {
         // hand vertex contained in the object (ref repair.py:56)
-        V3 x = shifted(ldv(D.hand_v, hv0 + (r - n_cross)), rr, n);
+        V3 x = shifted(ldv(D.hand_v, hv0 + (r - n_cross_k)), rr, n);
         hit = !outside_box(x, olo, ohi) &&
               winding(x, D.obj_v, D.obj_t, ot0, ot1, ov0, V3{0, 0, 0}, false) > 0.5;
       } else {
         // object's first vertex swallowed by a link (ref repair.py:59)
-        const int li = r - n_cross - HV, l = l0 + li;
+        const int li = r - n_cross_k - HV, l = l0 + li;
         V3 d = V3{__dmul_rn(rr, n.x), __dmul_rn(rr, n.y), __dmul_rn(rr, n.z)};
         V3 x = ldv(D.obj_v, ov0);
         bool skip = false;
