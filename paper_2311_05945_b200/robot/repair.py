@@ -63,6 +63,22 @@ def _hand_points(gripper) -> np.ndarray:
                            for b in gripper.bodies()])
 
 
+def _hand_points_batch(g0, link_q) -> np.ndarray:
+    """_hand_points of E placements of one gripper model at once: link_q maps
+    link name -> (E, 12) affine DoFs. Same operations as world_vertices() +
+    surface_samples() per env, stacked (bit-identical). Returns (E, P, 3)."""
+    out = []
+    for ln in sorted(g0.links):
+        b = g0.links[ln]
+        q = np.asarray(link_q[ln], dtype=np.float64)
+        a = q[:, 3:].reshape(-1, 3, 3)
+        v = b.mesh.vertices[None] @ np.transpose(a, (0, 2, 1)) + q[:, None, :3]
+        e = np.asarray(b.mesh.edges, dtype=np.int64)
+        t = np.asarray(b.mesh.triangles, dtype=np.int64)
+        out += [v, 0.5 * (v[:, e[:, 0]] + v[:, e[:, 1]]), v[:, t].mean(axis=2)]
+    return np.concatenate(out, axis=1)
+
+
 def _i32(a):
     return np.ascontiguousarray(a, dtype=np.int32)
 
@@ -233,16 +249,21 @@ def repair_batch(model, objects, poses, joint_values, open_offset: float = 0.01,
     Geometry: one retraction launch for every env; dynamics: the cleared envs
     share one BatchGrasp world running AutoGrasp only, with link targets at
     the input poses; penetration before/after: one batched query each."""
-    from .batch import BatchGrasp
+    from .batch import BatchGrasp, batch_fk
 
     E = len(objects)
     poses = np.asarray(poses, dtype=np.float64).reshape(E, 4, 4)
     joint_values = np.asarray(joint_values, dtype=np.float64).reshape(E, -1)
     grippers = clone_grippers(model, E, density)
     meshes = [_world_mesh(o) for o in objects]
-    for g, p, q in zip(grippers, poses, joint_values):
-        g.place(p, q)
-    pen_before = max_penetration_batch([_hand_points(g) for g in grippers], meshes)
+    # penetration before: hand samples at the input placements (vectorized FK)
+    g0 = grippers[0]
+    lo = np.array([j.lower for j in g0.joints])
+    hi = np.array([j.upper for j in g0.joints])
+    fk = batch_fk(g0, poses, np.clip(joint_values, lo, hi))
+    q0 = {ln: np.concatenate([fk[ln][:, :3, 3], fk[ln][:, :3, :3].reshape(-1, 9)], axis=1)
+          for ln in g0.links}
+    pen_before = max_penetration_batch(list(_hand_points_batch(g0, q0)), meshes)
     opened = np.array([g.clamp_joints(q - open_offset) for g, q in zip(grippers, joint_values)])
     cleared, retraction, _ = retract_batch(grippers, poses, opened, meshes)
 
@@ -265,7 +286,8 @@ def repair_batch(model, objects, poses, joint_values, open_offset: float = 0.01,
                     autograsp_only=True, **scene_kwargs)
     bg.run(max_ticks)
     bg.sync_scenes()
-    pen_after = max_penetration_batch([_hand_points(grippers[e]) for e in live],
+    qa = {ln: np.array([grippers[e].links[ln].q for e in live]) for ln in g0.links}
+    pen_after = max_penetration_batch(list(_hand_points_batch(g0, qa)),
                                       [_world_mesh(objects[e]) for e in live])
     for i, e in enumerate(live):
         t = trials[e]
