@@ -404,6 +404,7 @@ struct ipc_world {
   }
 
   void alloc_cands(CandStore& cs, const std::vector<long long>& ptc, const std::vector<long long>& eec) {
+    drop_graphs();  // captured graphs hold the old buffer pointers by value
     cs.pt_cap = ptc;
     cs.ee_cap = eec;
     std::vector<long long> po(n_env + 1, 0), eo(n_env + 1, 0);
@@ -448,6 +449,7 @@ struct ipc_world {
   }
 
   void alloc_pairbufs(PairBufs& b, const CandStore& cs, bool derivs) {
+    drop_graphs();
     for (void* p : {(void*)b.pt_val, (void*)b.ee_val, (void*)b.pt_g, (void*)b.pt_h, (void*)b.ee_g,
                     (void*)b.ee_h, (void*)b.pt_act, (void*)b.ee_act})
       if (p) pool.free_one(p);
@@ -472,6 +474,7 @@ struct ipc_world {
   }
 
   void alloc_lags() {
+    drop_graphs();
     std::vector<long long> lo(n_env + 1, 0);
     for (int e = 0; e < n_env; ++e) lo[e + 1] = lo[e] + dcd.pt_cap[e] + dcd.ee_cap[e];
     long long tot = lo[n_env];

@@ -169,8 +169,8 @@ IPC_HD int ee_region(V3 a0, V3 a1, V3 b0, V3 b1, bool* parallel) {
   double a = dotx(d1, d1), e = dotx(d2, d2), f = dotx(d2, r), c = dotx(d1, r), b = dotx(d1, d2);
   double ae = __dmul_rn(a, e);
   double den = __dsub_rn(ae, __dmul_rn(b, b));
-  if (parallel) *parallel = den < __dmul_rn(1e-3, ae);
-  bool degen = den <= __dmul_rn(1e-12, ae);
+  if (parallel) *parallel = den < __dmul_rn(__dmul_rn(1e-3, a), e);  // (eps*a)*e as numpy
+  bool degen = den <= __dmul_rn(__dmul_rn(1e-12, a), e);
   double s = degen ? 0.0 : __ddiv_rn(__dsub_rn(__dmul_rn(b, f), __dmul_rn(c, e)), den);
   s = fmin(fmax(s, 0.0), 1.0);
   double t = __ddiv_rn(__dadd_rn(__dmul_rn(b, s), f), e);

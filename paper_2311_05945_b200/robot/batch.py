@@ -190,8 +190,8 @@ class BatchGrasp:
         for e in np.nonzero(ph == SHAKE)[0]:
             self.k[e] += 1
             self.pose[e] = self.lifted[e]
-            self.pose[e, 0, 3] += gc.shake_amplitude * math.sin(
-                2.0 * math.pi * gc.shake_hz * self.k[e] * self.sc.h)
+            t = self.k[e] * self.sc.h  # ref robot/grasp.py:205-209 evaluates t first
+            self.pose[e, 0, 3] += gc.shake_amplitude * math.sin(2.0 * math.pi * gc.shake_hz * t)
             if self.k[e] == self.n_shake:
                 nxt[e], self.k[e] = SETTLE, 0
         for e in np.nonzero(ph == SETTLE)[0]:
