@@ -17,6 +17,7 @@ import math
 
 import numpy as np
 
+from ..solver import _scatter_velocity
 from ..world import GpuWorld
 from .grasp import GraspConfig, GraspOutcome, build_grasp_scene
 from .gripper import Gripper, _rodrigues
@@ -218,7 +219,7 @@ class BatchGrasp:
         for sc in self.scenes:
             n = len(sc.state.gather())
             sc.state.scatter(x[off:off + n])
-            sc.state.scatter_velocity(v[off:off + n])
+            _scatter_velocity(sc.state, v[off:off + n])
             off += n
 
     def run(self, max_ticks=100_000):

@@ -16,6 +16,7 @@ kinematic multipliers. ``GpuWorld`` (world.py) keeps batches resident.
 from __future__ import annotations
 
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -84,10 +85,28 @@ class StepReport:
         return rep
 
 
+_ENGINES: dict = {}  # id(scene) -> GpuWorld, dropped when the scene is collected
+
+
 def engine_of(scene) -> GpuWorld:
-    if scene.engine is None:
-        scene.engine = GpuWorld([scene])
-    return scene.engine
+    """The device world bound to ``scene``, created on first use.
+
+    The cache lives here, keyed by the scene's identity and released by a
+    weakref finalizer, so any object with the reference Scene's fields works
+    (an unmodified ``srsim.scene.Scene`` has no engine slot, ref
+    scene.py:112; the dataclass is unhashable, hence no WeakKeyDictionary)."""
+    key = id(scene)
+    w = _ENGINES.get(key)
+    if w is None:
+        w = GpuWorld([scene])
+        _ENGINES[key] = w
+        weakref.finalize(scene, _ENGINES.pop, key, None)
+    return w
+
+
+def release_engine(scene) -> None:
+    """Drop the device world of ``scene`` (the next step re-uploads it)."""
+    _ENGINES.pop(id(scene), None)
 
 
 def convergence_check(p, h: float, tol: float) -> bool:
@@ -102,10 +121,22 @@ def _sync_to_device(scene, w: GpuWorld):
     w.set_kappa(np.array([scene.barrier.kappa]))
 
 
+def _scatter_velocity(state, v) -> None:
+    """Velocities through the bodies' own fields (q_dot / v), as ref
+    bodies.py:315-326 finalize_step writes them; the reference GlobalState
+    has no scatter_velocity."""
+    for blk in state.blocks:
+        seg = np.array(v[blk.offset:blk.offset + blk.dof], dtype=np.float64)
+        if blk.is_affine:
+            blk.body.q_dot = seg
+        else:
+            blk.body.v = seg.reshape(-1, 3)
+
+
 def _sync_from_device(scene, w: GpuWorld, h):
     x, v = w.get_state()
     scene.state.scatter(x)
-    scene.state.scatter_velocity(v)
+    _scatter_velocity(scene.state, v)
     k = float(w.get_kappa()[0])
     if k != scene.barrier.kappa:
         scene.barrier = type(scene.barrier)(scene.barrier.dhat, k)
@@ -114,6 +145,8 @@ def _sync_from_device(scene, w: GpuWorld, h):
         for c, l, kk in zip(scene.constraints, lam, kap):
             c.lam = l.copy()
             c.kappa = float(kk)
+            if c.body.target_q is not None:  # ref solver.py:399-400
+                c.target = np.asarray(c.body.target_q, dtype=np.float64).copy()
 
 
 def step(scene, config: SolverConfig):

@@ -13,7 +13,7 @@ import ctypes as C
 import numpy as np
 
 from . import _native as N
-from .bodies import MODEL_ID, SoftBody
+from .bodies import MODEL_ID, affine_gravity_acceleration
 
 
 def _i32(a):
@@ -58,10 +58,12 @@ class Packed:
                     aff_idx[id(b)] = A0 + na
                     A["aff_dof"].append([D + blk.offset])
                     A["aff_M"].append(b.M_b.ravel())
-                    A["aff_acc"].append(b.gravity_acceleration(sc.gravity))
+                    A["aff_acc"].append(affine_gravity_acceleration(b, sc.gravity))
                     A["aff_ortho"].append([b.stiffness * b.volume])
                     na += 1
                 else:
+                    if not hasattr(b, "rest_volumes"):
+                        raise NotImplementedError("shell bodies are outside the GPU step's scope")
                     n = b.n_verts
                     A["vert_dof"].append(D + blk.offset + 3 * np.arange(n))
                     A["vert_mass"].append(b.mass)

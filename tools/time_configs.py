@@ -12,7 +12,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2311_05945_b200 import workloads as WL  # noqa: E402
-from paper_2311_05945_b200.solver import SolverConfig, step  # noqa: E402
+from paper_2311_05945_b200.solver import SolverConfig, engine_of, step  # noqa: E402
 
 
 def run(name, scene, n_steps, drive=None):
@@ -61,7 +61,7 @@ def profile_config2(div=12, n=8):
     for k in range(4):
         g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, 0.0262))
         step(sc, cfg)
-    w = sc.engine
+    w = engine_of(sc)
     w.profile(True)
     st0 = w.stats()
     t0 = time.perf_counter()
