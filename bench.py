@@ -1,16 +1,24 @@
 """Benchmark: batched grasp-scene time steps (BASELINE.json config 3).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--envs E] [--impl ours|reference]
+                    [--scaling strong|weak] [--workload grasp|repair]
 
 One *step* = one implicit time step of every environment in the batch
-(parallel grasp generation: E gripper + rigid-object envs per GPU, weak
-scaling). Metric: env-steps/s over all ranks. `value` runs the device-resident
-command stream (no host inputs); `e2e` runs the same steps through the public
-Python API with host targets uploaded and the state read back every step.
-`--impl reference` times the CPU oracle (numpy restatement of the reference
-path, oracle/) on a bounded sample of the same environments with every host
-core. For N > 1 launch with torchrun; one process per GPU, envs sharded by
-rank, NCCL only to gather the timings.
+(parallel grasp generation: gripper + rigid-object envs). Metric: env-steps/s
+over all ranks. Default scaling is STRONG, as BASELINE config 3 states: E
+envs in total (1024) sharded across the N GPUs, rank r owning the contiguous
+slice ``shard_range(E, N, r)``; ``--scaling weak`` gives every rank its own E
+envs instead. `value` runs the device-resident command stream (no host
+inputs); `e2e` runs the same steps through the public Python API with host
+targets uploaded and the state read back every step. `--impl reference`
+times the CPU oracle (numpy restatement of the reference path, oracle/) on a
+bounded sample of the same environments with every host core.
+
+``--gpus N`` with WORLD_SIZE unset re-launches itself under
+``torch.distributed.run`` (one process per GPU, 127.0.0.1 rendezvous); under
+torchrun each rank steps its slice with no data-path collective, and NCCL
+only gathers the timings (max over ranks) and the per-env results (ordered by
+env index, ref batch.py:39-57) to rank 0.
 """
 
 from __future__ import annotations
@@ -39,8 +47,13 @@ def _dist():
 
 
 def shard_seed(seed: int, rank: int) -> int:
-    """Each rank owns a disjoint, reproducible slice of environments (weak scaling)."""
+    """Weak scaling: each rank owns its own reproducible batch of environments."""
     return seed + 1000 * rank
+
+
+def shard_range(n_total: int, ws: int, rank: int):
+    """Strong scaling: rank's contiguous slice [lo, hi) of the n_total envs."""
+    return n_total * rank // ws, n_total * (rank + 1) // ws
 
 
 def gather_timing(total_ms: float, newton: float, device=None):
@@ -55,6 +68,49 @@ def gather_timing(total_ms: float, newton: float, device=None):
     return max(float(x[0]) for x in g), sum(float(x[1]) for x in g)
 
 
+def gather_env_rows(rows, device=None):
+    """Per-env result rows of every rank, concatenated in rank order (= env
+    order for ``shard_range`` slices): rows (n_local, k) float64 -> (n_total, k)
+    on every rank. Ragged slices are padded to the largest and trimmed."""
+    import torch
+    import torch.distributed as dist
+
+    rows = np.asarray(rows, dtype=np.float64)
+    k = rows.shape[1]
+    n = torch.tensor([rows.shape[0]], dtype=torch.int64, device=device)
+    ns = [torch.zeros_like(n) for _ in range(dist.get_world_size())]
+    dist.all_gather(ns, n)
+    ns = [int(x.item()) for x in ns]
+    pad = np.zeros((max(ns), k))
+    pad[:rows.shape[0]] = rows
+    t = torch.from_numpy(pad).to(device)
+    g = [torch.zeros_like(t) for _ in ns]
+    dist.all_gather(g, t)
+    return np.concatenate([x.cpu().numpy()[:m] for x, m in zip(g, ns)], axis=0)
+
+
+def _free_port():
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def maybe_spawn(n_gpus: int) -> bool:
+    """`--gpus N` outside torchrun: re-run this command as N ranks under
+    torch.distributed.run (rank 0 prints the line). Returns True if it did."""
+    if n_gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n_gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc:
+        raise SystemExit(rc)
+    return True
+
+
 def _cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -67,43 +123,77 @@ def _cores():
 # ---------------------------------------------------------------------------
 
 
-def _cpu_worker(args):
-    sample, worker, n_workers, seed, warmup, steps = args
+def _cpu_env_task(args):
+    """One env of the CPU sample: its W + K steps through the oracle; returns
+    (timed env-steps, timed seconds, per-step DoFs, per-step Newton counts)."""
+    n_total, env, seed, warmup, steps, sched_row = args
     sys.path.insert(0, ROOT)
     from oracle import stepper as OS
     from paper_2311_05945_b200 import workloads as WL
 
-    scenes, grippers, half, poses = WL.grasp_batch(sample, seed=seed)
-    sched = WL.schedule(grippers, half, poses, warmup + steps)
-    nl = len(grippers[0].links)
-    mine = list(range(worker, sample, n_workers))
-    lays = {e: OS.Layout(scenes[e]) for e in mine}
+    scenes, grippers, half, poses = WL.grasp_batch(n_total, seed=seed, select=[env])
+    sc = scenes[0]
+    lay = OS.Layout(sc)
     cfg = OS.Config()
-    t_timed, newton = 0.0, 0
+    nl = len(grippers[0].links)
+    t_timed, xs, its = 0.0, [], []
     for k in range(warmup + steps):
-        tgt = sched[k].reshape(sample, nl, 12)
+        tgt = sched_row[k].reshape(nl, 12)
         t0 = time.perf_counter()
-        for e in mine:
-            for c, t12 in zip(scenes[e].constraints, tgt[e]):
-                c.body.target_q = t12
-            r = OS.step(scenes[e], cfg, lays[e])
-            if k >= warmup:
-                newton += r.newton_iters
+        for c, t12 in zip(sc.constraints, tgt):
+            c.body.target_q = t12
+        r = OS.step(sc, cfg, lay)
         if k >= warmup:
             t_timed += time.perf_counter() - t0
-    return len(mine) * steps, t_timed, newton
+        xs.append(sc.state.gather())
+        its.append(r.newton_iters)
+    return steps, t_timed, np.array(xs), np.array(its)
 
 
-def cpu_arm(sample, seed, warmup, steps, cores):
+def cpu_arm(n_total, sample, seed, warmup, steps, cores):
+    """The oracle on envs 0..sample-1 of the n_total-env batch, one task per
+    env on a pool of `cores` processes (load-balanced). Rate = timed env-steps
+    ÷ (summed timed task seconds ÷ workers): the throughput of the pool with
+    every core busy, not biased by the slowest env."""
     import multiprocessing as mp
 
+    from paper_2311_05945_b200 import workloads as WL
+
+    scenes, grippers, half, poses = WL.grasp_batch(n_total, seed=seed, select=range(sample))
+    sched = WL.schedule(grippers, half, poses, warmup + steps)
+    nl = len(grippers[0].links)
+    rows = sched.reshape(warmup + steps, sample, nl * 12)
     n_workers = min(cores, sample)
-    jobs = [(sample, w, n_workers, seed, warmup, steps) for w in range(n_workers)]
+    jobs = [(n_total, e, seed, warmup, steps, rows[:, e]) for e in range(sample)]
+    t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(n_workers) as pool:
-        res = pool.map(_cpu_worker, jobs)
+        res = pool.map(_cpu_env_task, jobs, chunksize=1)
+    wall = time.perf_counter() - t0
     env_steps = sum(r[0] for r in res)
-    t = max(r[1] for r in res)
-    return env_steps / t, t, sum(r[2] for r in res), n_workers
+    t = sum(r[1] for r in res) / n_workers
+    traj = {"x": [r[2] for r in res], "newton": [r[3] for r in res]}
+    return env_steps / t, t, int(sum(r[3][warmup:].sum() for r in res)), n_workers, traj, wall
+
+
+def parity_block(traj, xs_gpu, its_gpu, dof_pre, free_flags):
+    """GPU envs 0..S-1 (e2e arm, every step) against the oracle's runs of the
+    same envs and steps: worst per-step DoF error relative to the step's
+    largest |DoF|, Newton-count mismatches over (env, step), and whether every
+    env of the batch ended every step intersection-free."""
+    max_rel, mism, n = 0.0, 0, 0
+    for e, (xc, ic) in enumerate(zip(traj["x"], traj["newton"])):
+        lo, hi = int(dof_pre[e]), int(dof_pre[e + 1])
+        for k in range(len(xc)):
+            xg = xs_gpu[k][lo:hi]
+            max_rel = max(max_rel, float(np.abs(xg - xc[k]).max() / np.abs(xc[k]).max()))
+            mism += int(its_gpu[k][e] != ic[k])
+            n += 1
+    return {"envs": len(traj["x"]), "steps": len(traj["x"][0]) if traj["x"] else 0,
+            "max_rel_dof": max_rel, "newton_mismatches": mism, "compared_env_steps": n,
+            "tolerance_rel_dof": 1e-6,
+            "all_envs_intersection_free_every_step": bool(free_flags["all"]),
+            "intersecting_env_steps": int(free_flags["bad"]),
+            "checked_env_steps": int(free_flags["n"])}
 
 
 # ---------------------------------------------------------------------------
@@ -166,42 +256,62 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _intersection_free(reps, acc, env_bad=None):
+    """Every env's step ended intersection-free: no error, min distance > 0."""
+    for e, r in enumerate(reps):
+        bad = bool(r.error) or not (r.min_dist_after > 0.0)
+        acc["bad"] += int(bad)
+        acc["n"] += 1
+        if env_bad is not None:
+            env_bad[e] += int(bad)
+    acc["all"] = acc["bad"] == 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--envs", type=int, default=1024, help="environments per GPU")
+    ap.add_argument("--envs", type=int, default=1024,
+                    help="environments in total (strong) or per GPU (weak)")
+    ap.add_argument("--scaling", choices=("strong", "weak"), default="strong")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--cpu-sample", type=int, default=0, help="envs in the CPU sample (0 = one per core)")
+    ap.add_argument("--cpu-sample", type=int, default=64, help="envs in the CPU sample")
     ap.add_argument("--cpu-steps", type=int, default=0, help="timed CPU steps (0 = the GPU's K)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--workload", choices=("grasp", "repair"), default="grasp",
                     help="grasp = config 3 (headline); repair = config 4 (penetrated-grasp repair)")
     args = ap.parse_args()
+    if maybe_spawn(args.gpus):
+        return
     ws, rank, lr = _dist()
     K, W = args.steps, max(args.warmup, 3)
     if args.workload == "repair":
         return repair_main(args, ws, rank, lr, K, W)
+    n_total = args.envs * (ws if args.scaling == "weak" else 1)
+    workload = (f"config3 parallel grasp generation: {n_total} envs of gripper + rigid object "
+                f"(boxes/spheres) {'sharded across' if args.scaling == 'strong' else 'replicated per'} "
+                f"{ws} GPU(s), scripted squeeze-and-lift command stream")
 
     if args.impl == "reference":
         if rank != 0:
             return
         cores = _cores()
-        sample = args.cpu_sample or cores
+        sample = min(args.cpu_sample, args.envs)
         ksteps = args.cpu_steps or K
-        v, t, newton, used = cpu_arm(sample, args.seed, W, ksteps, cores)
-        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": ksteps, "warmup": W, "ms_per_step": 1e3 * t / ksteps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic",
-                "config": {"workload": "config3 parallel grasp generation (CPU oracle sample)",
-                           "envs_sampled": sample, "seed": args.seed},
+        v, t, newton, used, _, wall = cpu_arm(args.envs, sample, args.seed, W, ksteps, cores)
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+                "steps": ksteps, "warmup": W, "ms_per_step": 1e3 * n_total / v,
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload, "envs": n_total, "envs_sampled": sample,
+                           "seed": args.seed},
                 "newton_iters_per_s": newton / t,
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": used, "kind": "port",
-                                 "sample": f"first {sample} envs of the batch, {ksteps} steps after "
-                                           f"{W} warm-up steps"},
+                                 "sample": f"envs 0..{sample - 1} of the batch, {ksteps} steps after "
+                                           f"{W} warm-up steps, one task per env on {used} "
+                                           f"processes ({wall:.1f} s wall)"},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -213,24 +323,33 @@ def main():
 
     lib = _native.load()
     _native.check(lib.ipc_set_device(lr))
+    dev = None
     if ws > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(lr)
         dist.init_process_group("nccl")
+        dev = f"cuda:{lr}"
     cfg = SolverConfig()
-    E = args.envs
-    seed = shard_seed(args.seed, rank)
-    scenes, grippers, half, poses = WL.grasp_batch(E, seed=seed)
+    if args.scaling == "strong":
+        lo, hi = shard_range(args.envs, ws, rank)
+        seed, select, E_all = args.seed, range(lo, hi), args.envs
+    else:
+        lo, hi = 0, args.envs
+        seed, select, E_all = shard_seed(args.seed, rank), None, args.envs
+    E = hi - lo
+    scenes, grippers, half, poses = WL.grasp_batch(E_all, seed=seed, select=select)
     sched = WL.schedule(grippers, half, poses, W + K)
     world = GpuWorld(scenes)
     world.upload_schedule(sched)
 
     # warm-up with full per-kernel profiling to identify the dominant kernel
+    free = {"bad": 0, "n": 0, "all": True}
+    env_bad = np.zeros(E)
     world.profile(True)
     for k in range(W):
-        world.step_scheduled(cfg, k, want_reports=False)
+        _intersection_free(world.step_scheduled(cfg, k), free, env_bad)
     prof, _ = world.profile_read()
     dom = max(prof, key=lambda n: prof[n][0])
     if os.environ.get("BENCH_PROFILE"):
@@ -241,6 +360,7 @@ def main():
     # timed region: device-resident inputs, L2 flushed between steps
     world.profile(True, kernels=None if os.environ.get("BENCH_PROFILE") == "2" else [dom])
     t_ms, newton = [], 0
+    newton_env = np.zeros(E)
     stats0 = world.stats()
     with Clocks(lr) as clk:
         for k in range(W, W + K):
@@ -250,9 +370,11 @@ def main():
             reps = world.step_scheduled(cfg, k)
             world.mark(1)
             t_ms.append(world.elapsed_ms(0, 1))
-            newton += sum(r.newton_iters for r in reps)
+            it = np.array([r.newton_iters for r in reps])
+            newton += int(it.sum())
+            newton_env += it
+            _intersection_free(reps, free, env_bad)
             if os.environ.get("BENCH_PROFILE"):
-                it = [r.newton_iters for r in reps]
                 st1 = world.stats()
                 d = {kk: st1[kk] - st0[kk] for kk in st1}
                 print(f"[step {k}] {t_ms[-1]:8.2f} ms newton mean {np.mean(it):.2f} max {max(it)} "
@@ -260,40 +382,60 @@ def main():
     prof, launches = world.profile_read()
     stats1 = world.stats()
     fused_iters = stats1["fused_env_iters"] - stats0["fused_env_iters"]
+    syncs_per_step = (stats1["syncs"] - stats0["syncs"]) / K
     if os.environ.get("BENCH_PROFILE") == "2":
         for n, (ms, c) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
             print(f"[timed profile] {n:14s} {ms:9.2f} ms {c:6d} launches "
                   f"{1e3 * ms / max(c, 1):9.1f} us/launch", file=sys.stderr)
         dom = max(prof, key=lambda n: prof[n][0])
     total_ms = float(np.sum(t_ms))
-    final_err = sum(r.error + r.line_search_failed for r in reps)
+    x_value, _ = world.get_state()
+    local_ms = total_ms
     if ws > 1:
-        total_ms, newton = gather_timing(total_ms, newton, device=f"cuda:{lr}")
-    value = E * ws * K / (total_ms * 1e-3)
+        total_ms, newton = gather_timing(total_ms, newton, device=dev)
+    value = n_total * K / (total_ms * 1e-3)
 
     # end-to-end through the public API: host targets in, state out, every step
-    scenes2, gr2, half2, poses2 = WL.grasp_batch(E, seed=seed)
+    scenes2, gr2, half2, poses2 = WL.grasp_batch(E_all, seed=seed, select=select)
     w2 = GpuWorld(scenes2)
+    S = min(args.cpu_sample, E) if (rank == 0 and ws == 1 and not args.no_cpu) else 0
+    ns_dof = int(w2.packed.pre["dof"][S])
+    xs_gpu, its_gpu = [], []
     for k in range(W):
-        w2.step(cfg, targets=sched[k], want_reports=False)
+        reps = w2.step(cfg, targets=sched[k], want_reports=True)
+        x, v = w2.get_state()
+        xs_gpu.append(x[:ns_dof].copy())
+        its_gpu.append([r.newton_iters for r in reps[:S]])
     w2.sync()
     t0 = time.perf_counter()
     for k in range(W, W + K):
-        w2.step(cfg, targets=sched[k], want_reports=True)
+        reps = w2.step(cfg, targets=sched[k], want_reports=True)
         x, v = w2.get_state()
+        xs_gpu.append(x[:ns_dof].copy())
+        its_gpu.append([r.newton_iters for r in reps[:S]])
     e2e_s = time.perf_counter() - t0
+    value_eq_e2e = bool(np.array_equal(x, x_value))
     if ws > 1:
-        e2e_s, _ = gather_timing(e2e_s, 0.0, device=f"cuda:{lr}")
-    e2e = E * ws * K / e2e_s
+        e2e_s, _ = gather_timing(e2e_s, 0.0, device=dev)
+    e2e = n_total * K / e2e_s
     h2d = 12 * 8 * world.n_cons
     d2h = 2 * 8 * world.n_dof
 
-    # asynchronous variant (reported beside `value`, not as it): each env runs
-    # its own K steps back to back (GpuWorld.run_scheduled), L2 flushed once
-    # before the single timed launch
+    # per-env results to rank 0, ordered by env index (ref batch.py:39-57)
+    rows = np.stack([np.arange(lo, hi), newton_env, env_bad], axis=1)
+    if ws > 1:
+        rows = gather_env_rows(rows, device=dev)
+        free["bad"] = int(rows[:, 2].sum())
+        free["all"] = free["bad"] == 0
+        free["n"] = int(gather_timing(0.0, float(free["n"]), device=dev)[1])
+    results = {"envs": int(len(rows)), "ordered": bool(np.array_equal(rows[:, 0], np.arange(n_total))),
+               "newton_iters_timed": int(rows[:, 1].sum()),
+               "rank_ms": local_ms, "value_state_equals_e2e_state": value_eq_e2e}
+
+    # asynchronous variant (reported beside `value`, not as it)
     async_line = None
     if os.environ.get("BENCH_ASYNC", "0") != "0":
-        scenes3, gr3, half3, poses3 = WL.grasp_batch(E, seed=seed)
+        scenes3, gr3, half3, poses3 = WL.grasp_batch(E_all, seed=seed, select=select)
         w3 = GpuWorld(scenes3)
         w3.upload_schedule(sched)
         for k in range(W):
@@ -304,70 +446,51 @@ def main():
         w3.mark(1)
         a_ms = w3.elapsed_ms(0, 1)
         if ws > 1:
-            a_ms, _ = gather_timing(a_ms, 0.0, device=f"cuda:{lr}")
-        async_line = {"value": E * ws * K / (a_ms * 1e-3), "unit": UNIT, "ms_total": a_ms,
+            a_ms, _ = gather_timing(a_ms, 0.0, device=dev)
+        async_line = {"value": n_total * K / (a_ms * 1e-3), "unit": UNIT, "ms_total": a_ms,
                       "note": "same envs and K steps; per-env asynchronous stepping in one launch "
                               "(envs never interact); not the per-step-synchronised headline value"}
         del w3
 
-    # roofline of the dominant kernel: algorithmic bytes / measured launch time
-    ms_dom, cnt_dom = prof[dom]
-    peak, peak_kind = _peaks()
-    algo = _algo_bytes(dom, world, fused_iters / max(prof[dom][1], 1))
-    avg_s = (ms_dom / max(cnt_dom, 1)) * 1e-3
-    achieved = algo / avg_s / 1e9 if avg_s > 0 else 0.0
-    traffic = None  # dram bytes per launch of the dominant kernel from a committed ncu --set full capture
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1f_fused_fp64.json")) as fh:
-            tj = json.load(fh)
-        if tj.get("kernel") == dom:
-            traffic = float(tj["dram_bytes_read"] + tj["dram_bytes_write"])
-    except (OSError, KeyError, ValueError):
-        pass
-    fp64 = None  # fp64 view of the same kernel from the committed ncu capture
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1f_fused_fp64.json")) as fh:
-            fj = json.load(fh)
-        if fj.get("kernel") == dom:
-            fl = float(fj["fp64_flops"])
-            fp64 = {"flops_per_launch_ncu": fl,
-                    "achieved_tflops": fl / avg_s / 1e12 if avg_s > 0 else None,
-                    "peak_tflops": FP64_PEAK_TFLOPS, "peak_kind": "nominal",
-                    "pipe_active_pct_ncu": fj["fp64_pipe_active_pct"],
-                    "sm_throughput_pct_ncu": fj["sm_throughput_pct"],
-                    "source": "profiles/r1f_fused_fp64.json"}
-    except (OSError, KeyError, ValueError):
-        pass
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
-            "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config3 parallel grasp generation: per GPU "
-                                   f"{E} envs of gripper + rigid object (boxes/spheres), "
-                                   "scripted squeeze-and-lift command stream",
-                       "envs_per_gpu": E, "seed": args.seed, "l2": "flushed between timed steps"},
+            "config": {"workload": workload, "envs": n_total, "envs_per_gpu": E,
+                       "seed": args.seed, "l2": "flushed between timed steps"},
             "newton_iters_per_s": newton / (total_ms * 1e-3),
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "algo_bytes_per_launch": algo, "launches": cnt_dom,
-                         "avg_launch_us": avg_s * 1e6,
-                         "share_of_step": ms_dom / total_ms if total_ms else None,
-                         "fp64": fp64},
+            "roofline": roofline_block(dom, prof, world, fused_iters, total_ms),
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": launches, "clocks": clk.summary(), "failed_envs_last_step": final_err,
-            "async": async_line}
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        cores = _cores()
-        sample = args.cpu_sample or cores
+            "gpu_launches": launches, "syncs_per_step": syncs_per_step, "clocks": clk.summary(),
+            "intersection_free": {"all_env_steps": bool(free["all"]), "bad": free["bad"],
+                                  "checked": free["n"]},
+            "results": results, "async": async_line}
+    if S:
         ksteps = args.cpu_steps or K
-        v, t, _, used = cpu_arm(sample, args.seed, W, ksteps, cores)
+        v, t, _, used, traj, wall = cpu_arm(args.envs, S, args.seed, W, ksteps, _cores())
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": used, "kind": "port",
-                                "sample": f"first {sample} envs of the same batch, the same {ksteps} timed "
-                                          f"steps after {W} warm-up steps, oracle/ numpy port, one env per core"}
+                                "sample": f"envs 0..{S - 1} of the same batch, the same {ksteps} "
+                                          f"timed steps after {W} warm-up steps, oracle/ numpy port, "
+                                          f"one task per env on {used} processes ({wall:.1f} s wall)"}
+        if ksteps == K:
+            line["parity"] = parity_block(traj, xs_gpu, its_gpu, w2.packed.pre["dof"], free)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def roofline_block(dom, prof, world, fused_iters, total_ms):
+    """Roofline of the dominant kernel: algorithmic bytes / measured launch time."""
+    ms_dom, cnt_dom = prof[dom]
+    peak, peak_kind = _peaks()
+    algo = _algo_bytes(dom, world, fused_iters / max(prof[dom][1], 1))
+    avg_s = (ms_dom / max(cnt_dom, 1)) * 1e-3
+    achieved = algo / avg_s / 1e9 if avg_s > 0 else 0.0
+    return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+            "algo_bytes_per_launch": algo, "launches": cnt_dom, "avg_launch_us": avg_s * 1e6,
+            "share_of_step": ms_dom / total_ms if total_ms else None}
 
 
 # ---------------------------------------------------------------------------

@@ -51,13 +51,21 @@ def grasp_object(rng, kind=None):
     return AffineBody(m, density=density), float(np.abs(m.vertices @ axis).max()), yaw
 
 
-def grasp_batch(n_env: int, seed: int = 0, mu: float = 0.5):
-    """Scenes, grippers and per-env half widths for config 3."""
+def grasp_batch(n_env: int, seed: int = 0, mu: float = 0.5, select=None):
+    """Scenes, grippers and per-env half widths for config 3.
+
+    ``select``: env indices (increasing) of the n_env-env batch to build —
+    a rank's shard, or one env of a CPU-sample task; the objects are drawn
+    from the same random stream, so env e is the same scene whichever subset
+    is built."""
     rng = np.random.default_rng(seed)
     model = gripper_model()
+    keep = None if select is None else set(int(e) for e in select)
     scenes, grippers, half, poses = [], [], [], []
-    for _ in range(n_env):
+    for e in range(n_env):
         obj, hw, yaw = grasp_object(rng)
+        if keep is not None and e not in keep:
+            continue
         top = float(obj.world_vertices()[:, 1].max())
         g = Gripper(model)
         q0 = max(0.0, HALF_APERTURE - hw - 3e-3)

@@ -217,7 +217,38 @@ def traj_grasp_steps(mu: float, name: str, n: int = 40):
          dhat=scene.barrier.dhat, kappa=scene.barrier.kappa)
 
 
+def traj_soft_grasp_config2(n: int = 12, divisions: int = 12, q0: float = 0.016):
+    """Config 2 at its full size: the gripper pinching a soft tet cube of
+    6·12³ = 10,368 tets (2,197 vertices) with friction μ = 0.5. The fingers
+    start 4 mm from the cube and close at 1 mm/step, so contact onset and
+    the squeeze fall inside the n recorded steps."""
+    gripper = Gripper(parse_urdf(data_path("pj_gripper.urdf")))
+    obj = SoftBody(box_tet(0.05, divisions, center=(0.0, CUBE_Y, 0.0)),
+                   Material(youngs_modulus=1e5, poisson_ratio=0.3, density=500.0))
+    pose = top_down_pose((0.0, CUBE_Y, 0.0))
+    scene = build_grasp_scene(obj, gripper, pose, [q0, q0], mu=0.5)
+    cfg = SolverConfig()
+    xs, iters, mind, als = [], [], [], []
+    for k in range(n):
+        gripper.set_targets(joint_values=np.minimum(gripper.joint_values + 1e-3, 0.0262))
+        _, rep = step(scene, cfg)
+        xs.append(scene.state.gather())
+        iters.append(rep.newton_iters)
+        mind.append(rep.min_dist_after)
+        als.append(rep.al_outer)
+        print("config2 step", k, rep.newton_iters, rep.min_dist_after, flush=True)
+    save("traj_soft_grasp_c2.npz", x=np.array(xs), newton_iters=np.array(iters),
+         min_dist=np.array(mind), al_outer=np.array(als), q0=q0, divisions=divisions,
+         dhat=scene.barrier.dhat, kappa=scene.barrier.kappa)
+
+
 if __name__ == "__main__":
+    import sys
+
+    if len(sys.argv) > 1:  # individual targets, e.g. traj_soft_grasp_config2
+        for name in sys.argv[1:]:
+            globals()[name]()
+        raise SystemExit(0)
     distances()
     barriers()
     elastic()

@@ -208,3 +208,35 @@ def test_broad_phase_variants_identical(monkeypatch, items):
         for which in range(3):
             assert np.array_equal(ca[e][which], cb[e][which]), (e, which)
     assert np.array_equal(xa, xb)
+
+
+def _config2_scene(z):
+    g = Gripper(parse_urdf(data_path("pj_gripper.urdf")))
+    d = int(z["divisions"])
+    obj = SoftBody(box_tet(0.05, d, center=(0.0, CUBE_Y, 0.0)),
+                   Material(youngs_modulus=1e5, poisson_ratio=0.3, density=500.0))
+    pose = top_down_pose((0.0, CUBE_Y, 0.0))
+    q0 = float(z["q0"])
+    return build_grasp_scene(obj, g, pose, [q0, q0], mu=0.5), g
+
+
+def test_config2_soft_grasp_10k_tets_matches_reference(golden):
+    """Config 2 at full size (10,368 tets, 6,627 DoFs, sparse BSR + PCG
+    path) against the unmodified reference (make_golden.py
+    traj_soft_grasp_config2): fingers close from 4 mm through contact onset
+    into a 6 mm squeeze; identical Newton counts and AL outer counts, DoFs
+    within 1e-6 relative every step, never intersecting."""
+    z = golden("traj_soft_grasp_c2.npz")
+    sc, g = _config2_scene(z)
+    assert sc.state.n_dof == z["x"].shape[1]
+    cfg = SolverConfig()
+    for k in range(len(z["x"])):
+        g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, 0.0262))
+        _, rep = step(sc, cfg)
+        x = sc.state.gather()
+        assert rep.newton_iters == z["newton_iters"][k], k
+        assert rep.al_outer == z["al_outer"][k], k
+        assert np.abs(x - z["x"][k]).max() <= REL * np.abs(z["x"][k]).max(), k
+        assert rep.min_dist_after > 0.0
+        assert rep.min_dist_after == pytest.approx(float(z["min_dist"][k]), rel=1e-6), k
+    assert sc.barrier.kappa == float(z["kappa"])

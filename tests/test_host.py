@@ -137,6 +137,27 @@ def test_workload_is_deterministic_and_feasible():
         assert np.isfinite(t.value) and md > 0
 
 
+def _oracle_rows(n_total, lo, hi, steps, seed=5):
+    """Per-env result rows of envs [lo, hi) of an n_total-env config-3 batch,
+    stepped by the oracle: (env, Newton total, final-DoF checksum)."""
+    from oracle import stepper as OS
+    from paper_2311_05945_b200 import workloads as WL
+
+    scenes, grippers, half, poses = WL.grasp_batch(n_total, seed=seed, select=range(lo, hi))
+    sched = WL.schedule(grippers, half, poses, steps)
+    nl = len(grippers[0].links)
+    rows = []
+    for i, sc in enumerate(scenes):
+        lay, tot = OS.Layout(sc), 0
+        for k in range(steps):
+            for c, t12 in zip(sc.constraints, sched[k].reshape(len(scenes), nl, 12)[i]):
+                c.body.target_q = t12
+            tot += OS.step(sc, OS.Config(), lay).newton_iters
+        x = sc.state.gather()
+        rows.append([lo + i, tot, float(np.sum(x * np.arange(1, len(x) + 1)))])
+    return np.array(rows)
+
+
 def _gloo_worker(rank, world, port, out):
     import torch.distributed as dist
 
@@ -145,14 +166,22 @@ def _gloo_worker(rank, world, port, out):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     t, n = bench.gather_timing(10.0 + rank, 100 * (rank + 1))
-    out[rank] = (t, n, bench.shard_seed(0, rank))
+    lo, hi = bench.shard_range(3, world, rank)  # ragged: 1 + 2 envs
+    rows = bench.gather_env_rows(_oracle_rows(3, lo, hi, steps=2))
+    out[rank] = (t, n, bench.shard_seed(0, rank), rows)
     dist.destroy_process_group()
 
 
-def test_multirank_gather_gloo():
+def test_multirank_shard_and_gather_gloo():
+    """Strong-scaling shards of a config-3 batch stepped on 2 ranks, per-env
+    results gathered in env order, equal a 1-process run of the whole batch."""
     import multiprocessing as mp
     import socket
 
+    import bench
+
+    assert [bench.shard_range(1024, 8, r) for r in (0, 7)] == [(0, 128), (896, 1024)]
+    assert sum(hi - lo for lo, hi in (bench.shard_range(1000, 3, r) for r in range(3))) == 1000
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
@@ -163,10 +192,13 @@ def test_multirank_gather_gloo():
     for p in ps:
         p.start()
     for p in ps:
-        p.join(120)
+        p.join(300)
         assert p.exitcode == 0
     assert out[0][:2] == out[1][:2] == (11.0, 300.0)
-    assert out[0][2] != out[1][2]  # disjoint env shards
+    assert out[0][2] != out[1][2]  # weak scaling: disjoint env batches
+    whole = _oracle_rows(3, 0, 3, steps=2)
+    for r in range(2):
+        np.testing.assert_array_equal(out[r][3], whole)
 
 
 def test_repair_packing_vectorized_equals_per_gripper(monkeypatch):
@@ -209,3 +241,21 @@ def test_repair_packing_vectorized_equals_per_gripper(monkeypatch):
     for k in a:
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
     np.testing.assert_array_equal(a["retr"], R.retraction_schedule()[0])
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` with WORLD_SIZE unset re-launches itself as 2
+    ranks (torch.distributed.run); rank 0 alone prints the reference-arm line."""
+    import json
+    import subprocess
+    import sys
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--steps", "1", "--warmup", "3", "--envs", "4",
+                          "--cpu-sample", "2"], capture_output=True, text=True, env=env,
+                         timeout=600, check=True)
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    assert lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+    assert lines[0]["scaling"] == "strong" and lines[0]["config"]["envs"] == 4

@@ -186,3 +186,22 @@ def test_grasp_trial_outcome(golden, name, soft):
     np.testing.assert_allclose(np.array(tr.forces), z["forces"], rtol=1e-6, atol=1e-6)
     x = sc.state.gather()
     assert np.abs(x - z["x_final"]).max() <= 1e-7 * np.abs(z["x_final"]).max()
+
+
+def test_config2_first_steps(golden):
+    """Oracle vs the reference on config 2 at full size (10,368 tets): the
+    first two steps (the GPU test covers all 12)."""
+    z = golden("traj_soft_grasp_c2.npz")
+    g = Gripper(parse_urdf(data_path("pj_gripper.urdf")))
+    d = int(z["divisions"])
+    obj = SoftBody(box_tet(0.05, d, center=(0.0, CUBE_Y, 0.0)),
+                   Material(youngs_modulus=1e5, poisson_ratio=0.3, density=500.0))
+    q0 = float(z["q0"])
+    sc = build_grasp_scene(obj, g, top_down_pose((0.0, CUBE_Y, 0.0)), [q0, q0], mu=0.5)
+    lay = S.Layout(sc)
+    for k in range(2):
+        g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, 0.0262))
+        r = S.step(sc, S.Config(), lay)
+        x = sc.state.gather()
+        assert r.newton_iters == z["newton_iters"][k]
+        assert np.abs(x - z["x"][k]).max() <= 1e-10 * np.abs(z["x"][k]).max()
