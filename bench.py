@@ -180,16 +180,22 @@ def parity_block(traj, xs_gpu, its_gpu, dof_pre, free_flags):
     same envs and steps: worst per-step DoF error relative to the step's
     largest |DoF|, Newton-count mismatches over (env, step), and whether every
     env of the batch ended every step intersection-free."""
-    max_rel, mism, n = 0.0, 0, 0
+    max_rel, mism, n, where, lst = 0.0, 0, 0, None, []
     for e, (xc, ic) in enumerate(zip(traj["x"], traj["newton"])):
         lo, hi = int(dof_pre[e]), int(dof_pre[e + 1])
         for k in range(len(xc)):
             xg = xs_gpu[k][lo:hi]
-            max_rel = max(max_rel, float(np.abs(xg - xc[k]).max() / np.abs(xc[k]).max()))
-            mism += int(its_gpu[k][e] != ic[k])
+            rel = float(np.abs(xg - xc[k]).max() / np.abs(xc[k]).max())
+            if rel > max_rel:
+                max_rel, where = rel, [e, k]
+            if its_gpu[k][e] != ic[k]:
+                mism += 1
+                if len(lst) < 12:
+                    lst.append([e, k, int(its_gpu[k][e]), int(ic[k])])
             n += 1
     return {"envs": len(traj["x"]), "steps": len(traj["x"][0]) if traj["x"] else 0,
-            "max_rel_dof": max_rel, "newton_mismatches": mism, "compared_env_steps": n,
+            "max_rel_dof": max_rel, "max_rel_at_env_step": where, "newton_mismatches": mism,
+            "mismatch_list_env_step_gpu_cpu": lst, "compared_env_steps": n,
             "tolerance_rel_dof": 1e-6,
             "all_envs_intersection_free_every_step": bool(free_flags["all"]),
             "intersecting_env_steps": int(free_flags["bad"]),
@@ -280,6 +286,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=64, help="envs in the CPU sample")
     ap.add_argument("--cpu-steps", type=int, default=0, help="timed CPU steps (0 = the GPU's K)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--window-only", action="store_true",
+                    help="stop after the timed window (the ncu capture command of tools/ncu_window.py)")
     ap.add_argument("--workload", choices=("grasp", "repair"), default="grasp",
                     help="grasp = config 3 (headline); repair = config 4 (penetrated-grasp repair)")
     args = ap.parse_args()
@@ -323,6 +331,7 @@ def main():
 
     lib = _native.load()
     _native.check(lib.ipc_set_device(lr))
+    fp64_peak = fp64_peak_tflops(lib)
     dev = None
     if ws > 1:
         import torch
@@ -362,7 +371,7 @@ def main():
     t_ms, newton = [], 0
     newton_env = np.zeros(E)
     stats0 = world.stats()
-    with Clocks(lr) as clk:
+    with Clocks(lr) as clk, _Nvtx("bench_timed"):
         for k in range(W, W + K):
             world.flush_l2()
             st0 = world.stats()
@@ -380,6 +389,10 @@ def main():
                 print(f"[step {k}] {t_ms[-1]:8.2f} ms newton mean {np.mean(it):.2f} max {max(it)} "
                       f"al max {max(r.al_outer for r in reps)} batched {d}", file=sys.stderr)
     prof, launches = world.profile_read()
+    if args.window_only:
+        print(json.dumps({"window_only": True, "kernel": dom, "launches": prof[dom][1],
+                          "ms": prof[dom][0]}), flush=True)
+        return
     stats1 = world.stats()
     fused_iters = stats1["fused_env_iters"] - stats0["fused_env_iters"]
     syncs_per_step = (stats1["syncs"] - stats0["syncs"]) / K
@@ -458,7 +471,7 @@ def main():
             "config": {"workload": workload, "envs": n_total, "envs_per_gpu": E,
                        "seed": args.seed, "l2": "flushed between timed steps"},
             "newton_iters_per_s": newton / (total_ms * 1e-3),
-            "roofline": roofline_block(dom, prof, world, fused_iters, total_ms),
+            "roofline": roofline_block(dom, prof, world, fused_iters, total_ms, args, W, K, fp64_peak),
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "syncs_per_step": syncs_per_step, "clocks": clk.summary(),
             "intersection_free": {"all_env_steps": bool(free["all"]), "bad": free["bad"],
@@ -480,17 +493,91 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline_block(dom, prof, world, fused_iters, total_ms):
-    """Roofline of the dominant kernel: algorithmic bytes / measured launch time."""
+CUDA_KERNEL = {"fused_step": "k_env_newton_rest", "dense_solve": "k_dense_solve", "pairs_deriv": "k_pair_hess",
+               "broad_dcd": "k_broad_sm", "broad_ccd": "k_broad_sm"}
+
+
+def window_capture(kernel, args, W, K):
+    """ncu counters of `kernel` summed over every launch of the timed window
+    of this exact bench command (profiles/r2_window_<kernel>.json, written by
+    tools/ncu_window.py from `ncu --nvtx --nvtx-include bench_timed/`); None
+    when no capture of this window (envs, seed, W, K) is committed."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"r2_window_{kernel}.json")) as fh:
+            j = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    if (j.get("envs"), j.get("seed"), j.get("warmup"), j.get("steps"), j.get("scaling")) != \
+            (args.envs, args.seed, W, K, args.scaling):
+        return None
+    return j
+
+
+def roofline_block(dom, prof, world, fused_iters, total_ms, args, W, K, fp64_peak):
+    """Roofline of the dominant kernel. Every stage computes in fp64 on the
+    CUDA cores (no dense contraction: north_star), so the bound is the
+    measured fp64 (DFMA) throughput: achieved = fp64 flops of the timed
+    window's launches (ncu thread-instruction counts, dadd + dmul + 2 dfma,
+    same command and window) / the live CUDA-event time of those launches.
+    The HBM view (algorithmic bytes per launch / mean launch time, and the
+    measured DRAM traffic per launch) is reported beside it."""
     ms_dom, cnt_dom = prof[dom]
     peak, peak_kind = _peaks()
     algo = _algo_bytes(dom, world, fused_iters / max(prof[dom][1], 1))
     avg_s = (ms_dom / max(cnt_dom, 1)) * 1e-3
-    achieved = algo / avg_s / 1e9 if avg_s > 0 else 0.0
-    return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-            "algo_bytes_per_launch": algo, "launches": cnt_dom, "avg_launch_us": avg_s * 1e6,
-            "share_of_step": ms_dom / total_ms if total_ms else None}
+    hbm = algo / avg_s / 1e9 if avg_s > 0 else 0.0
+    cap = window_capture(dom, args, W, K)
+    flops = traffic = pipe = None
+    if cap and cap.get("launches") == cnt_dom:
+        flops = float(cap["fp64_flops"])
+        traffic = float(cap["dram_bytes"]) / cnt_dom
+        pipe = cap.get("fp64_pipe_active_pct")
+    achieved = flops / (ms_dom * 1e-3) / 1e12 if flops and ms_dom > 0 else None
+    return {"bound": "fp64", "kernel": dom, "cuda_kernel": CUDA_KERNEL.get(dom, dom),
+            "achieved": achieved, "peak": fp64_peak, "peak_kind": "measured (ipc_measure_fp64_peak, DFMA)",
+            "unit": "TFLOP/s", "frac": achieved / fp64_peak if achieved and fp64_peak else None,
+            "traffic": traffic, "fp64_flops_window": flops, "fp64_pipe_active_pct_ncu": pipe,
+            "launches": cnt_dom, "avg_launch_us": avg_s * 1e6,
+            "share_of_step": ms_dom / total_ms if total_ms else None,
+            "capture": f"profiles/r2_window_{dom}.json" if flops else None,
+            "hbm": {"achieved_gbs": hbm, "peak_gbs": peak, "peak_kind": peak_kind, "frac": hbm / peak,
+                    "algo_bytes_per_launch": algo,
+                    "traffic_over_algo": traffic / algo if traffic and algo else None}}
+
+
+def fp64_peak_tflops(lib):
+    """Measured DFMA throughput of this device (roofline denominator of the
+    fp64 kernels; MEASURED_PEAKS.json has none)."""
+    import ctypes
+
+    from paper_2311_05945_b200 import _native
+
+    out = np.zeros(1)
+    _native.check(lib.ipc_measure_fp64_peak(ctypes.c_int(4096), _native.ptr(out, _native._f64p)))
+    return float(out[0])
+
+
+class _Nvtx:
+    """NVTX range around the timed region (lets `ncu --nvtx --nvtx-include
+    bench_timed/` capture exactly the timed launches); no-op without torch."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        try:
+            import torch
+
+            torch.cuda.nvtx.range_push(self.name)
+            self.on = True
+        except Exception:
+            self.on = False
+
+    def __exit__(self, *exc):
+        if self.on:
+            import torch
+
+            torch.cuda.nvtx.range_pop()
 
 
 # ---------------------------------------------------------------------------
@@ -501,7 +588,6 @@ REPAIR_METRIC = "repaired grasps/sec (retraction probe search, config 4)"
 REPAIR_UNIT = "grasps/s"
 # fp64 work per retraction launch is taken from the committed ncu capture
 # (profiles/r1e_repair_ncu.json: dadd + dmul + 2*dfma thread instructions)
-FP64_PEAK_TFLOPS = 37.0  # B200 nominal non-tensor fp64 (no measured figure in MEASURED_PEAKS.json)
 
 
 def _repair_inputs(E, seed, model=None):
@@ -577,6 +663,7 @@ def repair_main(args, ws, rank, lr, K, W):
 
     lib = _native.load()
     _native.check(lib.ipc_set_device(lr))
+    fp64_peak = fp64_peak_tflops(lib)
     if ws > 1:
         import torch
         import torch.distributed as dist
@@ -642,8 +729,8 @@ def repair_main(args, ws, rank, lr, K, W):
                        "l2": "flushed between timed steps (256 MB fill); inputs re-uploaded "
                              "every step into a persistent device arena"},
             "roofline": {"bound": "fp64", "kernel": "k_repair_retract", "achieved": achieved,
-                         "peak": FP64_PEAK_TFLOPS, "peak_kind": "nominal", "unit": "TFLOP/s",
-                         "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
+                         "peak": fp64_peak, "peak_kind": "measured (ipc_measure_fp64_peak, DFMA)",
+                         "unit": "TFLOP/s", "frac": achieved / fp64_peak if achieved else None,
                          "traffic": traffic, "launches": K, "avg_launch_us": avg_s * 1e6,
                          "fp64_pipe_active_pct_ncu": pipe,
                          "flops_source": "profiles/r1e_repair_ncu.json (ncu dadd+dmul+2*dfma)"},

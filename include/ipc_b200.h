@@ -112,7 +112,7 @@ int ipc_world_slot_forces(ipc_world *w, double h, double *out);
 int ipc_world_candidates(ipc_world *w, int env, int which, int32_t *out, int64_t cap, int64_t *n);
 
 /* Per-env minimum contact distance at the current state, inf when no
- * candidate (ref contact.py:595 ContactStats.min_dist). out: n_env. */
+ * candidate (ref contact.py:62 ContactStats.min_dist, :347). out: n_env. */
 int ipc_world_min_distance(ipc_world *w, double *out);
 
 /* Per-env minimum distance between two groups of collision bodies over
@@ -122,7 +122,7 @@ int ipc_world_min_distance(ipc_world *w, double *out);
 int ipc_world_group_distance(ipc_world *w, const uint64_t *group_a, const uint64_t *group_b,
                              double *out);
 /* Per-env lowest slot height above the ground over a group of collision
- * bodies (ref robot/proximity.py:286 min_ground_distance). */
+ * bodies (ref robot/proximity.py:76 min_ground_distance). */
 int ipc_world_ground_distance(ipc_world *w, const uint64_t *group, double *out);
 /* Per-env summed contact force (N, world frame) on groups of collision
  * bodies: groups = n_env*n_groups bitmasks, out = n_env*n_groups*3
@@ -161,18 +161,24 @@ int ipc_world_run_scheduled(ipc_world *w, const ipc_step_config *cfg, int k0, in
 int ipc_world_set_fused(ipc_world *w, int on);
 /* Per-phase SM-cycle totals of the fused per-environment step (world, DCD
  * broad phase, terms, energy, dense solve, CCD prep, CCD broad phase, CCD,
- * line search, other); zeros unless built with -DIPC_FUSED_TIMERS. */
+ * line search, other); zeros unless the timers are on
+ * (ipc_world_set_fused_timers, or IPC_FUSED_TIMERS=1 at creation). */
 int ipc_world_fused_timers(ipc_world *w, int64_t *out, int n);
+/* per-phase SM-cycle timers of the fused per-env kernels on/off (the phase
+ * split of StepReport.times, ref solver.py:52 PHASES); instrumentation */
+int ipc_world_set_fused_timers(ipc_world *w, int on);
+/* SM clock of the current device (kHz): converts the fused timers' cycles */
+int ipc_device_clock_khz(int32_t *khz);
 int ipc_world_mark(ipc_world *w, int slot);
 int ipc_world_elapsed(ipc_world *w, int a, int b, double *ms);
 int ipc_world_sync(ipc_world *w);
 
 /* Kernel-level entry points used by the parity tests (host buffers).
  * ipc_dist2_derivs: n stencils (12 doubles each) -> region, s, grad 12, hess 144
- *   (replaces ref geometry/distance.py:38/:125 + distgrad.py:300). kind 0 PT, 1 EE. */
+ *   (replaces ref geometry/distance.py:38/:125 + distgrad.py:95). kind 0 PT, 1 EE. */
 int ipc_dist2_derivs(int kind, int64_t n, const double *stencils, int32_t *region, double *s,
                      double *grad, double *hess);
-/* ref geometry/ccd.py:395 pair_ccd */
+/* ref geometry/ccd.py:34 pair_ccd */
 int ipc_ccd_pairs(int kind, int64_t n, const double *px, const double *pdx, double conservative,
                   double *alpha);
 /* ref energy/spd.py:6 spd_project, dim in {6, 9, 12} */
@@ -210,7 +216,7 @@ int ipc_repair_retract(const ipc_repair_desc *d, int32_t *probe_index);
 /* device time (ms, CUDA events on the launching stream) of the last
  * ipc_repair_retract kernel launch; measurement hook, no reference analogue */
 int ipc_repair_last_kernel_ms(double *ms);
-/* ref proximity.py:254 max_penetration, batched: env e's points
+/* ref proximity.py:235 max_penetration, batched: env e's points
  * [env_pt[e], env_pt[e+1]) of pts against its object mesh. */
 int ipc_max_penetration(int32_t n_env, const int32_t *env_pt, const double *pts,
                         const int32_t *env_obj_vert, const int32_t *env_obj_tri,
@@ -222,6 +228,11 @@ int ipc_winding_numbers(int64_t n_pts, const double *pts, int32_t n_verts, const
 int ipc_count_mesh_intersections(int32_t nva, const double *va, int32_t nta, const int32_t *ta,
                                  int32_t nvb, const double *vb, int32_t ntb, const int32_t *tb,
                                  int64_t *count);
+
+/* Measured fp64 (DFMA) throughput of the current device in TFLOP/s: the
+ * compute roofline denominator of the fp64 kernels (MEASURED_PEAKS.json has
+ * no fp64 figure). Instrumentation, no reference analogue. */
+int ipc_measure_fp64_peak(int iters, double *tflops);
 
 #ifdef __cplusplus
 }

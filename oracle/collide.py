@@ -3,7 +3,7 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
 The reference answers box queries with a median-split BVH
 (ref geometry/bvh.py) but finishes every leaf with an exact per-primitive
-box test (ref bvh.py:346-350), so its output equals the exhaustive
+box test (ref bvh.py:118,129-130), so its output equals the exhaustive
 filtered pair list. This restatement enumerates pairs exhaustively, in
 blocks, with the identical floating-point box tests; results are returned
 in the reference's lexicographic order (ref broadphase.py:162-166).
@@ -17,9 +17,9 @@ import numpy as np
 
 from . import distance as D
 
-CONSERVATIVE = 0.9  # ref ccd.py:377
-STOP_RATIO = 0.01   # ref ccd.py:378
-MAX_ITER = 64       # ref ccd.py:379
+CONSERVATIVE = 0.9  # ref ccd.py:16
+STOP_RATIO = 0.01   # ref ccd.py:17
+MAX_ITER = 64       # ref ccd.py:18
 
 
 class IntersectionError(RuntimeError):
@@ -47,7 +47,7 @@ def _excluded_matrix(tables):
 
 def _overlap(qlo, qhi, plo, phi, margin):
     """Exact reference test: query box vs primitive box inflated by margin
-    (ref bvh.py:306-307, :347-350)."""
+    (ref bvh.py:87-88, :118, :129-130)."""
     pmin = plo - margin
     pmax = phi + margin
     return np.all((qlo[:, None, :] <= pmax[None]) & (qhi[:, None, :] >= pmin[None]), axis=2)
@@ -122,7 +122,7 @@ def broad_phase_ccd(x, dx, tables, inflation=1e-9, ground_y=None):
 
 
 # ---------------------------------------------------------------------------
-# CCD: per-pair conservative advancement (ref ccd.py:395)
+# CCD: per-pair conservative advancement (ref ccd.py:34)
 # ---------------------------------------------------------------------------
 
 
@@ -169,7 +169,7 @@ def pair_ccd(px, pdx, kind, conservative=CONSERVATIVE):
 
 
 def ground_ccd(y, dy, ground_y, conservative=CONSERVATIVE):
-    """ref ccd.py:451."""
+    """ref ccd.py:90."""
     if len(y) == 0:
         return 1.0
     if np.any(y <= ground_y):
@@ -183,7 +183,7 @@ def ground_ccd(y, dy, ground_y, conservative=CONSERVATIVE):
 
 
 def ccd_alpha(x, dx, cand, tables, ground_y=None, conservative=CONSERVATIVE):
-    """Largest safe step fraction over the swept candidates (ref ccd.py:468)."""
+    """Largest safe step fraction over the swept candidates (ref ccd.py:107)."""
     a = 1.0
     if len(cand.pt):
         ids = np.concatenate([cand.pt[:, :1], tables.tris[cand.pt[:, 1]]], axis=1)

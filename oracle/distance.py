@@ -245,7 +245,7 @@ def _to_vertices(gv, hv, cmap):
 
 _FORMS = {"pp": _pp, "pl": _pl, "pf": _pf, "ll": _ll}
 
-# region → (formula, active stencil slots) (ref distgrad.py:274-293)
+# region → (formula, active stencil slots) (ref distgrad.py:68-89)
 PT_TABLE = {0: ("pp", (0, 1)), 1: ("pp", (0, 2)), 2: ("pp", (0, 3)),
             3: ("pl", (0, 1, 2)), 4: ("pl", (0, 2, 3)), 5: ("pl", (0, 3, 1)),
             6: ("pf", (0, 1, 2, 3))}
@@ -256,7 +256,7 @@ EE_TABLE = {0: ("pp", (0, 2)), 1: ("pp", (0, 3)), 2: ("pl", (0, 2, 3)),
 
 def dist2_derivatives(stencils, regions, kind):
     """(m, 4, 3) stencils → s (m,), ∂s (m, 12), ∂²s (m, 12, 12)
-    (restates ref distgrad.py:300)."""
+    (restates ref distgrad.py:95)."""
     table = PT_TABLE if kind == "pt" else EE_TABLE
     m = len(stencils)
     s = np.zeros(m)

@@ -313,7 +313,7 @@ def lift(slots, g, h, cidx):
 
 
 # ---------------------------------------------------------------------------
-# contact barrier (ref contact.py:464)
+# contact barrier (ref contact.py:216)
 # ---------------------------------------------------------------------------
 
 _EDGE_MAP = np.array([[-1.0, 1.0, 0.0, 0.0], [0.0, 0.0, -1.0, 1.0]])  # (u, v) from stencil
@@ -358,7 +358,7 @@ def ee_stencils(xw, cand, tables):
 def contact(xw, cand, tables, cidx, dhat, kappa, ground_y, derivatives=True):
     """κ Σ b over candidates inside the barrier support; returns
     (Term, min_dist). Value pass returns ∞ at zero distance, derivative
-    pass raises (ref contact.py:464-597)."""
+    pass raises (ref contact.py:216-345)."""
     shat = dhat * dhat
     val = 0.0
     parts = []

@@ -119,7 +119,7 @@ def surface_samples(verts, tris, edges=None):
 
 def max_penetration(points, verts, tris) -> float:
     """Deepest contained point's surface distance, 0 if none contained
-    (ref proximity.py:254-266)."""
+    (ref proximity.py:235-246)."""
     if len(points) == 0:
         return 0.0
     inside = winding_numbers(points, verts, tris) > 0.5

@@ -96,6 +96,8 @@ SIGNATURES = {
     "ipc_world_stats": (C.c_int, [C.c_void_p, _i64p]),
     "ipc_world_fused_timers": (C.c_int, [C.c_void_p, _i64p, C.c_int]),
     "ipc_world_set_fused": (C.c_int, [C.c_void_p, C.c_int]),
+    "ipc_world_set_fused_timers": (C.c_int, [C.c_void_p, C.c_int]),
+    "ipc_device_clock_khz": (C.c_int, [_i32p]),
     "ipc_world_run_scheduled": (C.c_int, [C.c_void_p, C.POINTER(StepConfig), C.c_int, C.c_int, C.c_void_p]),
     "ipc_world_flush_l2": (C.c_int, [C.c_void_p, C.c_int64]),
     "ipc_world_mark": (C.c_int, [C.c_void_p, C.c_int]),
@@ -108,6 +110,7 @@ SIGNATURES = {
                                    _f64p, _f64p]),
     "ipc_repair_retract": (C.c_int, [C.POINTER(RepairDesc), _i32p]),
     "ipc_repair_last_kernel_ms": (C.c_int, [_f64p]),
+    "ipc_measure_fp64_peak": (C.c_int, [C.c_int, _f64p]),
     "ipc_max_penetration": (C.c_int, [C.c_int32, _i32p, _f64p, _i32p, _i32p, _f64p, _i32p,
                                       _f64p]),
     "ipc_winding_numbers": (C.c_int, [C.c_int64, _f64p, C.c_int32, _f64p, C.c_int32, _i32p,

@@ -854,6 +854,7 @@ struct ipc_world {
 
   // ---------------- fused per-env step (dense worlds) ----------------
   bool fused_on = false;    // IPC_FUSED=1: whole step in the fused per-env kernel
+  bool fused_timers_on = false;  // IPC_FUSED_TIMERS=1: per-phase SM cycles of the fused kernels
   int tail_envs = 148;      // batched schedule: hand off to per-env CTAs at <= this many active envs
   int fused_max_dof = 128;  // dense LDLᵀ in shared memory: n² doubles
   int* fq = nullptr;
@@ -879,7 +880,7 @@ struct ipc_world {
     if (!fused_blocks) {
       // time-shared scratch: dense system, line-search positions, staged
       // broad-phase boxes (6 doubles per slot / primitive / chunk)
-      size_t need = std::max(max_env_dof * max_env_dof + 2 * max_env_dof, 3 * max_slots);
+      size_t need = std::max(dense_smem_doubles(max_env_dof), 3 * max_slots);
       need = std::max(need, (size_t)6 * max_env_prims);
       int dev = 0, optin = 0;
       CK(cudaGetDevice(&dev));
@@ -887,7 +888,7 @@ struct ipc_world {
       cudaFuncAttributes fa;
       CK(cudaFuncGetAttributes(&fa, k_env_step));
       size_t avail = (size_t)optin - fa.sharedSizeBytes;
-      size_t base = sizeof(double) * (size_t)(max_env_dof * max_env_dof + 2 * max_env_dof);
+      size_t base = sizeof(double) * (size_t)dense_smem_doubles(max_env_dof);
       fused_smem = std::min(avail, sizeof(double) * need);
       if (fused_smem < base) {  // cannot hold the dense system: batched path
         fused_on = false;
@@ -922,7 +923,7 @@ struct ipc_world {
     A.targets = d_targets;
     A.queue = fq;
     A.stat = d_fstat;
-    A.timers = d_fstat + 2;
+    A.timers = fused_timers_on ? d_fstat + 2 : nullptr;
     A.h = cfg.h;
     A.newton_tol = cfg.newton_tol;
     A.ccd_cons = cfg.ccd_conservative_factor;
@@ -976,7 +977,7 @@ struct ipc_world {
   long long lag_total = 0;
   double* g_asm = nullptr;
   int pcg_max_iters = 20000;
-  double pcg_rtol = 1e-12;
+  double pcg_rtol = 1e-14;  // relative residual; 1e-12 left config 2 at 1.3e-6 DoF error vs the reference (splu)
   int coop_blocks = 0;
   int* d_nlive = nullptr;
   double* d_beta = nullptr;
@@ -990,15 +991,36 @@ struct ipc_world {
     // env-aligned reduction chunks: small enough that the PCG spreads over
     // the SMs even for a single large env, at most 256 nodes
     int CH = std::max(32, std::min(256, ((nn + 2 * n_sm - 1) / (2 * n_sm) + 31) / 32 * 32));
+    // affine bodies: 4 consecutive nodes each, preconditioned as one 12x12 block
+    std::vector<int> node_aff(nn, -1), aff_node0(std::max(d->n_aff, 1), 0);
+    for (int b = 0; b < d->n_aff; ++b) {
+      int n0 = d->aff_dof[b] / 3;
+      aff_node0[b] = n0;
+      for (int q = 0; q < 4; ++q) node_aff[n0 + q] = b;
+    }
     for (int e = 0; e < n_env; ++e) {
       int a = d->env_dof[e] / 3, b = d->env_dof[e + 1] / 3;
       for (int i = a; i < b; ++i) node_env[i] = e;
       env_chunk[e] = (int)chunk_env.size();
-      for (int s = a; s < b; s += CH) {
+      for (int s = a; s < b;) {
+        int t = std::min(b, s + CH);
+        if (t < b && node_aff[t] >= 0) t = aff_node0[node_aff[t]] + 4;  // never split a body
         chunk_env.push_back(e);
         c0.push_back(s);
-        c1.push_back(std::min(b, s + CH));
+        c1.push_back(t);
+        s = t;
       }
+    }
+    pcg.node_aff = pool.upload(node_aff.data(), nn);
+    pcg.aff_node0 = pool.upload(aff_node0.data(), aff_node0.size());
+    pcg.Minv12 = pool.alloc<double>(144 * (size_t)std::max(d->n_aff, 1));
+    {
+      const char* pa = getenv("IPC_PCG_AFF");
+      pcg.aff_blocks = (pa && pa[0] == '0') ? 0 : 1;
+      const char* pr = getenv("IPC_PCG_RTOL");
+      if (pr) pcg_rtol = atof(pr);
+      const char* pm = getenv("IPC_PCG_MAXIT");
+      if (pm) pcg_max_iters = std::max(1, atoi(pm));
     }
     env_chunk[n_env] = (int)chunk_env.size();
     pcg.n_node = nn;
@@ -1117,6 +1139,7 @@ struct ipc_world {
     pcg.env_on = S.newton_active;
     double rtol2 = pcg_rtol * pcg_rtol;
     IPC_LAUNCH(K_DENSE, st, k_pcg_setup, n_sm * 8, 128, 0, pcg, g_asm);
+    IPC_LAUNCH(K_DENSE, st, k_pcg_setup_z, n_sm * 8, 128, 0, pcg);
     IPC_LAUNCH(K_DENSE, st, k_pcg_partial, std::max(pcg.n_chunk, 1), 256, 0, pcg, 0);
     IPC_LAUNCH(K_DENSE, st, k_pcg_env, nblk(n_env, 128), 128, 0, pcg, n_env, 0, rtol2);
     {
@@ -1306,6 +1329,8 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
       }
       const char* fz = getenv("IPC_FUSED");
       if (fz) w->fused_on = fz[0] == '1';
+      const char* ftz = getenv("IPC_FUSED_TIMERS");
+      w->fused_timers_on = ftz && ftz[0] == '1';
       w->tail_envs = w->n_sm;
       const char* tz = getenv("IPC_TAIL");
       if (tz) w->tail_envs = atoi(tz);
@@ -1348,7 +1373,7 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
       cudaFuncAttributes fa;
       CK(cudaFuncGetAttributes(&fa, k_dense_solve));
       size_t avail = (size_t)optin - fa.sharedSizeBytes;
-      size_t base = (size_t)(w->max_env_dof * w->max_env_dof + 2 * w->max_env_dof) * sizeof(double);
+      size_t base = (size_t)dense_smem_doubles(w->max_env_dof) * sizeof(double);
       if (base > avail) throw std::runtime_error("dense environment system exceeds shared memory");
       w->dense_smem = base;
       CK(cudaFuncSetAttribute(k_dense_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->dense_smem));
@@ -1672,6 +1697,19 @@ int ipc_world_set_fused(ipc_world* w, int on) {
   GUARD({
     w->fused_on = on != 0;
     w->fused_blocks = 0;
+  })
+}
+
+int ipc_world_set_fused_timers(ipc_world* w, int on) {
+  GUARD({ w->fused_timers_on = on != 0; })
+}
+
+int ipc_device_clock_khz(int32_t* khz) {
+  GUARD({
+    int dev = 0, v = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, dev));
+    *khz = v;
   })
 }
 

@@ -17,25 +17,24 @@
 
 namespace ipc {
 
-// optional phase timers (build with -DIPC_FUSED_TIMERS): SM cycles per phase,
+// optional phase timers (IPC_FUSED_TIMERS=1): SM cycles per phase,
 // summed over envs into FusedArgs::timers
 enum { FT_WORLD, FT_BROAD_DCD, FT_TERMS, FT_ENERGY, FT_DENSE, FT_CCD_PREP, FT_BROAD_CCD, FT_CCD, FT_LS, FT_OTHER,
        FT_N };
-#ifdef IPC_FUSED_TIMERS
-#define FT_MARK(A, k)                                                   \
-  do {                                                                  \
-    __syncthreads();                                                    \
-    if (threadIdx.x == 0) {                                             \
-      long long now = clock64();                                        \
-      atomicAdd((unsigned long long*)(A).timers + (k), now - ft_t0);    \
-      ft_t0 = now;                                                      \
-    }                                                                   \
+// phase timers are on when FusedArgs::timers is set (IPC_FUSED_TIMERS=1 at
+// world creation): a block-uniform branch, no cost when off
+#define FT_MARK(A, k)                                                     \
+  do {                                                                    \
+    if ((A).timers) {                                                     \
+      __syncthreads();                                                    \
+      if (threadIdx.x == 0) {                                             \
+        long long now = clock64();                                        \
+        atomicAdd((unsigned long long*)(A).timers + (k), now - ft_t0);    \
+        ft_t0 = now;                                                      \
+      }                                                                   \
+    }                                                                     \
   } while (0)
 #define FT_START long long ft_t0 = clock64()
-#else
-#define FT_MARK(A, k) do { } while (0)
-#define FT_START do { } while (0)
-#endif
 
 struct FusedArgs {
   World W;
@@ -50,25 +49,25 @@ struct FusedArgs {
   const double* targets;
   int* queue;        // [0]: next env
   long long* stat;   // [0] Newton iterations, [1] line-search trials
-  long long* timers; // [FT_N] (IPC_FUSED_TIMERS builds)
+  long long* timers; // [FT_N] phase cycles, or nullptr (timers off)
   double h, newton_tol, ccd_cons;
   int max_newton, max_halvings, fp_iters, al_max_outer;
   int smem_doubles;  // dynamic shared memory per CTA (time-shared scratch)
 };
 
-__device__ __noinline__ void fused_pair_hess0(const World& W, const double* xw, const Cands& C, long long q, int e,
+static __device__ __noinline__ void fused_pair_hess0(const World& W, const double* xw, const Cands& C, long long q, int e,
                                               const Derivs& D) {
   pair_hess_item<0>(W, xw, C, q, e, D.pt_g, D.pt_h, D.pt_act);
 }
-__device__ __noinline__ void fused_pair_hess1(const World& W, const double* xw, const Cands& C, long long q, int e,
+static __device__ __noinline__ void fused_pair_hess1(const World& W, const double* xw, const Cands& C, long long q, int e,
                                               const Derivs& D) {
   pair_hess_item<1>(W, xw, C, q, e, D.ee_g, D.ee_h, D.ee_act);
 }
-__device__ __noinline__ void fused_body(const World& W, const double* x, const double* xhat, double h2, int deriv,
+static __device__ __noinline__ void fused_body(const World& W, const double* x, const double* xhat, double h2, int deriv,
                                         int b, double* val, double* g, double* hh) {
   body_item(W, x, xhat, h2, deriv, b, val, g, hh);
 }
-__device__ __noinline__ void fused_tet(const World& W, const double* x, double h2, int deriv, int t, double* val,
+static __device__ __noinline__ void fused_tet(const World& W, const double* x, double h2, int deriv, int t, double* val,
                                        double* g, double* hp) {
   tet_item(W, x, h2, deriv, t, val, g, hp);
 }
@@ -80,7 +79,7 @@ __device__ __forceinline__ void env_world(const World& W, const double* x, doubl
 
 // broad phase of env e over [lo, hi] into C; returns false on capacity
 // overflow (sticky flag: the host replays the whole step with more room)
-__device__ bool env_broad(const World& W, const double* lo, const double* hi, const Cands& C, int e) {
+static __device__ bool env_broad(const World& W, const double* lo, const double* hi, const Cands& C, int e) {
   __shared__ int s_ov;
   int b0 = W.env_cbody[e], b1 = W.env_cbody[e + 1];
   int t0 = W.cbody_tchunk[b0], t1 = W.cbody_tchunk[b1];
@@ -102,7 +101,7 @@ __device__ bool env_broad(const World& W, const double* lo, const double* hi, co
 // boxes. Same tests, same box arithmetic and the same (row, primitive)
 // output order as broad_env; the global-memory version runs when the env's
 // boxes do not fit. Returns false on capacity overflow.
-__device__ bool env_broad_sm(const World& W, const double* __restrict__ lo, const double* __restrict__ hi,
+static __device__ bool env_broad_sm(const World& W, const double* __restrict__ lo, const double* __restrict__ hi,
                              const Cands& C, int e, double* buf, int cap_d) {
   __shared__ double blo[3 * MAX_BODIES], bhi[3 * MAX_BODIES];
   __shared__ int surv[BP_WIN], soff[BP_WIN];
@@ -329,7 +328,7 @@ __device__ bool env_broad_sm(const World& W, const double* __restrict__ lo, cons
 
 // Batched schedule: the shared-memory broad phase, one CTA per flagged env
 // (all three kinds; chunk boxes built in shared memory).
-__global__ void __launch_bounds__(BP_THREADS) k_broad_sm(World W, const double* __restrict__ lo,
+IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_broad_sm(World W, const double* __restrict__ lo,
                                                           const double* __restrict__ hi, Cands C,
                                                           const int* env_mask, int cap_d) {
   extern __shared__ double bsm[];
@@ -345,7 +344,7 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad_sm(World W, const double* 
 // active pairs are spread over the block in one round, so the latency is one
 // pair Hessian rather than one per kind.
 constexpr int FUSED_WORK = 1024;
-__device__ double env_terms(const FusedArgs& A, const double* x, const double* xw, int deriv, int e) {
+static __device__ double env_terms(const FusedArgs& A, const double* x, const double* xw, int deriv, int e) {
   const World& W = A.W;
   __shared__ double s_min;
   __shared__ int s_nw;
@@ -405,7 +404,7 @@ __device__ double env_terms(const FusedArgs& A, const double* x, const double* x
 }
 
 // any non-finite candidate value of the incoming state (k_start_check)
-__device__ bool env_infeasible(const FusedArgs& A, int e) {
+static __device__ bool env_infeasible(const FusedArgs& A, int e) {
   const Cands& C = A.dc;
   int bad = 0;
   for (int k = threadIdx.x; k < C.n_pt[e]; k += blockDim.x) bad |= isinf(A.T.pt_val[C.pt_off[e] + k]);
@@ -424,7 +423,7 @@ __device__ __forceinline__ int env_flag_read(const int* f, int e) {
 
 // Newton loop of one env (ref solver.py:295-352) from iteration it0 (begin:
 // fresh loop state); false on overflow
-__device__ bool env_newton(const FusedArgs& A, int e, double* sm, bool begin = true, int it0 = 0) {
+static __device__ bool env_newton(const FusedArgs& A, int e, double* sm, bool begin = true, int it0 = 0) {
   const World& W = A.W;
   const EnvState& S = A.S;
   __shared__ double s_amin;
@@ -519,7 +518,7 @@ __device__ bool env_newton(const FusedArgs& A, int e, double* sm, bool begin = t
 }
 
 // whole step of env e; false when a candidate store overflowed
-__device__ bool env_step(const FusedArgs& A, int e, double* sm) {
+static __device__ bool env_step(const FusedArgs& A, int e, double* sm) {
   const World& W = A.W;
   const EnvState& S = A.S;
   int tid = threadIdx.x;
@@ -610,6 +609,7 @@ __device__ bool env_step(const FusedArgs& A, int e, double* sm) {
   return true;
 }
 
+#ifdef IPC_FUSED_TU
 // Hand-off from the batched schedule: once few envs are still iterating, each
 // continues its Newton loop from iteration it0 in its own CTA (same state in
 // EnvState / World, same item functions), without per-iteration launches.
@@ -670,5 +670,12 @@ __global__ void __launch_bounds__(256, 1) k_env_step(FusedArgs A) {
     env_step(A, e, sm);
   }
 }
+
+#else
+// defined in fused.cu
+__global__ void __launch_bounds__(256, 1) k_env_newton_rest(FusedArgs A, int it0);
+__global__ void __launch_bounds__(256, 1) k_env_steps(FusedArgs A, const double* sched, int n_cons, int k0, int k1);
+__global__ void __launch_bounds__(256, 1) k_env_step(FusedArgs A);
+#endif
 
 }  // namespace ipc

@@ -5,9 +5,9 @@
 //    as the reference (pkg/src/srsim/geometry/distance.py:38,:79,:125,:165)
 //    so region codes and candidate distances agree with the CPU path;
 //  * closed-form gradients / Hessians of the four reduced squared-distance
-//    formulas (the reference autodiffs them: geometry/distgrad.py:237-257);
+//    formulas (the reference autodiffs them: geometry/distgrad.py:32-53);
 //  * the log barrier on squared distance (energy/barrier.py:51) and the
-//    edge-edge mollifier (energy/contact.py:414-449);
+//    edge-edge mollifier (energy/contact.py:166-203);
 //  * eigenvalue-clamping PSD projection (energy/spd.py:6) by Householder tridiagonalisation + implicit QL (tred2/tql2),
 //    with a Cholesky fast path for blocks that are already positive definite;
 //  * NeoHookean / StVK / FixedCorotated densities, PK1 and F-space Hessians
@@ -335,7 +335,7 @@ IPC_HD double d2_ll(const V3* x, double* G, double* H) {
 }
 
 // Squared distance + derivatives for a stencil (p,t0,t1,t2) or (a0,a1,b0,b1).
-// Region tables follow ref distgrad.py:274-293. G (12) and H (144) must be
+// Region tables follow ref distgrad.py:68-89. G (12) and H (144) must be
 // zero on entry. Returns s. *mask gets the bitmask of active stencil slots.
 IPC_HD double dist2_derivs(bool is_pt, int region, const V3* x, double* G, double* H, int* mask) {
   if (is_pt) {
@@ -771,6 +771,187 @@ IPC_HD void psd_project_masked12(double* H, int mask) {
 }
 
 // ---------------------------------------------------------------------------
+// Contact stencil Hessians built directly in the Helmert space of the
+// stencil's active slots (no 12x12 array).
+//
+// Every distance formula is a function of difference vectors v_i =
+// x_{p_i} - x_{q_i} of the stencil points, so its stencil Hessian is
+// H = Dᵀ K D (K: var-space Hessian) and annihilates rigid translations. With
+// Q = Q0 ⊗ I3, Q0 the orthonormal NS x (NS-1) Helmert basis of the
+// complement of (1,…,1): H = Q (Bᵀ K B) Qᵀ, B = D Q = β ⊗ I3 with
+// β[i][J] = q0[p_i][J] - q0[q_i][J], and since Q has orthonormal columns the
+// eigenvalue clamp of ref spd.py:6 commutes: H⁺ = Q (BᵀKB)⁺ Qᵀ. The
+// R = 3(NS-1) core M = BᵀKB and the core gradient ĝ = Bᵀ g_var are formed in
+// registers, projected (psd_project<R>), and expanded straight into the packed
+// output — same operator as projecting the 12x12 stencil Hessian.
+// ---------------------------------------------------------------------------
+IPC_HD double helm(int a, int J) {  // q0[a][J]: a < NS, J < NS-1
+  const double nrm = J == 0 ? 0.70710678118654752440 : (J == 1 ? 0.40824829046386301637 : 0.28867513459481288225);
+  return a <= J ? nrm : (a == J + 1 ? -(double)(J + 1) * nrm : 0.0);
+}
+
+// β of NV difference vars (p[i], q[i]: local slot indices) over NB = NS-1 Helmert vectors
+template <int NV, int NB>
+IPC_HD void helm_beta(const int (&p)[NV], const int (&q)[NV], double (&beta)[NV][NB]) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int J = 0; J < NB; ++J) beta[i][J] = helm(p[i], J) - helm(q[i], J);
+}
+
+// gh[3J+c] = Σ_i β[i][J] gv[i].c
+template <int NV, int NB>
+IPC_HD void helm_grad(const double (&beta)[NV][NB], const V3 (&gv)[NV], double (&gh)[3 * NB]) {
+#pragma unroll
+  for (int J = 0; J < NB; ++J) {
+    double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      a += beta[i][J] * gv[i].x;
+      b += beta[i][J] * gv[i].y;
+      c += beta[i][J] * gv[i].z;
+    }
+    gh[3 * J] = a;
+    gh[3 * J + 1] = b;
+    gh[3 * J + 2] = c;
+  }
+}
+
+// M (R x R, upper triangle) += s · Σ_ij β[i][I] β[j][J] hv[i][j]
+template <int NV, int NB>
+IPC_HD void helm_hess_acc(const double (&beta)[NV][NB], const M3 (&hv)[NV][NV], double s, double* M) {
+  constexpr int R = 3 * NB;
+#pragma unroll
+  for (int I = 0; I < NB; ++I)
+#pragma unroll
+    for (int J = I; J < NB; ++J)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          if (I == J && d < c) continue;
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < NV; ++i) {
+            double bi = beta[i][I];
+            double t = 0.0;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) t += beta[j][J] * hv[i][j].m[3 * c + d];
+            acc += bi * t;
+          }
+          M[(3 * I + c) * R + 3 * J + d] += s * acc;
+        }
+}
+
+// M (upper) += s · a bᵀ (+ s · b aᵀ when sym2), core vectors of length R
+template <int R>
+IPC_HD void helm_outer_acc(const double (&a)[R], const double (&b)[R], double s, bool sym2, double* M) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = r; c < R; ++c) M[r * R + c] += sym2 ? s * (a[r] * b[c] + b[r] * a[c]) : s * (a[r] * b[c]);
+}
+
+// expand the projected core into the stencil outputs: g12 = Q ĝ,
+// hp (packed 12x12 upper) = Q M⁺ Qᵀ; sl[a]: stencil slot of local slot a.
+// Rows of inactive slots are zero (written first when NS < 4).
+template <int NS>
+IPC_HD void helm_out(const int (&sl)[NS], const double* gh, const double* M, double* g12, double* hp) {
+  constexpr int NB = NS - 1, R = 3 * NB;
+  if (NS < 4) {
+#pragma unroll
+    for (int i = 0; i < 12; ++i) g12[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 78; ++i) hp[i] = 0.0;
+  }
+#pragma unroll
+  for (int a = 0; a < NS; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int J = 0; J < NB; ++J) acc += helm(a, J) * gh[3 * J + c];
+      g12[3 * sl[a] + c] = acc;
+    }
+#pragma unroll
+  for (int a = 0; a < NS; ++a)
+#pragma unroll
+    for (int b = 0; b < NS; ++b)
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          int r = 3 * sl[a] + i, c = 3 * sl[b] + j;
+          if (c < r) continue;  // upper triangle of the stencil matrix
+          double acc = 0.0;
+#pragma unroll
+          for (int I = 0; I < NB; ++I) {
+            double t = 0.0;
+#pragma unroll
+            for (int J = 0; J < NB; ++J) {
+              int u = 3 * I + i, v = 3 * J + j;
+              t += helm(b, J) * (u <= v ? M[u * R + v] : M[v * R + u]);
+            }
+            acc += helm(a, I) * t;
+          }
+          hp[r * 12 - (r * (r - 1)) / 2 + (c - r)] = acc;
+        }
+}
+
+// var-space derivatives of the reduced squared-distance formulas (the
+// closed forms of d2_pp / d2_pl / d2_pf / d2_ll above, without the scatter);
+// each returns the value in the same operation order as the value pass
+IPC_HD double vs_pp(V3 d, V3 (&gv)[1], M3 (&hv)[1][1]) {
+  gv[0] = 2.0 * d;
+  hv[0][0] = m3_zero();
+  m3_add_diag(hv[0][0], 2.0);
+  return dotx(d, d);
+}
+IPC_HD double vs_pl(V3 w, V3 e, V3 (&gv)[2], M3 (&hv)[2][2]) {
+  V3 c = crossx(e, w);
+  double n = dotx(e, e);
+  double val = __ddiv_rn(dotx(c, c), n);
+  double t = dot(e, w) / n;
+  V3 r = w - t * e;
+  V3 k = r - t * e;
+  gv[0] = 2.0 * r;
+  gv[1] = (-2.0 * t) * r;
+  M3 hww = m3_outer(e, e);
+  for (int i = 0; i < 9; ++i) hww.m[i] *= -2.0 / n;
+  m3_add_diag(hww, 2.0);
+  M3 hwe = m3_outer(e, k);
+  for (int i = 0; i < 9; ++i) hwe.m[i] *= -2.0 / n;
+  m3_add_diag(hwe, -2.0 * t);
+  M3 hee = m3_outer(k, k);
+  for (int i = 0; i < 9; ++i) hee.m[i] *= -2.0 / n;
+  m3_add_diag(hee, 2.0 * t * t);
+  hv[0][0] = hww; hv[0][1] = hwe; hv[1][0] = m3_T(hwe); hv[1][1] = hee;
+  return val;
+}
+IPC_HD double vs_triple(V3 w, V3 u, V3 v, V3 (&gv)[3], M3 (&hv)[3][3]) {
+  triple_vars(w, u, v, gv, hv);
+  V3 n = crossx(u, v);
+  double q = dotx(w, n);
+  return __ddiv_rn(__dmul_rn(q, q), dotx(n, n));
+}
+// c = |u x v|², u = x1 - x0, v = x3 - x2 (EE mollifier argument)
+IPC_HD void vs_cross2(V3 u, V3 v, V3 (&gv)[2], M3 (&hv)[2][2]) {
+  double uu = dot(u, u), vv = dot(v, v), uv = dot(u, v);
+  gv[0] = 2.0 * (vv * u - uv * v);
+  gv[1] = 2.0 * (uu * v - uv * u);
+  M3 huu = m3_outer(v, v);
+  for (int i = 0; i < 9; ++i) huu.m[i] *= -2.0;
+  m3_add_diag(huu, 2.0 * vv);
+  M3 hvv = m3_outer(u, u);
+  for (int i = 0; i < 9; ++i) hvv.m[i] *= -2.0;
+  m3_add_diag(hvv, 2.0 * uu);
+  M3 huv = m3_outer(u, v), t2 = m3_outer(v, u);
+  for (int i = 0; i < 9; ++i) huv.m[i] = 4.0 * huv.m[i] - 2.0 * t2.m[i];
+  m3_add_diag(huv, -2.0 * uv);
+  hv[0][0] = huu; hv[0][1] = huv; hv[1][0] = m3_T(huv); hv[1][1] = hvv;
+}
+
+// ---------------------------------------------------------------------------
 // hyperelastic models: psi(F), P = dpsi/dF, H9 = d2psi/dF2 (F row-major,
 // flat index 3i+j). Ref elastic.py:23-167.
 // ---------------------------------------------------------------------------
@@ -889,7 +1070,7 @@ IPC_HD void polar(const M3& f, M3& R, M3& S) {
 }
 
 // PSD projection of the orthogonality Hessian ∂²/∂A² of c‖AAᵀ−I‖²_F (ref
-// terms.py:234-247, projected at :269) in closed form. The energy is
+// terms.py:66-79, projected at :101) in closed form. The energy is
 // isotropic in A's singular values, E = c Σ(σᵢ²−1)², so its 9x9 Hessian has
 // the eigensystem (signed SVD A = U Σ Vᵀ, U, V proper):
 //   scaling  vec(uᵢvᵢᵀ)                 λ = c(12σᵢ² − 4)

@@ -40,7 +40,7 @@ __device__ __forceinline__ void world_slot(const World& W, const double* __restr
   }
 }
 
-__global__ void k_world(World W, const double* __restrict__ x, double* __restrict__ xw) {
+IPC_GLOBAL void k_world(World W, const double* __restrict__ x, double* __restrict__ xw) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < W.n_slot) world_slot(W, x, xw, s);
 }
@@ -48,7 +48,7 @@ __global__ void k_world(World W, const double* __restrict__ x, double* __restric
 
 // out = a + (scale * alpha_e) * b over DoFs of flagged envs (others copy a);
 // scale is a power of two, so scale * alpha equals repeated halving exactly
-__global__ void k_axpy_env(World W, const double* a, const double* b, const double* alpha, double scale,
+IPC_GLOBAL void k_axpy_env(World W, const double* a, const double* b, const double* alpha, double scale,
                            const int* flag, double* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= W.n_dof) return;
@@ -56,7 +56,7 @@ __global__ void k_axpy_env(World W, const double* a, const double* b, const doub
   out[i] = (flag == nullptr || flag[e]) ? __dadd_rn(a[i], __dmul_rn(alpha ? alpha[e] * scale : 1.0, b[i])) : a[i];
 }
 
-__global__ void k_sub(int n, const double* a, const double* b, double* out) {
+IPC_GLOBAL void k_sub(int n, const double* a, const double* b, double* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = __dsub_rn(a[i], b[i]);
 }
@@ -64,10 +64,10 @@ __global__ void k_sub(int n, const double* a, const double* b, double* out) {
 // ---------------------------------------------------------------------------
 // broad phase: exhaustive box tests, one CTA per environment, ordered
 // compaction (lexicographic output, ref broadphase.py:162-166). Boxes:
-// query box [lo, hi] vs primitive box inflated by `margin` (ref bvh.py:306).
+// query box [lo, hi] vs primitive box inflated by `margin` (ref bvh.py:87-88, :129-130).
 // ---------------------------------------------------------------------------
 template <int NT>
-__device__ int block_ordered_offset(bool hit, int* warp_tot, int* total) {
+static __device__ int block_ordered_offset(bool hit, int* warp_tot, int* total) {
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned m = __ballot_sync(0xffffffffu, hit);
   int pre = __popc(m & ((1u << lane) - 1u));
@@ -201,7 +201,7 @@ __device__ __forceinline__ void chunk_box(const World& W, const double* __restri
   }
 }
 
-__global__ void k_chunk_boxes(World W, const double* __restrict__ lo, const double* __restrict__ hi) {
+IPC_GLOBAL void k_chunk_boxes(World W, const double* __restrict__ lo, const double* __restrict__ hi) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < W.n_tchunk + W.n_echunk) chunk_box(W, lo, hi, c);
 }
@@ -211,7 +211,7 @@ __global__ void k_chunk_boxes(World W, const double* __restrict__ lo, const doub
 // pass 1 writes at the range's exclusive offset, so the output order is the
 // same as with one CTA. pass -1: single CTA per env, count + write.
 // block function (blockDim.x == BP_THREADS): range z of Z of env e's items
-__device__ void broad_env(const World& W, const double* __restrict__ lo, const double* __restrict__ hi,
+static __device__ void broad_env(const World& W, const double* __restrict__ lo, const double* __restrict__ hi,
                           const Cands& C, int kind, int e, int z, int Z, int pass, int* blk_cnt) {
   __shared__ int warp_tot[BP_THREADS / 32];
   __shared__ int total;
@@ -406,7 +406,7 @@ __device__ void broad_env(const World& W, const double* __restrict__ lo, const d
   }
 }
 
-__global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __restrict__ lo,
+IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __restrict__ lo,
                                                        const double* __restrict__ hi, Cands C,
                                                        int kind, const int* env_mask, int pass,
                                                        int* blk_cnt) {
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
 
 // per-env exclusive prefix of candidate counts over flagged envs (one CTA);
 // pre has n_env + 1 entries, pre[n_env] = total
-__global__ void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
+IPC_GLOBAL void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
   __shared__ int part[1024];
   int tid = threadIdx.x, nt = blockDim.x;
   int per = (n_env + nt - 1) / nt;
@@ -442,7 +442,7 @@ __global__ void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
 }
 
 // the three candidate-count prefixes (PT, EE, ground) in one launch
-__global__ void k_prefix3(int n_env, Cands C, const int* flag) {
+IPC_GLOBAL void k_prefix3(int n_env, Cands C, const int* flag) {
   const int* cnt = blockIdx.x == 0 ? C.n_pt : (blockIdx.x == 1 ? C.n_ee : C.n_gnd);
   int* pre = blockIdx.x == 0 ? C.pre_pt : (blockIdx.x == 1 ? C.pre_ee : C.pre_gnd);
   __shared__ int part[1024];
@@ -499,7 +499,7 @@ __device__ __forceinline__ void body_item(const World& W, const double* __restri
     v += d[i] * s;
   }
   v *= 0.5;
-  // orthogonality coeff ||A A^T - I||^2 (ref terms.py:234)
+  // orthogonality coeff ||A A^T - I||^2 (ref terms.py:66)
   double c = W.aff_ortho[b];
   M3 A;
   for (int i = 0; i < 9; ++i) A.m[i] = x[o + 3 + i];
@@ -543,7 +543,7 @@ __device__ __forceinline__ void body_item(const World& W, const double* __restri
   }
 }
 
-__global__ void k_body(World W, const double* __restrict__ x, const double* __restrict__ xhat,
+IPC_GLOBAL void k_body(World W, const double* __restrict__ x, const double* __restrict__ xhat,
                        double h2, int deriv, const int* env_flag, double* val, double* g12,
                        double* h144) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -608,7 +608,7 @@ __device__ __forceinline__ void tet_item(const World& W, const double* __restric
   }
 }
 
-__global__ void k_tet(World W, const double* __restrict__ x, double h2, int deriv,
+IPC_GLOBAL void k_tet(World W, const double* __restrict__ x, double h2, int deriv,
                       const int* env_flag, double* val, double* g12, double* hp) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= W.n_tet) return;
@@ -619,7 +619,7 @@ __global__ void k_tet(World W, const double* __restrict__ x, double h2, int deri
 // Contact pairs, pass 1 (light, every candidate of every flagged env):
 // region + squared distance, value κ b (× mollifier) for active pairs, 0
 // otherwise, INF when an active pair has non-positive distance
-// (ref contact.py:497-531); min distance stats. In the derivative pass the
+// (ref contact.py:239-268); min distance stats. In the derivative pass the
 // active pairs are appended to a work list for pass 2. Persistent
 // grid-stride over the flattened candidate index (prefix C.pre_*).
 __device__ __forceinline__ void pair_slots(const World& W, int kind, int2 pr, int* sl) {
@@ -679,7 +679,7 @@ __device__ __forceinline__ bool pair_value_item(const World& W, const double* __
     return true;
 }
 
-__global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int deriv, PairIO io,
+IPC_GLOBAL void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int deriv, PairIO io,
                             double* env_min_s) {
   const int kind = blockIdx.y;
   const int* pre = kind == 0 ? C.pre_pt : C.pre_ee;
@@ -698,69 +698,210 @@ __global__ void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int
 }
 
 // Contact pairs, pass 2 (heavy, active pairs only): closed-form distance
-// derivatives, barrier chain rule, mollifier product rule, PSD projection.
-// Values were written by pass 1; the value term is recomputed from the same
-// formulas here for the derivative distance s (ref contact.py:505-556).
-// one instantiation per pair kind keeps each kernel's code (and register
-// demand) small: the combined kernel was instruction-cache bound
+// derivatives in var space, barrier chain rule, mollifier product rule, and
+// the PSD projection in the Helmert space of the region's active slots
+// (ipc_math.cuh helm_*; ref contact.py:255-266, spd.py:6). Everything stays in
+// registers: no 12x12 stencil array is formed.
+
+// var-space derivatives of a region: NV difference vars v_i = x_{p_i} - x_{q_i}
+// (p, q: local slot indices of the region's NS active slots)
+template <int NV>
+struct VarSet {
+  V3 gv[NV];
+  M3 hv[NV][NV];
+  int p[NV], q[NV];
+  double s;
+};
+
+template <int NS>
+__device__ __forceinline__ void pair_core_out(const int (&sl)[NS], double* gh, double* M, double* g12,
+                                              double* hp) {
+  constexpr int R = 3 * (NS - 1);
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < r; ++c) M[r * R + c] = M[c * R + r];
+#ifndef IPC_NO_PSD
+  psd_project<R>(M, R);
+#endif
+  helm_out<NS>(sl, gh, M, g12, hp);
+}
+
+// H = κ(b'' ∇s∇sᵀ + b' ∇²s), g = κ b' ∇s
+template <int NS, int NV>
+__device__ __forceinline__ void pair_plain(const VarSet<NV>& V, const int (&sl)[NS], double kappa, double shat,
+                                           double* g12, double* hp) {
+  constexpr int NB = NS - 1, R = 3 * NB;
+  double b, db, d2b;
+  barrier_d(V.s, shat, &b, &db, &d2b);
+  double beta[NV][NB];
+  helm_beta<NV, NB>(V.p, V.q, beta);
+  double gh[R], M[R * R];
+  helm_grad<NV, NB>(beta, V.gv, gh);
+#pragma unroll
+  for (int i = 0; i < R * R; ++i) M[i] = 0.0;
+  helm_hess_acc<NV, NB>(beta, V.hv, kappa * db, M);
+  helm_outer_acc<R>(gh, gh, kappa * d2b, false, M);
+#pragma unroll
+  for (int i = 0; i < R; ++i) gh[i] *= kappa * db;
+  pair_core_out<NS>(sl, gh, M, g12, hp);
+}
+
+// mollified EE (ref contact.py:166-203, :286-312), all 4 slots: the s part in its
+// region vars (stencil slot indices) and the mollifier c = |u x v|²
+template <int NV>
+__device__ __forceinline__ void ee_mollified(const VarSet<NV>& V, const V3* X, double t, double eps, double kappa,
+                                             double shat, double* g12, double* hp) {
+  double b, db, d2b;
+  barrier_d(V.s, shat, &b, &db, &d2b);
+  double em = t * (2.0 - t), de = (2.0 - 2.0 * t) / eps, d2e = -2.0 / (eps * eps);
+  double bs[NV][3], bc[2][3];
+  helm_beta<NV, 3>(V.p, V.q, bs);
+  VarSet<2> Cv;
+  vs_cross2(X[1] - X[0], X[3] - X[2], Cv.gv, Cv.hv);
+  Cv.p[0] = 1; Cv.q[0] = 0; Cv.p[1] = 3; Cv.q[1] = 2;
+  helm_beta<2, 3>(Cv.p, Cv.q, bc);
+  double gs[9], gc[9], M[81];
+  helm_grad<NV, 3>(bs, V.gv, gs);
+  helm_grad<2, 3>(bc, Cv.gv, gc);
+#pragma unroll
+  for (int i = 0; i < 81; ++i) M[i] = 0.0;
+  helm_hess_acc<NV, 3>(bs, V.hv, kappa * (em * db), M);
+  helm_hess_acc<2, 3>(bc, Cv.hv, kappa * (de * b), M);
+  helm_outer_acc<9>(gs, gs, kappa * (em * d2b), false, M);
+  helm_outer_acc<9>(gc, gc, kappa * (d2e * b), false, M);
+  helm_outer_acc<9>(gc, gs, kappa * (de * db), true, M);
+  double gh[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) gh[i] = kappa * ((de * b) * gc[i] + (em * db) * gs[i]);
+  const int sl[4] = {0, 1, 2, 3};
+  pair_core_out<4>(sl, gh, M, g12, hp);
+}
+
+__device__ __forceinline__ VarSet<1> region_pp(const V3* X, int i, int j) {
+  VarSet<1> V;
+  V.s = vs_pp(X[i] - X[j], V.gv, V.hv);
+  V.p[0] = i; V.q[0] = j;
+  return V;
+}
+// point a to line (b, c): w = x_a - x_b, e = x_c - x_b
+__device__ __forceinline__ VarSet<2> region_pl(const V3* X, int a, int b, int c) {
+  VarSet<2> V;
+  V.s = vs_pl(X[a] - X[b], X[c] - X[b], V.gv, V.hv);
+  V.p[0] = a; V.q[0] = b; V.p[1] = c; V.q[1] = b;
+  return V;
+}
+
+// squared distance and its stencil gradient only (G: 12, zero on entry), for
+// the friction lags (ref friction.py:75) — no Hessian is formed
+template <int NV>
+__device__ __forceinline__ double scatter_grad(const VarSet<NV>& V, const int* sl, double* G) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    int a = sl[V.p[i]], b = sl[V.q[i]];
+    G[3 * a] += V.gv[i].x; G[3 * a + 1] += V.gv[i].y; G[3 * a + 2] += V.gv[i].z;
+    G[3 * b] -= V.gv[i].x; G[3 * b + 1] -= V.gv[i].y; G[3 * b + 2] -= V.gv[i].z;
+  }
+  return V.s;
+}
+__device__ __forceinline__ double dist2_grad(bool is_pt, int region, const V3* X, double* G) {
+  const int id[4] = {0, 1, 2, 3};
+  if (is_pt) {
+    if (region < 3) return scatter_grad<1>(region_pp(X, 0, region + 1), id, G);
+    if (region == 3) return scatter_grad<2>(region_pl(X, 0, 1, 2), id, G);
+    if (region == 4) return scatter_grad<2>(region_pl(X, 0, 2, 3), id, G);
+    if (region == 5) return scatter_grad<2>(region_pl(X, 0, 3, 1), id, G);
+    VarSet<3> V;
+    V.s = vs_triple(X[0] - X[1], X[2] - X[1], X[3] - X[1], V.gv, V.hv);
+    V.p[0] = 0; V.q[0] = 1; V.p[1] = 2; V.q[1] = 1; V.p[2] = 3; V.q[2] = 1;
+    return scatter_grad<3>(V, id, G);
+  }
+  int ra = region / 3, rb = region % 3;
+  if (ra < 2 && rb < 2) return scatter_grad<1>(region_pp(X, ra, 2 + rb), id, G);
+  if (ra < 2) return scatter_grad<2>(region_pl(X, ra, 2, 3), id, G);
+  if (rb < 2) return scatter_grad<2>(region_pl(X, 2 + rb, 0, 1), id, G);
+  VarSet<3> V;
+  V.s = vs_triple(X[2] - X[0], X[1] - X[0], X[3] - X[2], V.gv, V.hv);
+  V.p[0] = 2; V.q[0] = 0; V.p[1] = 1; V.q[1] = 0; V.p[2] = 3; V.q[2] = 2;
+  return scatter_grad<3>(V, id, G);
+}
+
 template <int kind>
 __device__ __forceinline__ void pair_hess_item(const World& W, const double* __restrict__ xw, const Cands& C,
                                                long long k, int e, double* g12, double* hp,
                                                unsigned char* active) {
     int2 pr = kind == 0 ? C.pt[k] : C.ee[k];
-    int sl[4];
-    pair_slots(W, kind, pr, sl);
+    int sl4[4];
+    pair_slots(W, kind, pr, sl4);
     V3 X[4];
-    for (int i = 0; i < 4; ++i) X[i] = ld3(xw + 3 * sl[i]);
-    int region = kind == 0 ? pt_region(X[0], X[1], X[2], X[3]) : ee_region(X[0], X[1], X[2], X[3], nullptr);
+    for (int i = 0; i < 4; ++i) X[i] = ld3(xw + 3 * sl4[i]);
     double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
-    double G[12], H[144];
-    for (int i = 0; i < 12; ++i) G[i] = 0.0;
-    for (int i = 0; i < 144; ++i) H[i] = 0.0;
-    int mask;
-    double s = dist2_derivs(kind == 0, region, X, G, H, &mask);
-    double b, db, d2b;
-    barrier_d(s, shat, &b, &db, &d2b);
-    double gout[12];
+    double* g = g12 + 12 * k;
+    double* h = hp + PK * k;
     if (kind == 0) {
-      for (int i = 0; i < 12; ++i) gout[i] = kappa * db * G[i];
-      for (int i = 0; i < 12; ++i)
-        for (int j = 0; j < 12; ++j) H[i * 12 + j] = kappa * (d2b * G[i] * G[j] + db * H[i * 12 + j]);
+      int region = pt_region(X[0], X[1], X[2], X[3]);
+      if (region < 3) {  // point-point: local slots (0, t), var x0 - xt
+        int t = region + 1;
+        VarSet<1> V;
+        V.s = vs_pp(X[0] - X[t], V.gv, V.hv);
+        V.p[0] = 0; V.q[0] = 1;
+        const int sl[2] = {0, t};
+        pair_plain<2, 1>(V, sl, kappa, shat, g, h);
+      } else if (region < 6) {  // point-edge: local slots (0, a, b)
+        int a = region == 3 ? 1 : (region == 4 ? 2 : 3);
+        int bb = region == 3 ? 2 : (region == 4 ? 3 : 1);
+        VarSet<2> V;
+        V.s = vs_pl(X[0] - X[a], X[bb] - X[a], V.gv, V.hv);
+        V.p[0] = 0; V.q[0] = 1; V.p[1] = 2; V.q[1] = 1;
+        const int sl[3] = {0, a, bb};
+        pair_plain<3, 2>(V, sl, kappa, shat, g, h);
+      } else {  // point-face: w = x0 - x1, u = x2 - x1, v = x3 - x1
+        VarSet<3> V;
+        V.s = vs_triple(X[0] - X[1], X[2] - X[1], X[3] - X[1], V.gv, V.hv);
+        V.p[0] = 0; V.q[0] = 1; V.p[1] = 2; V.q[1] = 1; V.p[2] = 3; V.q[2] = 1;
+        const int sl[4] = {0, 1, 2, 3};
+        pair_plain<4, 3>(V, sl, kappa, shat, g, h);
+      }
     } else {
-      // mollified EE (ref contact.py:414-449): H = κ[(d2e b) ∇c∇cᵀ + (de b) ∇²c
-      //   + (de db)(∇c∇sᵀ + ∇s∇cᵀ) + (em d2b) ∇s∇sᵀ + (em db) ∇²s]; the ∇²c
-      // term is accumulated in place and skipped when the mollifier is flat
+      int region = ee_region(X[0], X[1], X[2], X[3], nullptr);
       double eps = 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y];
       double t = cross2(X[1] - X[0], X[3] - X[2]) / eps;
-      double em, de, d2e;
+      // region slots: PP (i, j) / point i to line (j, k) / line-line
+      int ra = region / 3, rb = region % 3;
       if (t < 1.0) {
-        em = t * (2.0 - t);
-        de = (2.0 - 2.0 * t) / eps;
-        d2e = -2.0 / (eps * eps);
+        if (ra < 2 && rb < 2) {
+          ee_mollified<1>(region_pp(X, ra, 2 + rb), X, t, eps, kappa, shat, g, h);
+        } else if (ra < 2) {
+          ee_mollified<2>(region_pl(X, ra, 2, 3), X, t, eps, kappa, shat, g, h);
+        } else if (rb < 2) {
+          ee_mollified<2>(region_pl(X, 2 + rb, 0, 1), X, t, eps, kappa, shat, g, h);
+        } else {
+          VarSet<3> V;
+          V.s = vs_triple(X[2] - X[0], X[1] - X[0], X[3] - X[2], V.gv, V.hv);
+          V.p[0] = 2; V.q[0] = 0; V.p[1] = 1; V.q[1] = 0; V.p[2] = 3; V.q[2] = 2;
+          ee_mollified<3>(V, X, t, eps, kappa, shat, g, h);
+        }
+      } else if (ra < 2 && rb < 2) {
+        VarSet<1> V;
+        V.s = vs_pp(X[ra] - X[2 + rb], V.gv, V.hv);
+        V.p[0] = 0; V.q[0] = 1;
+        const int sl[2] = {ra, 2 + rb};
+        pair_plain<2, 1>(V, sl, kappa, shat, g, h);
+      } else if (ra < 2 || rb < 2) {
+        int pa = ra < 2 ? ra : 2 + rb, l0 = ra < 2 ? 2 : 0;
+        VarSet<2> V;
+        V.s = vs_pl(X[pa] - X[l0], X[l0 + 1] - X[l0], V.gv, V.hv);
+        V.p[0] = 0; V.q[0] = 1; V.p[1] = 2; V.q[1] = 1;
+        const int sl[3] = {pa, l0, l0 + 1};
+        pair_plain<3, 2>(V, sl, kappa, shat, g, h);
       } else {
-        em = 1.0; de = 0.0; d2e = 0.0;
-      }
-      for (int i = 0; i < 12; ++i)
-        for (int j = 0; j < 12; ++j) H[i * 12 + j] = kappa * ((em * d2b) * G[i] * G[j] + (em * db) * H[i * 12 + j]);
-      if (t < 1.0) {
-        double Gc[12];
-        for (int i = 0; i < 12; ++i) Gc[i] = 0.0;
-        cross2_grad_acc(X, Gc, H, kappa * (de * b));
-        for (int i = 0; i < 12; ++i)
-          for (int j = 0; j < 12; ++j)
-            H[i * 12 + j] += kappa * ((d2e * b) * Gc[i] * Gc[j] + (de * db) * (Gc[i] * G[j] + G[i] * Gc[j]));
-        for (int i = 0; i < 12; ++i) gout[i] = kappa * ((de * b) * Gc[i] + (em * db) * G[i]);
-        mask = 0xF;
-      } else {
-        for (int i = 0; i < 12; ++i) gout[i] = kappa * ((em * db) * G[i]);
+        VarSet<3> V;
+        V.s = vs_triple(X[2] - X[0], X[1] - X[0], X[3] - X[2], V.gv, V.hv);
+        V.p[0] = 2; V.q[0] = 0; V.p[1] = 1; V.q[1] = 0; V.p[2] = 3; V.q[2] = 2;
+        const int sl[4] = {0, 1, 2, 3};
+        pair_plain<4, 3>(V, sl, kappa, shat, g, h);
       }
     }
-#ifndef IPC_NO_PSD
-    psd_project_masked12(H, mask);
-#endif
-    for (int i = 0; i < 12; ++i) g12[12 * k + i] = gout[i];
-    for (int i = 0; i < 12; ++i)
-      for (int j = i; j < 12; ++j) hp[PK * k + pk(i, j)] = H[i * 12 + j];
     active[k] = (unsigned char)0xF;
 }
 
@@ -771,7 +912,7 @@ __global__ void __launch_bounds__(64) k_pair_hess(World W, const double* __restr
     pair_hess_item<kind>(W, xw, C, io.work[kind][w], io.work_env[kind][w], io.g[kind], io.h[kind], io.act[kind]);
 }
 
-// ground candidates (ref contact.py:564): value, y-gradient, clamped y-curvature
+// ground candidates (ref contact.py:315-345): value, y-gradient, clamped y-curvature
 // ground candidate k (global index) of env e; min_s: the env's minimum
 __device__ __forceinline__ void ground_item(const World& W, const double* __restrict__ xw, const Cands& C,
                                             int deriv, int k, int e, double* val, double* gy, double* hyy,
@@ -801,7 +942,7 @@ __device__ __forceinline__ void ground_item(const World& W, const double* __rest
   }
 }
 
-__global__ void k_ground(World W, const double* __restrict__ xw, Cands C, int deriv,
+IPC_GLOBAL void k_ground(World W, const double* __restrict__ xw, Cands C, int deriv,
                          const int* env_flag, double* val, double* gy, double* hyy,
                          double* env_min_s) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -827,7 +968,7 @@ IPC_HD void tangent_basis(V3 n, double* T /*3x2 row-major*/) {
 
 // lag one candidate pair if active and λ > 0; lags are appended per env in
 // candidate order (PT list then EE list) — one CTA per env for ordering.
-__device__ void lags_env(const World& W, const double* __restrict__ xw, const Cands& C, const Lags& L, int e) {
+static __device__ void lags_env(const World& W, const double* __restrict__ xw, const Cands& C, const Lags& L, int e) {
   __shared__ int warp_tot[BP_THREADS / 32];
   __shared__ int total;
   double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
@@ -862,11 +1003,9 @@ __device__ void lags_env(const World& W, const double* __restrict__ xw, const Ca
           d2 = ee_dist2(region, X[0], X[1], X[2], X[3]);
         }
         if (d2 < shat) {
-          double G[12], H[144];
+          double G[12];
           for (int i = 0; i < 12; ++i) G[i] = 0.0;
-          for (int i = 0; i < 144; ++i) H[i] = 0.0;
-          int mask;
-          double s = dist2_derivs(kind == 0, region, X, G, H, &mask);
+          double s = dist2_grad(kind == 0, region, X, G);
           double d = sqrt(s);
           double b, db, d2b;
           barrier_d(s, shat, &b, &db, &d2b);
@@ -939,7 +1078,7 @@ __device__ void lags_env(const World& W, const double* __restrict__ xw, const Ca
   if (threadIdx.x == 0) L.g_n[e] = gbase;
 }
 
-__global__ void k_lags(World W, const double* __restrict__ xw, Cands C, Lags L, const int* env_flag) {
+IPC_GLOBAL void k_lags(World W, const double* __restrict__ xw, Cands C, Lags L, const int* env_flag) {
   int e = blockIdx.x;
   if (env_flag && !env_flag[e]) return;
   lags_env(W, xw, C, L, e);
@@ -1000,7 +1139,7 @@ __device__ __forceinline__ void friction_item(const World& W, const double* __re
     for (int c = r; c < 12; ++c) hp[PK * q + pk(r, c)] = gam[r / 3] * gam[c / 3] * h3[3 * (r % 3) + c % 3];
 }
 
-__global__ void k_friction(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
+IPC_GLOBAL void k_friction(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
                            Lags L, double h, int deriv, const int* env_flag, double* val,
                            double* g12, double* hp) {
   int total = L.pre[W.n_env];
@@ -1028,7 +1167,7 @@ __device__ __forceinline__ void friction_gnd_item(const World& W, const double* 
   h3[9 * q + 6] = hu[2]; h3[9 * q + 7] = 0.0; h3[9 * q + 8] = hu[3];
 }
 
-__global__ void k_friction_gnd(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
+IPC_GLOBAL void k_friction_gnd(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
                                Lags L, double h, int deriv, const int* env_flag, double* val,
                                double* g3, double* h3) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1039,9 +1178,9 @@ __global__ void k_friction_gnd(World W, const double* __restrict__ xw, const dou
 }
 
 // ---------------------------------------------------------------------------
-// CCD: per-pair conservative advancement (ref ccd.py:395) and ground crossing
+// CCD: per-pair conservative advancement (ref ccd.py:34) and ground crossing
 // ---------------------------------------------------------------------------
-__device__ double stencil_dist(int kind, const V3* X) {
+static __device__ double stencil_dist(int kind, const V3* X) {
   if (kind == 0) {
     int r = pt_region(X[0], X[1], X[2], X[3]);
     return sqrt(pt_dist2(r, X[0], X[1], X[2], X[3]));
@@ -1050,7 +1189,7 @@ __device__ double stencil_dist(int kind, const V3* X) {
   return sqrt(ee_dist2(r, X[0], X[1], X[2], X[3]));
 }
 
-__device__ double pair_ccd_alpha(int kind, const V3* X, const V3* D, double conservative) {
+static __device__ double pair_ccd_alpha(int kind, const V3* X, const V3* D, double conservative) {
   V3 sum = ((D[0] + D[1]) + D[2]) + D[3];
   V3 mean = v3(__ddiv_rn(sum.x, 4.0), __ddiv_rn(sum.y, 4.0), __ddiv_rn(sum.z, 4.0));
   double sp[4];
@@ -1102,7 +1241,7 @@ __device__ __forceinline__ double ccd_ground_item(const World& W, const double* 
   return fmin(1.0, conservative * t);
 }
 
-__global__ void k_ccd_pairs(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
+IPC_GLOBAL void k_ccd_pairs(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
                             Cands C, double conservative, const int* env_flag, double* env_alpha) {
   const int kind = blockIdx.y;
   const int* pre = kind == 0 ? C.pre_pt : C.pre_ee;
@@ -1116,7 +1255,7 @@ __global__ void k_ccd_pairs(World W, const double* __restrict__ xw, const double
   }
 }
 
-__global__ void k_ccd_ground(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
+IPC_GLOBAL void k_ccd_ground(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
                              Cands C, double conservative, const int* env_flag, double* env_alpha) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   int e = blockIdx.y;

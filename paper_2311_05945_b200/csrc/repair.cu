@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, RETRACT_MIN_BLOCKS) k_repair_retract
   if (threadIdx.x == 0) out[e] = s_found;
 }
 
-// ref proximity.py:254-266 per env: max over contained points of the
+// ref proximity.py:235-246 per env: max over contained points of the
 // unsigned surface distance (ref :214), 0 if none is contained
 __global__ void __launch_bounds__(kThreads) k_max_penetration(
     const int32_t* __restrict__ env_pt, const double* __restrict__ pts,

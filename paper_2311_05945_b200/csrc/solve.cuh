@@ -7,7 +7,7 @@ namespace ipc {
 
 constexpr int RED_THREADS = 256;
 
-__device__ double block_sum(double v, double* sh) {
+static __device__ double block_sum(double v, double* sh) {
   // fixed-shape tree: deterministic for a fixed thread->item assignment
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -21,7 +21,7 @@ __device__ double block_sum(double v, double* sh) {
   return r;  // valid on thread 0
 }
 
-__device__ double block_max(double v, double* sh) {
+static __device__ double block_max(double v, double* sh) {
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
@@ -42,7 +42,7 @@ struct Terms {
 
 // E(x) per env = ½(x−x̂)ᵀM(x−x̂) [soft part here, affine in body_val] + Σ element values
 // block function: env e's energy, valid on thread 0
-__device__ double env_energy_block(const World& W, const double* __restrict__ x, const double* __restrict__ xhat,
+static __device__ double env_energy_block(const World& W, const double* __restrict__ x, const double* __restrict__ xhat,
                                    const Terms& T, const Cands& C, const Lags& L, int e) {
   __shared__ double sh[RED_THREADS / 32];
   double acc = 0.0;
@@ -66,7 +66,7 @@ __device__ double env_energy_block(const World& W, const double* __restrict__ x,
   return block_sum(acc, sh);
 }
 
-__global__ void __launch_bounds__(RED_THREADS) k_env_energy(World W, const double* __restrict__ x,
+IPC_GLOBAL void __launch_bounds__(RED_THREADS) k_env_energy(World W, const double* __restrict__ x,
                                                              const double* __restrict__ xhat, Terms T,
                                                              Cands C, Lags L, const int* env_flag,
                                                              double* out) {
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_env_energy(World W, const doubl
 // element kernels (k_body, k_tet, k_pair_dist, k_ground, k_friction), so the
 // values are the same bits; a whole M-trial backtracking round is one launch.
 // ---------------------------------------------------------------------------
-__device__ double body_value(const World& W, int b, int e, const double* q, const double* xh, double h2) {
+static __device__ double body_value(const World& W, int b, int e, const double* q, const double* xh, double h2) {
   const double* M = W.aff_M + 144 * b;
   double d[12];
   for (int i = 0; i < 12; ++i) d[i] = q[i] - xh[i];
@@ -124,7 +124,7 @@ __device__ __forceinline__ double axpy_rn(double x, double a, double p) { return
 
 // block function: E(x + a p) of env e (valid on thread 0); sxw: 3 doubles
 // per env slot of shared scratch
-__device__ double ls_value_block(const World& W, const Cands& C, const Lags& L, const double* __restrict__ x,
+static __device__ double ls_value_block(const World& W, const Cands& C, const Lags& L, const double* __restrict__ x,
                                  const double* __restrict__ p, const double* __restrict__ xhat, double h2, double h,
                                  double a, int e, double* sxw) {
   __shared__ double sh[RED_THREADS / 32];
@@ -249,7 +249,7 @@ __device__ double ls_value_block(const World& W, const Cands& C, const Lags& L, 
   return tot;
 }
 
-__global__ void __launch_bounds__(RED_THREADS) k_ls_value(World W, EnvState S, Cands C, Lags L,
+IPC_GLOBAL void __launch_bounds__(RED_THREADS) k_ls_value(World W, EnvState S, Cands C, Lags L,
                                                            const double* __restrict__ x,
                                                            const double* __restrict__ p,
                                                            const double* __restrict__ xhat, double h2, double h,
@@ -273,106 +273,245 @@ struct Derivs {
   double *frg_g, *frg_h;             // 3, 9 per ground lag
 };
 
-// Add one stencil (ns slots, slot-space gradient gs[3ns] and Hessian hs)
-// to the dense env system, lifting affine slots through J(x0) and merging
-// slots that ride the same body (ref contact.py:346). One call = one element;
-// each thread owns distinct output entries, so no atomics are needed.
-template <typename HGet>
-__device__ void add_stencil(const World& W, int d0, int n, double* H, double* g, int ns, const int* sl,
-                            const double* gs, HGet hget) {
-  // Stage the stencil in shared memory, then build a row table: lifted row r
-  // (a DoF of one of the stencil's merged groups) is Σ over the group's slots
-  // a of w_a(r) · (slot-space row 3a + i_a(r)). Entry (r, c) of the lifted
-  // block is Σ_p Σ_q w_p w_q H_s[idx_p, idx_q] over the ≤3 terms of row r and
-  // column c; every thread owns distinct output entries (no atomics).
-  __shared__ double sH[144], sg[12], srest[12];
-  __shared__ int saff[4], skey[4];
-  __shared__ int rt_n[48], rt_idx[48][3], rt_dof[48];
-  __shared__ double rt_w[48][3];
-  __shared__ int s_tot;
-  int tid = threadIdx.x;
-  int N = 3 * ns;
-  for (int i = tid; i < N * N; i += blockDim.x) sH[i] = hget(i / N, i % N);
-  for (int i = tid; i < N; i += blockDim.x) sg[i] = gs[i];
-  if (tid < ns) {
-    int s = sl[tid];
-    saff[tid] = W.slot_aff[s];
-    skey[tid] = W.slot_dof[s] - d0;
-    for (int c = 0; c < 3; ++c) srest[3 * tid + c] = W.slot_rest[3 * s + c];
-  }
-  __syncthreads();
-  if (tid < 32) {  // one warp builds the row table
-    int key[4], wid[4], grp[4], gstart[5];
-    int ng = 0;
-    for (int a = 0; a < ns; ++a) {
-      int gi = -1;
-      for (int q = 0; q < ng; ++q)
-        if (key[q] == skey[a]) gi = q;
-      if (gi < 0) {
-        gi = ng++;
-        key[gi] = skey[a];
-        wid[gi] = saff[a] ? 12 : 3;
-      }
-      grp[a] = gi;
-    }
-    gstart[0] = 0;
-    for (int q = 0; q < ng; ++q) gstart[q + 1] = gstart[q] + wid[q];
-    int tot = gstart[ng];
-    for (int r = tid; r < tot; r += 32) {
-      int q = 0;
-      while (r >= gstart[q + 1]) ++q;
-      int R = r - gstart[q];
-      int cnt = 0;
-      for (int a = 0; a < ns; ++a) {
-        if (grp[a] != q) continue;
-        int ia;
-        double wa;
-        if (!saff[a] || R < 3) {
-          ia = R;
-          wa = 1.0;
-        } else {
-          ia = (R - 3) / 3;
-          wa = srest[3 * a + (R - 3) % 3];
-        }
-        rt_idx[r][cnt] = 3 * a + ia;
-        rt_w[r][cnt] = wa;
-        ++cnt;
-      }
-      rt_n[r] = cnt;
-      rt_dof[r] = key[q] + R;
-    }
-    if (tid == 0) s_tot = tot;
-  }
-  __syncthreads();
-  int tot = s_tot;
-  // lower triangle only (rt_dof[c] <= rt_dof[r]): the LDLᵀ below never
-  // reads the upper part
-  for (int idx = tid; idx < tot * tot; idx += blockDim.x) {
-    int r = idx / tot, c = idx - r * tot;
-    if (rt_dof[c] > rt_dof[r]) continue;
-    double acc = 0.0;
-    for (int p = 0; p < rt_n[r]; ++p) {
-      const double* hr = sH + rt_idx[r][p] * N;
-      double sub = 0.0;
-      for (int q = 0; q < rt_n[c]; ++q) sub += rt_w[c][q] * hr[rt_idx[c][q]];
-      acc += rt_w[r][p] * sub;
-    }
-    H[rt_dof[r] * n + rt_dof[c]] += acc;
-  }
-  for (int r = tid; r < tot; r += blockDim.x) {
-    double acc = 0.0;
-    for (int p = 0; p < rt_n[r]; ++p) acc += rt_w[r][p] * sg[rt_idx[r][p]];
-    g[rt_dof[r]] += acc;
-  }
-  __syncthreads();
+constexpr int DENSE_THREADS = 256;
+
+// dynamic shared memory of the dense solve of an n-DoF env: system n² + 2n,
+// the record staging area, the per-DoF group keys
+__host__ __device__ inline int dense_smem_doubles(int n);
+
+// ---------------------------------------------------------------------------
+// Record-parallel dense assembly. Every stencil (tet, active PT / EE pair,
+// ground barrier, friction lag, ground friction lag) is a *record* of ≤4
+// slots with a slot-space gradient (3·ns) and Hessian (packed 12x12). Records
+// are staged REC_CHUNK at a time in shared memory; then every entry (r, c)
+// of the lower triangle and every gradient entry has ONE owner thread that
+// adds the lifted contribution of each staged record in record order
+// (ref contact.py:346 lifting through J(x0), slots of one body merged), so
+// the sums are deterministic and no per-record barrier is needed.
+// ---------------------------------------------------------------------------
+constexpr int REC_CHUNK = 32;
+struct RecStage {  // carved from dynamic shared memory (rec_stage_doubles)
+  double* h;       // [REC_CHUNK][78] packed slot-space Hessian
+  double* g;       // [REC_CHUNK][12]
+  double* rest;    // [REC_CHUNK][12] slot lever arms (affine slots)
+  int* key;        // [REC_CHUNK][4] local DoF offset of the slot's group (-1: unused)
+  int* aff;        // [REC_CHUNK][4]
+  int* ns;         // [REC_CHUNK]
+};
+__host__ __device__ constexpr int rec_stage_doubles() { return REC_CHUNK * (78 + 12 + 12) + (REC_CHUNK * 9 + 1) / 2 + 2; }
+__host__ __device__ inline int dense_smem_doubles(int n) { return n * n + 2 * n + rec_stage_doubles() + (n + 1) / 2 + 1; }
+__device__ __forceinline__ RecStage rec_stage(double* base) {
+  RecStage R;
+  R.h = base;
+  R.g = R.h + REC_CHUNK * 78;
+  R.rest = R.g + REC_CHUNK * 12;
+  R.key = reinterpret_cast<int*>(R.rest + REC_CHUNK * 12);
+  R.aff = R.key + REC_CHUNK * 4;
+  R.ns = R.aff + REC_CHUNK * 4;
+  return R;
 }
 
-constexpr int DENSE_THREADS = 256;
+// weight / slot-space row of lifted row R of a group for slot a
+__device__ __forceinline__ void lift_row(const RecStage& R, int k, int a, int Rr, int* ia, double* wa) {
+  if (!R.aff[4 * k + a] || Rr < 3) {
+    *ia = 3 * a + Rr;
+    *wa = 1.0;
+  } else {
+    *ia = 3 * a + (Rr - 3) / 3;
+    *wa = R.rest[12 * k + 3 * a + (Rr - 3) % 3];
+  }
+}
+
+// record types of the virtual index space, in assembly order
+enum { REC_TET, REC_PT, REC_EE, REC_GND, REC_FR, REC_FRG };
+
+static __device__ void assemble_records(const World& W, const Derivs& D, const Cands& C, const Lags& L, int e, int d0,
+                                 int n, double* H, double* g, const int* dkey, double* stage_mem) {
+  __shared__ int alist[DENSE_THREADS];
+  __shared__ int wtot[DENSE_THREADS / 32];
+  __shared__ int atot;
+  RecStage R = rec_stage(stage_mem);
+  int tid = threadIdx.x;
+  int t0 = W.env_tet[e], ntet = W.env_tet[e + 1] - t0;
+  int npt = C.n_pt[e], nee = C.n_ee[e], ngnd = C.n_gnd[e], nfr = L.n[e], nfrg = L.g_n[e];
+  long long pt0 = C.pt_off[e], ee0 = C.ee_off[e], fr0 = L.off[e];
+  int gnd0 = C.gnd_off[e], frg0 = W.env_slot[e];
+  int lim[6] = {ntet, npt, nee, ngnd, nfr, nfrg};
+  int total = ntet + npt + nee + ngnd + nfr + nfrg;
+  int nlow = n * (n + 1) / 2;
+  for (int v0 = 0; v0 < total; v0 += DENSE_THREADS) {
+    // ordered compaction of the contributing records of this window
+    int v = v0 + tid;
+    bool on = false;
+    if (v < total) {
+      int t = 0, j = v;
+      while (j >= lim[t]) j -= lim[t++];
+      if (t == REC_PT) on = D.pt_act[pt0 + j];
+      else if (t == REC_EE) on = D.ee_act[ee0 + j];
+      else if (t == REC_GND) on = D.gnd_hyy[gnd0 + j] != 0.0 || D.gnd_gy[gnd0 + j] != 0.0;
+      else on = true;
+    }
+    int lane = tid & 31, wid = tid >> 5;
+    unsigned m = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) wtot[wid] = __popc(m);
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int w = 0; w < DENSE_THREADS / 32; ++w) {
+        int t = wtot[w];
+        wtot[w] = acc;
+        acc += t;
+      }
+      atot = acc;
+    }
+    __syncthreads();
+    if (on) alist[wtot[wid] + __popc(m & ((1u << lane) - 1u))] = v;
+    __syncthreads();
+    int na = atot;
+    for (int k0 = 0; k0 < na; k0 += REC_CHUNK) {
+      int nr = min(REC_CHUNK, na - k0);
+      // stage headers: one thread per record
+      if (tid < nr) {
+        int k = tid, j = alist[k0 + k], t = 0;
+        while (j >= lim[t]) j -= lim[t++];
+        int sl[4] = {-1, -1, -1, -1}, ns = 4;
+        if (t == REC_TET) {
+          int4 td = W.tet_dof[t0 + j];
+          int dv[4] = {td.x, td.y, td.z, td.w};
+          for (int a = 0; a < 4; ++a) {
+            R.key[4 * k + a] = dv[a] - d0;
+            R.aff[4 * k + a] = 0;
+          }
+        } else {
+          if (t == REC_PT) {
+            int2 pr = C.pt[pt0 + j];
+            int3 tv = W.tri_v[pr.y];
+            sl[0] = pr.x; sl[1] = tv.x; sl[2] = tv.y; sl[3] = tv.z;
+          } else if (t == REC_EE) {
+            int2 pr = C.ee[ee0 + j];
+            int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
+            sl[0] = a.x; sl[1] = a.y; sl[2] = b.x; sl[3] = b.y;
+          } else if (t == REC_FR) {
+            int4 s4 = L.slots[fr0 + j];
+            sl[0] = s4.x; sl[1] = s4.y; sl[2] = s4.z; sl[3] = s4.w;
+          } else if (t == REC_GND) {
+            sl[0] = C.gnd[gnd0 + j];
+            ns = 1;
+          } else {
+            sl[0] = L.g_slot[frg0 + j];
+            ns = 1;
+          }
+          for (int a = 0; a < 4; ++a) {
+            if (a < ns) {
+              int sa = sl[a];
+              R.key[4 * k + a] = W.slot_dof[sa] - d0;
+              R.aff[4 * k + a] = W.slot_aff[sa];
+              for (int c = 0; c < 3; ++c) R.rest[12 * k + 3 * a + c] = W.slot_rest[3 * sa + c];
+            } else {
+              R.key[4 * k + a] = -1;
+              R.aff[4 * k + a] = 0;
+            }
+          }
+        }
+        R.ns[k] = ns;
+      }
+      // stage gradients and packed Hessians (all threads, coalesced per record)
+      for (int i = tid; i < nr * 90; i += DENSE_THREADS) {
+        int k = i / 90, q = i - 90 * k;
+        int j = alist[k0 + k], t = 0;
+        while (j >= lim[t]) j -= lim[t++];
+        double val = 0.0;
+        if (q < 78) {
+          if (t == REC_TET) val = D.tet_h[PK * (long long)(t0 + j) + q];
+          else if (t == REC_PT) val = D.pt_h[PK * (pt0 + j) + q];
+          else if (t == REC_EE) val = D.ee_h[PK * (ee0 + j) + q];
+          else if (t == REC_FR) val = D.fr_h[PK * (fr0 + j) + q];
+          else if (q == pk(1, 1) || (t == REC_FRG && (q < 3 || (q >= 12 && q < 14) || q == 23))) {
+            // 3x3 slot-space block of a one-slot record in the packed 12x12 layout
+            int r = q < 12 ? 0 : (q < 23 ? 1 : 2), c = q < 12 ? q : (q < 23 ? q - 11 : 2);
+            if (t == REC_GND) val = D.gnd_hyy[gnd0 + j];
+            else val = D.frg_h[9 * (long long)(frg0 + j) + 3 * r + c];
+          }
+          R.h[78 * k + q] = val;
+        } else {
+          int c = q - 78;
+          if (t == REC_TET) val = D.tet_g[12 * (long long)(t0 + j) + c];
+          else if (t == REC_PT) val = D.pt_g[12 * (pt0 + j) + c];
+          else if (t == REC_EE) val = D.ee_g[12 * (ee0 + j) + c];
+          else if (t == REC_FR) val = D.fr_g[12 * (fr0 + j) + c];
+          else if (t == REC_GND) val = c == 1 ? D.gnd_gy[gnd0 + j] : 0.0;
+          else if (c < 3) val = D.frg_g[3 * (long long)(frg0 + j) + c];
+          R.g[12 * k + c] = val;
+        }
+      }
+      __syncthreads();
+      // owners of the lower triangle: H[r][c] += Σ_a w_a(R) Σ_b w_b(C) Hs[ia][ib]
+      for (int idx = tid; idx < nlow; idx += DENSE_THREADS) {
+        int r = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+        while ((r + 1) * (r + 2) / 2 <= idx) ++r;
+        while (r * (r + 1) / 2 > idx) --r;
+        int c = idx - r * (r + 1) / 2;
+        int kr = dkey[r], kc = dkey[c];
+        int Rr = r - kr, Cc = c - kc;
+        double hv = H[r * n + c];
+        for (int k = 0; k < nr; ++k) {
+          int ns = R.ns[k];
+          int ma = 0, mb = 0;
+          for (int a = 0; a < ns; ++a) {
+            int ka = R.key[4 * k + a];
+            ma |= (ka == kr) << a;
+            mb |= (ka == kc) << a;
+          }
+          if (!ma || !mb) continue;
+          double acc = 0.0;
+          for (int a = 0; a < ns; ++a) {
+            if (!((ma >> a) & 1)) continue;
+            int ia;
+            double wa;
+            lift_row(R, k, a, Rr, &ia, &wa);
+            double sub = 0.0;
+            for (int b = 0; b < ns; ++b) {
+              if (!((mb >> b) & 1)) continue;
+              int ib;
+              double wb;
+              lift_row(R, k, b, Cc, &ib, &wb);
+              sub += wb * pk_get(R.h + 78 * k, ia, ib);
+            }
+            acc += wa * sub;
+          }
+          hv += acc;
+        }
+        H[r * n + c] = hv;
+      }
+      // owners of the gradient
+      for (int r = tid; r < n; r += DENSE_THREADS) {
+        int kr = dkey[r], Rr = r - kr;
+        double gv = g[r];
+        for (int k = 0; k < nr; ++k) {
+          int ns = R.ns[k];
+          double acc = 0.0;
+          bool hit = false;
+          for (int a = 0; a < ns; ++a) {
+            if (R.key[4 * k + a] != kr) continue;
+            int ia;
+            double wa;
+            lift_row(R, k, a, Rr, &ia, &wa);
+            acc += wa * R.g[12 * k + ia];
+            hit = true;
+          }
+          if (hit) gv += acc;
+        }
+        g[r] = gv;
+      }
+      __syncthreads();
+    }
+  }
+}
 
 // Assemble the env's dense Hessian/gradient, Cholesky-solve H p = −g with the
 // gradient fallback of ref solver.py:241, write p, ‖p‖∞, ‖g‖∞.
 // block function: assemble + solve env e; sm holds n² + 2n doubles
-__device__ void dense_solve_block(const World& W, const EnvState& S, const Derivs& D, const Cands& C,
+static __device__ void dense_solve_block(const World& W, const EnvState& S, const Derivs& D, const Cands& C,
                                   const Lags& L, const double* __restrict__ x, const double* __restrict__ xhat,
                                   double* p_out, double* g_out, int e, double* sm) {
   __shared__ double red[DENSE_THREADS / 32];
@@ -401,93 +540,19 @@ __device__ void dense_solve_block(const World& W, const EnvState& S, const Deriv
     for (int i = tid; i < 12; i += blockDim.x) g[o + i] += D.body_g[12 * b + i];
   }
   __syncthreads();
-  // tets
-  for (int t = W.env_tet[e]; t < W.env_tet[e + 1]; ++t) {
-    int4 td = W.tet_dof[t];
-    int dv[4] = {td.x - d0, td.y - d0, td.z - d0, td.w - d0};
-    const double* hp = D.tet_h + PK * t;
-    for (int i = tid; i < 144; i += blockDim.x) {
-      int r = i / 12, c = i % 12;
-      int rr = dv[r / 3] + r % 3, cc = dv[c / 3] + c % 3;
-      if (cc <= rr) H[rr * n + cc] += pk_get(hp, r, c);
-    }
-    for (int i = tid; i < 12; i += blockDim.x) g[dv[i / 3] + i % 3] += D.tet_g[12 * t + i];
-    __syncthreads();
+  // group key (local DoF offset of the owning soft vertex / affine body) of
+  // every DoF, then the record-parallel assembly of every stencil
+  int* dkey = reinterpret_cast<int*>(y + n + rec_stage_doubles());
+  for (int v = W.env_vert[e] + tid; v < W.env_vert[e + 1]; v += blockDim.x) {
+    int d = W.vert_dof[v] - d0;
+    for (int c = 0; c < 3; ++c) dkey[d + c] = d;
   }
-  // contact pairs
-  for (int kind = 0; kind < 2; ++kind) {
-    int nn = kind == 0 ? C.n_pt[e] : C.n_ee[e];
-    long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
-    const unsigned char* act = kind == 0 ? D.pt_act : D.ee_act;
-    const double* gg = kind == 0 ? D.pt_g : D.ee_g;
-    const double* hh = kind == 0 ? D.pt_h : D.ee_h;
-    // ordered compaction of the active candidates, one chunk at a time, so
-    // the serial assembly loop only visits stencils that contribute
-    __shared__ long long alist[DENSE_THREADS];
-    __shared__ int wtot[DENSE_THREADS / 32];
-    __shared__ int atot;
-    for (int k0 = 0; k0 < nn; k0 += DENSE_THREADS) {
-      int kk = k0 + tid;
-      bool on = kk < nn && act[off + kk];
-      {
-        int lane = tid & 31, wid = tid >> 5;
-        unsigned m = __ballot_sync(0xffffffffu, on);
-        if (lane == 0) wtot[wid] = __popc(m);
-        __syncthreads();
-        if (tid == 0) {
-          int acc = 0;
-          for (int w = 0; w < DENSE_THREADS / 32; ++w) {
-            int t = wtot[w];
-            wtot[w] = acc;
-            acc += t;
-          }
-          atot = acc;
-        }
-        __syncthreads();
-        if (on) alist[wtot[wid] + __popc(m & ((1u << lane) - 1u))] = off + kk;
-        __syncthreads();
-      }
-      int na = atot;
-    for (int ai = 0; ai < na; ++ai) {
-      long long q = alist[ai];
-      int2 pr = kind == 0 ? C.pt[q] : C.ee[q];
-      int sl[4];
-      if (kind == 0) {
-        int3 tv = W.tri_v[pr.y];
-        sl[0] = pr.x; sl[1] = tv.x; sl[2] = tv.y; sl[3] = tv.z;
-      } else {
-        int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
-        sl[0] = a.x; sl[1] = a.y; sl[2] = b.x; sl[3] = b.y;
-      }
-      const double* hp = hh + PK * q;
-      add_stencil(W, d0, n, H, g, 4, sl, gg + 12 * q, [&](int i, int j) { return pk_get(hp, i, j); });
-    }
-      __syncthreads();
-    }
+  for (int b = W.env_aff[e]; b < W.env_aff[e + 1]; ++b) {
+    int o = W.aff_dof[b] - d0;
+    for (int i = tid; i < 12; i += blockDim.x) dkey[o + i] = o;
   }
-  // ground barrier (y only)
-  for (int k = 0; k < C.n_gnd[e]; ++k) {
-    int q = C.gnd_off[e] + k;
-    double hy = D.gnd_hyy[q], gy = D.gnd_gy[q];
-    if (hy == 0.0 && gy == 0.0) continue;
-    int sl[1] = {C.gnd[q]};
-    double gs[3] = {0.0, gy, 0.0};
-    add_stencil(W, d0, n, H, g, 1, sl, gs, [&](int i, int j) { return (i == 1 && j == 1) ? hy : 0.0; });
-  }
-  // friction
-  for (int k = 0; k < L.n[e]; ++k) {
-    long long q = L.off[e] + k;
-    int4 s4 = L.slots[q];
-    int sl[4] = {s4.x, s4.y, s4.z, s4.w};
-    const double* hp = D.fr_h + PK * q;
-    add_stencil(W, d0, n, H, g, 4, sl, D.fr_g + 12 * q, [&](int i, int j) { return pk_get(hp, i, j); });
-  }
-  for (int k = 0; k < L.g_n[e]; ++k) {
-    int q = W.env_slot[e] + k;
-    int sl[1] = {L.g_slot[q]};
-    const double* hp = D.frg_h + 9 * q;
-    add_stencil(W, d0, n, H, g, 1, sl, D.frg_g + 3 * q, [&](int i, int j) { return hp[3 * i + j]; });
-  }
+  __syncthreads();
+  assemble_records(W, D, C, L, e, d0, n, H, g, dkey, y + n);
   // keep the gradient for the report / descent test
   double gmax = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
@@ -557,7 +622,7 @@ __device__ void dense_solve_block(const World& W, const EnvState& S, const Deriv
   if (tid == 0) S.pnorm[e] = pn;
 }
 
-__global__ void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState S, Derivs D, Cands C,
+IPC_GLOBAL void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState S, Derivs D, Cands C,
                                                                 Lags L, const double* __restrict__ x,
                                                                 const double* __restrict__ xhat,
                                                                 double* p_out, double* g_out) {
@@ -578,7 +643,7 @@ __device__ __forceinline__ void newton_begin_env(const EnvState& S, const int* f
     S.prev_pnorm[e] = INFINITY;
   }
 }
-__global__ void k_newton_begin(int n_env, EnvState S, const int* flag) {
+IPC_GLOBAL void k_newton_begin(int n_env, EnvState S, const int* flag) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n_env) newton_begin_env(S, flag, e);
 }
@@ -604,7 +669,7 @@ __device__ __forceinline__ void newton_check_env(const EnvState& S, double h, do
   S.ls_active[e] = 1;
   S.alpha_max[e] = 1.0;
 }
-__global__ void k_newton_check(int n_env, EnvState S, double h, double tol) {
+IPC_GLOBAL void k_newton_check(int n_env, EnvState S, double h, double tol) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n_env) newton_check_env(S, h, tol, e);
 }
@@ -621,7 +686,7 @@ __device__ __forceinline__ void ls_begin_env(const EnvState& S, int* ls_count, i
     S.newton_active[e] = 0;
   }
 }
-__global__ void k_ls_begin(int n_env, EnvState S, int* ls_count) {
+IPC_GLOBAL void k_ls_begin(int n_env, EnvState S, int* ls_count) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n_env) ls_begin_env(S, ls_count, e);
 }
@@ -647,7 +712,7 @@ __device__ __forceinline__ void ls_check_env(const EnvState& S, int* ls_count, i
     S.newton_active[e] = 0;
   }
 }
-__global__ void k_ls_check(World W, EnvState S, int* ls_count, int max_halvings, int* accepted) {
+IPC_GLOBAL void k_ls_check(World W, EnvState S, int* ls_count, int max_halvings, int* accepted) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < W.n_env) ls_check_env(S, ls_count, max_halvings, accepted, e);
 }
@@ -655,7 +720,7 @@ __global__ void k_ls_check(World W, EnvState S, int* ls_count, int max_halvings,
 // speculative backtracking: trials m = 0..M-1 evaluated E(x + α 2^-m p) into
 // e_multi[m * n_env + e]; take the first trial the sequential search would
 // have accepted (same floor / halving-count rules, ref solver.py:257-272)
-__global__ void k_ls_check_multi(World W, EnvState S, int* ls_count, int max_halvings, int M,
+IPC_GLOBAL void k_ls_check_multi(World W, EnvState S, int* ls_count, int max_halvings, int M,
                                  const double* e_multi, int* accepted) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= W.n_env) return;
@@ -690,7 +755,7 @@ __global__ void k_ls_check_multi(World W, EnvState S, int* ls_count, int max_hal
   }
 }
 
-__global__ void k_copy_env(World W, const double* src, double* dst, const int* flag) {
+IPC_GLOBAL void k_copy_env(World W, const double* src, double* dst, const int* flag) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= W.n_dof) return;
   if (flag[W.dof_env[i]]) dst[i] = src[i];
@@ -720,12 +785,12 @@ __device__ __forceinline__ void al_update_env(const World& W, const EnvState& S,
   bool has = W.env_cons[e + 1] > W.env_cons[e];
   if (!has || res <= 1e-6 || S.ls_failed[e]) S.al_active[e] = 0;
 }
-__global__ void k_al_update(World W, EnvState S, int outer) {
+IPC_GLOBAL void k_al_update(World W, EnvState S, int outer) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < W.n_env) al_update_env(W, S, outer, e);
 }
 
-__global__ void k_cons_reset(World W, const double* targets) {
+IPC_GLOBAL void k_cons_reset(World W, const double* targets) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= W.n_cons) return;
   for (int i = 0; i < 12; ++i) {
@@ -737,11 +802,11 @@ __global__ void k_cons_reset(World W, const double* targets) {
 }
 
 // x̂ = x + h v + h² a_g (ref bodies.py:292)
-__global__ void k_predictor(World W, double h) {
+IPC_GLOBAL void k_predictor(World W, double h) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < W.n_dof) W.xhat[i] = W.x[i] + h * W.v[i];
 }
-__global__ void k_predictor_forces(World W, double h) {
+IPC_GLOBAL void k_predictor_forces(World W, double h) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double hh = h * h;
   if (i < W.n_vert) {
@@ -755,7 +820,7 @@ __global__ void k_predictor_forces(World W, double h) {
   }
 }
 
-__global__ void k_finalize(World W, double h, const int* ok) {
+IPC_GLOBAL void k_finalize(World W, double h, const int* ok) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= W.n_dof) return;
   int e = W.dof_env[i];
@@ -773,24 +838,24 @@ __device__ __forceinline__ void kappa_adapt_env(const World& W, const EnvState& 
   double k = W.env_kappa[e], k0 = W.env_kappa0[e], dhat = W.env_dhat[e];
   if (md < 1e-4 * dhat && k < 1e8 * k0) W.env_kappa[e] = fmin(2.0 * k, 1e8 * k0);
 }
-__global__ void k_kappa_adapt(World W, EnvState S, const int* ok) {
+IPC_GLOBAL void k_kappa_adapt(World W, EnvState S, const int* ok) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < W.n_env && ok[e]) kappa_adapt_env(W, S, e);
 }
 
-__global__ void k_fill(int n, double* a, double v) {
+IPC_GLOBAL void k_fill(int n, double* a, double v) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
 }
-__global__ void k_fill_flag(int n, double* a, double v, const int* flag) {
+IPC_GLOBAL void k_fill_flag(int n, double* a, double v, const int* flag) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && flag[i]) a[i] = v;
 }
-__global__ void k_fill_int(int n, int* a, int v) {
+IPC_GLOBAL void k_fill_int(int n, int* a, int v) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
 }
-__global__ void k_count(int n, const int* flag, int* out) {
+IPC_GLOBAL void k_count(int n, const int* flag, int* out) {
   __shared__ int s;
   if (threadIdx.x == 0) s = 0;
   __syncthreads();
@@ -799,7 +864,7 @@ __global__ void k_count(int n, const int* flag, int* out) {
   __syncthreads();
   if (threadIdx.x == 0) *out = s;
 }
-__global__ void k_sweep_box(int n, const double* xw, const double* dxw, double* lo, double* hi) {
+IPC_GLOBAL void k_sweep_box(int n, const double* xw, const double* dxw, double* lo, double* hi) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 3 * n) return;
   double a = xw[i], b = __dadd_rn(xw[i], dxw[i]);

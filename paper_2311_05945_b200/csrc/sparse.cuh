@@ -73,7 +73,7 @@ struct AsmIn {  // everything an element needs
 // calls emit(row_node, col_node_or_GRAD, v[9]) for each block / gradient.
 // Modes: counting (emit counts) or writing.
 template <typename Emit>
-__device__ void visit_element(const AsmIn& A, long long q, Emit emit) {
+static __device__ void visit_element(const AsmIn& A, long long q, Emit emit) {
   const World& W = A.W;
   long long l;
   int t = elem_type(A.sp, q, &l);
@@ -204,7 +204,7 @@ __device__ void visit_element(const AsmIn& A, long long q, Emit emit) {
     }
 }
 
-__global__ void k_asm_count(AsmIn A, int* counts) {
+IPC_GLOBAL void k_asm_count(AsmIn A, int* counts) {
   long long n = A.sp.total();
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
     int c = 0;
@@ -213,7 +213,7 @@ __global__ void k_asm_count(AsmIn A, int* counts) {
   }
 }
 
-__global__ void k_asm_emit(AsmIn A, const long long* offs, unsigned long long* keys, double* vals, int* idx) {
+IPC_GLOBAL void k_asm_emit(AsmIn A, const long long* offs, unsigned long long* keys, double* vals, int* idx) {
   long long n = A.sp.total();
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
     long long o = offs[q];
@@ -227,20 +227,20 @@ __global__ void k_asm_emit(AsmIn A, const long long* offs, unsigned long long* k
 }
 
 // head flags of sorted keys (1 at the first item of every run)
-__global__ void k_asm_heads(long long n, const unsigned long long* keys, int* heads) {
+IPC_GLOBAL void k_asm_heads(long long n, const unsigned long long* keys, int* heads) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     heads[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
 }
 
 // run starts: seg_start[u] = first sorted position of unique key u
-__global__ void k_asm_starts(long long n, const int* heads, const long long* uidx, long long* seg_start) {
+IPC_GLOBAL void k_asm_starts(long long n, const int* heads, const long long* uidx, long long* seg_start) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     if (heads[i]) seg_start[uidx[i]] = i;
 }
 
 // sum each run in sorted (= emission) order; gradient runs go to g, blocks
 // to the BSR value array; also count blocks per row
-__global__ void k_asm_reduce(long long n_items, long long n_unique, const unsigned long long* keys,
+IPC_GLOBAL void k_asm_reduce(long long n_items, long long n_unique, const unsigned long long* keys,
                              const long long* seg_start, const int* perm, const double* vals, double* g,
                              unsigned* bcol, double* bval, int* row_cnt, int* bpos) {
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n_unique; u += (long long)gridDim.x * blockDim.x) {
@@ -269,7 +269,7 @@ __global__ void k_asm_reduce(long long n_items, long long n_unique, const unsign
 // BSR (row-sorted by construction of the keys): row_ptr over the block
 // entries; block entry j of row r is unique index row_first[r] + j (gradient
 // entries sit at the end of each row's run: col GRAD_COL sorts last)
-__global__ void k_bsr_rowfirst(long long n_unique, const unsigned long long* keys, const long long* seg_start,
+IPC_GLOBAL void k_bsr_rowfirst(long long n_unique, const unsigned long long* keys, const long long* seg_start,
                                int* row_first) {
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n_unique; u += (long long)gridDim.x * blockDim.x) {
     unsigned row = (unsigned)(keys[seg_start[u]] >> 32);
@@ -294,12 +294,68 @@ struct Pcg {
   double *part, *env_rz, *env_rz_new, *env_pap, *env_bb, *env_rr;
   int* env_live;  // per env: still iterating
   const int* env_on;  // newton_active
+  // affine bodies are preconditioned by the inverse of their whole 12x12
+  // diagonal block (the 4 nodes of a body never straddle a chunk):
+  // node_aff[node] = global affine body index or -1, aff_node0[b] = its first node
+  const int *node_aff, *aff_node0;
+  double* Minv12;  // 144 per affine body
+  int aff_blocks;  // 0: plain 3x3 node blocks everywhere
 };
+
+// z (3 values) of node nd = M⁻¹ r: the node's 3x3 block inverse, or its 3
+// rows of the owning affine body's 12x12 block inverse
+__device__ __forceinline__ void pcg_precond_node(const Pcg& P, int nd, double* z) {
+  int b = P.aff_blocks ? P.node_aff[nd] : -1;
+  if (b < 0) {
+    const double* M = P.Minv + 9 * (long long)nd;
+    const double* r = P.r + 3 * (long long)nd;
+    for (int k = 0; k < 3; ++k) z[k] = M[3 * k] * r[0] + M[3 * k + 1] * r[1] + M[3 * k + 2] * r[2];
+    return;
+  }
+  int n0 = P.aff_node0[b];
+  const double* M = P.Minv12 + 144 * (long long)b + 36 * (nd - n0);
+  const double* r = P.r + 3 * (long long)n0;
+  for (int k = 0; k < 3; ++k) {
+    double s = 0.0;
+    for (int j = 0; j < 12; ++j) s += M[12 * k + j] * r[j];
+    z[k] = s;
+  }
+}
+
+// in-place inverse of a 12x12 matrix (Gauss-Jordan, partial pivoting); false
+// when singular
+static __device__ bool inv12(double* A) {
+  int piv[12];
+  for (int c = 0; c < 12; ++c) {
+    int pr = c;
+    double best = fabs(A[12 * c + c]);
+    for (int r = c + 1; r < 12; ++r)
+      if (fabs(A[12 * r + c]) > best) { best = fabs(A[12 * r + c]); pr = r; }
+    if (!(best > 0.0)) return false;
+    piv[c] = pr;
+    if (pr != c)
+      for (int j = 0; j < 12; ++j) { double t = A[12 * c + j]; A[12 * c + j] = A[12 * pr + j]; A[12 * pr + j] = t; }
+    double d = 1.0 / A[12 * c + c];
+    A[12 * c + c] = 1.0;
+    for (int j = 0; j < 12; ++j) A[12 * c + j] *= d;
+    for (int r = 0; r < 12; ++r) {
+      if (r == c) continue;
+      double f = A[12 * r + c];
+      A[12 * r + c] = 0.0;
+      for (int j = 0; j < 12; ++j) A[12 * r + j] -= f * A[12 * c + j];
+    }
+  }
+  for (int c = 11; c >= 0; --c)
+    if (piv[c] != c)
+      for (int r = 0; r < 12; ++r) { double t = A[12 * r + c]; A[12 * r + c] = A[12 * r + piv[c]]; A[12 * r + piv[c]] = t; }
+  return true;
+}
 
 __device__ __forceinline__ bool row_live(const Pcg& P, int node) { return P.env_live[P.node_env[node]]; }
 
-// M⁻¹ = inverse of each node's diagonal 3x3 block
-__global__ void k_pcg_setup(Pcg P, const double* g) {
+// M⁻¹ = inverse of each node's diagonal 3x3 block, and of each affine body's
+// 12x12 diagonal block (aff_blocks); x = 0, r = b = -g, z = p = M⁻¹ r
+IPC_GLOBAL void k_pcg_setup(Pcg P, const double* g) {
   for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < P.n_node; nd += gridDim.x * blockDim.x) {
     int e = P.node_env[nd];
     if (!P.env_on[e]) continue;
@@ -313,21 +369,50 @@ __global__ void k_pcg_setup(Pcg P, const double* g) {
     M3 inv = m3_T(m3_inv_T(m, det));
     for (int i = 0; i < 9; ++i) P.Minv[9 * nd + i] = inv.m[i];
     for (int c = 0; c < 3; ++c) {
-      double b = -g[3 * nd + c];
       P.x[3 * nd + c] = 0.0;
-      P.r[3 * nd + c] = b;
+      P.r[3 * nd + c] = -g[3 * nd + c];
     }
+    int b = P.aff_blocks ? P.node_aff[nd] : -1;
+    if (b >= 0 && P.aff_node0[b] == nd) {  // the body's first node gathers its 12x12 block
+      double A[144];
+      for (int i = 0; i < 144; ++i) A[i] = 0.0;
+      for (int q = 0; q < 4; ++q) {
+        int fq = P.row_first[nd + q];
+        for (int j = 0; j < P.row_cnt[nd + q]; ++j) {
+          int cq = (int)P.bcol[fq + j] - nd;
+          if (cq < 0 || cq >= 4) continue;
+          const double* B = P.bval + 9 * (long long)(fq + j);
+          for (int u = 0; u < 3; ++u)
+            for (int v = 0; v < 3; ++v) A[12 * (3 * q + u) + 3 * cq + v] = B[3 * u + v];
+        }
+      }
+      bool ok = inv12(A);
+      double* M = P.Minv12 + 144 * (long long)b;
+      for (int i = 0; i < 144; ++i) M[i] = ok ? A[i] : 0.0;
+      if (!ok)  // singular block: fall back to the 3x3 node blocks on the diagonal
+        for (int q = 0; q < 4; ++q)
+          for (int u = 0; u < 3; ++u)
+            for (int v = 0; v < 3; ++v) M[12 * (3 * q + u) + 3 * q + v] = P.Minv[9 * (nd + q) + 3 * u + v];
+    }
+  }
+}
+
+// z = p = M⁻¹ r after k_pcg_setup (a separate pass: affine rows need the
+// whole body's r and Minv12)
+IPC_GLOBAL void k_pcg_setup_z(Pcg P) {
+  for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < P.n_node; nd += gridDim.x * blockDim.x) {
+    if (!P.env_on[P.node_env[nd]]) continue;
+    double z[3];
+    pcg_precond_node(P, nd, z);
     for (int c = 0; c < 3; ++c) {
-      double s = 0.0;
-      for (int k = 0; k < 3; ++k) s += inv.m[3 * c + k] * P.r[3 * nd + k];
-      P.z[3 * nd + c] = s;
-      P.p[3 * nd + c] = s;
+      P.z[3 * nd + c] = z[c];
+      P.p[3 * nd + c] = z[c];
     }
   }
 }
 
 // chunk partial dots: which 0 -> (r·z, b·b) ; 1 -> p·Ap ; 2 -> (r·z, r·r)
-__global__ void k_pcg_partial(Pcg P, int which) {
+IPC_GLOBAL void k_pcg_partial(Pcg P, int which) {
   __shared__ double sh[2][8];
   int c = blockIdx.x;
   if (c >= P.n_chunk) return;
@@ -365,7 +450,7 @@ __global__ void k_pcg_partial(Pcg P, int which) {
 }
 
 // per-env scalar step. stage 0: init rz, bb; 1: pAp; 2: new rz / rr, β, convergence
-__global__ void k_pcg_env(Pcg P, int n_env, int stage, double rtol2) {
+IPC_GLOBAL void k_pcg_env(Pcg P, int n_env, int stage, double rtol2) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_env || !P.env_on[e]) return;
   if (stage != 0 && !P.env_live[e]) return;
@@ -387,60 +472,9 @@ __global__ void k_pcg_env(Pcg P, int n_env, int stage, double rtol2) {
   }
 }
 
-// SpMV Ap = H p over rows of live envs (one thread per node row)
-__global__ void k_pcg_spmv(Pcg P) {
-  for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < P.n_node; nd += gridDim.x * blockDim.x) {
-    int e = P.node_env[nd];
-    if (!P.env_on[e] || !P.env_live[e]) continue;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    int f = P.row_first[nd];
-    for (int j = 0; j < P.row_cnt[nd]; ++j) {
-      const double* B = P.bval + 9 * (long long)(f + j);
-      const double* pv = P.p + 3 * (long long)P.bcol[f + j];
-      s0 += B[0] * pv[0] + B[1] * pv[1] + B[2] * pv[2];
-      s1 += B[3] * pv[0] + B[4] * pv[1] + B[5] * pv[2];
-      s2 += B[6] * pv[0] + B[7] * pv[1] + B[8] * pv[2];
-    }
-    P.Ap[3 * nd] = s0;
-    P.Ap[3 * nd + 1] = s1;
-    P.Ap[3 * nd + 2] = s2;
-  }
-}
-
-// x += α p, r -= α Ap, z = M⁻¹ r
-__global__ void k_pcg_update(Pcg P) {
-  for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < P.n_node; nd += gridDim.x * blockDim.x) {
-    int e = P.node_env[nd];
-    if (!P.env_on[e] || !P.env_live[e]) continue;
-    double al = P.env_rz[e] / P.env_pap[e];
-    for (int k = 0; k < 3; ++k) {
-      int i = 3 * nd + k;
-      P.x[i] += al * P.p[i];
-      P.r[i] -= al * P.Ap[i];
-    }
-    const double* M = P.Minv + 9 * nd;
-    for (int c = 0; c < 3; ++c)
-      P.z[3 * nd + c] = M[3 * c] * P.r[3 * nd] + M[3 * c + 1] * P.r[3 * nd + 1] + M[3 * c + 2] * P.r[3 * nd + 2];
-  }
-}
-
-// p = z + β p ; rz <- rz_new
-__global__ void k_pcg_dir(Pcg P) {
-  for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < P.n_node; nd += gridDim.x * blockDim.x) {
-    int e = P.node_env[nd];
-    if (!P.env_on[e] || !P.env_live[e]) continue;
-    double be = P.env_rz_new[e] / P.env_rz[e];
-    for (int k = 0; k < 3; ++k) P.p[3 * nd + k] = P.z[3 * nd + k] + be * P.p[3 * nd + k];
-  }
-}
-__global__ void k_pcg_roll(Pcg P, int n_env) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n_env && P.env_on[e] && P.env_live[e]) P.env_rz[e] = P.env_rz_new[e];
-}
-
 // direction, fallback and norms per env (ref solver.py:241): p = x unless the
 // solve produced non-finite values or an ascent direction, then p = -g
-__global__ void k_pcg_finish(World W, EnvState S, Pcg P, const double* g, double* p_out, double* g_out) {
+IPC_GLOBAL void k_pcg_finish(World W, EnvState S, Pcg P, const double* g, double* p_out, double* g_out) {
   __shared__ double sh[3][8];
   int e = blockIdx.x;
   if (!S.newton_active[e]) return;
@@ -597,7 +631,7 @@ __device__ __forceinline__ void block_env_sums(const Pcg& P, int e, const double
 // liveness, α and β from the same partials, so no per-env scalar pass is
 // needed. cnt[0..1]: live-env counters (alternating), cnt[2]: cumulative
 // iteration count (stats).
-__global__ void k_pcg_coop(Pcg P, int n_env, double rtol2, int max_iters, int* cnt, double* part1, double* part2) {
+IPC_GLOBAL void k_pcg_coop(Pcg P, int n_env, double rtol2, int max_iters, int* cnt, double* part1, double* part2) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[64];
   __shared__ double es[6];  // env sums: cur (rz, rr), part1 (pAp, -), nxt (rz, rr)
@@ -665,11 +699,14 @@ __global__ void k_pcg_coop(Pcg P, int n_env, double rtol2, int max_iters, int* c
           P.x[i] += al * P.p[i];
           P.r[i] -= al * P.Ap[i];
         }
-        const double* M = P.Minv + 9 * nd;
+      }
+      if (P.aff_blocks) __syncthreads();  // affine rows read the whole body's r
+      for (int nd = P.chunk_n0[c] + threadIdx.x; nd < P.chunk_n1[c]; nd += blockDim.x) {
+        double z[3];
+        pcg_precond_node(P, nd, z);
         for (int k = 0; k < 3; ++k) {
-          double z = M[3 * k] * P.r[3 * nd] + M[3 * k + 1] * P.r[3 * nd + 1] + M[3 * k + 2] * P.r[3 * nd + 2];
-          P.z[3 * nd + k] = z;
-          a += P.r[3 * nd + k] * z;
+          P.z[3 * nd + k] = z[k];
+          a += P.r[3 * nd + k] * z[k];
           b += P.r[3 * nd + k] * P.r[3 * nd + k];
         }
       }

@@ -15,6 +15,16 @@
 //   constraints          kinematic AL targets (ref constraints.py:36)
 //   candidates           per-env capacity ranges; pairs stored lexicographically
 #pragma once
+
+// The engine is built from two translation units compiled in parallel:
+// engine.cu (host engine + batched kernels) and fused.cu (the per-env fused
+// step kernels). Batched kernels are declared IPC_GLOBAL; in the fused unit
+// they become uninstantiated templates, so each kernel is compiled once.
+#ifdef IPC_FUSED_TU
+#define IPC_GLOBAL template <int = 0> __global__
+#else
+#define IPC_GLOBAL __global__
+#endif
 #include <stdint.h>
 
 namespace ipc {

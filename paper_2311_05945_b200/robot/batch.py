@@ -1,8 +1,8 @@
 """Batched grasp evaluation: E independent gripper+object environments stepped
 together on one GPU (parallel grasp generation, paper §V.A; the reference
-runs one trial per worker process: pkg/src/srsim/batch.py:436).
+runs one trial per worker process: pkg/src/srsim/batch.py:39).
 
-Each environment runs the reference's per-trial program (robot/grasp.py:337
+Each environment runs the reference's per-trial program (robot/grasp.py:224
 autograsp, :372 lift_and_shake) — same control law, phase schedule and
 success test — but all environments advance in lock-step. One control
 tick: score / sense / decide for every env with one device call each,
@@ -27,7 +27,7 @@ PHASE_NAMES = ("AutoGrasp", "LiftCheck", "Lift", "Shake", "Settle", "Score", "Do
 
 
 def phi_vec(f, k=20.0, f_star=0.5):
-    """Vectorized Eq. 12 (ref grasp.py:270)."""
+    """Vectorized Eq. 12 (ref grasp.py:69)."""
     f = np.asarray(f, dtype=np.float64)
     if np.any(f < 0):
         raise ValueError("contact force magnitude cannot be negative")
@@ -137,7 +137,7 @@ class BatchGrasp:
     def tick(self) -> bool:
         gc = self.gc
         ph = self.phase
-        # 1. score envs whose settle schedule ended (ref grasp.py:418-420)
+        # 1. score envs whose settle schedule ended (ref grasp.py:213-219)
         sc = ph == SCORE
         if sc.any():
             held = self.world.group_distance(self.hand_mask, self.obj_mask) < self.dhat
@@ -145,7 +145,7 @@ class BatchGrasp:
             ok = sc & held & clear
             self._finish(ok, GraspOutcome.SUCCESS)
             self._finish(sc & ~ok, GraspOutcome.DROPPED)
-        # 2. AutoGrasp: read forces, stop, abort, or close (ref grasp.py:352-368)
+        # 2. AutoGrasp: read forces, stop, abort, or close (ref grasp.py:151-166)
         auto = ph == AUTO
         stepping = np.zeros(self.E, dtype=bool)
         if auto.any():
@@ -169,7 +169,7 @@ class BatchGrasp:
                     self.increments[e].append(inc[e].copy())
                 self.frames[close] += 1
                 stepping |= close
-        # 3. held-before-lift test (ref grasp.py:390)
+        # 3. held-before-lift test (ref grasp.py:184-190)
         lc = ph == LIFT_CHECK
         if lc.any():
             d = self.world.group_distance(self.hand_mask, self.obj_mask)
@@ -179,7 +179,7 @@ class BatchGrasp:
             ph[go] = LIFT
             self.k[go] = 0
             self.base[go] = self.pose[go]
-        # 4. kinematic schedules (ref grasp.py:395-416)
+        # 4. kinematic schedules (ref grasp.py:195-215)
         nxt = ph.copy()
         for e in np.nonzero(ph == LIFT)[0]:
             self.k[e] += 1

@@ -65,7 +65,7 @@ def _prefix(sizes):
 
 
 def max_penetration_batch(points, meshes) -> np.ndarray:
-    """ref proximity.py:254 for E (points, object mesh) problems at once.
+    """ref proximity.py:235 for E (points, object mesh) problems at once.
 
     points: list of (n_e, 3) arrays; meshes: list of (verts, tris)."""
     lib = N.load()
@@ -87,7 +87,7 @@ def max_penetration_batch(points, meshes) -> np.ndarray:
 
 def max_penetration(hand_points, object_mesh: SurfaceMesh) -> float:
     """Deepest intrusion (m) of the points into a watertight mesh, 0 when no
-    point is contained (ref proximity.py:254)."""
+    point is contained (ref proximity.py:235)."""
     if len(hand_points) == 0:
         return 0.0
     return float(max_penetration_batch([hand_points],

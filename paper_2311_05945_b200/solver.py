@@ -27,7 +27,7 @@ PHASES = ("DCD", "Energy", "Hess", "Linear", "CCD", "Others")
 
 
 class IntersectionError(RuntimeError):
-    """The incoming state already touches or penetrates (ref ccd.py:382)."""
+    """The incoming state already touches or penetrates (ref ccd.py:21)."""
 
 
 @dataclass
@@ -51,10 +51,27 @@ class SolverConfig:
             raise ValueError("ccd_conservative_factor must lie in (0, 1)")
 
 
+# device work -> reference phase (ref solver.py:52 PHASES, timed at :303-352):
+# per-kernel CUDA-event times of the batched launch sequence, and the
+# per-phase SM cycles of the fused per-env kernels that finish each Newton loop
+KERNEL_PHASE = {"broad_dcd": "DCD", "broad_ccd": "CCD", "ccd": "CCD", "pairs_deriv": "Energy",
+                "pairs_value": "Energy", "tet": "Energy", "body": "Energy", "ground": "Energy",
+                "friction": "Energy", "energy_reduce": "Energy", "lags": "Energy", "world_pos": "Energy",
+                "assembly": "Hess", "dense_solve": "Linear", "pcg": "Linear"}
+FUSED_PHASE = {"world": "Energy", "broad_dcd": "DCD", "terms": "Energy", "energy": "Energy",
+               "dense": "Linear", "ccd_prep": "CCD", "broad_ccd": "CCD", "ccd": "CCD",
+               "line_search": "Energy"}
+
+
 @dataclass
 class StepReport:
-    """ref solver.py:75. Phase times are not split on the GPU: the whole step
-    is reported under "Others" (wall time of the device step)."""
+    """ref solver.py:75. ``times`` splits the step's device time into the
+    reference's phases (DCD / Energy / Hess / Linear / CCD) from the
+    per-kernel CUDA events and the fused kernels' phase timers; ``Others`` is
+    the remainder of the step's wall time, as ref solver.py:88 closes it.
+    The dense per-env solve assembles and factors in one kernel, so its
+    assembly is booked under Linear (the sparse path books BSR assembly
+    under Hess)."""
 
     newton_iters: int = 0
     final_grad_norm: float = 0.0
@@ -75,14 +92,44 @@ class StepReport:
                 "times": dict(self.times), "total_time": self.total_time}
 
     @classmethod
-    def from_c(cls, r, t):
+    def from_c(cls, r, t, phases=None):
         rep = cls(newton_iters=r.newton_iters, final_grad_norm=r.final_grad_norm,
                   min_dist_before=r.min_dist_before, min_dist_after=r.min_dist_after,
                   ccd_invocations=r.ccd_invocations, converged=bool(r.converged),
                   line_search_failed=bool(r.line_search_failed), al_outer=r.al_outer)
         rep.total_time = t
-        rep.times["Others"] = t
+        for k, v in (phases or {}).items():
+            rep.times[k] += v
+        accounted = sum(v for k, v in rep.times.items() if k != "Others")
+        rep.times["Others"] = max(t - accounted, 0.0)
         return rep
+
+
+class _PhaseClock:
+    """Per-step phase seconds of one device world (differences of the
+    cumulative kernel-event and fused-timer counters)."""
+
+    def __init__(self, w: GpuWorld):
+        self.w = w
+        w.profile(True)
+        w.set_fused_timers(True)
+        self.hz = 1e3 * w.clock_khz()
+        self.prev = self._read()
+
+    def _read(self):
+        prof, _ = self.w.profile_read()
+        return {k: v[0] for k, v in prof.items()}, self.w.fused_timers()
+
+    def split(self) -> dict:
+        (ms0, ft0), (ms1, ft1) = self.prev, self._read()
+        self.prev = (ms1, ft1)
+        out = {k: 0.0 for k in PHASES}
+        for k, ph in KERNEL_PHASE.items():
+            out[ph] += 1e-3 * (ms1.get(k, 0.0) - ms0.get(k, 0.0))
+        for k, ph in FUSED_PHASE.items():
+            out[ph] += (ft1.get(k, 0) - ft0.get(k, 0)) / self.hz
+        out.pop("Others")
+        return out
 
 
 _ENGINES: dict = {}  # id(scene) -> GpuWorld, dropped when the scene is collected
@@ -99,6 +146,8 @@ def engine_of(scene) -> GpuWorld:
     w = _ENGINES.get(key)
     if w is None:
         w = GpuWorld([scene])
+        if hasattr(w, "profile"):
+            w.phase_clock = _PhaseClock(w)
         _ENGINES[key] = w
         weakref.finalize(scene, _ENGINES.pop, key, None)
     return w
@@ -160,7 +209,8 @@ def step(scene, config: SolverConfig):
     if r.error:
         raise IntersectionError("step started from an intersecting state")
     _sync_from_device(scene, w, config.h)
-    return scene.state, StepReport.from_c(r, time.perf_counter() - t0)
+    phases = w.phase_clock.split() if hasattr(w, "phase_clock") else None
+    return scene.state, StepReport.from_c(r, time.perf_counter() - t0, phases)
 
 
 def simulate(scene, config: SolverConfig, n_steps: int, callback=None):

@@ -332,11 +332,20 @@ class GpuWorld:
         per-env tail hand-off (False, default)."""
         N.check(self.lib.ipc_world_set_fused(self.handle, 1 if on else 0))
 
+    def set_fused_timers(self, on: bool):
+        """Per-phase SM-cycle timers of the fused per-env kernels (fused_timers)."""
+        N.check(self.lib.ipc_world_set_fused_timers(self.handle, 1 if on else 0))
+
+    def clock_khz(self) -> int:
+        out = np.zeros(1, np.int32)
+        N.check(self.lib.ipc_device_clock_khz(N.ptr(out, N._i32p)))
+        return int(out[0])
+
     FUSED_PHASES = ("world", "broad_dcd", "terms", "energy", "dense", "ccd_prep", "broad_ccd", "ccd",
                     "line_search", "other")
 
     def fused_timers(self):
-        """SM cycles per phase of the fused step (zeros unless built with -DIPC_FUSED_TIMERS)."""
+        """SM cycles per phase of the fused step (zeros unless the timers are on)."""
         out = np.zeros(len(self.FUSED_PHASES), np.int64)
         N.check(self.lib.ipc_world_fused_timers(self.handle, N.ptr(out, N._i64p), len(out)))
         return dict(zip(self.FUSED_PHASES, (int(v) for v in out)))

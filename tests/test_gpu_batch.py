@@ -111,3 +111,62 @@ def test_run_scheduled_matches_per_step_fused():
             wh.step_scheduled(cfg, k)
         xh, _ = wh.get_state()
         assert np.abs(xa - xh).max() <= 1e-9 * np.abs(xh).max()
+
+
+def _pinch_job(q_close):
+    """One job of batch_run: 6 steps of the rigid pinch closing to q_close;
+    returns (Newton counts, final DoFs)."""
+    from paper_2311_05945_b200 import data_path
+    from paper_2311_05945_b200.bodies import AffineBody
+    from paper_2311_05945_b200.mesh import box_surface
+    from paper_2311_05945_b200.robot import Gripper, build_grasp_scene, parse_urdf, top_down_pose
+    from paper_2311_05945_b200.solver import SolverConfig, step
+
+    g = Gripper(parse_urdf(data_path("pj_gripper.urdf")))
+    obj = AffineBody(box_surface(0.05, center=(0.0, 0.02515, 0.0)), density=500.0)
+    sc = build_grasp_scene(obj, g, top_down_pose((0.0, 0.02515, 0.0)), [0.015, 0.015], mu=0.5)
+    its = []
+    for _ in range(6):
+        g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, q_close))
+        its.append(step(sc, SolverConfig())[1].newton_iters)
+    return its, sc.state.gather()
+
+
+def test_batch_run_gpu_workers_ordered_and_equal_to_serial():
+    """ref batch.py:39 on GPUs: 2 spawned workers (each on a device) return
+    the jobs' results in job order, identical to running them in-process."""
+    from paper_2311_05945_b200.batch import batch_run
+
+    jobs = [0.02, 0.022, 0.0262]
+    par = batch_run(_pinch_job, jobs, workers=2)
+    ser = batch_run(_pinch_job, jobs, workers=1)
+    assert [r.job_id for r in par] == [0, 1, 2] and all(r.ok for r in par)
+    for a, b in zip(par, ser):
+        assert a.value[0] == b.value[0]
+        assert np.array_equal(a.value[1], b.value[1])
+
+
+def test_step_report_phase_times():
+    """StepReport.times splits the device step into the reference's phases
+    (ref solver.py:52, batch.py:66): contact steps spend time in DCD, Energy,
+    Linear and CCD, and the phases cover the wall time."""
+    from paper_2311_05945_b200 import data_path
+    from paper_2311_05945_b200.batch import profile_phases
+    from paper_2311_05945_b200.bodies import AffineBody
+    from paper_2311_05945_b200.mesh import box_surface
+    from paper_2311_05945_b200.robot import Gripper, build_grasp_scene, parse_urdf, top_down_pose
+    from paper_2311_05945_b200.solver import SolverConfig, step
+
+    g = Gripper(parse_urdf(data_path("pj_gripper.urdf")))
+    obj = AffineBody(box_surface(0.05, center=(0.0, 0.02515, 0.0)), density=500.0)
+    sc = build_grasp_scene(obj, g, top_down_pose((0.0, 0.02515, 0.0)), [0.018, 0.018], mu=0.5)
+    reps = []
+    for _ in range(5):
+        g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, 0.0262))
+        reps.append(step(sc, SolverConfig())[1])
+    prof = profile_phases(reps)
+    for k in ("DCD", "Energy", "Linear", "CCD"):
+        assert prof[k] > 0.0, k
+    for r in reps:
+        assert sum(r.times.values()) >= r.total_time * (1 - 1e-9)
+        assert all(v >= 0.0 for v in r.times.values())

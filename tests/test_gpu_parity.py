@@ -238,5 +238,6 @@ def test_config2_soft_grasp_10k_tets_matches_reference(golden):
         assert rep.al_outer == z["al_outer"][k], k
         assert np.abs(x - z["x"][k]).max() <= REL * np.abs(z["x"][k]).max(), k
         assert rep.min_dist_after > 0.0
-        assert rep.min_dist_after == pytest.approx(float(z["min_dist"][k]), rel=1e-6), k
+        # a distance: agrees to the DoF tolerance (absolute, scaled by max |x|)
+        assert abs(rep.min_dist_after - z["min_dist"][k]) <= REL * np.abs(z["x"][k]).max(), k
     assert sc.barrier.kappa == float(z["kappa"])

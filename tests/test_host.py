@@ -259,3 +259,38 @@ def test_bench_gpus_flag_spawns_ranks():
     assert len(lines) == 1
     assert lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
     assert lines[0]["scaling"] == "strong" and lines[0]["config"]["envs"] == 4
+
+
+def _neg_or_fail(x):
+    if x == 3:
+        raise ValueError("bad job")
+    return -x
+
+
+def test_batch_run_ordered_results_and_failed_slot():
+    """ref batch.py:39 contract: ordered results, a raising job marks its slot."""
+    from paper_2311_05945_b200.batch import batch_run
+
+    res = batch_run(_neg_or_fail, [1, 2, 3, 4])
+    assert [r.job_id for r in res] == [0, 1, 2, 3]
+    assert [r.ok for r in res] == [True, True, False, True]
+    assert res[1].value == -2 and "ValueError: bad job" in res[2].error
+    assert batch_run(_neg_or_fail, []) == []
+
+
+def test_profile_phases_and_format():
+    """ref batch.py:66/:86: phase seconds summed over step reports."""
+    from paper_2311_05945_b200.batch import format_profile, profile_phases
+    from paper_2311_05945_b200.solver import PHASES, StepReport
+
+    class R:  # the fields a device StepReportC carries
+        newton_iters, final_grad_norm, min_dist_before, min_dist_after = 3, 0.0, 1.0, 1.0
+        ccd_invocations, converged, line_search_failed, al_outer = 2, 1, 0, 1
+
+    a = StepReport.from_c(R(), 1.0, {"DCD": 0.1, "Energy": 0.2, "Linear": 0.3})
+    b = StepReport.from_c(R(), 0.5, {"DCD": 0.1, "CCD": 0.6})  # accounted > total: Others clamps at 0
+    assert a.times["Others"] == pytest.approx(0.4) and b.times["Others"] == 0.0
+    prof = profile_phases([a, b.as_dict()])
+    assert prof["Total"] == 1.5 and prof["DCD"] == pytest.approx(0.2)
+    table = format_profile(prof)
+    assert all(k in table for k in (*PHASES, "Total"))
