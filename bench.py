@@ -136,7 +136,7 @@ def _cpu_env_task(args):
     lay = OS.Layout(sc)
     cfg = OS.Config()
     nl = len(grippers[0].links)
-    t_timed, xs, its = 0.0, [], []
+    t_timed, xs, its, pl = 0.0, [], [], []
     for k in range(warmup + steps):
         tgt = sched_row[k].reshape(nl, 12)
         t0 = time.perf_counter()
@@ -147,7 +147,8 @@ def _cpu_env_task(args):
             t_timed += time.perf_counter() - t0
         xs.append(sc.state.gather())
         its.append(r.newton_iters)
-    return steps, t_timed, np.array(xs), np.array(its)
+        pl.append(r.pnorms[-1] / cfg.h if r.pnorms else 0.0)
+    return steps, t_timed, np.array(xs), np.array(its), np.array(pl)
 
 
 def cpu_arm(n_total, sample, seed, warmup, steps, cores):
@@ -171,8 +172,81 @@ def cpu_arm(n_total, sample, seed, warmup, steps, cores):
     wall = time.perf_counter() - t0
     env_steps = sum(r[0] for r in res)
     t = sum(r[1] for r in res) / n_workers
-    traj = {"x": [r[2] for r in res], "newton": [r[3] for r in res]}
+    traj = {"x": [r[2] for r in res], "newton": [r[3] for r in res], "last_p": [r[4] for r in res]}
     return env_steps / t, t, int(sum(r[3][warmup:].sum() for r in res)), n_workers, traj, wall
+
+
+def _closed_loop_inputs(n_total, seed, select=None):
+    """Objects, initial poses and joint values of the config-3 batch (the
+    same synthetic envs the step benchmark uses), for full grasp trials."""
+    from paper_2311_05945_b200 import workloads as WL
+
+    scenes, grippers, half, poses = WL.grasp_batch(n_total, seed=seed, select=select)
+    objs = [sc.state.affine_bodies[0] for sc in scenes]
+    joints = np.array([g.joint_values for g in grippers])
+    return objs, np.array(poses), joints
+
+
+def _cpu_trial_task(args):
+    """One env's full grasp trial through the oracle (ref robot/grasp.py:224
+    run_grasp_trial: AutoGrasp under force feedback, lift, shake, score)."""
+    n_total, env, seed = args
+    sys.path.insert(0, ROOT)
+    from oracle.robot import OracleBackend
+    from paper_2311_05945_b200.robot import (Gripper, GraspTrial, autograsp, build_grasp_scene,
+                                             lift_and_shake)
+    from paper_2311_05945_b200 import workloads as WL
+
+    objs, poses, joints = _closed_loop_inputs(n_total, seed, select=[env])
+    g = Gripper(WL.gripper_model())
+    sc = build_grasp_scene(objs[0], g, poses[0], joints[0], mu=0.5)
+    tr = GraspTrial(poses[0], joints[0].copy())
+    be = OracleBackend()
+    t0 = time.perf_counter()
+    autograsp(sc, g, tr, backend=be)
+    lift_and_shake(sc, g, objs[0], tr, backend=be)
+    return env, tr.outcome, int(tr.steps), time.perf_counter() - t0
+
+
+def closed_loop_arm(n_total, seed, sample, cores, lr):
+    """Parallel grasp generation as the reference runs it (ref batch.py:39 jobs
+    of robot/grasp.py:224 run_grasp_trial): every env's full closed-loop
+    trial — AutoGrasp with per-frame force sensing and the φ control law,
+    lift, shake, settle, score — through the public BatchGrasp API (one
+    device world, one step + sensing calls per control tick). Envs 0..S-1
+    are replayed by the oracle and must give the same outcome flags and
+    step counts."""
+    from paper_2311_05945_b200 import workloads as WL
+    from paper_2311_05945_b200.robot.batch import BatchGrasp
+
+    objs, poses, joints = _closed_loop_inputs(n_total, seed)
+    t0 = time.perf_counter()
+    bg = BatchGrasp(WL.gripper_model(), objs, poses, joints, mu=0.5)
+    t1 = time.perf_counter()
+    out = bg.run()
+    t2 = time.perf_counter()
+    steps = int(bg.steps.sum())
+    counts = {}
+    for o in out:
+        counts[str(o)] = counts.get(str(o), 0) + 1
+    res = {"envs": n_total, "env_steps": steps, "seconds": t2 - t1, "build_seconds": t1 - t0,
+           "env_steps_per_s": steps / (t2 - t1), "trials_per_s": n_total / (t2 - t1),
+           "outcomes": counts,
+           "note": "full closed-loop trials (force-feedback AutoGrasp, lift, shake, score) through "
+                   "robot.batch.BatchGrasp; wall clock incl. sensing and host control per tick"}
+    if sample:
+        import multiprocessing as mp
+
+        with mp.get_context("spawn").Pool(min(cores, sample)) as pool:
+            cpu = pool.map(_cpu_trial_task, [(n_total, e, seed) for e in range(sample)], chunksize=1)
+        match = [(str(o) == str(out[e])) and (s == int(bg.steps[e])) for e, o, s, _ in cpu]
+        cpu_s = sum(r[3] for r in cpu)
+        cpu_steps = sum(r[2] for r in cpu)
+        res.update({"outcomes_match": bool(all(match)), "sampled_envs": sample,
+                    "mismatched_envs": [int(cpu[i][0]) for i, m in enumerate(match) if not m],
+                    "cpu_env_steps_per_s": cpu_steps / cpu_s * min(cores, sample),
+                    "cpu_cores": min(cores, sample)})
+    return res
 
 
 def parity_block(traj, xs_gpu, its_gpu, dof_pre, free_flags):
@@ -180,7 +254,7 @@ def parity_block(traj, xs_gpu, its_gpu, dof_pre, free_flags):
     same envs and steps: worst per-step DoF error relative to the step's
     largest |DoF|, Newton-count mismatches over (env, step), and whether every
     env of the batch ended every step intersection-free."""
-    max_rel, mism, n, where, lst = 0.0, 0, 0, None, []
+    max_rel, mism, n, where, lst, noise = 0.0, 0, 0, None, [], 0
     for e, (xc, ic) in enumerate(zip(traj["x"], traj["newton"])):
         lo, hi = int(dof_pre[e]), int(dof_pre[e + 1])
         for k in range(len(xc)):
@@ -190,12 +264,17 @@ def parity_block(traj, xs_gpu, its_gpu, dof_pre, free_flags):
                 max_rel, where = rel, [e, k]
             if its_gpu[k][e] != ic[k]:
                 mism += 1
+                lp = float(traj["last_p"][e][k])
+                # the stop rule compares ‖p‖ with the previous ‖p‖ (ref solver.py:326-332);
+                # below 1e-6·tol both are rounding noise and the comparison is a coin flip
+                noise += int(lp <= 1e-6 * 1e-2)
                 if len(lst) < 12:
-                    lst.append([e, k, int(its_gpu[k][e]), int(ic[k])])
+                    lst.append([e, k, int(its_gpu[k][e]), int(ic[k]), lp])
             n += 1
     return {"envs": len(traj["x"]), "steps": len(traj["x"][0]) if traj["x"] else 0,
             "max_rel_dof": max_rel, "max_rel_at_env_step": where, "newton_mismatches": mism,
-            "mismatch_list_env_step_gpu_cpu": lst, "compared_env_steps": n,
+            "newton_mismatches_at_noise_level_p": noise,
+            "mismatch_list_env_step_gpu_cpu_cpu_last_p_over_h": lst, "compared_env_steps": n,
             "tolerance_rel_dof": 1e-6,
             "all_envs_intersection_free_every_step": bool(free_flags["all"]),
             "intersecting_env_steps": int(free_flags["bad"]),
@@ -286,6 +365,9 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=64, help="envs in the CPU sample")
     ap.add_argument("--cpu-steps", type=int, default=0, help="timed CPU steps (0 = the GPU's K)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-closed-loop", action="store_true", help="skip the closed-loop grasp-trial arm")
+    ap.add_argument("--closed-loop-sample", type=int, default=16,
+                    help="envs of the closed-loop arm replayed by the oracle")
     ap.add_argument("--window-only", action="store_true",
                     help="stop after the timed window (the ncu capture command of tools/ncu_window.py)")
     ap.add_argument("--workload", choices=("grasp", "repair"), default="grasp",
@@ -477,6 +559,9 @@ def main():
             "intersection_free": {"all_env_steps": bool(free["all"]), "bad": free["bad"],
                                   "checked": free["n"]},
             "results": results, "async": async_line}
+    if rank == 0 and ws == 1 and not args.no_closed_loop:
+        line["closed_loop"] = closed_loop_arm(args.envs, args.seed,
+                                              0 if args.no_cpu else args.closed_loop_sample, _cores(), lr)
     if S:
         ksteps = args.cpu_steps or K
         v, t, _, used, traj, wall = cpu_arm(args.envs, S, args.seed, W, ksteps, _cores())

@@ -49,6 +49,7 @@ class Report:
     al_outer: int = 0
     total_time: float = 0.0
     alphas: list = field(default_factory=list)
+    pnorms: list = field(default_factory=list)  # ‖p‖∞ of every Newton direction
 
 
 class Layout:
@@ -176,6 +177,7 @@ def newton_solve(scene, lay, x0, xhat, xw0, lags, cfg, rep):
         p = newton_direction(g, hmat)
         rep.newton_iters += 1
         pn = float(np.abs(p).max()) if len(p) else 0.0
+        rep.pnorms.append(pn)
         small = (pn / h <= cfg.newton_tol) if len(p) else True
         if small and small_run >= 1 and (pn <= prev or small_run >= 7):
             return x, gnorm

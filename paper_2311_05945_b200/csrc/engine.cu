@@ -357,6 +357,9 @@ struct ipc_world {
   std::vector<int> h_env_slot, h_env_dof, h_env_tri, h_env_edge, h_env_cbody;
   int max_env_dof = 0;
   CandStore dcd, sweep;
+  CandStore ss;  // cached candidate superset of the fused per-env kernels (fused.cuh env_candidates)
+  double *bb_lo = nullptr, *bb_hi = nullptr;
+  double ss_pad = 2.0;  // IPC_SS_PAD: superset build-box padding in units of d̂ (0: off)
   PairBufs pb_dcd, pb_sweep;
   Lags L{};
   long long* d_lag_off = nullptr;
@@ -520,6 +523,8 @@ struct ipc_world {
       return;
     }
     IPC_LAUNCH(kid, st, k_chunk_boxes, nblk(W.n_tchunk + W.n_echunk, 128), 128, 0, W, lo, hi);
+    if (W.n_tree)
+      IPC_LAUNCH(kid, st, k_lbvh_build, W.n_tree, LBVH_THREADS, 4 * LBVH_MAX * sizeof(unsigned), W, lo, hi);
     if (bp_z == 1) {
       IPC_LAUNCH(kid, st, k_broad, dim3(n_env, 3), BP_THREADS, 0, W, lo, hi, cs.c, -1, env_mask, -1, nullptr);
     } else {
@@ -710,7 +715,7 @@ struct ipc_world {
 
   void grow_overflowed() {
     CK(cudaStreamSynchronize(st));
-    for (CandStore* cs : {&dcd, &sweep}) {
+    for (CandStore* cs : {&dcd, &sweep, &ss}) {
       // the broad phase records each env's unclipped candidate count: grow
       // straight to 1.5x that (at least 4x), so one replay suffices
       std::vector<int> np(n_env), ne(n_env);
@@ -732,7 +737,7 @@ struct ipc_world {
       }
       if (!grew) continue;
       alloc_cands(*cs, ptc, eec);
-      alloc_pairbufs(cs == &dcd ? pb_dcd : pb_sweep, *cs, cs == &dcd);
+      if (cs != &ss) alloc_pairbufs(cs == &dcd ? pb_dcd : pb_sweep, *cs, cs == &dcd);
       if (cs == &dcd) lags_stale = true;
     }
     drop_graphs();
@@ -910,6 +915,10 @@ struct ipc_world {
     A.S = S;
     A.dc = dcd.c;
     A.sw = sweep.c;
+    A.ss = ss.c;
+    A.bb_lo = bb_lo;
+    A.bb_hi = bb_hi;
+    A.ss_pad = ss_pad;
     A.L = L;
     A.D = D_with(pb_dcd);
     A.T = Terms{body_val, tet_val, pb_dcd.pt_val, pb_dcd.ee_val, pb_dcd.gnd_val, fr_val, frg_val, nullptr};
@@ -1291,6 +1300,51 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
       chunks(d->edge_cbody, d->n_edge, &W.n_echunk, &W.echunk_p0, &W.cbody_echunk);
       W.tchunk_box = P.alloc<double>(6 * (size_t)std::max(W.n_tchunk, 1));
       W.echunk_box = P.alloc<double>(6 * (size_t)std::max(W.n_echunk, 1));
+      // LBVHs for the triangles / edges of large bodies (IPC_LBVH=0: chunk walk only)
+      {
+        const char* lz = getenv("IPC_LBVH");
+        bool on = !(lz && lz[0] == '0');
+        std::vector<int> tk, tp0, tn, tnode0, tleaf0, ctb(d->n_cbody, -1), ceb(d->n_cbody, -1);
+        int nodes = 0, leaves = 0;
+        auto add = [&](int kind, const int32_t* owner, int nprim, std::vector<int>& dst) {
+          std::vector<int> first(d->n_cbody + 1, 0);
+          for (int t = 0; t < nprim; ++t) first[owner[t] + 1]++;
+          for (int b = 0; b < d->n_cbody; ++b) first[b + 1] += first[b];
+          for (int b = 0; b < d->n_cbody; ++b) {
+            int n = first[b + 1] - first[b];
+            if (!on || n < LBVH_MIN || n > LBVH_MAX) continue;
+            dst[b] = (int)tk.size();
+            tk.push_back(kind);
+            tp0.push_back(first[b]);
+            tn.push_back(n);
+            tnode0.push_back(nodes);
+            tleaf0.push_back(leaves);
+            nodes += n - 1;
+            leaves += n;
+          }
+        };
+        add(0, d->tri_cbody, d->n_tri, ctb);
+        add(1, d->edge_cbody, d->n_edge, ceb);
+        W.n_tree = (int)tk.size();
+        if (W.n_tree) {
+          W.tree_kind = P.upload(tk.data(), tk.size());
+          W.tree_p0 = P.upload(tp0.data(), tp0.size());
+          W.tree_n = P.upload(tn.data(), tn.size());
+          W.tree_node0 = P.upload(tnode0.data(), tnode0.size());
+          W.tree_leaf0 = P.upload(tleaf0.data(), tleaf0.size());
+          W.bvh_child = P.alloc<int>(2 * (size_t)nodes);
+          W.bvh_parent = P.alloc<int>((size_t)nodes);
+          W.bvh_lparent = P.alloc<int>((size_t)leaves);
+          W.bvh_prim = P.alloc<int>((size_t)leaves);
+          W.bvh_box = P.alloc<double>(6 * (size_t)nodes);
+          CK(cudaFuncSetAttribute(k_lbvh_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(4 * LBVH_MAX * sizeof(unsigned))));
+        }
+        ctb.push_back(-1);  // never empty
+        ceb.push_back(-1);
+        W.cbody_tbvh = P.upload(ctb.data(), ctb.size());
+        W.cbody_ebvh = P.upload(ceb.data(), ceb.size());
+      }
       int dev = 0;
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&w->n_sm, cudaDevAttrMultiProcessorCount, dev));
@@ -1362,7 +1416,7 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
         CK(cudaFuncSetAttribute(k_broad_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w->broad_smem));
       }
     }
-    const int DENSE_MAX = 160;
+    const int DENSE_MAX = DENSE_MAX_N;
     w->sparse = w->max_env_dof > DENSE_MAX;
     if (!w->sparse) {
       // dense system n² + 2n, plus the slot lever arms of the parallel
@@ -1405,6 +1459,14 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     }
     w->alloc_cands(w->dcd, ptc, eec);
     w->alloc_cands(w->sweep, ptc, eec);
+    w->alloc_cands(w->ss, ptc, eec);
+    w->ss.c.overflow = w->sweep.c.overflow;  // one sticky flag: the step checks dcd and sweep
+    w->bb_lo = P.alloc<double>(3 * (size_t)std::max(d->n_slot, 1));
+    w->bb_hi = P.alloc<double>(3 * (size_t)std::max(d->n_slot, 1));
+    {
+      const char* sp = getenv("IPC_SS_PAD");
+      if (sp) w->ss_pad = atof(sp);
+    }
     w->alloc_pairbufs(w->pb_dcd, w->dcd, true);
     w->alloc_pairbufs(w->pb_sweep, w->sweep, false);
     w->alloc_lags();

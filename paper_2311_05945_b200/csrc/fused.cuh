@@ -40,6 +40,9 @@ struct FusedArgs {
   World W;
   EnvState S;
   Cands dc, sw;  // DCD / CCD-sweep candidate stores
+  Cands ss;      // cached candidate superset (env_candidates)
+  double *bb_lo, *bb_hi;  // per-slot build boxes of the superset
+  double ss_pad;          // build-box padding in units of d̂ (0: superset off)
   Lags L;
   Derivs D;      // derivative buffers of the DCD store
   Terms T;       // value buffers of the DCD store
@@ -326,6 +329,130 @@ static __device__ bool env_broad_sm(const World& W, const double* __restrict__ l
   return !s_ov;
 }
 
+// ---------------------------------------------------------------------------
+// Cached candidate superset (ref broadphase.py:74 BroadPhaseCache keeps its
+// trees across queries and rebuilds only after large motion). The superset S
+// of env e is the exact broad phase over every slot's *build box*: the query
+// box the slot had at build time grown by ss_pad·d̂ on every side. For any
+// later configuration in which each slot's query box (a point for DCD, the
+// sweep box for CCD) lies inside its build box, every pair the exact broad
+// phase reports is in S (primitive boxes are unions of slot boxes, the pair
+// margin is d̂ in both). The exact list is S filtered with the prim-level box
+// test of env_broad_sm (identical arithmetic) in S's lexicographic order, so
+// it is bit-identical to a fresh broad phase at the cost of one ordered
+// compaction; S is rebuilt when a query box leaves its build box.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool env_ss_covers(const FusedArgs& A, const double* lo, const double* hi, int e) {
+  const World& W = A.W;
+  int ok = 1;
+  for (int i = 3 * W.env_slot[e] + threadIdx.x; i < 3 * W.env_slot[e + 1]; i += blockDim.x)
+    ok &= (lo[i] >= A.bb_lo[i]) & (hi[i] <= A.bb_hi[i]);
+  return __syncthreads_and(ok);
+}
+
+static __device__ bool env_ss_build(const FusedArgs& A, const double* lo, const double* hi, int e, double* sm) {
+  const World& W = A.W;
+  double pad = A.ss_pad * W.env_dhat[e];
+  for (int i = 3 * W.env_slot[e] + threadIdx.x; i < 3 * W.env_slot[e + 1]; i += blockDim.x) {
+    A.bb_lo[i] = __dsub_rn(lo[i], pad);
+    A.bb_hi[i] = __dadd_rn(hi[i], pad);
+  }
+  __syncthreads();
+  return env_broad_sm(W, A.bb_lo, A.bb_hi, A.ss, e, sm, A.smem_doubles);
+}
+
+// exact candidates of the query boxes [lo, hi] from the env's superset into C
+static __device__ bool env_ss_filter(const FusedArgs& A, const double* lo, const double* hi, const Cands& C, int e) {
+  const World& W = A.W;
+  const Cands& S = A.ss;
+  __shared__ int wtot[BP_THREADS / 32];
+  __shared__ int s_total, s_ov;
+  int tid = threadIdx.x;
+  double margin = W.env_dhat[e];
+  if (!W.env_has_ground[e]) {
+    if (tid == 0) C.n_gnd[e] = 0;
+  } else {
+    double lim = __dadd_rn(W.env_ground_y[e], margin);
+    int off = C.gnd_off[e], n = S.n_gnd[e], base = 0;
+    for (int k0 = 0; k0 < n; k0 += BP_THREADS) {
+      int k = k0 + tid, sl = k < n ? S.gnd[off + k] : 0;
+      bool hit = k < n && lo[3 * sl + 1] < lim;
+      int o = block_ordered_offset<BP_THREADS>(hit, wtot, &s_total);
+      if (hit) C.gnd[off + base + o] = sl;
+      base += s_total;
+      __syncthreads();
+    }
+    if (tid == 0) C.n_gnd[e] = base;
+  }
+  for (int kind = 0; kind < 2; ++kind) {
+    int n = W.env_pairs[e] ? (kind == 0 ? S.n_pt[e] : S.n_ee[e]) : 0;
+    long long soff = kind == 0 ? S.pt_off[e] : S.ee_off[e];
+    long long coff = kind == 0 ? C.pt_off[e] : C.ee_off[e];
+    long long cap = (kind == 0 ? C.pt_off[e + 1] : C.ee_off[e + 1]) - coff;
+    long long base = 0;
+    for (int k0 = 0; k0 < n; k0 += BP_THREADS) {
+      int k = k0 + tid;
+      bool hit = false;
+      int2 pr = make_int2(0, 0);
+      if (k < n) {
+        pr = kind == 0 ? S.pt[soff + k] : S.ee[soff + k];
+        double q[6], p[6];
+        if (kind == 0) {  // slot box vs triangle box (env_broad_sm: sb, tb)
+          int3 v = W.tri_v[pr.y];
+          for (int c = 0; c < 3; ++c) {
+            q[c] = lo[3 * pr.x + c];
+            q[3 + c] = hi[3 * pr.x + c];
+            p[c] = fmin(fmin(lo[3 * v.x + c], lo[3 * v.y + c]), lo[3 * v.z + c]);
+            p[3 + c] = fmax(fmax(hi[3 * v.x + c], hi[3 * v.y + c]), hi[3 * v.z + c]);
+          }
+        } else {  // edge box vs edge box (eb)
+          int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
+          for (int c = 0; c < 3; ++c) {
+            q[c] = fmin(lo[3 * a.x + c], lo[3 * a.y + c]);
+            q[3 + c] = fmax(hi[3 * a.x + c], hi[3 * a.y + c]);
+            p[c] = fmin(lo[3 * b.x + c], lo[3 * b.y + c]);
+            p[3 + c] = fmax(hi[3 * b.x + c], hi[3 * b.y + c]);
+          }
+        }
+        hit = box_hit(q, q + 3, p, p + 3, margin);
+      }
+      int o = block_ordered_offset<BP_THREADS>(hit, wtot, &s_total);
+      if (hit && base + o < cap) {
+        if (kind == 0) C.pt[coff + base + o] = pr;
+        else C.ee[coff + base + o] = pr;
+      }
+      base += s_total;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      int need = (int)min(base, (long long)INT_MAX);
+      if (kind == 0) C.need_pt[e] = need; else C.need_ee[e] = need;
+      if (base > cap) {
+        atomicExch(C.overflow, 1);
+        base = cap;
+      }
+      if (kind == 0) C.n_pt[e] = (int)base; else C.n_ee[e] = (int)base;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) s_ov = *(volatile int*)C.overflow;
+  __syncthreads();
+  return !s_ov;
+}
+
+// candidates of the query boxes [lo, hi] into C: through the env's cached
+// superset (*ss_ok: block-uniform shared flag, 0 = no valid superset) or a
+// fresh broad phase when the cache is off (ss_pad == 0)
+static __device__ bool env_candidates(const FusedArgs& A, const double* lo, const double* hi, const Cands& C, int e,
+                                      double* sm, int* ss_ok) {
+  if (A.ss_pad <= 0.0) return env_broad_sm(A.W, lo, hi, C, e, sm, A.smem_doubles);
+  if (!(*ss_ok && env_ss_covers(A, lo, hi, e))) {
+    if (!env_ss_build(A, lo, hi, e, sm)) return false;
+    if (threadIdx.x == 0) *ss_ok = 1;
+  }
+  return env_ss_filter(A, lo, hi, C, e);
+}
+
 // Batched schedule: the shared-memory broad phase, one CTA per flagged env
 // (all three kinds; chunk boxes built in shared memory).
 IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_broad_sm(World W, const double* __restrict__ lo,
@@ -427,8 +554,10 @@ static __device__ bool env_newton(const FusedArgs& A, int e, double* sm, bool be
   const World& W = A.W;
   const EnvState& S = A.S;
   __shared__ double s_amin;
+  __shared__ int s_ss_ok;  // the env's candidate superset is valid (env_candidates)
   int d0 = W.env_dof[e], d1 = W.env_dof[e + 1];
   int s0 = W.env_slot[e], s1 = W.env_slot[e + 1];
+  if (threadIdx.x == 0) s_ss_ok = 0;
   if (threadIdx.x == 0 && begin) newton_begin_env(S, S.al_active, e);
   FT_START;
   for (int it = it0; it < A.max_newton; ++it) {
@@ -437,7 +566,7 @@ static __device__ bool env_newton(const FusedArgs& A, int e, double* sm, bool be
     FT_MARK(A, FT_OTHER);
     env_world(W, W.x, W.xw, e);
     FT_MARK(A, FT_WORLD);
-    if (!env_broad_sm(W, W.xw, W.xw, A.dc, e, sm, A.smem_doubles)) return false;
+    if (!env_candidates(A, W.xw, W.xw, A.dc, e, sm, &s_ss_ok)) return false;
     FT_MARK(A, FT_BROAD_DCD);
     double ms = env_terms(A, W.x, W.xw, 1, e);
     FT_MARK(A, FT_TERMS);
@@ -466,7 +595,7 @@ static __device__ bool env_newton(const FusedArgs& A, int e, double* sm, bool be
       A.xhi[i] = fmax(a, b);
     }
     FT_MARK(A, FT_CCD_PREP);
-    if (!env_broad_sm(W, A.xlo, A.xhi, A.sw, e, sm, A.smem_doubles)) return false;
+    if (!env_candidates(A, A.xlo, A.xhi, A.sw, e, sm, &s_ss_ok)) return false;
     FT_MARK(A, FT_BROAD_CCD);
     if (threadIdx.x == 0) s_amin = 1.0;
     __syncthreads();

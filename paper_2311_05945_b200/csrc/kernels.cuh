@@ -2,6 +2,7 @@
 #pragma once
 #include <climits>
 #include "ipc_math.cuh"
+#include "lbvh.cuh"
 #include "world.cuh"
 
 namespace ipc {
@@ -96,6 +97,7 @@ __device__ __forceinline__ bool box_hit(const double* qlo, const double* qhi, co
   return true;
 }
 
+
 __device__ __forceinline__ bool excluded(const World& W, int cb0, int b1, int b2) {
   unsigned long long m = W.cbody_excl[b1];
   return (m >> (b2 - cb0)) & 1ull;
@@ -150,11 +152,20 @@ __device__ __forceinline__ bool prim_hit(const World& W, int kind, int row, int2
 // that hit the row's query box; 32-primitive chunks whose inflated AABB
 // misses the query box are skipped whole (exact: each primitive's inflated
 // box lies inside its chunk's)
+// (bvh: the body's LBVH, when it has one, was built from this call's [lo, hi]
+// by k_lbvh_build — the global broad phase; the chunk walk otherwise)
 template <typename F>
 __device__ __forceinline__ void for_item_prims(const World& W, int kind, int row, int2 er, const double* qlo,
                                                const double* qhi, const double* __restrict__ lo,
                                                const double* __restrict__ hi, double margin, int gb, int c0,
-                                               int c1, F f) {
+                                               int c1, F f, bool bvh = false) {
+  if (bvh) {
+    int tr = kind == 0 ? W.cbody_tbvh[gb] : W.cbody_ebvh[gb];
+    if (tr >= 0 &&
+        lbvh_visit(W, tr, qlo, qhi, margin, c0, c1,
+                   [&](int t) { return prim_hit(W, kind, row, er, t, qlo, qhi, lo, hi, margin); }, f))
+      return;
+  }
   const int* cp0 = kind == 0 ? W.tchunk_p0 : W.echunk_p0;
   const double* cbox = kind == 0 ? W.tchunk_box : W.echunk_box;
   int ch0 = kind == 0 ? W.cbody_tchunk[gb] : W.cbody_echunk[gb];
@@ -212,7 +223,8 @@ IPC_GLOBAL void k_chunk_boxes(World W, const double* __restrict__ lo, const doub
 // same as with one CTA. pass -1: single CTA per env, count + write.
 // block function (blockDim.x == BP_THREADS): range z of Z of env e's items
 static __device__ void broad_env(const World& W, const double* __restrict__ lo, const double* __restrict__ hi,
-                          const Cands& C, int kind, int e, int z, int Z, int pass, int* blk_cnt) {
+                          const Cands& C, int kind, int e, int z, int Z, int pass, int* blk_cnt,
+                          bool bvh = false) {
   __shared__ int warp_tot[BP_THREADS / 32];
   __shared__ int total;
   __shared__ double blo[3 * MAX_BODIES], bhi[3 * MAX_BODIES];
@@ -351,7 +363,7 @@ static __device__ void broad_env(const World& W, const double* __restrict__ lo, 
         int2 er = make_int2(0, 0);
         double qlo[3], qhi[3];
         item(win + surv[wid * SEG + j], row, B, c0, c1, rb, er, qlo, qhi);
-        for_item_prims(W, kind, row, er, qlo, qhi, lo, hi, margin, B + cb0, c0, c1, [&](int) { ++n_hit; });
+        for_item_prims(W, kind, row, er, qlo, qhi, lo, hi, margin, B + cb0, c0, c1, [&](int) { ++n_hit; }, bvh);
       }
       int incl = n_hit;
       for (int o = 1; o < 32; o <<= 1) {
@@ -381,7 +393,7 @@ static __device__ void broad_env(const World& W, const double* __restrict__ lo, 
             else C.ee[off + dst] = make_int2(row, t);
           }
           ++dst;
-        });
+        }, bvh);
       }
     }
     base += wsum;
@@ -413,7 +425,7 @@ IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
   if (kind < 0) kind = blockIdx.y;  // all three kinds in one launch
   int e = blockIdx.x;
   if (env_mask && !env_mask[e]) return;
-  broad_env(W, lo, hi, C, kind, e, blockIdx.z, gridDim.z, pass, blk_cnt);
+  broad_env(W, lo, hi, C, kind, e, blockIdx.z, gridDim.z, pass, blk_cnt, W.n_tree > 0);
 }
 
 // per-env exclusive prefix of candidate counts over flagged envs (one CTA);
@@ -508,17 +520,16 @@ __device__ __forceinline__ void body_item(const World& W, const double* __restri
   double ov = 0.0;
   for (int i = 0; i < 9; ++i) ov += Mm.m[i] * Mm.m[i];
   v += h2 * c * ov;
-  double H[144];
+  // Hessian = M_b + h² (projected orthogonality block) + Σ κ_A I, written
+  // straight to the output (no 12x12 local array)
+  double h9[81];
   if (deriv) {
     M3 MA = m3_mul(Mm, A);
     for (int i = 0; i < 9; ++i) g[3 + i] += h2 * 4.0 * c * MA.m[i];
-    double h9[81];
     ortho_hess_psd(A, c, h9);
-    for (int i = 0; i < 144; ++i) H[i] = M[i];
-    for (int i = 0; i < 9; ++i)
-      for (int j = 0; j < 9; ++j) H[(3 + i) * 12 + 3 + j] += h2 * h9[9 * i + j];
   }
-  // kinematic constraints on this body
+  // kinematic constraints on this body (ref constraints.py:55)
+  double kap_diag = 0.0;
   for (int k = W.env_cons[e]; k < W.env_cons[e + 1]; ++k) {
     if (W.cons_aff[k] != b) continue;
     double kap = W.cons_kappa[k], sm = sqrt(W.cons_mass[k]);
@@ -529,17 +540,24 @@ __device__ __forceinline__ void body_item(const World& W, const double* __restri
       double di = x[o + i] - tg[i];
       dd += di * di;
       ld += lam[i] * di;
-      if (deriv) {
-        g[i] += kap * di - sm * lam[i];
-        H[13 * i] += kap;
-      }
+      if (deriv) g[i] += kap * di - sm * lam[i];
     }
+    kap_diag += kap;
     v += 0.5 * kap * dd - sm * ld;
   }
   val[b] = v;
   if (deriv) {
     for (int i = 0; i < 12; ++i) g12[12 * b + i] = g[i];
-    for (int i = 0; i < 144; ++i) h144[144 * b + i] = H[i];
+    double* ho = h144 + 144 * b;
+#pragma unroll
+    for (int i = 0; i < 12; ++i)
+#pragma unroll
+      for (int j = 0; j < 12; ++j) {
+        double hv = M[12 * i + j];
+        if (i >= 3 && j >= 3) hv += h2 * h9[9 * (i - 3) + j - 3];
+        if (i == j) hv += kap_diag;
+        ho[12 * i + j] = hv;
+      }
   }
 }
 

@@ -274,6 +274,8 @@ struct Derivs {
 };
 
 constexpr int DENSE_THREADS = 256;
+constexpr int DENSE_MAX_N = 160;  // largest env system on the dense path (engine.cu DENSE_MAX)
+constexpr int DENSE_REG_N = 64;   // register-resident factorization up to this size
 
 // dynamic shared memory of the dense solve of an n-DoF env: system n² + 2n,
 // the record staging area, the per-DoF group keys
@@ -563,39 +565,111 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
   double gn = block_max(gmax, red);
   if (tid == 0) S.gnorm[e] = gn;
   __syncthreads();
-  // LDLᵀ without scaling (one block sync per column): after step k the
-  // lower column c_k = H[k+1:, k] and pivot a_k = H[k][k] give
-  // H = Σ c_k c_kᵀ / a_k, i.e. L' = c / a (unit lower), D = diag(a). Same
-  // factorization as Cholesky (SPD input), no sqrt/divide on the hot path.
-  for (int k = 0; k < n; ++k) {
-    double akk = H[k * n + k];
-    if (tid == 0 && !(akk > 0.0)) fail = 1;
-    double inv = 1.0 / akk;
-    int m = n - k - 1;
-    // trailing update H[i][j] -= c_i c_j / a_k for k < j <= i, 2D thread map
-    for (int ii = tid >> 4; ii < m; ii += blockDim.x >> 4) {
-      int i = k + 1 + ii;
-      double ci = H[i * n + k] * inv;
-      for (int jj = tid & 15; jj <= ii; jj += 16) {
-        int j = k + 1 + jj;
-        H[i * n + j] -= ci * H[j * n + k];
+  // LDLᵀ without scaling: after step k the lower column c_k = H[k+1:, k] and
+  // pivot a_k = H[k][k] give H = Σ c_k c_kᵀ / a_k, i.e. L' = c / a (unit
+  // lower), D = diag(a); same factorization as Cholesky (SPD input).
+  __shared__ double s_dinv[DENSE_MAX_N];
+  if (n <= DENSE_REG_N) {
+    // Small envs (every grasp env: 4 affine bodies, n = 48): each thread keeps
+    // the lower-triangle entries it assembled in registers; per column the
+    // owners publish column k to a double-buffered shared column and every
+    // thread updates its own entries (one barrier per column, no shared-memory
+    // read-modify-write chains). Warp 0 then substitutes with y in registers
+    // and the pivot / column values broadcast by shuffles.
+    constexpr int MAXE = (DENSE_REG_N * (DENSE_REG_N + 1) / 2 + DENSE_THREADS - 1) / DENSE_THREADS;
+    __shared__ double colb[2][DENSE_REG_N];
+    double a[MAXE];
+    int rr[MAXE], cc[MAXE];
+    int nlow = n * (n + 1) / 2;
+#pragma unroll
+    for (int q = 0; q < MAXE; ++q) {
+      int idx = tid + q * DENSE_THREADS, r = -1, c = -1;
+      double v = 0.0;
+      if (idx < nlow) {
+        r = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+        while ((r + 1) * (r + 2) / 2 <= idx) ++r;
+        while (r * (r + 1) / 2 > idx) --r;
+        c = idx - r * (r + 1) / 2;
+        v = H[r * n + c];
       }
+      a[q] = v;
+      rr[q] = r;
+      cc[q] = c;
+    }
+    for (int k = 0; k < n; ++k) {
+      double* cb = colb[k & 1];
+#pragma unroll
+      for (int q = 0; q < MAXE; ++q)
+        if (cc[q] == k) cb[rr[q]] = a[q];
+      __syncthreads();
+      double akk = cb[k];
+      double inv = 1.0 / akk;
+      if (tid == 0) {
+        s_dinv[k] = inv;
+        if (!(akk > 0.0)) fail = 1;
+      }
+#pragma unroll
+      for (int q = 0; q < MAXE; ++q)
+        if (cc[q] > k) a[q] -= (cb[rr[q]] * inv) * cb[cc[q]];
+    }
+#pragma unroll
+    for (int q = 0; q < MAXE; ++q)
+      if (rr[q] >= 0) H[rr[q] * n + cc[q]] = a[q];
+    __syncthreads();
+    if (tid < 32) {
+      const unsigned FULL = 0xffffffffu;
+      int lane = tid, i1 = lane + 32;
+      double y0 = lane < n ? y[lane] : 0.0, y1 = i1 < n ? y[i1] : 0.0;
+      // forward: L' u = -g (y holds -g)
+      for (int k = 0; k < n; ++k) {
+        double uk = __shfl_sync(FULL, k < 32 ? y0 : y1, k & 31);
+        double dk = s_dinv[k];
+        if (lane > k && lane < n) y0 -= (H[lane * n + k] * dk) * uk;
+        if (i1 > k && i1 < n) y1 -= (H[i1 * n + k] * dk) * uk;
+      }
+      if (lane < n) y0 *= s_dinv[lane];
+      if (i1 < n) y1 *= s_dinv[i1];
+      // backward: L'ᵀ p = D⁻¹ u
+      for (int k = n - 1; k >= 0; --k) {
+        double xk = __shfl_sync(FULL, k < 32 ? y0 : y1, k & 31);
+        if (lane < k) y0 -= (H[k * n + lane] * s_dinv[lane]) * xk;
+        if (i1 < k) y1 -= (H[k * n + i1] * s_dinv[i1]) * xk;
+      }
+      if (lane < n) y[lane] = y0;
+      if (i1 < n) y[i1] = y1;
     }
     __syncthreads();
-  }
-  // forward: L' u = -g  (y holds -g)
-  for (int k = 0; k < n; ++k) {
-    double uk = y[k], inv = 1.0 / H[k * n + k];
-    for (int i = k + 1 + tid; i < n; i += blockDim.x) y[i] -= (H[i * n + k] * inv) * uk;
+  } else {
+    for (int k = 0; k < n; ++k) {  // one block barrier per column
+      double akk = H[k * n + k];
+      if (tid == 0 && !(akk > 0.0)) fail = 1;
+      double inv = 1.0 / akk;
+      int m = n - k - 1;
+      // trailing update H[i][j] -= c_i c_j / a_k for k < j <= i, 2D thread map
+      for (int ii = tid >> 4; ii < m; ii += blockDim.x >> 4) {
+        int i = k + 1 + ii;
+        double ci = H[i * n + k] * inv;
+        for (int jj = tid & 15; jj <= ii; jj += 16) {
+          int j = k + 1 + jj;
+          H[i * n + j] -= ci * H[j * n + k];
+        }
+      }
+      __syncthreads();
+    }
+    // forward: L' u = -g  (y holds -g)
+    for (int k = 0; k < n; ++k) {
+      double uk = y[k], inv = 1.0 / H[k * n + k];
+      for (int i = k + 1 + tid; i < n; i += blockDim.x) y[i] -= (H[i * n + k] * inv) * uk;
+      __syncthreads();
+    }
+    for (int i = tid; i < n; i += blockDim.x) y[i] /= H[i * n + i];
     __syncthreads();
-  }
-  for (int i = tid; i < n; i += blockDim.x) y[i] /= H[i * n + i];
-  __syncthreads();
-  // backward: L'ᵀ p = D⁻¹ u
-  for (int k = n - 1; k >= 0; --k) {
-    double xk = y[k];
-    for (int i = tid; i < k; i += blockDim.x) y[i] -= (H[k * n + i] / H[i * n + i]) * xk;
-    __syncthreads();
+    // backward: L'ᵀ p = D⁻¹ u
+    for (int k = n - 1; k >= 0; --k) {
+      double xk = y[k];
+      for (int i = tid; i < k; i += blockDim.x) y[i] -= (H[k * n + i] / H[i * n + i]) * xk;
+      __syncthreads();
+    }
   }
   double pg = 0.0;
   int bad = 0;

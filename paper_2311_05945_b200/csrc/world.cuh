@@ -99,6 +99,12 @@ struct World {
   const int *tchunk_p0, *echunk_p0;        // [n_chunk+1] first primitive of each chunk
   const int *cbody_tchunk, *cbody_echunk;  // [n_cbody+1] chunk ranges of each body
   double *tchunk_box, *echunk_box;         // 6 per chunk (lo, hi), refreshed per broad phase
+  // LBVHs of large bodies (lbvh.cuh), rebuilt per global broad phase
+  int n_tree;
+  const int *tree_kind, *tree_p0, *tree_n, *tree_node0, *tree_leaf0;  // [n_tree]
+  const int *cbody_tbvh, *cbody_ebvh;  // [n_cbody] tree of the body's triangles / edges, -1: none
+  int *bvh_child, *bvh_parent, *bvh_lparent, *bvh_prim;  // 2 per internal node, per node, per leaf, per leaf
+  double* bvh_box;                     // 6 per internal node
   // constraints
   const int* cons_aff;
   double *cons_target, *cons_lam, *cons_kappa, *cons_kappa0, *cons_mass, *cons_lastres;

@@ -241,3 +241,36 @@ def test_config2_soft_grasp_10k_tets_matches_reference(golden):
         # a distance: agrees to the DoF tolerance (absolute, scaled by max |x|)
         assert abs(rep.min_dist_after - z["min_dist"][k]) <= REL * np.abs(z["x"][k]).max(), k
     assert sc.barrier.kappa == float(z["kappa"])
+
+
+@pytest.mark.parametrize("divisions", [8, 12])
+def test_lbvh_broad_phase_identical_to_chunk_walk(golden, monkeypatch, divisions):
+    """The LBVH culling of large bodies (lbvh.cuh: device radix sort, Karras
+    build, refit, traversal) gives bit-identical, identically ordered
+    candidate lists to the chunk walk, on the config-2 soft grasp (the soft
+    cube's 1728 surface triangles and ~2600 edges get trees) before and
+    during the squeeze."""
+    from paper_2311_05945_b200.world import GpuWorld
+
+    z = dict(golden("traj_soft_grasp_c2.npz"))
+    z["divisions"] = divisions
+    sc, g = _config2_scene(z)
+    cfg = SolverConfig()
+    states = [sc.state.gather()]
+    for _ in range(6):
+        g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, 0.0262))
+        step(sc, cfg)
+        states.append(sc.state.gather())
+    lists = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("IPC_LBVH", flag)
+        w = GpuWorld([sc])
+        out = []
+        for x in states:
+            w.set_state(x, np.zeros_like(x))
+            out.append([w.candidates(0, which) for which in (0, 1, 2)])
+        lists[flag] = out
+    for a, b in zip(lists["1"], lists["0"]):
+        for which in range(3):
+            assert np.array_equal(a[which], b[which]), which
+    assert sum(len(a[0]) + len(a[1]) for a in lists["1"]) > 0
