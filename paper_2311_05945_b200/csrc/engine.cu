@@ -878,7 +878,8 @@ struct ipc_world {
   bool fused_setup() {
     if (!fq) {
       fq = pool.alloc<int>(1);
-      d_fstat = pool.alloc<long long>(2 + FT_N);
+      d_fstat = pool.alloc<long long>(2 + FT_TOTAL);
+      CK(cudaMemset(d_fstat, 0, sizeof(long long) * (2 + FT_TOTAL)));
       v_save = pool.alloc<double>(W.n_dof);
       kappa_save = pool.alloc<double>(n_env);
     }
@@ -1780,7 +1781,7 @@ int ipc_world_fused_timers(ipc_world* w, int64_t* out, int n) {
     for (int k = 0; k < n; ++k) out[k] = 0;
     if (w->d_fstat) {
       CK(cudaStreamSynchronize(w->st));
-      CK(cudaMemcpy(out, w->d_fstat + 2, sizeof(long long) * std::min(n, (int)FT_N), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(out, w->d_fstat + 2, sizeof(long long) * std::min(n, (int)FT_TOTAL), cudaMemcpyDeviceToHost));
     }
   })
 }

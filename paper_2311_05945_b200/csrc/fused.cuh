@@ -21,6 +21,19 @@ namespace ipc {
 // summed over envs into FusedArgs::timers
 enum { FT_WORLD, FT_BROAD_DCD, FT_TERMS, FT_ENERGY, FT_DENSE, FT_CCD_PREP, FT_BROAD_CCD, FT_CCD, FT_LS, FT_OTHER,
        FT_N };
+// per-item latency of the terms phase's heavy items, after the phases:
+// (cycle sum, count, max) for PT pair Hessians, EE pair Hessians, affine
+// bodies, friction stencils
+enum { FT_IT_PT, FT_IT_EE, FT_IT_BODY, FT_IT_FR, FT_NIT };
+constexpr int FT_TOTAL = FT_N + 3 * FT_NIT;
+__device__ __forceinline__ void ft_item(long long* timers, int type, long long t0) {
+  if (!timers) return;
+  long long dt = clock64() - t0;
+  unsigned long long* p = (unsigned long long*)timers + FT_N + 3 * type;
+  atomicAdd(p, (unsigned long long)dt);
+  atomicAdd(p + 1, 1ull);
+  atomicMax(p + 2, (unsigned long long)dt);
+}
 // phase timers are on when FusedArgs::timers is set (IPC_FUSED_TIMERS=1 at
 // world creation): a block-uniform branch, no cost when off
 #define FT_MARK(A, k)                                                     \
@@ -507,8 +520,10 @@ static __device__ double env_terms(const FusedArgs& A, const double* x, const do
     int t0 = W.env_tet[e], ntet = W.env_tet[e + 1] - t0;
     int total = nbody + ntet + nw;
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      long long c0 = clock64();
       if (i < nbody) {
         fused_body(W, x, W.xhat, h2, 1, b0 + i, A.T.body_val, A.D.body_g, A.D.body_h);
+        ft_item(A.timers, FT_IT_BODY, c0);
       } else if (i < nbody + ntet) {
         fused_tet(W, x, h2, 1, t0 + (i - nbody), A.T.tet_val, A.D.tet_g, A.D.tet_h);
       } else {
@@ -516,11 +531,15 @@ static __device__ double env_terms(const FusedArgs& A, const double* x, const do
         int kind = w >> 30, j = w & ((1 << 30) - 1);
         if (kind == 0) fused_pair_hess0(W, xw, C, pt_off + j, e, A.D);
         else fused_pair_hess1(W, xw, C, ee_off + j, e, A.D);
+        ft_item(A.timers, kind == 0 ? FT_IT_PT : FT_IT_EE, c0);
       }
     }
     const Lags& L = A.L;
-    for (int k = threadIdx.x; k < L.n[e]; k += blockDim.x)
+    for (int k = threadIdx.x; k < L.n[e]; k += blockDim.x) {
+      long long c0 = clock64();
       friction_item(W, xw, W.xw0, L, A.h, 1, L.off[e] + k, e, A.T.fr_val, A.D.fr_g, A.D.fr_h);
+      ft_item(A.timers, FT_IT_FR, c0);
+    }
     for (int k = threadIdx.x; k < L.g_n[e]; k += blockDim.x)
       friction_gnd_item(W, xw, W.xw0, L, A.h, 1, W.env_slot[e] + k, e, A.T.frg_val, A.D.frg_g, A.D.frg_h);
   }

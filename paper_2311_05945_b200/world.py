@@ -342,7 +342,10 @@ class GpuWorld:
         return int(out[0])
 
     FUSED_PHASES = ("world", "broad_dcd", "terms", "energy", "dense", "ccd_prep", "broad_ccd", "ccd",
-                    "line_search", "other")
+                    "line_search", "other",
+                    # per-item latency of the terms phase: cycle sum, count, max
+                    "pt_cycles", "pt_items", "pt_max", "ee_cycles", "ee_items", "ee_max",
+                    "body_cycles", "body_items", "body_max", "fr_cycles", "fr_items", "fr_max")
 
     def fused_timers(self):
         """SM cycles per phase of the fused step (zeros unless the timers are on)."""

@@ -23,11 +23,18 @@ def phases(w, st0, st1, t0, t1, label):
     it = st1["fused_env_iters"] - st0["fused_env_iters"]
     ls = st1["fused_ls_trials"] - st0["fused_ls_trials"]
     d = {k: t1[k] - t0[k] for k in t1}
+    items = {}
+    for kind in ("pt", "ee", "body", "fr"):
+        n = d.pop(f"{kind}_items", 0)
+        cyc = d.pop(f"{kind}_cycles", 0)
+        d.pop(f"{kind}_max", 0)
+        items[kind] = {"per_iter": n / max(it, 1), "mean_us": cyc / max(n, 1) / 1965.0,
+                       "max_us_cumulative": t1[f"{kind}_max"] / 1965.0}
     tot = sum(d.values())
     out = {"label": label, "newton_iters": it, "ls_trials": ls,
            "cycles_per_iter": {k: v / max(it, 1) for k, v in d.items()},
            "share": {k: v / max(tot, 1) for k, v in d.items()},
-           "us_per_iter_at_1965MHz": tot / max(it, 1) / 1965.0}
+           "us_per_iter_at_1965MHz": tot / max(it, 1) / 1965.0, "items": items}
     print(json.dumps(out), flush=True)
 
 
