@@ -515,8 +515,23 @@ struct ipc_world {
   int bp_z = 1;
   int* bp_cnt = nullptr;
   size_t broad_smem = 0;  // k_broad_sm: staged boxes of the largest env (0: unused)
+  // broad phase over [lo, hi] into cs: through the cached candidate superset
+  // (k_ss_check flags the envs whose query boxes left their build boxes, the
+  // superset of those is rebuilt over the padded build boxes, k_ss_filter
+  // extracts the exact lists; fused.cuh env_candidates), or directly
+  int* ss_valid = nullptr;    // [n_env] superset holds the broad phase of the current build boxes
+  int* ss_rebuild = nullptr;  // [n_env] scratch: envs to rebuild in this call
   void launch_broad(CandStore& cs, const double* lo, const double* hi, const int* env_mask) {
     int kid = &cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD;
+    if (ss_pad > 0.0 && &cs != &ss) {
+      IPC_LAUNCH(kid, st, k_ss_check, n_env, 256, 0, W, lo, hi, bb_lo, bb_hi, ss_pad, env_mask, ss_valid, ss_rebuild);
+      launch_broad_raw(ss, bb_lo, bb_hi, ss_rebuild, kid);
+      IPC_LAUNCH(kid, st, k_ss_filter, n_env, BP_THREADS, 0, W, lo, hi, ss.c, cs.c, env_mask);
+      return;
+    }
+    launch_broad_raw(cs, lo, hi, env_mask, kid);
+  }
+  void launch_broad_raw(CandStore& cs, const double* lo, const double* hi, const int* env_mask, int kid) {
     if (broad_smem && bp_z == 1) {
       IPC_LAUNCH(kid, st, k_broad_sm, n_env, BP_THREADS, broad_smem, W, lo, hi, cs.c, env_mask,
                  (int)(broad_smem / sizeof(double)));
@@ -540,32 +555,23 @@ struct ipc_world {
   // run broad phase; grow capacities and retry on overflow
   void broad(CandStore& cs, PairBufs& pb, bool derivs, const double* lo, const double* hi,
              const int* env_mask) {
+    (void)pb;
+    (void)derivs;
     for (int attempt = 0; attempt < 8; ++attempt) {
+      // the superset store shares the sweep store's sticky flag
       CK(cudaMemsetAsync(cs.c.overflow, 0, sizeof(int), st));
+      CK(cudaMemsetAsync(sweep.c.overflow, 0, sizeof(int), st));
       launch_broad(cs, lo, hi, env_mask);
       CK(cudaGetLastError());
-      int ov = 0;
       CK(cudaMemcpyAsync(h_count, cs.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_status, sweep.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      ov = *h_count;
-      if (!ov) {
+      if (!*h_count && !*h_status) {
         IPC_LAUNCH(K_MISC, st, k_prefix3, 3, 1024, 0, n_env, cs.c, env_mask);
         return;
       }
-      // grow the overflowed envs to 1.5x their unclipped counts (at least 4x)
-      std::vector<int> np(n_env), nq(n_env);
-      CK(cudaMemcpy(np.data(), cs.c.need_pt, 4 * n_env, cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(nq.data(), cs.c.need_ee, 4 * n_env, cudaMemcpyDeviceToHost));
-      std::vector<long long> ptc = cs.pt_cap, eec = cs.ee_cap;
-      for (int e = 0; e < n_env; ++e) {
-        long long nv = h_env_slot[e + 1] - h_env_slot[e], nt = h_env_tri[e + 1] - h_env_tri[e];
-        long long ne = h_env_edge[e + 1] - h_env_edge[e];
-        if (np[e] > ptc[e]) ptc[e] = std::min(nv * nt, std::max(4 * ptc[e], (long long)np[e] * 3 / 2));
-        if (nq[e] > eec[e]) eec[e] = std::min(ne * ne, std::max(4 * eec[e], (long long)nq[e] * 3 / 2));
-      }
-      alloc_cands(cs, ptc, eec);
-      alloc_pairbufs(pb, cs, derivs);
-      if (&cs == &dcd) lags_stale = true;
+      // grow the overflowed stores to 1.5x their unclipped counts (at least 4x)
+      grow_overflowed();
     }
     throw std::runtime_error("broad phase capacity overflow persists");
   }
@@ -740,6 +746,7 @@ struct ipc_world {
       if (cs != &ss) alloc_pairbufs(cs == &dcd ? pb_dcd : pb_sweep, *cs, cs == &dcd);
       if (cs == &dcd) lags_stale = true;
     }
+    if (ss_valid) CK(cudaMemsetAsync(ss_valid, 0, sizeof(int) * n_env, st));
     drop_graphs();
   }
 
@@ -1462,6 +1469,9 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     w->alloc_cands(w->sweep, ptc, eec);
     w->alloc_cands(w->ss, ptc, eec);
     w->ss.c.overflow = w->sweep.c.overflow;  // one sticky flag: the step checks dcd and sweep
+    w->ss_valid = P.alloc<int>(ne);
+    w->ss_rebuild = P.alloc<int>(ne);
+    CK(cudaMemset(w->ss_valid, 0, sizeof(int) * ne));
     w->bb_lo = P.alloc<double>(3 * (size_t)std::max(d->n_slot, 1));
     w->bb_hi = P.alloc<double>(3 * (size_t)std::max(d->n_slot, 1));
     {

@@ -505,9 +505,10 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
         V[j * N + i] = 0.0;
       }
     } else {
+      const double iscale = 1.0 / scale;  // one division on the chain, then products
 #pragma unroll
       for (int k = 0; k < i; ++k) {
-        d[k] /= scale;
+        d[k] *= iscale;
         h += d[k] * d[k];
       }
       double f = d[i - 1];
@@ -531,9 +532,10 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
         e[j] = g;
       }
       f = 0.0;
+      const double ih = 1.0 / h;
 #pragma unroll
       for (int j = 0; j < i; ++j) {
-        e[j] /= h;
+        e[j] *= ih;
         f += e[j] * d[j];
       }
       double hh = f / (h + h);
@@ -557,8 +559,9 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
     V[i * N + i] = 1.0;
     double h = d[i + 1];
     if (h != 0.0) {
+      const double ih = 1.0 / h;
 #pragma unroll
-      for (int k = 0; k <= i; ++k) d[k] = V[k * N + i + 1] / h;
+      for (int k = 0; k <= i; ++k) d[k] = V[k * N + i + 1] * ih;
 #pragma unroll
       for (int j = 0; j <= i; ++j) {
         double g = 0.0;
@@ -596,7 +599,7 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
       for (int iter = 0; iter < 60; ++iter) {
         double g = d[l];
         double p = (d[l + 1] - g) / (2.0 * e[l]);
-        double r = hypot(p, 1.0);
+        double r = sqrt(fma(p, p, 1.0));  // hypot(p, 1) without the scaling (|p| << 1e150 here)
         if (p < 0) r = -r;
         d[l] = e[l] / (p + r);
         d[l + 1] = e[l] * (p + r);
@@ -618,10 +621,14 @@ IPC_HD void sym_eigen(double* V, double* d, double* e) {
             s2 = s;
             g = c * e[i];
             h = c * p;
-            r = hypot(p, e[i]);
+            // Givens pair from one reciprocal square root (hypot and two
+            // divisions were the latency of the QL sweep)
+            double ei = e[i], rr = fma(p, p, ei * ei);
+            double ir = rsqrt(rr);
+            r = rr * ir;
             e[i + 1] = s * r;
-            s = e[i] / r;
-            c = p / r;
+            s = ei * ir;
+            c = p * ir;
             p = c * d[i] - s * g;
             d[i + 1] = h + s * (c * g + s * d[i]);
 #pragma unroll

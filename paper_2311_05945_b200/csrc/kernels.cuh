@@ -428,6 +428,122 @@ IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
   broad_env(W, lo, hi, C, kind, e, blockIdx.z, gridDim.z, pass, blk_cnt, W.n_tree > 0);
 }
 
+// Exact candidates of the query boxes [lo, hi] of env e from its cached
+// superset S into C (fused.cuh env_candidates explains the superset): the
+// prim-level box test of the broad phase, same arithmetic, in S's order.
+static __device__ bool ss_filter_env(const World& W, const Cands& S, const double* lo, const double* hi,
+                                     const Cands& C, int e) {
+  __shared__ int wtot[BP_THREADS / 32];
+  __shared__ int s_total, s_ov;
+  int tid = threadIdx.x;
+  double margin = W.env_dhat[e];
+  if (!W.env_has_ground[e]) {
+    if (tid == 0) C.n_gnd[e] = 0;
+  } else {
+    double lim = __dadd_rn(W.env_ground_y[e], margin);
+    int off = C.gnd_off[e], n = S.n_gnd[e], base = 0;
+    for (int k0 = 0; k0 < n; k0 += BP_THREADS) {
+      int k = k0 + tid, sl = k < n ? S.gnd[off + k] : 0;
+      bool hit = k < n && lo[3 * sl + 1] < lim;
+      int o = block_ordered_offset<BP_THREADS>(hit, wtot, &s_total);
+      if (hit) C.gnd[off + base + o] = sl;
+      base += s_total;
+      __syncthreads();
+    }
+    if (tid == 0) C.n_gnd[e] = base;
+  }
+  for (int kind = 0; kind < 2; ++kind) {
+    int n = W.env_pairs[e] ? (kind == 0 ? S.n_pt[e] : S.n_ee[e]) : 0;
+    long long soff = kind == 0 ? S.pt_off[e] : S.ee_off[e];
+    long long coff = kind == 0 ? C.pt_off[e] : C.ee_off[e];
+    long long cap = (kind == 0 ? C.pt_off[e + 1] : C.ee_off[e + 1]) - coff;
+    long long base = 0;
+    for (int k0 = 0; k0 < n; k0 += BP_THREADS) {
+      int k = k0 + tid;
+      bool hit = false;
+      int2 pr = make_int2(0, 0);
+      if (k < n) {
+        pr = kind == 0 ? S.pt[soff + k] : S.ee[soff + k];
+        double q[6], p[6];
+        if (kind == 0) {  // slot box vs triangle box (env_broad_sm: sb, tb)
+          int3 v = W.tri_v[pr.y];
+          for (int c = 0; c < 3; ++c) {
+            q[c] = lo[3 * pr.x + c];
+            q[3 + c] = hi[3 * pr.x + c];
+            p[c] = fmin(fmin(lo[3 * v.x + c], lo[3 * v.y + c]), lo[3 * v.z + c]);
+            p[3 + c] = fmax(fmax(hi[3 * v.x + c], hi[3 * v.y + c]), hi[3 * v.z + c]);
+          }
+        } else {  // edge box vs edge box (eb)
+          int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
+          for (int c = 0; c < 3; ++c) {
+            q[c] = fmin(lo[3 * a.x + c], lo[3 * a.y + c]);
+            q[3 + c] = fmax(hi[3 * a.x + c], hi[3 * a.y + c]);
+            p[c] = fmin(lo[3 * b.x + c], lo[3 * b.y + c]);
+            p[3 + c] = fmax(hi[3 * b.x + c], hi[3 * b.y + c]);
+          }
+        }
+        hit = box_hit(q, q + 3, p, p + 3, margin);
+      }
+      int o = block_ordered_offset<BP_THREADS>(hit, wtot, &s_total);
+      if (hit && base + o < cap) {
+        if (kind == 0) C.pt[coff + base + o] = pr;
+        else C.ee[coff + base + o] = pr;
+      }
+      base += s_total;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      int need = (int)min(base, (long long)INT_MAX);
+      if (kind == 0) C.need_pt[e] = need; else C.need_ee[e] = need;
+      if (base > cap) {
+        atomicExch(C.overflow, 1);
+        base = cap;
+      }
+      if (kind == 0) C.n_pt[e] = (int)base; else C.n_ee[e] = (int)base;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) s_ov = *(volatile int*)C.overflow;
+  __syncthreads();
+  return !s_ov;
+}
+
+// Batched superset check (one CTA per env): does every slot's query box lie
+// inside its build box? If not, write fresh build boxes (query box ± pad·d̂)
+// and flag the env for a superset rebuild.
+IPC_GLOBAL void k_ss_check(World W, const double* __restrict__ lo, const double* __restrict__ hi, double* bb_lo,
+                           double* bb_hi, double pad, const int* env_mask, int* valid, int* rebuild) {
+  int e = blockIdx.x;
+  if (env_mask && !env_mask[e]) {
+    if (threadIdx.x == 0) rebuild[e] = 0;
+    return;
+  }
+  int i0 = 3 * W.env_slot[e], i1 = 3 * W.env_slot[e + 1];
+  int ok = valid[e];
+  if (ok)
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) ok &= (lo[i] >= bb_lo[i]) & (hi[i] <= bb_hi[i]);
+  ok = __syncthreads_and(ok);
+  if (!ok) {
+    double p = pad * W.env_dhat[e];
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      bb_lo[i] = __dsub_rn(lo[i], p);
+      bb_hi[i] = __dadd_rn(hi[i], p);
+    }
+  }
+  if (threadIdx.x == 0) {
+    rebuild[e] = !ok;
+    valid[e] = 1;
+  }
+}
+
+IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_ss_filter(World W, const double* __restrict__ lo,
+                                                          const double* __restrict__ hi, Cands S, Cands C,
+                                                          const int* env_mask) {
+  int e = blockIdx.x;
+  if (env_mask && !env_mask[e]) return;
+  ss_filter_env(W, S, lo, hi, C, e);
+}
+
 // per-env exclusive prefix of candidate counts over flagged envs (one CTA);
 // pre has n_env + 1 entries, pre[n_env] = total
 IPC_GLOBAL void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {

@@ -144,3 +144,29 @@ def repair_batch(n_env: int, seed: int = 0):
         poses.append(pose)
         joints.append(q)
     return objs, np.array(poses), np.array(joints)
+
+
+def hand_model():
+    """Three-finger revolute hand (data/dex_hand.urdf) of config 4."""
+    return parse_urdf(data_path("dex_hand.urdf"))
+
+
+def repair_batch_hand(n_env: int, seed: int = 0):
+    """Config 4 with the dexterous hand: penetrated grasps of the three-finger
+    revolute hand (data/dex_hand.urdf) on the synthetic objects of
+    ``grasp_object``. The palm face is pushed 0-15 mm into the object top
+    and every joint is curled to 0.3-0.8 rad, so phalanges cut into the
+    object. Returns (objects, poses (E,4,4), joints (E,6))."""
+    rng = np.random.default_rng(seed)
+    objs, poses, joints = [], [], []
+    for _ in range(n_env):
+        obj, hw, yaw = grasp_object(rng)
+        top = float(obj.world_vertices()[:, 1].max())
+        depth = float(rng.uniform(0.0, 0.015))
+        # the palm face (local z = 0.01) sits 0.065 above the grasp target
+        pose = top_down_pose((0.0, top - 0.065 - depth, 0.0), yaw=float(rng.uniform(0, 2 * np.pi)))
+        q = rng.uniform(0.3, 0.8, size=6)
+        objs.append(obj)
+        poses.append(pose)
+        joints.append(q)
+    return objs, np.array(poses), np.array(joints)

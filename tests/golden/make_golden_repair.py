@@ -176,7 +176,40 @@ def repair_full():
     save("repair_full.npz", n=len(rows), **arrs)
 
 
+def repair_geom_hand(n=16, seed=4):
+    """The geometric repair of config 4 with the three-finger revolute hand
+    (paper_2311_05945_b200/data/dex_hand.urdf, a URDF the reference's own
+    parser and Gripper load): n synthetic penetrated grasps
+    (workloads.repair_batch_hand)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from paper_2311_05945_b200 import data_path as our_data
+    from paper_2311_05945_b200.workloads import repair_batch_hand
+
+    urdf = our_data("dex_hand.urdf")
+    objs, poses, joints = repair_batch_hand(n, seed=seed)
+    arrs = {}
+    pen, ret, clr = [], [], []
+    for k, (o, p, q) in enumerate(zip(objs, poses, joints)):
+        v, t = o.world_vertices(), o.mesh.triangles
+        obj = RAffine(RSurface(v, t), density=500.0)
+        g = RGripper(parse_urdf(urdf))
+        pb, r, c = _geom_repair(obj, g, np.asarray(p, np.float64), np.asarray(q, np.float64))
+        pen.append(pb)
+        ret.append(r)
+        clr.append(c)
+        arrs[f"s{k}_v"] = np.asarray(v, np.float64)
+        arrs[f"s{k}_t"] = np.asarray(t, np.int64)
+        arrs[f"s{k}_pose"] = np.asarray(p, np.float64)
+        arrs[f"s{k}_q"] = np.asarray(q, np.float64)
+        print("hand", k, pb, r, c, flush=True)
+    save("repair_geom_hand.npz", pen_before=np.array(pen), retraction=np.array(ret),
+         cleared=np.array(clr), n=n, **arrs)
+
+
 if __name__ == "__main__":
+    if "--hand" in sys.argv:
+        repair_geom_hand()
+        raise SystemExit(0)
     proximity()
     repair_geom()
     if "--dynamics" in sys.argv:
