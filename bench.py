@@ -368,6 +368,8 @@ def main():
     ap.add_argument("--no-closed-loop", action="store_true", help="skip the closed-loop grasp-trial arm")
     ap.add_argument("--closed-loop-sample", type=int, default=16,
                     help="envs of the closed-loop arm replayed by the oracle")
+    ap.add_argument("--hand", choices=("pj", "dex"), default="dex",
+                    help="config 4 hand: parallel-jaw gripper or the three-finger revolute hand")
     ap.add_argument("--window-only", action="store_true",
                     help="stop after the timed window (the ncu capture command of tools/ncu_window.py)")
     ap.add_argument("--workload", choices=("grasp", "repair"), default="grasp",
@@ -675,25 +677,30 @@ REPAIR_UNIT = "grasps/s"
 # (profiles/r1e_repair_ncu.json: dadd + dmul + 2*dfma thread instructions)
 
 
-def _repair_inputs(E, seed, model=None):
-    from paper_2311_05945_b200 import data_path
+def _repair_inputs(E, seed, hand="pj"):
+    """Config-4 inputs: the parallel-jaw gripper (hand="pj") or the
+    three-finger revolute hand (hand="dex", data/dex_hand.urdf)."""
     from paper_2311_05945_b200 import workloads as WL
-    from paper_2311_05945_b200.robot import Gripper, parse_urdf
+    from paper_2311_05945_b200.robot import Gripper
     from paper_2311_05945_b200.robot.repair import _world_mesh
 
-    model = model or parse_urdf(data_path("pj_gripper.urdf"))
-    objs, poses, joints = WL.repair_batch(E, seed=seed)
+    if hand == "dex":
+        model = WL.hand_model()
+        objs, poses, joints = WL.repair_batch_hand(E, seed=seed)
+    else:
+        model = WL.gripper_model()
+        objs, poses, joints = WL.repair_batch(E, seed=seed)
     grippers = [Gripper(model) for _ in range(E)]
     opened = np.array([g.clamp_joints(q - 0.01) for g, q in zip(grippers, joints)])
     return model, objs, poses, joints, grippers, opened, [_world_mesh(o) for o in objs]
 
 
 def _cpu_repair_worker(args):
-    E, worker, n_workers, seed, budget_s = args
+    E, worker, n_workers, seed, budget_s, hand = args
     sys.path.insert(0, ROOT)
     from oracle import proximity as OP
 
-    _, objs, poses, _, grippers, opened, meshes = _repair_inputs(E, seed)
+    _, objs, poses, _, grippers, opened, meshes = _repair_inputs(E, seed, hand)
     done, t = 0, 0.0
     for e in range(worker, E, n_workers):
         t0 = time.perf_counter()
@@ -705,11 +712,11 @@ def _cpu_repair_worker(args):
     return done, t
 
 
-def repair_cpu_arm(E, seed, cores, budget_s=15.0):
+def repair_cpu_arm(E, seed, cores, budget_s=15.0, hand="pj"):
     import multiprocessing as mp
 
     n_workers = min(cores, E)
-    jobs = [(E, w, n_workers, seed, budget_s) for w in range(n_workers)]
+    jobs = [(E, w, n_workers, seed, budget_s, hand) for w in range(n_workers)]
     with mp.get_context("spawn").Pool(n_workers) as pool:
         res = pool.map(_cpu_repair_worker, jobs)
     done = sum(r[0] for r in res)
@@ -726,13 +733,18 @@ def repair_main(args, ws, rank, lr, K, W):
     beside it."""
     E = args.envs if args.envs != 1024 else 4096
     seed = shard_seed(args.seed, rank)
-    workload = (f"config4 penetrated-grasp repair: per GPU {E} parallel-jaw grasps on synthetic "
-                "boxes/spheres, palm 0-15 mm inside, fingers up to 5 mm past contact")
+    if args.hand == "dex":
+        workload = (f"config4 penetrated-grasp repair: per GPU {E} three-finger revolute-hand grasps "
+                    "(data/dex_hand.urdf, 7 links, 84 triangles) on synthetic boxes/spheres, palm "
+                    "0-15 mm inside, every joint curled 0.3-0.8 rad")
+    else:
+        workload = (f"config4 penetrated-grasp repair: per GPU {E} parallel-jaw grasps on synthetic "
+                    "boxes/spheres, palm 0-15 mm inside, fingers up to 5 mm past contact")
     if args.impl == "reference":
         if rank != 0:
             return
         cores = _cores()
-        v, done, used = repair_cpu_arm(E, args.seed, cores)
+        v, done, used = repair_cpu_arm(E, args.seed, cores, hand=args.hand)
         line = {"impl": "reference", "metric": REPAIR_METRIC, "value": v, "unit": REPAIR_UNIT,
                 "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": 1e3 * E / v,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -755,7 +767,7 @@ def repair_main(args, ws, rank, lr, K, W):
 
         torch.cuda.set_device(lr)
         dist.init_process_group("nccl")
-    model, objs, poses, joints, grippers, opened, meshes = _repair_inputs(E, seed)
+    model, objs, poses, joints, grippers, opened, meshes = _repair_inputs(E, seed, args.hand)
     import torch
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{lr}")
@@ -795,11 +807,12 @@ def repair_main(args, ws, rank, lr, K, W):
                 "autograsp_env_steps": int(sum(x.trial.steps for x in res)),
                 "note": "host scene build + retraction + AutoGrasp on the GPU engine + "
                         "penetration query, wall clock, one run"}
-    flops, traffic, pipe = None, None, None
+    flops, traffic, pipe, cap = None, None, None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "r1e_repair_ncu.json")) as fh:
+        cap = "r1e_repair_ncu.json" if args.hand == "pj" else f"r2_repair_ncu_{args.hand}.json"
+        with open(os.path.join(ROOT, "profiles", cap)) as fh:
             nj = json.load(fh)
-        if nj.get("envs") == E and nj.get("seed") == args.seed:
+        if nj.get("envs") == E and nj.get("seed") == args.seed and nj.get("hand", "pj") == args.hand:
             flops = float(nj["fp64_flops"])
             traffic = float(nj["dram_bytes_read"] + nj["dram_bytes_write"])
             pipe = float(nj["fp64_pipe_active_pct"])
@@ -818,14 +831,14 @@ def repair_main(args, ws, rank, lr, K, W):
                          "unit": "TFLOP/s", "frac": achieved / fp64_peak if achieved else None,
                          "traffic": traffic, "launches": K, "avg_launch_us": avg_s * 1e6,
                          "fp64_pipe_active_pct_ncu": pipe,
-                         "flops_source": "profiles/r1e_repair_ncu.json (ncu dadd+dmul+2*dfma)"},
+                         "flops_source": (f"profiles/{cap} (ncu dadd+dmul+2*dfma)" if flops else None)},
             "e2e": {"value": E * ws * K / e2e_s, "unit": REPAIR_UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": K, "clocks": clk.summary(),
             "cleared": int(cleared.sum()), "mean_probe": float(idx[cleared].mean()),
             "full_repair": full}
     if rank == 0 and ws == 1 and not args.no_cpu:
-        v, done, used = repair_cpu_arm(E, args.seed, _cores())
+        v, done, used = repair_cpu_arm(E, args.seed, _cores(), hand=args.hand)
         line["cpu_baseline"] = {"value": v, "unit": REPAIR_UNIT, "cores": used, "kind": "port",
                                 "sample": f"{done} grasps of the same batch, oracle/ numpy port "
                                           "of the probe loop, ~15 s per core"}

@@ -721,25 +721,41 @@ struct ipc_world {
 
   void grow_overflowed() {
     CK(cudaStreamSynchronize(st));
-    for (CandStore* cs : {&dcd, &sweep, &ss}) {
-      // the broad phase records each env's unclipped candidate count: grow
-      // straight to 1.5x that (at least 4x), so one replay suffices
+    // the broad phase records each env's unclipped candidate count: grow
+    // straight to 1.5x that (at least 4x), so one replay suffices. An env that
+    // overflowed one store grows all three (DCD ⊆ sweep ⊆ superset in practice),
+    // so a step replay does not discover the same env again in another store.
+    CandStore* stores[3] = {&dcd, &sweep, &ss};
+    std::vector<long long> want_pt(n_env, 0), want_ee(n_env, 0);
+    std::vector<int> hit(n_env, 0);
+    for (CandStore* cs : stores) {
       std::vector<int> np(n_env), ne(n_env);
       CK(cudaMemcpy(np.data(), cs->c.need_pt, 4 * n_env, cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(ne.data(), cs->c.need_ee, 4 * n_env, cudaMemcpyDeviceToHost));
+      for (int e = 0; e < n_env; ++e) {
+        if (np[e] > cs->pt_cap[e] || ne[e] > cs->ee_cap[e]) hit[e] = 1;
+        want_pt[e] = std::max(want_pt[e], (long long)np[e]);
+        want_ee[e] = std::max(want_ee[e], (long long)ne[e]);
+        if (getenv("IPC_DEBUG_OVERFLOW") && (np[e] > cs->pt_cap[e] || ne[e] > cs->ee_cap[e]))
+          fprintf(stderr, "[overflow] store %s env %d need pt %d / cap %lld, ee %d / cap %lld\n",
+                  cs == &dcd ? "dcd" : (cs == &sweep ? "sweep" : "superset"), e, np[e], cs->pt_cap[e], ne[e],
+                  cs->ee_cap[e]);
+      }
+    }
+    for (CandStore* cs : stores) {
       std::vector<long long> ptc = cs->pt_cap, eec = cs->ee_cap;
       bool grew = false;
       for (int e = 0; e < n_env; ++e) {
+        if (!hit[e]) continue;
         long long nv = h_env_slot[e + 1] - h_env_slot[e], nt = h_env_tri[e + 1] - h_env_tri[e];
         long long nE = h_env_edge[e + 1] - h_env_edge[e];
-        if (np[e] > ptc[e] && ptc[e] < nv * nt) {
-          ptc[e] = std::min(nv * nt, std::max(4 * std::max(ptc[e], 1LL), (long long)np[e] * 3 / 2));
-          grew = true;
-        }
-        if (ne[e] > eec[e] && eec[e] < nE * nE) {
-          eec[e] = std::min(nE * nE, std::max(4 * std::max(eec[e], 1LL), (long long)ne[e] * 3 / 2));
-          grew = true;
-        }
+        long long p2 = std::min(nv * nt, std::max(want_pt[e] * 3 / 2, ptc[e]));
+        long long e2 = std::min(nE * nE, std::max(want_ee[e] * 3 / 2, eec[e]));
+        if (want_pt[e] > ptc[e]) p2 = std::min(nv * nt, std::max(p2, 4 * std::max(ptc[e], 1LL)));
+        if (want_ee[e] > eec[e]) e2 = std::min(nE * nE, std::max(e2, 4 * std::max(eec[e], 1LL)));
+        if (p2 != ptc[e] || e2 != eec[e]) grew = true;
+        ptc[e] = p2;
+        eec[e] = e2;
       }
       if (!grew) continue;
       alloc_cands(*cs, ptc, eec);
@@ -1673,7 +1689,7 @@ static int step_impl(ipc_world* w, const ipc_step_config* cfg, const double* tar
         step_core(w, cfg, targets, sched_k, enable, rep);
         break;
       } catch (const OverflowRetry&) {
-        if (attempt >= 6) throw std::runtime_error("candidate capacity overflow persists");
+        if (attempt >= 24) throw std::runtime_error("candidate capacity overflow persists");
         // replay the step from x_prev with larger candidate capacities
         CK(cudaMemcpyAsync(w->W.x, w->W.x_prev, sizeof(double) * w->W.n_dof, cudaMemcpyDeviceToDevice, w->st));
         w->grow_overflowed();
@@ -1709,7 +1725,7 @@ int ipc_world_run_scheduled(ipc_world* w, const ipc_step_config* cfg, int k0, in
       CK(cudaMemcpyAsync(w->h_status + 1, w->sweep.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, w->st));
       CK(cudaStreamSynchronize(w->st));
       if (!w->h_status[0] && !w->h_status[1]) break;
-      if (attempt >= 6) throw std::runtime_error("candidate capacity overflow persists");
+      if (attempt >= 24) throw std::runtime_error("candidate capacity overflow persists");
       // replay the whole range from its start with larger capacities
       CK(cudaMemcpyAsync(W.x, x0, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, w->st));
       CK(cudaMemcpyAsync(W.v, w->v_save, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, w->st));

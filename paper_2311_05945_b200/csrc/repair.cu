@@ -209,7 +209,7 @@ __device__ void block_box(const double* __restrict__ v, int v0, int v1, V3& lo, 
 constexpr int kMaxLinks = 32;
 // triangle boxes staged in shared memory when an env fits (hand at probe 0,
 // object); larger envs test boxes from the vertices in global memory
-constexpr int kStageHT = 64, kStageOT = 448;
+constexpr int kStageHT = 128, kStageOT = 448;  // 128: the three-finger hand has 84 triangles
 
 // ref repair.py:103-113 for one env per CTA; out[e] = first clear probe or n_probe.
 // Items of one probe, crossing pairs first (cheap, box-filtered, and the

@@ -50,9 +50,16 @@ def batch_fk(gripper: Gripper, poses, joints):
                 mo = np.broadcast_to(np.eye(4), (E, 4, 4)).copy()
                 if j.type == "prismatic":
                     mo[:, :3, 3] = j.axis[None, :] * joints[:, jidx[j.name]][:, None]
-                else:
-                    for e in range(E):
-                        mo[e, :3, :3] = _rodrigues(j.axis, joints[e, jidx[j.name]])
+                else:  # Rodrigues for all E angles at once (= _rodrigues per env)
+                    a = np.asarray(j.axis, dtype=np.float64)
+                    k = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]])
+                    th = joints[:, jidx[j.name]]
+                    # scalar sin/cos per angle, as ref gripper.py:38 evaluates them
+                    # (numpy's vectorized loops may round differently)
+                    sn = np.array([np.sin(t) for t in th])
+                    cs = np.array([np.cos(t) for t in th])
+                    mo[:, :3, :3] = (np.eye(3)[None] + sn[:, None, None] * k[None]
+                                     + (1 - cs)[:, None, None] * (k @ k)[None])
                 t = t @ mo
             out[j.child] = t
             todo.append(j.child)

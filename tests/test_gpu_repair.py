@@ -217,3 +217,33 @@ def test_repair_soft_object():
     sv, st = _world_mesh(cube)
     for b in g.bodies():
         assert count_mesh_intersections(b.world_vertices(), b.mesh.triangles, sv, st) == 0
+
+
+def test_dexterous_hand_repair_matches_reference(golden):
+    """Config 4 with the three-finger revolute hand (data/dex_hand.urdf, 7
+    links, 84 triangles — past round 1's 64-triangle staging cap): cleared
+    flags and retraction distances bit-identical to the unmodified
+    reference's repair loop, penetration-before within 1e-12."""
+    from paper_2311_05945_b200 import workloads as WL
+    from paper_2311_05945_b200.robot import Gripper
+    from paper_2311_05945_b200.robot.proximity import max_penetration_batch
+    from paper_2311_05945_b200.robot.repair import _hand_points, retract_batch
+
+    z = golden("repair_geom_hand.npz")
+    n = int(z["n"])
+    model = WL.hand_model()
+    poses = [z[f"s{k}_pose"] for k in range(n)]
+    meshes = [(z[f"s{k}_v"], z[f"s{k}_t"]) for k in range(n)]
+    gs = [Gripper(model) for _ in range(n)]
+    assert sum(len(b.mesh.triangles) for b in gs[0].bodies()) == 84
+    opened = [g.clamp_joints(z[f"s{k}_q"] - 0.01) for k, g in enumerate(gs)]
+    cleared, r, _ = retract_batch(gs, poses, opened, meshes)
+    np.testing.assert_array_equal(cleared, z["cleared"])
+    np.testing.assert_array_equal(r, z["retraction"])
+    pts = []
+    for k in range(n):
+        g = Gripper(model)
+        g.place(z[f"s{k}_pose"], z[f"s{k}_q"])
+        pts.append(_hand_points(g))
+    got = max_penetration_batch(pts, meshes)
+    np.testing.assert_allclose(got, z["pen_before"], rtol=1e-12, atol=1e-15)
