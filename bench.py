@@ -799,8 +799,12 @@ def repair_main(args, ws, rank, lr, K, W):
     full = None
     if os.environ.get("BENCH_REPAIR_FULL", "1") != "0":
         t0 = time.perf_counter()
-        res = repair_batch(model, objs, poses, joints)
+        try:
+            res = repair_batch(model, objs, poses, joints)
+        except Exception as ex:  # reported in the line, not fatal for the retraction metric
+            res, full = None, {"error": f"{type(ex).__name__}: {ex}"}
         full_s = time.perf_counter() - t0
+    if os.environ.get("BENCH_REPAIR_FULL", "1") != "0" and res is not None:
         full = {"seconds": full_s, "grasps_per_s": E / full_s,
                 "cleared": int(sum(x.cleared for x in res)),
                 "max_penetration_after_m": max(x.penetration_after_m for x in res),

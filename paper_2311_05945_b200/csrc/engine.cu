@@ -185,6 +185,54 @@ __global__ void k_status(int n_env, const int* newton, const int* ls, const int*
     out[2] = *ov1 | *ov2;
   }
 }
+// Device-driven Newton loop control (the body of the loop graph's WHILE
+// node, after the SWITCH that ran one Newton iteration (mode 0) or one
+// line-search round (mode 1)). Mirrors the host loop of newton_solve: line
+// search rounds while any env is still backtracking and fewer than
+// max_halvings+1 trials were made, then the next iteration unless no env is
+// active, the iteration cap is reached, the active count fits the per-env
+// tail hand-off, or a candidate store overflowed (the host then replays).
+// ctl: [0] iterations run, [1] line-search trials of this iteration,
+// [2] line-search rounds (stats), [3] active envs at exit, [4] overflow,
+// [5] mode of the body that just ran (set here for the next one; 0 at launch)
+__global__ void k_loop_ctl(int n_env, const int* newton, const int* ls, const int* ov1, const int* ov2, int* ctl,
+                           int max_iters, int max_halvings, int ls_m, int tail, cudaGraphConditionalHandle h_loop,
+                           cudaGraphConditionalHandle h_mode) {
+  __shared__ int a, b;
+  if (threadIdx.x == 0) a = b = 0;
+  __syncthreads();
+  int ca = 0, cb = 0;
+  for (int e = threadIdx.x; e < n_env; e += blockDim.x) {
+    ca += newton[e] != 0;
+    cb += ls[e] != 0;
+  }
+  atomicAdd(&a, ca);
+  atomicAdd(&b, cb);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int ov = *ov1 | *ov2;
+  // the trials of the mode that just ran
+  if (ctl[5] == 0) {
+    ctl[0] += 1;
+    ctl[1] = 1;
+  } else {
+    ctl[1] += ls_m;
+  }
+  ctl[2] += 1;
+  ctl[3] = a;
+  ctl[4] = ov;
+  unsigned loop = 1, mode = 0;
+  if (ov) {
+    loop = 0;
+  } else if (b && ctl[1] < max_halvings + 1) {
+    mode = 1;
+  } else if (a == 0 || ctl[0] >= max_iters || (tail > 0 && a <= tail)) {
+    loop = 0;
+  }
+  ctl[5] = (int)mode;
+  cudaGraphSetConditional(h_mode, mode);
+  cudaGraphSetConditional(h_loop, loop);
+}
 // dxw = xw(x + p) - xw(x); sweep boxes over [xw, xw + dxw] (ref broadphase.py:206)
 __global__ void k_sweep_box2(int n, const double* xwt, const double* xw, double* dxw, double* lo, double* hi) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -733,7 +781,9 @@ struct ipc_world {
       CK(cudaMemcpy(np.data(), cs->c.need_pt, 4 * n_env, cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(ne.data(), cs->c.need_ee, 4 * n_env, cudaMemcpyDeviceToHost));
       for (int e = 0; e < n_env; ++e) {
-        if (np[e] > cs->pt_cap[e] || ne[e] > cs->ee_cap[e]) hit[e] = 1;
+        // overflowed, or within 25 % of overflowing: grow now rather than in a
+        // later replay of the same step
+        if (4 * (long long)np[e] > 3 * cs->pt_cap[e] || 4 * (long long)ne[e] > 3 * cs->ee_cap[e]) hit[e] = 1;
         want_pt[e] = std::max(want_pt[e], (long long)np[e]);
         want_ee[e] = std::max(want_ee[e], (long long)ne[e]);
         if (getenv("IPC_DEBUG_OVERFLOW") && (np[e] > cs->pt_cap[e] || ne[e] > cs->ee_cap[e]))
@@ -767,6 +817,8 @@ struct ipc_world {
   }
 
   void drop_graphs() {
+    if (loop_exec) cudaGraphExecDestroy(loop_exec);
+    loop_exec = nullptr;
     for (Graph* g : {&g_iter, &g_ls}) {
       if (g->exec) cudaGraphExecDestroy(g->exec);
       g->exec = nullptr;
@@ -846,10 +898,109 @@ struct ipc_world {
     return Status{h_status[0], h_status[1], h_status[2]};
   }
 
+  // ---- device-driven Newton loop: one graph launch per Newton solve ------
+  // WHILE(h_loop) { SWITCH(h_mode) { 0: Newton iteration (g_iter's
+  // sequence), 1: line-search round (g_ls's) }; k_loop_ctl } — no host round
+  // trip per iteration or per line-search round. Used when no kernel of the
+  // loop is being event-timed (conditional bodies take no event nodes).
+  cudaGraphExec_t loop_exec = nullptr;
+  ipc_step_config loop_cfg{};
+  int loop_tail = -1;
+  int* d_loopctl = nullptr;
+  bool use_loop_graph = getenv("IPC_LOOP_GRAPH") == nullptr || getenv("IPC_LOOP_GRAPH")[0] != '0';  // 0: host loop
+
+  void build_loop_graph(const ipc_step_config& cfg, int tail) {
+    if (loop_exec) cudaGraphExecDestroy(loop_exec);
+    loop_exec = nullptr;
+    if (!d_loopctl) d_loopctl = pool.alloc<int>(8);
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_loop, h_mode;
+    CK(cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = h_loop;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CK(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    CK(cudaGraphConditionalHandleCreate(&h_mode, body, 0, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams sp = {};
+    sp.type = cudaGraphNodeTypeConditional;
+    sp.conditional.handle = h_mode;
+    sp.conditional.type = cudaGraphCondTypeSwitch;
+    sp.conditional.size = 2;
+    cudaGraphNode_t snode;
+    CK(cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
+    cudaGraph_t b_iter = sp.conditional.phGraph_out[0], b_ls = sp.conditional.phGraph_out[1];
+    auto capture_into = [&](cudaGraph_t target, const cudaGraphNode_t* deps, size_t ndep, auto fn) {
+      long long l0 = prof.launches;
+      prof.capturing = true;
+      CK(cudaStreamBeginCaptureToGraph(st, target, deps, nullptr, ndep, cudaStreamCaptureModeThreadLocal));
+      fn();
+      cudaGraph_t out;
+      CK(cudaStreamEndCapture(st, &out));
+      prof.capturing = false;
+      prof.launches = l0;
+    };
+    capture_into(b_iter, nullptr, 0, [&] {
+      seq_head(cfg);
+      seq_ccd(cfg);
+      seq_ls(cfg);
+    });
+    capture_into(b_ls, nullptr, 0, [&] { seq_ls_multi(cfg); });
+    // the control kernel follows the SWITCH in the body
+    capture_into(body, &snode, 1, [&] {
+      k_loop_ctl<<<1, 1024, 0, st>>>(n_env, S.newton_active, S.ls_active, dcd.c.overflow, sweep.c.overflow,
+                                     d_loopctl, cfg.max_newton_iters, cfg.max_line_search_halvings, LS_M, tail,
+                                     h_loop, h_mode);
+      CK(cudaPeekAtLastError());
+    });
+    CK(cudaGraphInstantiate(&loop_exec, g, 0));
+    CK(cudaGraphDestroy(g));
+    loop_cfg = cfg;
+    loop_tail = tail;
+  }
+
+  bool loop_graph_usable() const {
+    if (!use_loop_graph || sparse || !use_graphs) return false;
+    // conditional bodies take no event nodes: only when no loop kernel is timed
+    const unsigned loop_kernels = ~((1u << K_FUSED) | (1u << K_SENSE));
+    return !(prof.on && (prof.mask & loop_kernels));
+  }
+
   void newton_solve(const ipc_step_config& cfg) {
     IPC_LAUNCH(K_MISC, st, k_newton_begin, nblk(n_env, 128), 128, 0, n_env, S, al_flag);
     bool graphs = use_graphs && !sparse;
     if (graphs) ensure_graphs(cfg);
+    if (graphs && loop_graph_usable()) {
+      // the loop hands off to the per-env tail kernel only when it can run
+      int tail = (tail_envs > 0 && fused_setup()) ? tail_envs : 0;
+      if (!loop_exec || !same_cfg(cfg, loop_cfg) || cfg.max_newton_iters != loop_cfg.max_newton_iters ||
+          loop_tail != tail)
+        build_loop_graph(cfg, tail);
+      CK(cudaMemsetAsync(d_loopctl, 0, 8 * sizeof(int), st));
+      CK(cudaGraphLaunch(loop_exec, st));
+      int ctl[5];
+      CK(cudaMemcpyAsync(h_status, d_loopctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_status + 4, d_loopctl + 4, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      ++stat_syncs;
+      for (int i = 0; i < 5; ++i) ctl[i] = h_status[i];
+      stat_iters += ctl[0];
+      stat_ls_rounds += ctl[2];
+      if (ctl[4]) throw OverflowRetry();
+      int active = ctl[3], it = ctl[0] - 1;
+      if (active > 0 && tail > 0 && active <= tail && it + 1 < cfg.max_newton_iters) {
+        CK(cudaMemsetAsync(fq, 0, sizeof(int), st));
+        FusedArgs A = fused_args(cfg);
+        IPC_LAUNCH(K_FUSED, st, k_env_newton_rest, std::min(active, fused_blocks), 256, fused_smem, A, it + 1);
+        status();
+      }
+      IPC_LAUNCH(K_MISC, st, k_mark_unconverged, nblk(n_env, 128), 128, 0, n_env, S);
+      return;
+    }
     for (int it = 0; it < cfg.max_newton_iters; ++it) {
       if (graphs) {
         run(g_iter);
@@ -1389,7 +1540,7 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     w->slot_force = P.alloc<double>(3 * (size_t)d->n_slot);
     w->d_status = P.alloc<int>(4);
     w->e_multi = P.alloc<double>((size_t)ipc_world::LS_M * ne);
-    CK(cudaMallocHost(&w->h_status, 4 * sizeof(int)));
+    CK(cudaMallocHost(&w->h_status, 8 * sizeof(int)));
     w->d_targets = P.alloc<double>(12 * (size_t)d->n_cons);
     w->h_env_slot.assign(d->env_slot, d->env_slot + ne + 1);
     w->h_env_dof.assign(d->env_dof, d->env_dof + ne + 1);
@@ -1689,7 +1840,7 @@ static int step_impl(ipc_world* w, const ipc_step_config* cfg, const double* tar
         step_core(w, cfg, targets, sched_k, enable, rep);
         break;
       } catch (const OverflowRetry&) {
-        if (attempt >= 24) throw std::runtime_error("candidate capacity overflow persists");
+        if (attempt >= 64) throw std::runtime_error("candidate capacity overflow persists");
         // replay the step from x_prev with larger candidate capacities
         CK(cudaMemcpyAsync(w->W.x, w->W.x_prev, sizeof(double) * w->W.n_dof, cudaMemcpyDeviceToDevice, w->st));
         w->grow_overflowed();
@@ -1725,7 +1876,7 @@ int ipc_world_run_scheduled(ipc_world* w, const ipc_step_config* cfg, int k0, in
       CK(cudaMemcpyAsync(w->h_status + 1, w->sweep.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, w->st));
       CK(cudaStreamSynchronize(w->st));
       if (!w->h_status[0] && !w->h_status[1]) break;
-      if (attempt >= 24) throw std::runtime_error("candidate capacity overflow persists");
+      if (attempt >= 64) throw std::runtime_error("candidate capacity overflow persists");
       // replay the whole range from its start with larger capacities
       CK(cudaMemcpyAsync(W.x, x0, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, w->st));
       CK(cudaMemcpyAsync(W.v, w->v_save, sizeof(double) * W.n_dof, cudaMemcpyDeviceToDevice, w->st));
