@@ -24,6 +24,7 @@ env index, ref batch.py:39-57) to rank 0.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -527,7 +528,8 @@ def main():
         free["n"] = int(gather_timing(0.0, float(free["n"]), device=dev)[1])
     results = {"envs": int(len(rows)), "ordered": bool(np.array_equal(rows[:, 0], np.arange(n_total))),
                "newton_iters_timed": int(rows[:, 1].sum()),
-               "rank_ms": local_ms, "value_state_equals_e2e_state": value_eq_e2e}
+               "rank_ms": local_ms, "value_state_equals_e2e_state": value_eq_e2e,
+               "state_sha16": hashlib.sha256(np.ascontiguousarray(x_value).tobytes()).hexdigest()[:16]}
 
     # asynchronous variant (reported beside `value`, not as it)
     async_line = None
@@ -560,7 +562,8 @@ def main():
             "gpu_launches": launches, "syncs_per_step": syncs_per_step, "clocks": clk.summary(),
             "intersection_free": {"all_env_steps": bool(free["all"]), "bad": free["bad"],
                                   "checked": free["n"]},
-            "results": results, "async": async_line}
+            "results": results, "async": async_line,
+            "step_ms": [round(t, 3) for t in t_ms]}
     if rank == 0 and ws == 1 and not args.no_closed_loop:
         line["closed_loop"] = closed_loop_arm(args.envs, args.seed,
                                               0 if args.no_cpu else args.closed_loop_sample, _cores(), lr)

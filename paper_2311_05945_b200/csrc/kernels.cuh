@@ -861,55 +861,68 @@ __device__ __forceinline__ void pair_core_out(const int (&sl)[NS], double* gh, d
   helm_out<NS>(sl, gh, M, g12, hp);
 }
 
-// H = κ(b'' ∇s∇sᵀ + b' ∇²s), g = κ b' ∇s
-template <int NS, int NV>
-__device__ __forceinline__ void pair_plain(const VarSet<NV>& V, const int (&sl)[NS], double kappa, double shat,
-                                           double* g12, double* hp) {
-  constexpr int NB = NS - 1, R = 3 * NB;
+// Every region of every pair kind reduces to one core: up to three difference
+// vars over the stencil's four slots (p, q: stencil slot indices; unused vars
+// have zero derivatives), projected in the 9-dim Helmert space of all four
+// slots. A region's stencil Hessian annihilates translations of the whole
+// stencil (inactive slots have zero rows), so Q4 (Q4ᵀHQ4)⁺ Q4ᵀ is the same
+// projection (ref spd.py:6) as in the region's own smaller Helmert space —
+// and one psd_project<9> per kernel keeps the code small (instruction-cache
+// bound otherwise).
+template <int NV>
+__device__ __forceinline__ void var_pad(const VarSet<NV>& A, const int* sl, VarSet<3>& V) {
+  V.s = A.s;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    V.p[i] = i < NV ? sl[A.p[i < NV ? i : 0]] : 0;
+    V.q[i] = i < NV ? sl[A.q[i < NV ? i : 0]] : 0;
+    V.gv[i] = i < NV ? A.gv[i < NV ? i : 0] : V3{0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) V.hv[i][j] = (i < NV && j < NV) ? A.hv[i < NV ? i : 0][j < NV ? j : 0] : m3_zero();
+  }
+}
+
+// H = κ(b'' ∇s∇sᵀ + b' ∇²s), g = κ b' ∇s (core, upper triangle of M)
+__device__ __forceinline__ void pair_plain_core(const VarSet<3>& V, double kappa, double shat, double (&gh)[9],
+                                                double (&M)[81]) {
   double b, db, d2b;
   barrier_d(V.s, shat, &b, &db, &d2b);
-  double beta[NV][NB];
-  helm_beta<NV, NB>(V.p, V.q, beta);
-  double gh[R], M[R * R];
-  helm_grad<NV, NB>(beta, V.gv, gh);
+  double beta[3][3];
+  helm_beta<3, 3>(V.p, V.q, beta);
+  helm_grad<3, 3>(beta, V.gv, gh);
 #pragma unroll
-  for (int i = 0; i < R * R; ++i) M[i] = 0.0;
-  helm_hess_acc<NV, NB>(beta, V.hv, kappa * db, M);
-  helm_outer_acc<R>(gh, gh, kappa * d2b, false, M);
+  for (int i = 0; i < 81; ++i) M[i] = 0.0;
+  helm_hess_acc<3, 3>(beta, V.hv, kappa * db, M);
+  helm_outer_acc<9>(gh, gh, kappa * d2b, false, M);
 #pragma unroll
-  for (int i = 0; i < R; ++i) gh[i] *= kappa * db;
-  pair_core_out<NS>(sl, gh, M, g12, hp);
+  for (int i = 0; i < 9; ++i) gh[i] *= kappa * db;
 }
 
 // mollified EE (ref contact.py:166-203, :286-312), all 4 slots: the s part in its
 // region vars (stencil slot indices) and the mollifier c = |u x v|²
-template <int NV>
-__device__ __forceinline__ void ee_mollified(const VarSet<NV>& V, const V3* X, double t, double eps, double kappa,
-                                             double shat, double* g12, double* hp) {
+__device__ __forceinline__ void ee_mollified_core(const VarSet<3>& V, const V3* X, double t, double eps, double kappa,
+                                                  double shat, double (&gh)[9], double (&M)[81]) {
   double b, db, d2b;
   barrier_d(V.s, shat, &b, &db, &d2b);
   double em = t * (2.0 - t), de = (2.0 - 2.0 * t) / eps, d2e = -2.0 / (eps * eps);
-  double bs[NV][3], bc[2][3];
-  helm_beta<NV, 3>(V.p, V.q, bs);
+  double bs[3][3], bc[2][3];
+  helm_beta<3, 3>(V.p, V.q, bs);
   VarSet<2> Cv;
   vs_cross2(X[1] - X[0], X[3] - X[2], Cv.gv, Cv.hv);
   Cv.p[0] = 1; Cv.q[0] = 0; Cv.p[1] = 3; Cv.q[1] = 2;
   helm_beta<2, 3>(Cv.p, Cv.q, bc);
-  double gs[9], gc[9], M[81];
-  helm_grad<NV, 3>(bs, V.gv, gs);
+  double gs[9], gc[9];
+  helm_grad<3, 3>(bs, V.gv, gs);
   helm_grad<2, 3>(bc, Cv.gv, gc);
 #pragma unroll
   for (int i = 0; i < 81; ++i) M[i] = 0.0;
-  helm_hess_acc<NV, 3>(bs, V.hv, kappa * (em * db), M);
+  helm_hess_acc<3, 3>(bs, V.hv, kappa * (em * db), M);
   helm_hess_acc<2, 3>(bc, Cv.hv, kappa * (de * b), M);
   helm_outer_acc<9>(gs, gs, kappa * (em * d2b), false, M);
   helm_outer_acc<9>(gc, gc, kappa * (d2e * b), false, M);
   helm_outer_acc<9>(gc, gs, kappa * (de * db), true, M);
-  double gh[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) gh[i] = kappa * ((de * b) * gc[i] + (em * db) * gs[i]);
-  const int sl[4] = {0, 1, 2, 3};
-  pair_core_out<4>(sl, gh, M, g12, hp);
 }
 
 __device__ __forceinline__ VarSet<1> region_pp(const V3* X, int i, int j) {
@@ -972,70 +985,55 @@ __device__ __forceinline__ void pair_hess_item(const World& W, const double* __r
     double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
     double* g = g12 + 12 * k;
     double* h = hp + PK * k;
+    // the region's vars over stencil slots
+    VarSet<3> V;
+    bool moll = false;
+    double t = 0.0, eps = 0.0;
     if (kind == 0) {
       int region = pt_region(X[0], X[1], X[2], X[3]);
-      if (region < 3) {  // point-point: local slots (0, t), var x0 - xt
-        int t = region + 1;
-        VarSet<1> V;
-        V.s = vs_pp(X[0] - X[t], V.gv, V.hv);
-        V.p[0] = 0; V.q[0] = 1;
-        const int sl[2] = {0, t};
-        pair_plain<2, 1>(V, sl, kappa, shat, g, h);
-      } else if (region < 6) {  // point-edge: local slots (0, a, b)
+      if (region < 3) {  // point-point: var x0 - xt
+        int tt = region + 1;
+        VarSet<1> A;
+        A.s = vs_pp(X[0] - X[tt], A.gv, A.hv);
+        A.p[0] = 0; A.q[0] = 1;
+        const int sl[2] = {0, tt};
+        var_pad<1>(A, sl, V);
+      } else if (region < 6) {  // point-edge (a, bb)
         int a = region == 3 ? 1 : (region == 4 ? 2 : 3);
         int bb = region == 3 ? 2 : (region == 4 ? 3 : 1);
-        VarSet<2> V;
-        V.s = vs_pl(X[0] - X[a], X[bb] - X[a], V.gv, V.hv);
-        V.p[0] = 0; V.q[0] = 1; V.p[1] = 2; V.q[1] = 1;
+        VarSet<2> A;
+        A.s = vs_pl(X[0] - X[a], X[bb] - X[a], A.gv, A.hv);
+        A.p[0] = 0; A.q[0] = 1; A.p[1] = 2; A.q[1] = 1;
         const int sl[3] = {0, a, bb};
-        pair_plain<3, 2>(V, sl, kappa, shat, g, h);
+        var_pad<2>(A, sl, V);
       } else {  // point-face: w = x0 - x1, u = x2 - x1, v = x3 - x1
-        VarSet<3> V;
         V.s = vs_triple(X[0] - X[1], X[2] - X[1], X[3] - X[1], V.gv, V.hv);
         V.p[0] = 0; V.q[0] = 1; V.p[1] = 2; V.q[1] = 1; V.p[2] = 3; V.q[2] = 1;
-        const int sl[4] = {0, 1, 2, 3};
-        pair_plain<4, 3>(V, sl, kappa, shat, g, h);
       }
     } else {
       int region = ee_region(X[0], X[1], X[2], X[3], nullptr);
-      double eps = 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y];
-      double t = cross2(X[1] - X[0], X[3] - X[2]) / eps;
+      eps = 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y];
+      t = cross2(X[1] - X[0], X[3] - X[2]) / eps;
+      moll = t < 1.0;
       // region slots: PP (i, j) / point i to line (j, k) / line-line
       int ra = region / 3, rb = region % 3;
-      if (t < 1.0) {
-        if (ra < 2 && rb < 2) {
-          ee_mollified<1>(region_pp(X, ra, 2 + rb), X, t, eps, kappa, shat, g, h);
-        } else if (ra < 2) {
-          ee_mollified<2>(region_pl(X, ra, 2, 3), X, t, eps, kappa, shat, g, h);
-        } else if (rb < 2) {
-          ee_mollified<2>(region_pl(X, 2 + rb, 0, 1), X, t, eps, kappa, shat, g, h);
-        } else {
-          VarSet<3> V;
-          V.s = vs_triple(X[2] - X[0], X[1] - X[0], X[3] - X[2], V.gv, V.hv);
-          V.p[0] = 2; V.q[0] = 0; V.p[1] = 1; V.q[1] = 0; V.p[2] = 3; V.q[2] = 2;
-          ee_mollified<3>(V, X, t, eps, kappa, shat, g, h);
-        }
-      } else if (ra < 2 && rb < 2) {
-        VarSet<1> V;
-        V.s = vs_pp(X[ra] - X[2 + rb], V.gv, V.hv);
-        V.p[0] = 0; V.q[0] = 1;
-        const int sl[2] = {ra, 2 + rb};
-        pair_plain<2, 1>(V, sl, kappa, shat, g, h);
-      } else if (ra < 2 || rb < 2) {
-        int pa = ra < 2 ? ra : 2 + rb, l0 = ra < 2 ? 2 : 0;
-        VarSet<2> V;
-        V.s = vs_pl(X[pa] - X[l0], X[l0 + 1] - X[l0], V.gv, V.hv);
-        V.p[0] = 0; V.q[0] = 1; V.p[1] = 2; V.q[1] = 1;
-        const int sl[3] = {pa, l0, l0 + 1};
-        pair_plain<3, 2>(V, sl, kappa, shat, g, h);
+      const int id[4] = {0, 1, 2, 3};
+      if (ra < 2 && rb < 2) {
+        var_pad<1>(region_pp(X, ra, 2 + rb), id, V);
+      } else if (ra < 2) {
+        var_pad<2>(region_pl(X, ra, 2, 3), id, V);
+      } else if (rb < 2) {
+        var_pad<2>(region_pl(X, 2 + rb, 0, 1), id, V);
       } else {
-        VarSet<3> V;
         V.s = vs_triple(X[2] - X[0], X[1] - X[0], X[3] - X[2], V.gv, V.hv);
         V.p[0] = 2; V.q[0] = 0; V.p[1] = 1; V.q[1] = 0; V.p[2] = 3; V.q[2] = 2;
-        const int sl[4] = {0, 1, 2, 3};
-        pair_plain<4, 3>(V, sl, kappa, shat, g, h);
       }
     }
+    double gh[9], M[81];
+    if (kind == 1 && moll) ee_mollified_core(V, X, t, eps, kappa, shat, gh, M);
+    else pair_plain_core(V, kappa, shat, gh, M);
+    const int sl[4] = {0, 1, 2, 3};
+    pair_core_out<4>(sl, gh, M, g, h);
     active[k] = (unsigned char)0xF;
 }
 

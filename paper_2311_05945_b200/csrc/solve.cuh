@@ -282,65 +282,86 @@ constexpr int DENSE_REG_N = 64;   // register-resident factorization up to this 
 __host__ __device__ inline int dense_smem_doubles(int n);
 
 // ---------------------------------------------------------------------------
-// Record-parallel dense assembly. Every stencil (tet, active PT / EE pair,
-// ground barrier, friction lag, ground friction lag) is a *record* of ≤4
-// slots with a slot-space gradient (3·ns) and Hessian (packed 12x12). Records
-// are staged REC_CHUNK at a time in shared memory; then every entry (r, c)
-// of the lower triangle and every gradient entry has ONE owner thread that
-// adds the lifted contribution of each staged record in record order
-// (ref contact.py:346 lifting through J(x0), slots of one body merged), so
-// the sums are deterministic and no per-record barrier is needed.
+// Group-tile dense assembly. Every stencil (tet, active PT / EE pair, ground
+// barrier, friction lag, ground friction lag) is a *record* of ≤4 slots with a
+// slot-space gradient (3·ns) and Hessian (12x12). The env's DoFs fall into
+// *groups* (a soft vertex: 3 DoFs, an affine body: 12), numbered 0..G-1 in DoF
+// order; a record touches the groups of its slots (bit mask rm). Records are
+// staged REC_CHUNK at a time in shared memory; for every group pair (A ≥ B)
+// one warp ballot gives the chunk's records touching it (pm). The lower
+// triangle is cut into *tiles* — one row × three consecutive DoFs of one group
+// (a translation triple, or one row of A) — each owned by one thread, which
+// adds the lifted contribution of exactly the records in pm of its group
+// pair, in record order (ref contact.py:346 lifting through J(x0), slots of
+// one body merged): deterministic sums and no per-record barrier, and the
+// arithmetic of every entry is Σ_a w_a (Σ_b w_b Hs[ia][ib]) per record, the
+// same operation order as the entry-owner assembly it replaces.
 // ---------------------------------------------------------------------------
 constexpr int REC_CHUNK = 32;
 struct RecStage {  // carved from dynamic shared memory (rec_stage_doubles)
-  double* h;       // [REC_CHUNK][78] packed slot-space Hessian
+  double* h;       // [REC_CHUNK][144] slot-space Hessian, unpacked
   double* g;       // [REC_CHUNK][12]
   double* rest;    // [REC_CHUNK][12] slot lever arms (affine slots)
-  int* key;        // [REC_CHUNK][4] local DoF offset of the slot's group (-1: unused)
-  int* aff;        // [REC_CHUNK][4]
-  int* ns;         // [REC_CHUNK]
+  unsigned long long* rm;  // [REC_CHUNK] groups touched
+  int* grp;        // [REC_CHUNK][4] group of the slot (-1: unused)
 };
-__host__ __device__ constexpr int rec_stage_doubles() { return REC_CHUNK * (78 + 12 + 12) + (REC_CHUNK * 9 + 1) / 2 + 2; }
-__host__ __device__ inline int dense_smem_doubles(int n) { return n * n + 2 * n + rec_stage_doubles() + (n + 1) / 2 + 1; }
+__host__ __device__ constexpr int rec_stage_doubles() { return REC_CHUNK * (144 + 12 + 12 + 1 + 2); }
+// per-DoF group key / ordinal (2n ints) and the chunk's pair masks (one u32 per
+// group pair, G ≤ n/3 groups)
+__host__ __device__ inline int dense_pairs(int n) { return (n / 3) * (n / 3 + 1) / 2; }
+__host__ __device__ inline int dense_smem_doubles(int n) {
+  return n * n + 2 * n + rec_stage_doubles() + n + (dense_pairs(n) + 1) / 2 + 4;
+}
 __device__ __forceinline__ RecStage rec_stage(double* base) {
   RecStage R;
   R.h = base;
-  R.g = R.h + REC_CHUNK * 78;
+  R.g = R.h + REC_CHUNK * 144;
   R.rest = R.g + REC_CHUNK * 12;
-  R.key = reinterpret_cast<int*>(R.rest + REC_CHUNK * 12);
-  R.aff = R.key + REC_CHUNK * 4;
-  R.ns = R.aff + REC_CHUNK * 4;
+  R.rm = reinterpret_cast<unsigned long long*>(R.rest + REC_CHUNK * 12);
+  R.grp = reinterpret_cast<int*>(R.rm + REC_CHUNK);
   return R;
-}
-
-// weight / slot-space row of lifted row R of a group for slot a
-__device__ __forceinline__ void lift_row(const RecStage& R, int k, int a, int Rr, int* ia, double* wa) {
-  if (!R.aff[4 * k + a] || Rr < 3) {
-    *ia = 3 * a + Rr;
-    *wa = 1.0;
-  } else {
-    *ia = 3 * a + (Rr - 3) / 3;
-    *wa = R.rest[12 * k + 3 * a + (Rr - 3) % 3];
-  }
 }
 
 // record types of the virtual index space, in assembly order
 enum { REC_TET, REC_PT, REC_EE, REC_GND, REC_FR, REC_FRG };
 
+// lower-triangle tile T -> (row r, first column c0 = 3 t3): rows come in
+// triples; row triple R3 holds 3 (R3 + 1) tiles
+__device__ __forceinline__ void tile_rc(int T, int* r, int* c0) {
+  int R3 = (int)((sqrtf(8.0f * (float)T / 3.0f + 1.0f) - 1.0f) * 0.5f);
+  while (3 * (R3 + 1) * (R3 + 2) / 2 <= T) ++R3;
+  while (3 * R3 * (R3 + 1) / 2 > T) --R3;
+  int rem = T - 3 * R3 * (R3 + 1) / 2;
+  *r = 3 * R3 + rem / (R3 + 1);
+  *c0 = 3 * (rem % (R3 + 1));
+}
+
+// lifted row index of DoF offset R inside its group: coordinate i, lever column
+// j (0: translation, 1..3: lever arm component j-1)
+__device__ __forceinline__ void lift_ij(int R, int* i, int* j) {
+  *i = R < 3 ? R : (R - 3) / 3;
+  *j = R < 3 ? 0 : 1 + (R - 3) % 3;
+}
+__device__ __forceinline__ double lift_w(const RecStage& R, int k, int a, int j) {
+  return j == 0 ? 1.0 : R.rest[12 * k + 3 * a + j - 1];
+}
+
 static __device__ void assemble_records(const World& W, const Derivs& D, const Cands& C, const Lags& L, int e, int d0,
-                                 int n, double* H, double* g, const int* dkey, double* stage_mem) {
+                                 int n, double* H, double* g, const int* dkey, const int* gi, unsigned* pm,
+                                 double* stage_mem) {
   __shared__ int alist[DENSE_THREADS];
   __shared__ int wtot[DENSE_THREADS / 32];
   __shared__ int atot;
   RecStage R = rec_stage(stage_mem);
-  int tid = threadIdx.x;
+  int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   int t0 = W.env_tet[e], ntet = W.env_tet[e + 1] - t0;
   int npt = C.n_pt[e], nee = C.n_ee[e], ngnd = C.n_gnd[e], nfr = L.n[e], nfrg = L.g_n[e];
   long long pt0 = C.pt_off[e], ee0 = C.ee_off[e], fr0 = L.off[e];
   int gnd0 = C.gnd_off[e], frg0 = W.env_slot[e];
   int lim[6] = {ntet, npt, nee, ngnd, nfr, nfrg};
   int total = ntet + npt + nee + ngnd + nfr + nfrg;
-  int nlow = n * (n + 1) / 2;
+  int G = gi[n - 1] + 1, npairs = G * (G + 1) / 2;
+  int ntile = 3 * (n / 3) * (n / 3 + 1) / 2;
   for (int v0 = 0; v0 < total; v0 += DENSE_THREADS) {
     // ordered compaction of the contributing records of this window
     int v = v0 + tid;
@@ -353,7 +374,6 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
       else if (t == REC_GND) on = D.gnd_hyy[gnd0 + j] != 0.0 || D.gnd_gy[gnd0 + j] != 0.0;
       else on = true;
     }
-    int lane = tid & 31, wid = tid >> 5;
     unsigned m = __ballot_sync(0xffffffffu, on);
     if (lane == 0) wtot[wid] = __popc(m);
     __syncthreads();
@@ -377,12 +397,14 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
         int k = tid, j = alist[k0 + k], t = 0;
         while (j >= lim[t]) j -= lim[t++];
         int sl[4] = {-1, -1, -1, -1}, ns = 4;
+        unsigned long long rm = 0ull;
         if (t == REC_TET) {
           int4 td = W.tet_dof[t0 + j];
           int dv[4] = {td.x, td.y, td.z, td.w};
           for (int a = 0; a < 4; ++a) {
-            R.key[4 * k + a] = dv[a] - d0;
-            R.aff[4 * k + a] = 0;
+            int gg = gi[dv[a] - d0];
+            R.grp[4 * k + a] = gg;
+            rm |= 1ull << gg;
           }
         } else {
           if (t == REC_PT) {
@@ -406,18 +428,18 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
           for (int a = 0; a < 4; ++a) {
             if (a < ns) {
               int sa = sl[a];
-              R.key[4 * k + a] = W.slot_dof[sa] - d0;
-              R.aff[4 * k + a] = W.slot_aff[sa];
+              int gg = gi[W.slot_dof[sa] - d0];
+              R.grp[4 * k + a] = gg;
+              rm |= 1ull << gg;
               for (int c = 0; c < 3; ++c) R.rest[12 * k + 3 * a + c] = W.slot_rest[3 * sa + c];
             } else {
-              R.key[4 * k + a] = -1;
-              R.aff[4 * k + a] = 0;
+              R.grp[4 * k + a] = -1;
             }
           }
         }
-        R.ns[k] = ns;
+        R.rm[k] = rm;
       }
-      // stage gradients and packed Hessians (all threads, coalesced per record)
+      // stage gradients and unpacked Hessians (all threads, coalesced per record)
       for (int i = tid; i < nr * 90; i += DENSE_THREADS) {
         int k = i / 90, q = i - 90 * k;
         int j = alist[k0 + k], t = 0;
@@ -434,7 +456,12 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
             if (t == REC_GND) val = D.gnd_hyy[gnd0 + j];
             else val = D.frg_h[9 * (long long)(frg0 + j) + 3 * r + c];
           }
-          R.h[78 * k + q] = val;
+          // packed upper index q -> (r, c), mirrored into the full block
+          int r = 0, rem = q;
+          while (rem >= 12 - r) rem -= 12 - r++;
+          int c = r + rem;
+          R.h[144 * k + 12 * r + c] = val;
+          R.h[144 * k + 12 * c + r] = val;
         } else {
           int c = q - 78;
           if (t == REC_TET) val = D.tet_g[12 * (long long)(t0 + j) + c];
@@ -447,61 +474,86 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
         }
       }
       __syncthreads();
-      // owners of the lower triangle: H[r][c] += Σ_a w_a(R) Σ_b w_b(C) Hs[ia][ib]
-      for (int idx = tid; idx < nlow; idx += DENSE_THREADS) {
-        int r = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
-        while ((r + 1) * (r + 2) / 2 <= idx) ++r;
-        while (r * (r + 1) / 2 > idx) --r;
-        int c = idx - r * (r + 1) / 2;
-        int kr = dkey[r], kc = dkey[c];
-        int Rr = r - kr, Cc = c - kc;
-        double hv = H[r * n + c];
-        for (int k = 0; k < nr; ++k) {
-          int ns = R.ns[k];
-          int ma = 0, mb = 0;
-          for (int a = 0; a < ns; ++a) {
-            int ka = R.key[4 * k + a];
-            ma |= (ka == kr) << a;
-            mb |= (ka == kc) << a;
-          }
-          if (!ma || !mb) continue;
-          double acc = 0.0;
-          for (int a = 0; a < ns; ++a) {
-            if (!((ma >> a) & 1)) continue;
-            int ia;
-            double wa;
-            lift_row(R, k, a, Rr, &ia, &wa);
-            double sub = 0.0;
-            for (int b = 0; b < ns; ++b) {
-              if (!((mb >> b) & 1)) continue;
-              int ib;
-              double wb;
-              lift_row(R, k, b, Cc, &ib, &wb);
-              sub += wb * pk_get(R.h + 78 * k, ia, ib);
-            }
-            acc += wa * sub;
-          }
-          hv += acc;
+      // records of the chunk touching each group pair (A ≥ B)
+      for (int P = wid; P < npairs; P += DENSE_THREADS / 32) {
+        int A = (int)((sqrtf(8.0f * (float)P + 1.0f) - 1.0f) * 0.5f);
+        while ((A + 1) * (A + 2) / 2 <= P) ++A;
+        while (A * (A + 1) / 2 > P) --A;
+        int B = P - A * (A + 1) / 2;
+        bool t = false;
+        if (lane < nr) {
+          unsigned long long rm = R.rm[lane];
+          t = ((rm >> A) & (rm >> B) & 1ull) != 0ull;
         }
-        H[r * n + c] = hv;
+        unsigned bm = __ballot_sync(0xffffffffu, t);
+        if (lane == 0) pm[P] = bm;
       }
-      // owners of the gradient
-      for (int r = tid; r < n; r += DENSE_THREADS) {
-        int kr = dkey[r], Rr = r - kr;
-        double gv = g[r];
-        for (int k = 0; k < nr; ++k) {
-          int ns = R.ns[k];
-          double acc = 0.0;
-          bool hit = false;
-          for (int a = 0; a < ns; ++a) {
-            if (R.key[4 * k + a] != kr) continue;
-            int ia;
-            double wa;
-            lift_row(R, k, a, Rr, &ia, &wa);
-            acc += wa * R.g[12 * k + ia];
-            hit = true;
+      __syncthreads();
+      // tile owners: H[r][c0..c0+2] += Σ_a w_a(r) Σ_b w_b(c) Hs[ia][ib] per record
+      for (int T = tid; T < ntile; T += DENSE_THREADS) {
+        int r, c0;
+        tile_rc(T, &r, &c0);
+        int gr = gi[r], gc = gi[c0];
+        int iR, jR, iC, jC;
+        lift_ij(r - dkey[r], &iR, &jR);
+        lift_ij(c0 - dkey[c0], &iC, &jC);
+        unsigned bm = pm[gr * (gr + 1) / 2 + gc];
+        if (!bm) continue;
+        int ncol = min(3, r - c0 + 1);  // columns c0..c0+ncol-1 are in the lower triangle
+        double h0 = H[r * n + c0], h1 = ncol > 1 ? H[r * n + c0 + 1] : 0.0, h2 = ncol > 2 ? H[r * n + c0 + 2] : 0.0;
+        while (bm) {
+          int k = __ffs(bm) - 1;
+          bm &= bm - 1;
+          const double* hk = R.h + 144 * k;
+          double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            if (R.grp[4 * k + a] != gr) continue;
+            double wa = lift_w(R, k, a, jR);
+            const double* hrow = hk + 12 * (3 * a + iR);
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (R.grp[4 * k + b] != gc) continue;
+              if (jC == 0) {  // translation triple: columns (i = 0..2, j = 0)
+                s0 += 1.0 * hrow[3 * b];
+                s1 += 1.0 * hrow[3 * b + 1];
+                s2 += 1.0 * hrow[3 * b + 2];
+              } else {  // row iC of A: columns (i = iC, j = 1..3)
+                double hv = hrow[3 * b + iC];
+                s0 += lift_w(R, k, b, 1) * hv;
+                s1 += lift_w(R, k, b, 2) * hv;
+                s2 += lift_w(R, k, b, 3) * hv;
+              }
+            }
+            acc0 += wa * s0;
+            acc1 += wa * s1;
+            acc2 += wa * s2;
           }
-          if (hit) gv += acc;
+          h0 += acc0;
+          h1 += acc1;
+          h2 += acc2;
+        }
+        H[r * n + c0] = h0;
+        if (ncol > 1) H[r * n + c0 + 1] = h1;
+        if (ncol > 2) H[r * n + c0 + 2] = h2;
+      }
+      // owners of the gradient: records touching the DoF's group
+      for (int r = tid; r < n; r += DENSE_THREADS) {
+        int gr = gi[r], iR, jR;
+        lift_ij(r - dkey[r], &iR, &jR);
+        unsigned bm = pm[gr * (gr + 1) / 2 + gr];
+        double gv = g[r];
+        while (bm) {
+          int k = __ffs(bm) - 1;
+          bm &= bm - 1;
+          double acc = 0.0;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            if (R.grp[4 * k + a] != gr) continue;
+            acc += lift_w(R, k, a, jR) * R.g[12 * k + 3 * a + iR];
+          }
+          gv += acc;
         }
         g[r] = gv;
       }
@@ -545,6 +597,8 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
   // group key (local DoF offset of the owning soft vertex / affine body) of
   // every DoF, then the record-parallel assembly of every stencil
   int* dkey = reinterpret_cast<int*>(y + n + rec_stage_doubles());
+  int* gi = dkey + n;
+  unsigned* pm = reinterpret_cast<unsigned*>(gi + n);
   for (int v = W.env_vert[e] + tid; v < W.env_vert[e + 1]; v += blockDim.x) {
     int d = W.vert_dof[v] - d0;
     for (int c = 0; c < 3; ++c) dkey[d + c] = d;
@@ -554,7 +608,25 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
     for (int i = tid; i < 12; i += blockDim.x) dkey[o + i] = o;
   }
   __syncthreads();
-  assemble_records(W, D, C, L, e, d0, n, H, g, dkey, y + n);
+  // group ordinal of every DoF: the number of group starts (dkey[d] == d) before it
+  {
+    __shared__ unsigned sb[DENSE_MAX_N / 32 + 1];
+    int nw = (n + 31) / 32;
+    for (int w0 = 0; w0 < nw; w0 += DENSE_THREADS / 32) {
+      int d = 32 * (w0 + (tid >> 5)) + (tid & 31);
+      unsigned b = __ballot_sync(0xffffffffu, d < n && dkey[d] == d);
+      if ((tid & 31) == 0 && w0 + (tid >> 5) < nw) sb[w0 + (tid >> 5)] = b;
+    }
+    __syncthreads();
+    for (int d = tid; d < n; d += blockDim.x) {
+      int c = 0;
+      for (int w = 0; w < d / 32; ++w) c += __popc(sb[w]);
+      c += __popc(sb[d / 32] & (0xffffffffu >> (31 - (d & 31))));
+      gi[d] = c - 1;
+    }
+    __syncthreads();
+  }
+  assemble_records(W, D, C, L, e, d0, n, H, g, dkey, gi, pm, y + n);
   // keep the gradient for the report / descent test
   double gmax = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
