@@ -934,6 +934,8 @@ struct ipc_world {
     cudaGraphNode_t snode;
     CK(cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
     cudaGraph_t b_iter = sp.conditional.phGraph_out[0], b_ls = sp.conditional.phGraph_out[1];
+    const bool prof_on = prof.on;
+    prof.on = false;  // conditional bodies take no event nodes
     auto capture_into = [&](cudaGraph_t target, const cudaGraphNode_t* deps, size_t ndep, auto fn) {
       long long l0 = prof.launches;
       prof.capturing = true;
@@ -959,6 +961,8 @@ struct ipc_world {
     });
     CK(cudaGraphInstantiate(&loop_exec, g, 0));
     CK(cudaGraphDestroy(g));
+    CK(cudaGraphUpload(loop_exec, st));
+    prof.on = prof_on;
     loop_cfg = cfg;
     loop_tail = tail;
   }
@@ -974,12 +978,17 @@ struct ipc_world {
     IPC_LAUNCH(K_MISC, st, k_newton_begin, nblk(n_env, 128), 128, 0, n_env, S, al_flag);
     bool graphs = use_graphs && !sparse;
     if (graphs) ensure_graphs(cfg);
-    if (graphs && loop_graph_usable()) {
-      // the loop hands off to the per-env tail kernel only when it can run
-      int tail = (tail_envs > 0 && fused_setup()) ? tail_envs : 0;
+    int tail = 0;
+    if (graphs && use_loop_graph) {
+      // the loop hands off to the per-env tail kernel only when it can run;
+      // built (and uploaded) even while kernel timing keeps the host loop in
+      // use, so switching the timers off never costs an instantiation
+      tail = (tail_envs > 0 && fused_setup()) ? tail_envs : 0;
       if (!loop_exec || !same_cfg(cfg, loop_cfg) || cfg.max_newton_iters != loop_cfg.max_newton_iters ||
           loop_tail != tail)
         build_loop_graph(cfg, tail);
+    }
+    if (graphs && loop_graph_usable()) {
       CK(cudaMemsetAsync(d_loopctl, 0, 8 * sizeof(int), st));
       CK(cudaGraphLaunch(loop_exec, st));
       int ctl[5];

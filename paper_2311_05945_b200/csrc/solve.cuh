@@ -275,7 +275,8 @@ struct Derivs {
 
 constexpr int DENSE_THREADS = 256;
 constexpr int DENSE_MAX_N = 160;  // largest env system on the dense path (engine.cu DENSE_MAX)
-constexpr int DENSE_REG_N = 64;   // register-resident factorization up to this size
+constexpr int DENSE_REG_N = 64;   // warp-register substitution up to this size
+constexpr int LDL_NB = 12;        // panel width of the blocked LDLᵀ
 
 // dynamic shared memory of the dense solve of an n-DoF env: system n² + 2n,
 // the record staging area, the per-DoF group keys
@@ -349,7 +350,14 @@ __device__ __forceinline__ double lift_w(const RecStage& R, int k, int a, int j)
 static __device__ void assemble_records(const World& W, const Derivs& D, const Cands& C, const Lags& L, int e, int d0,
                                  int n, double* H, double* g, const int* dkey, const int* gi, unsigned* pm,
                                  double* stage_mem) {
-  __shared__ int alist[DENSE_THREADS];
+  // headers of the window's active records, resolved once by the compacting
+  // thread (source, slots, groups): the chunk loop then reads the derivative
+  // buffers and lever arms with a single level of indirection
+  __shared__ int hsrc[DENSE_THREADS];                 // type << 28 | index in type
+  __shared__ int hsl[4 * DENSE_THREADS];              // slots (-1: none / tet vertex)
+  __shared__ signed char hgrp[4 * DENSE_THREADS];     // groups (-1: unused)
+  __shared__ unsigned long long hrm[DENSE_THREADS];   // groups touched
+  __shared__ unsigned char s_pkrc[78];                // packed 12x12 index -> row << 4 | col
   __shared__ int wtot[DENSE_THREADS / 32];
   __shared__ int atot;
   RecStage R = rec_stage(stage_mem);
@@ -362,12 +370,16 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
   int total = ntet + npt + nee + ngnd + nfr + nfrg;
   int G = gi[n - 1] + 1, npairs = G * (G + 1) / 2;
   int ntile = 3 * (n / 3) * (n / 3 + 1) / 2;
+  if (tid < 78) {
+    int r = 0, rem = tid;
+    while (rem >= 12 - r) rem -= 12 - r++;
+    s_pkrc[tid] = (unsigned char)(r << 4 | (r + rem));
+  }
   for (int v0 = 0; v0 < total; v0 += DENSE_THREADS) {
     // ordered compaction of the contributing records of this window
-    int v = v0 + tid;
+    int v = v0 + tid, t = 0, j = v;
     bool on = false;
     if (v < total) {
-      int t = 0, j = v;
       while (j >= lim[t]) j -= lim[t++];
       if (t == REC_PT) on = D.pt_act[pt0 + j];
       else if (t == REC_EE) on = D.ee_act[ee0 + j];
@@ -380,70 +392,63 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
     if (tid == 0) {
       int acc = 0;
       for (int w = 0; w < DENSE_THREADS / 32; ++w) {
-        int t = wtot[w];
+        int c = wtot[w];
         wtot[w] = acc;
-        acc += t;
+        acc += c;
       }
       atot = acc;
     }
     __syncthreads();
-    if (on) alist[wtot[wid] + __popc(m & ((1u << lane) - 1u))] = v;
+    if (on) {
+      int pos = wtot[wid] + __popc(m & ((1u << lane) - 1u));
+      hsrc[pos] = (t << 28) | j;
+      int sl[4] = {-1, -1, -1, -1}, gg[4] = {-1, -1, -1, -1};
+      if (t == REC_TET) {
+        int4 td = W.tet_dof[t0 + j];
+        gg[0] = gi[td.x - d0]; gg[1] = gi[td.y - d0]; gg[2] = gi[td.z - d0]; gg[3] = gi[td.w - d0];
+      } else {
+        if (t == REC_PT) {
+          int2 pr = C.pt[pt0 + j];
+          int3 tv = W.tri_v[pr.y];
+          sl[0] = pr.x; sl[1] = tv.x; sl[2] = tv.y; sl[3] = tv.z;
+        } else if (t == REC_EE) {
+          int2 pr = C.ee[ee0 + j];
+          int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
+          sl[0] = a.x; sl[1] = a.y; sl[2] = b.x; sl[3] = b.y;
+        } else if (t == REC_FR) {
+          int4 s4 = L.slots[fr0 + j];
+          sl[0] = s4.x; sl[1] = s4.y; sl[2] = s4.z; sl[3] = s4.w;
+        } else if (t == REC_GND) {
+          sl[0] = C.gnd[gnd0 + j];
+        } else {
+          sl[0] = L.g_slot[frg0 + j];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+          if (sl[a] >= 0) gg[a] = gi[W.slot_dof[sl[a]] - d0];
+      }
+      unsigned long long rm = 0ull;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        hsl[4 * pos + a] = sl[a];
+        hgrp[4 * pos + a] = (signed char)gg[a];
+        if (gg[a] >= 0) rm |= 1ull << gg[a];
+      }
+      hrm[pos] = rm;
+    }
     __syncthreads();
     int na = atot;
     for (int k0 = 0; k0 < na; k0 += REC_CHUNK) {
       int nr = min(REC_CHUNK, na - k0);
-      // stage headers: one thread per record
       if (tid < nr) {
-        int k = tid, j = alist[k0 + k], t = 0;
-        while (j >= lim[t]) j -= lim[t++];
-        int sl[4] = {-1, -1, -1, -1}, ns = 4;
-        unsigned long long rm = 0ull;
-        if (t == REC_TET) {
-          int4 td = W.tet_dof[t0 + j];
-          int dv[4] = {td.x, td.y, td.z, td.w};
-          for (int a = 0; a < 4; ++a) {
-            int gg = gi[dv[a] - d0];
-            R.grp[4 * k + a] = gg;
-            rm |= 1ull << gg;
-          }
-        } else {
-          if (t == REC_PT) {
-            int2 pr = C.pt[pt0 + j];
-            int3 tv = W.tri_v[pr.y];
-            sl[0] = pr.x; sl[1] = tv.x; sl[2] = tv.y; sl[3] = tv.z;
-          } else if (t == REC_EE) {
-            int2 pr = C.ee[ee0 + j];
-            int2 a = W.edge_v[pr.x], b = W.edge_v[pr.y];
-            sl[0] = a.x; sl[1] = a.y; sl[2] = b.x; sl[3] = b.y;
-          } else if (t == REC_FR) {
-            int4 s4 = L.slots[fr0 + j];
-            sl[0] = s4.x; sl[1] = s4.y; sl[2] = s4.z; sl[3] = s4.w;
-          } else if (t == REC_GND) {
-            sl[0] = C.gnd[gnd0 + j];
-            ns = 1;
-          } else {
-            sl[0] = L.g_slot[frg0 + j];
-            ns = 1;
-          }
-          for (int a = 0; a < 4; ++a) {
-            if (a < ns) {
-              int sa = sl[a];
-              int gg = gi[W.slot_dof[sa] - d0];
-              R.grp[4 * k + a] = gg;
-              rm |= 1ull << gg;
-              for (int c = 0; c < 3; ++c) R.rest[12 * k + 3 * a + c] = W.slot_rest[3 * sa + c];
-            } else {
-              R.grp[4 * k + a] = -1;
-            }
-          }
-        }
-        R.rm[k] = rm;
+        R.rm[tid] = hrm[k0 + tid];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) R.grp[4 * tid + a] = hgrp[4 * (k0 + tid) + a];
       }
-      // stage gradients and unpacked Hessians (all threads, coalesced per record)
-      for (int i = tid; i < nr * 90; i += DENSE_THREADS) {
-        int k = i / 90, q = i - 90 * k;
-        int j = alist[k0 + k], t = 0;
-        while (j >= lim[t]) j -= lim[t++];
+      // stage Hessians (unpacked), gradients and lever arms (all threads)
+      for (int i = tid; i < nr * 102; i += DENSE_THREADS) {
+        int k = i / 102, q = i - 102 * k;
+        int src = hsrc[k0 + k], t = src >> 28, j = src & ((1 << 28) - 1);
         double val = 0.0;
         if (q < 78) {
           if (t == REC_TET) val = D.tet_h[PK * (long long)(t0 + j) + q];
@@ -457,12 +462,10 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
             else val = D.frg_h[9 * (long long)(frg0 + j) + 3 * r + c];
           }
           // packed upper index q -> (r, c), mirrored into the full block
-          int r = 0, rem = q;
-          while (rem >= 12 - r) rem -= 12 - r++;
-          int c = r + rem;
+          int rc = s_pkrc[q], r = rc >> 4, c = rc & 15;
           R.h[144 * k + 12 * r + c] = val;
           R.h[144 * k + 12 * c + r] = val;
-        } else {
+        } else if (q < 90) {
           int c = q - 78;
           if (t == REC_TET) val = D.tet_g[12 * (long long)(t0 + j) + c];
           else if (t == REC_PT) val = D.pt_g[12 * (pt0 + j) + c];
@@ -471,6 +474,10 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
           else if (t == REC_GND) val = c == 1 ? D.gnd_gy[gnd0 + j] : 0.0;
           else if (c < 3) val = D.frg_g[3 * (long long)(frg0 + j) + c];
           R.g[12 * k + c] = val;
+        } else {
+          int a = (q - 90) / 3, c = q - 90 - 3 * a;
+          int sa = hsl[4 * (k0 + k) + a];
+          if (sa >= 0) R.rest[12 * k + 3 * a + c] = W.slot_rest[3 * sa + c];
         }
       }
       __syncthreads();
@@ -642,52 +649,136 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
   // lower), D = diag(a); same factorization as Cholesky (SPD input).
   __shared__ double s_dinv[DENSE_MAX_N];
   if (n <= DENSE_REG_N) {
-    // Small envs (every grasp env: 4 affine bodies, n = 48): each thread keeps
-    // the lower-triangle entries it assembled in registers; per column the
-    // owners publish column k to a double-buffered shared column and every
-    // thread updates its own entries (one barrier per column, no shared-memory
-    // read-modify-write chains). Warp 0 then substitutes with y in registers
-    // and the pivot / column values broadcast by shuffles.
-    constexpr int MAXE = (DENSE_REG_N * (DENSE_REG_N + 1) / 2 + DENSE_THREADS - 1) / DENSE_THREADS;
-    __shared__ double colb[2][DENSE_REG_N];
-    double a[MAXE];
-    int rr[MAXE], cc[MAXE];
-    int nlow = n * (n + 1) / 2;
+    // Small envs (every grasp env: 4 affine bodies, n = 48): 3x3 register
+    // tiles of the lower triangle, one per thread, and 3-column panels. Per
+    // panel the diagonal tile factors its 3 columns, the tiles below it apply
+    // those 3 steps to their rows, and every trailing tile takes the rank-3
+    // update from the published panel — two barriers per 3 columns. Each
+    // entry receives exactly the column-by-column sequence
+    // a_ij -= (c_i / a_k) c_j, k increasing, with the same operands.
+    __shared__ double pan[2][3 * DENSE_REG_N];  // panel columns, double-buffered
+    const int T3 = n / 3, ntile = T3 * (T3 + 1) / 2;
+    int I = -1, J = -1;
+    double t[9];
+    if (tid < ntile) {
+      I = (int)((sqrtf(8.0f * (float)tid + 1.0f) - 1.0f) * 0.5f);
+      while ((I + 1) * (I + 2) / 2 <= tid) ++I;
+      while (I * (I + 1) / 2 > tid) --I;
+      J = tid - I * (I + 1) / 2;
 #pragma unroll
-    for (int q = 0; q < MAXE; ++q) {
-      int idx = tid + q * DENSE_THREADS, r = -1, c = -1;
-      double v = 0.0;
-      if (idx < nlow) {
-        r = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
-        while ((r + 1) * (r + 2) / 2 <= idx) ++r;
-        while (r * (r + 1) / 2 > idx) --r;
-        c = idx - r * (r + 1) / 2;
-        v = H[r * n + c];
-      }
-      a[q] = v;
-      rr[q] = r;
-      cc[q] = c;
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) t[3 * a + b] = (I > J || b <= a) ? H[(3 * I + a) * n + 3 * J + b] : 0.0;
     }
-    for (int k = 0; k < n; ++k) {
-      double* cb = colb[k & 1];
+    for (int P = 0; P < T3; ++P) {
+      double* pc = pan[P & 1];
+      if (I == P && J == P) {  // diagonal tile: its three steps
 #pragma unroll
-      for (int q = 0; q < MAXE; ++q)
-        if (cc[q] == k) cb[rr[q]] = a[q];
+        for (int k = 0; k < 3; ++k) {
+          double akk = t[4 * k];
+          double inv = __drcp_rn(akk);  // correctly rounded: the bits of 1.0 / akk
+          s_dinv[3 * P + k] = inv;
+          if (!(akk > 0.0)) fail = 1;
+#pragma unroll
+          for (int a = k + 1; a < 3; ++a)
+#pragma unroll
+            for (int b = k + 1; b <= a; ++b) t[3 * a + b] -= (t[3 * a + k] * inv) * t[3 * b + k];
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b <= a; ++b) pc[3 * (3 * P + a) + b] = t[3 * a + b];
+      }
       __syncthreads();
-      double akk = cb[k];
-      double inv = 1.0 / akk;
-      if (tid == 0) {
-        s_dinv[k] = inv;
-        if (!(akk > 0.0)) fail = 1;
+      if (J == P && I > P) {  // panel tile: the three steps on its rows
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          double inv = s_dinv[3 * P + k];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = k + 1; b < 3; ++b) t[3 * a + b] -= (t[3 * a + k] * inv) * pc[3 * (3 * P + b) + k];
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) pc[9 * I + q] = t[q];
       }
+      __syncthreads();
+      if (J > P) {  // trailing tile: rank-3 update, steps in order
 #pragma unroll
-      for (int q = 0; q < MAXE; ++q)
-        if (cc[q] > k) a[q] -= (cb[rr[q]] * inv) * cb[cc[q]];
+        for (int k = 0; k < 3; ++k) {
+          double inv = s_dinv[3 * P + k];
+          double ci[3], cj[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            ci[a] = pc[3 * (3 * I + a) + k];
+            cj[a] = pc[3 * (3 * J + a) + k];
+          }
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+              if (I > J || b <= a) t[3 * a + b] -= (ci[a] * inv) * cj[b];
+        }
+      }
     }
+    if (tid < ntile) {
 #pragma unroll
-    for (int q = 0; q < MAXE; ++q)
-      if (rr[q] >= 0) H[rr[q] * n + cc[q]] = a[q];
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          if (I > J || b <= a) H[(3 * I + a) * n + 3 * J + b] = t[3 * a + b];
+    }
     __syncthreads();
+  } else {
+  // Blocked right-looking form: panels of LDL_NB columns; warp 0 factors the
+    // diagonal block, one thread per row applies the panel's steps to the rows
+    // below it, then every trailing entry takes the panel's rank-LDL_NB update.
+    // Each entry receives exactly the column-by-column update sequence
+    // a_ij -= (c_i / a_k) c_j, k increasing, with the same operands (so the same
+    // bits), at three block barriers per panel instead of one per column.
+    for (int K0 = 0; K0 < n; K0 += LDL_NB) {
+      int K1 = min(n, K0 + LDL_NB);
+      if (tid < 32) {
+        for (int k = K0; k < K1; ++k) {
+          double akk = H[k * n + k];
+          double inv = __drcp_rn(akk);  // correctly rounded: the bits of 1.0 / akk
+          if (tid == 0) {
+            s_dinv[k] = inv;
+            if (!(akk > 0.0)) fail = 1;
+          }
+          int i = K0 + tid;
+          if (i > k && i < K1) {
+            double ci = H[i * n + k] * inv;
+            for (int j = k + 1; j <= i; ++j) H[i * n + j] -= ci * H[j * n + k];
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (int i = K1 + tid; i < n; i += blockDim.x) {
+        for (int k = K0; k < K1; ++k) {
+          double ci = H[i * n + k] * s_dinv[k];
+          for (int j = k + 1; j < K1; ++j) H[i * n + j] -= ci * H[j * n + k];
+        }
+      }
+      __syncthreads();
+      int m = n - K1;
+      for (int idx = tid; idx < m * (m + 1) / 2; idx += blockDim.x) {
+        int ii = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
+        while ((ii + 1) * (ii + 2) / 2 <= idx) ++ii;
+        while (ii * (ii + 1) / 2 > idx) --ii;
+        int i = K1 + ii, j = K1 + (idx - ii * (ii + 1) / 2);
+        double a = H[i * n + j];
+        for (int k = K0; k < K1; ++k) a -= (H[i * n + k] * s_dinv[k]) * H[j * n + k];
+        H[i * n + j] = a;
+      }
+      __syncthreads();
+    }
+  }
+  if (n <= DENSE_REG_N) {
+    // Small envs (every grasp env: 4 affine bodies, n = 48): warp 0
+    // substitutes with y in registers, the pivot / column values broadcast by
+    // shuffles.
     if (tid < 32) {
       const unsigned FULL = 0xffffffffu;
       int lane = tid, i1 = lane + 32;
@@ -712,22 +803,6 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
     }
     __syncthreads();
   } else {
-    for (int k = 0; k < n; ++k) {  // one block barrier per column
-      double akk = H[k * n + k];
-      if (tid == 0 && !(akk > 0.0)) fail = 1;
-      double inv = 1.0 / akk;
-      int m = n - k - 1;
-      // trailing update H[i][j] -= c_i c_j / a_k for k < j <= i, 2D thread map
-      for (int ii = tid >> 4; ii < m; ii += blockDim.x >> 4) {
-        int i = k + 1 + ii;
-        double ci = H[i * n + k] * inv;
-        for (int jj = tid & 15; jj <= ii; jj += 16) {
-          int j = k + 1 + jj;
-          H[i * n + j] -= ci * H[j * n + k];
-        }
-      }
-      __syncthreads();
-    }
     // forward: L' u = -g  (y holds -g)
     for (int k = 0; k < n; ++k) {
       double uk = y[k], inv = 1.0 / H[k * n + k];
