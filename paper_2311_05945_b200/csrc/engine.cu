@@ -710,7 +710,7 @@ struct ipc_world {
       IPC_LAUNCH(K_ENERGY, side[0], k_env_energy, n_env, RED_THREADS, 0, W, W.x, W.xhat, T, dcd.c, L, S.newton_active,
                  S.e0);
       IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, dense_smem, W, S, D_with(pb_dcd), dcd.c, L, W.x,
-                 W.xhat, W.p, W.grad);
+                 W.xhat, W.p, W.grad, dense_timers());
       join_from(side[0], fj[1]);
     }
     IPC_LAUNCH(K_MISC, st, k_newton_check, nblk(n_env, 128), 128, 0, n_env, S, cfg.h, cfg.newton_tol);
@@ -1056,6 +1056,9 @@ struct ipc_world {
   bool use_fused() const { return fused_on && !sparse && max_env_dof <= fused_max_dof; }
 
   void read_reports(ipc_step_report* rep);
+  // dense sub-phase timers (IPC_FUSED_TIMERS=1) of the batched k_dense_solve:
+  // the same counters as the fused kernels' dense_solve_block
+  long long* dense_timers() { return (fused_timers_on && d_fstat) ? d_fstat + 2 + FT_DENSE_SUB : nullptr; }
 
   // shared setup of the fused kernels; false when the env systems do not fit
   bool fused_setup() {
@@ -1666,6 +1669,7 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     CK(cudaStreamCreateWithFlags(&w->st, cudaStreamNonBlocking));
     for (int i = 0; i < 3; ++i) CK(cudaStreamCreateWithFlags(&w->side[i], cudaStreamNonBlocking));
     for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&w->fj[i], cudaEventDisableTiming));
+    if (w->fused_timers_on && !w->sparse) w->fused_setup();  // timer block for the batched solve too
     CK(cudaDeviceSynchronize());
     *out = w;
     return 0;

@@ -25,7 +25,9 @@ enum { FT_WORLD, FT_BROAD_DCD, FT_TERMS, FT_ENERGY, FT_DENSE, FT_CCD_PREP, FT_BR
 // (cycle sum, count, max) for PT pair Hessians, EE pair Hessians, affine
 // bodies, friction stencils
 enum { FT_IT_PT, FT_IT_EE, FT_IT_BODY, FT_IT_FR, FT_NIT };
-constexpr int FT_TOTAL = FT_N + 3 * FT_NIT;
+// sub-phases of the dense solve (dense_solve_block dtm), after the items
+constexpr int FT_DENSE_SUB = FT_N + 3 * FT_NIT, FT_NDS = 9;
+constexpr int FT_TOTAL = FT_DENSE_SUB + FT_NDS;
 __device__ __forceinline__ void ft_item(long long* timers, int type, long long t0) {
   if (!timers) return;
   long long dt = clock64() - t0;
@@ -40,9 +42,10 @@ __device__ __forceinline__ void ft_item(long long* timers, int type, long long t
   do {                                                                    \
     if ((A).timers) {                                                     \
       __syncthreads();                                                    \
-      if (threadIdx.x == 0) {                                             \
+      if (threadIdx.x < 32) { /* whole warp 0: no lane-0 divergence */    \
         long long now = clock64();                                        \
-        atomicAdd((unsigned long long*)(A).timers + (k), now - ft_t0);    \
+        atomicAdd((unsigned long long*)(A).timers + (k),                  \
+                  threadIdx.x == 0 ? (unsigned long long)(now - ft_t0) : 0ull); \
         ft_t0 = now;                                                      \
       }                                                                   \
     }                                                                     \
@@ -521,7 +524,8 @@ static __device__ bool env_newton(const FusedArgs& A, int e, double* sm, bool be
       S.e0[e] = e0;
     }
     FT_MARK(A, FT_ENERGY);
-    dense_solve_block(W, S, A.D, A.dc, A.L, W.x, W.xhat, W.p, W.grad, e, sm);
+    dense_solve_block(W, S, A.D, A.dc, A.L, W.x, W.xhat, W.p, W.grad, e, sm,
+                      A.timers ? A.timers + FT_DENSE_SUB : nullptr);
     FT_MARK(A, FT_DENSE);
     if (threadIdx.x == 0) {
       newton_check_env(S, A.h, A.newton_tol, e);

@@ -369,12 +369,12 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
   int lim[6] = {ntet, npt, nee, ngnd, nfr, nfrg};
   int total = ntet + npt + nee + ngnd + nfr + nfrg;
   int G = gi[n - 1] + 1, npairs = G * (G + 1) / 2;
-  int ntile = 3 * (n / 3) * (n / 3 + 1) / 2;
   if (tid < 78) {
     int r = 0, rem = tid;
     while (rem >= 12 - r) rem -= 12 - r++;
     s_pkrc[tid] = (unsigned char)(r << 4 | (r + rem));
   }
+  int ntile = 3 * (n / 3) * (n / 3 + 1) / 2;
   for (int v0 = 0; v0 < total; v0 += DENSE_THREADS) {
     // ordered compaction of the contributing records of this window
     int v = v0 + tid, t = 0, j = v;
@@ -569,12 +569,60 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
   }
 }
 
+// Forward / backward substitution of the factored small env system by one
+// warp (y in two registers per lane, the pivot / column values broadcast by
+// shuffles). Its own function so that the caller's register pressure (the
+// fused kernels run at 255) cannot turn the loop's predicated updates into
+// branches and re-materialised special-register reads (8x slower, measured).
+static __device__ __noinline__ void warp_substitute(const double* H, const double* dinv, double* y, int n) {
+  const unsigned FULL = 0xffffffffu;
+  __syncwarp();  // enter converged: a diverged warp takes every SHFL's slow path (measured 7x)
+  int lane = threadIdx.x & 31, i1 = lane + 32;
+  double y0 = lane < n ? y[lane] : 0.0, y1 = i1 < n ? y[i1] : 0.0;
+  // forward: L' u = -g (y holds -g); column k of L' is read from its mirror
+  // in the upper triangle (row k: consecutive, conflict-free)
+  for (int k = 0; k < n; ++k) {
+    double uk = __shfl_sync(FULL, k < 32 ? y0 : y1, k & 31);
+    double dk = dinv[k];
+    double c0 = (lane > k && lane < n) ? H[k * n + lane] * dk : 0.0;
+    double c1 = (i1 > k && i1 < n) ? H[k * n + i1] * dk : 0.0;
+    y0 -= c0 * uk;
+    y1 -= c1 * uk;
+  }
+  if (lane < n) y0 *= dinv[lane];
+  if (i1 < n) y1 *= dinv[i1];
+  // backward: L'ᵀ p = D⁻¹ u
+  double dl0 = lane < n ? dinv[lane] : 0.0, dl1 = i1 < n ? dinv[i1] : 0.0;
+  for (int k = n - 1; k >= 0; --k) {
+    double xk = __shfl_sync(FULL, k < 32 ? y0 : y1, k & 31);
+    double c0 = lane < k ? H[k * n + lane] * dl0 : 0.0;
+    double c1 = i1 < k ? H[k * n + i1] * dl1 : 0.0;
+    y0 -= c0 * xk;
+    y1 -= c1 * xk;
+  }
+  if (lane < n) y[lane] = y0;
+  if (i1 < n) y[i1] = y1;
+}
+
 // Assemble the env's dense Hessian/gradient, Cholesky-solve H p = −g with the
 // gradient fallback of ref solver.py:241, write p, ‖p‖∞, ‖g‖∞.
 // block function: assemble + solve env e; sm holds n² + 2n doubles
+// dtm (optional phase timers, IPC_FUSED_TIMERS=1): SM cycles of the solve's
+// sub-phases — setup, record assembly, gradient norm, LDLᵀ, substitution, tail
 static __device__ void dense_solve_block(const World& W, const EnvState& S, const Derivs& D, const Cands& C,
                                   const Lags& L, const double* __restrict__ x, const double* __restrict__ xhat,
-                                  double* p_out, double* g_out, int e, double* sm) {
+                                  double* p_out, double* g_out, int e, double* sm, long long* dtm = nullptr) {
+  long long dt0 = dtm ? clock64() : 0;
+  auto dmark = [&](int k) {
+    if (dtm) {
+      __syncthreads();
+      if (threadIdx.x < 32) {  // all of warp 0 (a lane-0 branch would leave it diverged)
+        long long now = clock64();
+        atomicAdd((unsigned long long*)dtm + k, threadIdx.x == 0 ? (unsigned long long)(now - dt0) : 0ull);
+        dt0 = now;
+      }
+    }
+  };
   __shared__ double red[DENSE_THREADS / 32];
   __shared__ int fail;
   int d0 = W.env_dof[e], n = W.env_dof[e + 1] - d0;
@@ -633,7 +681,9 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
     }
     __syncthreads();
   }
+  dmark(0);
   assemble_records(W, D, C, L, e, d0, n, H, g, dkey, gi, pm, y + n);
+  dmark(1);
   // keep the gradient for the report / descent test
   double gmax = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
@@ -644,6 +694,7 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
   double gn = block_max(gmax, red);
   if (tid == 0) S.gnorm[e] = gn;
   __syncthreads();
+  dmark(2);
   // LDLᵀ without scaling: after step k the lower column c_k = H[k+1:, k] and
   // pivot a_k = H[k][k] give H = Σ c_k c_kᵀ / a_k, i.e. L' = c / a (unit
   // lower), D = diag(a); same factorization as Cholesky (SPD input).
@@ -721,12 +772,15 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
         }
       }
     }
-    if (tid < ntile) {
+    if (tid < ntile) {  // L' and D, mirrored into the upper triangle for the forward substitution
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int b = 0; b < 3; ++b)
-          if (I > J || b <= a) H[(3 * I + a) * n + 3 * J + b] = t[3 * a + b];
+          if (I > J || b <= a) {
+            H[(3 * I + a) * n + 3 * J + b] = t[3 * a + b];
+            H[(3 * J + b) * n + 3 * I + a] = t[3 * a + b];
+          }
     }
     __syncthreads();
   } else {
@@ -775,33 +829,14 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
       __syncthreads();
     }
   }
+  dmark(3);
   if (n <= DENSE_REG_N) {
     // Small envs (every grasp env: 4 affine bodies, n = 48): warp 0
     // substitutes with y in registers, the pivot / column values broadcast by
     // shuffles.
-    if (tid < 32) {
-      const unsigned FULL = 0xffffffffu;
-      int lane = tid, i1 = lane + 32;
-      double y0 = lane < n ? y[lane] : 0.0, y1 = i1 < n ? y[i1] : 0.0;
-      // forward: L' u = -g (y holds -g)
-      for (int k = 0; k < n; ++k) {
-        double uk = __shfl_sync(FULL, k < 32 ? y0 : y1, k & 31);
-        double dk = s_dinv[k];
-        if (lane > k && lane < n) y0 -= (H[lane * n + k] * dk) * uk;
-        if (i1 > k && i1 < n) y1 -= (H[i1 * n + k] * dk) * uk;
-      }
-      if (lane < n) y0 *= s_dinv[lane];
-      if (i1 < n) y1 *= s_dinv[i1];
-      // backward: L'ᵀ p = D⁻¹ u
-      for (int k = n - 1; k >= 0; --k) {
-        double xk = __shfl_sync(FULL, k < 32 ? y0 : y1, k & 31);
-        if (lane < k) y0 -= (H[k * n + lane] * s_dinv[lane]) * xk;
-        if (i1 < k) y1 -= (H[k * n + i1] * s_dinv[i1]) * xk;
-      }
-      if (lane < n) y[lane] = y0;
-      if (i1 < n) y[i1] = y1;
-    }
+    if (tid < 32) warp_substitute(H, s_dinv, y, n);
     __syncthreads();
+    dmark(4);
   } else {
     // forward: L' u = -g  (y holds -g)
     for (int k = 0; k < n; ++k) {
@@ -841,16 +876,17 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
   }
   double pn = block_max(pmax, red);
   if (tid == 0) S.pnorm[e] = pn;
+  dmark(5);
 }
 
 IPC_GLOBAL void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState S, Derivs D, Cands C,
                                                                 Lags L, const double* __restrict__ x,
                                                                 const double* __restrict__ xhat,
-                                                                double* p_out, double* g_out) {
+                                                                double* p_out, double* g_out, long long* dtm) {
   extern __shared__ double sm[];
   int e = blockIdx.x;
   if (!S.newton_active[e]) return;
-  dense_solve_block(W, S, D, C, L, x, xhat, p_out, g_out, e, sm);
+  dense_solve_block(W, S, D, C, L, x, xhat, p_out, g_out, e, sm, dtm);
 }
 
 // ---------------------------------------------------------------------------

@@ -345,7 +345,10 @@ class GpuWorld:
                     "line_search", "other",
                     # per-item latency of the terms phase: cycle sum, count, max
                     "pt_cycles", "pt_items", "pt_max", "ee_cycles", "ee_items", "ee_max",
-                    "body_cycles", "body_items", "body_max", "fr_cycles", "fr_items", "fr_max")
+                    "body_cycles", "body_items", "body_max", "fr_cycles", "fr_items", "fr_max",
+                    # sub-phases of "dense"
+                    "dense_setup", "dense_asm", "dense_gnorm", "dense_ldlt", "dense_subst", "dense_tail",
+                    "dense_fwd_warp", "dense_bwd_warp", "dense_diverged")
 
     def fused_timers(self):
         """SM cycles per phase of the fused step (zeros unless the timers are on)."""

@@ -30,11 +30,13 @@ def phases(w, st0, st1, t0, t1, label):
         d.pop(f"{kind}_max", 0)
         items[kind] = {"per_iter": n / max(it, 1), "mean_us": cyc / max(n, 1) / 1965.0,
                        "max_us_cumulative": t1[f"{kind}_max"] / 1965.0}
+    sub = {k: d.pop(k) / max(it, 1) for k in list(d) if k.startswith("dense_")}
     tot = sum(d.values())
     out = {"label": label, "newton_iters": it, "ls_trials": ls,
            "cycles_per_iter": {k: v / max(it, 1) for k, v in d.items()},
            "share": {k: v / max(tot, 1) for k, v in d.items()},
-           "us_per_iter_at_1965MHz": tot / max(it, 1) / 1965.0, "items": items}
+           "us_per_iter_at_1965MHz": tot / max(it, 1) / 1965.0, "items": items,
+           "dense_sub_cycles_per_iter": sub}
     print(json.dumps(out), flush=True)
 
 
