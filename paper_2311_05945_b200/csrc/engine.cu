@@ -734,7 +734,7 @@ struct ipc_world {
   // one backtracking round (ref solver.py:257): M speculative halvings
   void seq_ls_round(const ipc_step_config& cfg, int M) {
     if (!sparse) {
-      IPC_LAUNCH(K_ENERGY, st, k_ls_value, dim3(n_env, M), RED_THREADS, (size_t)3 * max_slots * sizeof(double), W, S,
+      IPC_LAUNCH(K_ENERGY, st, k_ls_value, dim3(n_env, M), LS_THREADS, (size_t)3 * max_slots * sizeof(double), W, S,
                  sweep.c, L, W.x, W.p, W.xhat, cfg.h * cfg.h, cfg.h, e_multi);
     } else {
       double scale = 1.0;

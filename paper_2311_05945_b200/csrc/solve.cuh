@@ -34,6 +34,27 @@ static __device__ double block_max(double v, double* sh) {
   return r;
 }
 
+// block_sum over RED_THREADS virtual lanes: part(vt) is virtual lane vt's
+// partial sum; thread t holds lanes t, t + blockDim.x, ...; the tree (warp
+// shuffles, then the virtual warps in order on thread 0) is block_sum's at
+// RED_THREADS threads. Valid on thread 0.
+template <class F>
+static __device__ double block_sum_virtual(F part, double* sh) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int vt = threadIdx.x; vt < RED_THREADS; vt += blockDim.x) {
+    double v = part(vt);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[wid + nw * (vt / blockDim.x)] = v;
+  }
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < RED_THREADS / 32; ++w) r += sh[w];
+  __syncthreads();
+  return r;
+}
+
 // Element value buffers of one energy evaluation.
 struct Terms {
   double *body_val, *tet_val, *pt_val, *ee_val, *gnd_val, *fr_val, *frg_val;
@@ -148,108 +169,116 @@ static __device__ double ls_value_block(const World& W, const Cands& C, const La
   }
   __syncthreads();
   auto XW = [&](int s) { return ld3(sxw + 3 * (s - s0)); };
-  double acc = 0.0;
-  for (int v = W.env_vert[e] + tid; v < W.env_vert[e + 1]; v += blockDim.x) {
-    int d = W.vert_dof[v];
-    double mass = W.vert_mass[v], sv = 0.0;
-    for (int c = 0; c < 3; ++c) {
-      double dd = axpy_rn(x[d + c], a, p[d + c]) - xhat[d + c];
-      sv += dd * mass * dd;
+  // every item sweep runs over RED_THREADS virtual lanes (stride RED_THREADS),
+  // each thread taking RED_THREADS / blockDim.x of them: the per-lane sums and
+  // the reduction tree are those of a RED_THREADS-thread block whatever the
+  // launch width, so E(x + a p) has the same bits at 128 and at 256 threads
+  auto sweep = [&](int tid) {
+    double acc = 0.0;
+    for (int v = W.env_vert[e] + tid; v < W.env_vert[e + 1]; v += RED_THREADS) {
+      int d = W.vert_dof[v];
+      double mass = W.vert_mass[v], sv = 0.0;
+      for (int c = 0; c < 3; ++c) {
+        double dd = axpy_rn(x[d + c], a, p[d + c]) - xhat[d + c];
+        sv += dd * mass * dd;
+      }
+      acc += 0.5 * sv;
     }
-    acc += 0.5 * sv;
-  }
-  for (int b = W.env_aff[e] + tid; b < W.env_aff[e + 1]; b += blockDim.x) {
-    int o = W.aff_dof[b];
-    double q[12];
-    for (int i = 0; i < 12; ++i) q[i] = axpy_rn(x[o + i], a, p[o + i]);
-    acc += body_value(W, b, e, q, xhat + o, h2);
-  }
-  for (int t = W.env_tet[e] + tid; t < W.env_tet[e + 1]; t += blockDim.x) {
-    int4 td = W.tet_dof[t];
-    int dv[4] = {td.x, td.y, td.z, td.w};
-    V3 X[4];
-    for (int k = 0; k < 4; ++k)
-      X[k] = v3(axpy_rn(x[dv[k]], a, p[dv[k]]), axpy_rn(x[dv[k] + 1], a, p[dv[k] + 1]),
-                axpy_rn(x[dv[k] + 2], a, p[dv[k] + 2]));
-    V3 e1 = X[1] - X[0], e2 = X[2] - X[0], e3 = X[3] - X[0];
-    M3 Ds;
-    Ds.m[0] = e1.x; Ds.m[1] = e2.x; Ds.m[2] = e3.x;
-    Ds.m[3] = e1.y; Ds.m[4] = e2.y; Ds.m[5] = e3.y;
-    Ds.m[6] = e1.z; Ds.m[7] = e2.z; Ds.m[8] = e3.z;
-    M3 Dmi;
-    for (int i = 0; i < 9; ++i) Dmi.m[i] = W.tet_Dminv[9 * t + i];
-    M3 F = m3_mul(Ds, Dmi);
-    double psi = psi_value(W.tet_model[t], F, W.tet_mu[t], W.tet_lam[t]);
-    acc += isinf(psi) ? INFINITY : (h2 * W.tet_vol[t]) * psi;
-  }
-  double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
-  for (int kind = 0; kind < 2; ++kind) {
-    int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
-    long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
-    for (int k = tid; k < n; k += blockDim.x) {
-      int2 pr = kind == 0 ? C.pt[off + k] : C.ee[off + k];
-      int sl[4];
-      pair_slots(W, kind, pr, sl);
+    for (int b = W.env_aff[e] + tid; b < W.env_aff[e + 1]; b += RED_THREADS) {
+      int o = W.aff_dof[b];
+      double q[12];
+      for (int i = 0; i < 12; ++i) q[i] = axpy_rn(x[o + i], a, p[o + i]);
+      acc += body_value(W, b, e, q, xhat + o, h2);
+    }
+    for (int t = W.env_tet[e] + tid; t < W.env_tet[e + 1]; t += RED_THREADS) {
+      int4 td = W.tet_dof[t];
+      int dv[4] = {td.x, td.y, td.z, td.w};
       V3 X[4];
-      for (int i = 0; i < 4; ++i) X[i] = XW(sl[i]);
-      double d2;
-      if (kind == 0) d2 = pt_dist2(pt_region(X[0], X[1], X[2], X[3]), X[0], X[1], X[2], X[3]);
-      else d2 = ee_dist2(ee_region(X[0], X[1], X[2], X[3], nullptr), X[0], X[1], X[2], X[3]);
-      if (!(d2 < shat)) continue;
-      if (d2 <= 0.0) {
-        acc += INFINITY;
-        continue;
-      }
-      double bv = barrier_val(d2, shat);
-      if (kind == 0) {
-        acc += kappa * bv;
-      } else {
-        double mo = mollifier_val(cross2(X[1] - X[0], X[3] - X[2]), 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y]);
-        acc += kappa * (mo * bv);
+      for (int k = 0; k < 4; ++k)
+        X[k] = v3(axpy_rn(x[dv[k]], a, p[dv[k]]), axpy_rn(x[dv[k] + 1], a, p[dv[k] + 1]),
+                  axpy_rn(x[dv[k] + 2], a, p[dv[k] + 2]));
+      V3 e1 = X[1] - X[0], e2 = X[2] - X[0], e3 = X[3] - X[0];
+      M3 Ds;
+      Ds.m[0] = e1.x; Ds.m[1] = e2.x; Ds.m[2] = e3.x;
+      Ds.m[3] = e1.y; Ds.m[4] = e2.y; Ds.m[5] = e3.y;
+      Ds.m[6] = e1.z; Ds.m[7] = e2.z; Ds.m[8] = e3.z;
+      M3 Dmi;
+      for (int i = 0; i < 9; ++i) Dmi.m[i] = W.tet_Dminv[9 * t + i];
+      M3 F = m3_mul(Ds, Dmi);
+      double psi = psi_value(W.tet_model[t], F, W.tet_mu[t], W.tet_lam[t]);
+      acc += isinf(psi) ? INFINITY : (h2 * W.tet_vol[t]) * psi;
+    }
+    double dhat = W.env_dhat[e], shat = dhat * dhat, kappa = W.env_kappa[e];
+    for (int kind = 0; kind < 2; ++kind) {
+      int n = kind == 0 ? C.n_pt[e] : C.n_ee[e];
+      long long off = kind == 0 ? C.pt_off[e] : C.ee_off[e];
+      for (int k = tid; k < n; k += RED_THREADS) {
+        int2 pr = kind == 0 ? C.pt[off + k] : C.ee[off + k];
+        int sl[4];
+        pair_slots(W, kind, pr, sl);
+        V3 X[4];
+        for (int i = 0; i < 4; ++i) X[i] = XW(sl[i]);
+        double d2;
+        if (kind == 0) d2 = pt_dist2(pt_region(X[0], X[1], X[2], X[3]), X[0], X[1], X[2], X[3]);
+        else d2 = ee_dist2(ee_region(X[0], X[1], X[2], X[3], nullptr), X[0], X[1], X[2], X[3]);
+        if (!(d2 < shat)) continue;
+        if (d2 <= 0.0) {
+          acc += INFINITY;
+          continue;
+        }
+        double bv = barrier_val(d2, shat);
+        if (kind == 0) {
+          acc += kappa * bv;
+        } else {
+          double mo = mollifier_val(cross2(X[1] - X[0], X[3] - X[2]), 1e-6 * W.edge_len2[pr.x] * W.edge_len2[pr.y]);
+          acc += kappa * (mo * bv);
+        }
       }
     }
-  }
-  if (W.env_has_ground[e]) {
-    double gy = W.env_ground_y[e];
-    for (int k = tid; k < C.n_gnd[e]; k += blockDim.x) {
-      int s = C.gnd[C.gnd_off[e] + k];
-      double d = sxw[3 * (s - s0) + 1] - gy;
-      if (d <= 0.0) {
-        acc += INFINITY;
-        continue;
+    if (W.env_has_ground[e]) {
+      double gy = W.env_ground_y[e];
+      for (int k = tid; k < C.n_gnd[e]; k += RED_THREADS) {
+        int s = C.gnd[C.gnd_off[e] + k];
+        double d = sxw[3 * (s - s0) + 1] - gy;
+        if (d <= 0.0) {
+          acc += INFINITY;
+          continue;
+        }
+        double ss = d * d;
+        if (ss < shat) acc += kappa * barrier_val(ss, shat);
       }
-      double ss = d * d;
-      if (ss < shat) acc += kappa * barrier_val(ss, shat);
     }
-  }
-  double eh = W.env_epsv[e] * h, mu = W.env_mu[e];
-  for (int k = tid; k < L.n[e]; k += blockDim.x) {
-    long long q = L.off[e] + k;
-    int4 s4 = L.slots[q];
-    int sl[4] = {s4.x, s4.y, s4.z, s4.w};
-    const double* gam = L.gamma + 4 * q;
-    const double* T = L.tangent + 6 * q;
-    double u3[3] = {0, 0, 0};
-    for (int i = 0; i < 4; ++i)
-      for (int c = 0; c < 3; ++c) u3[c] += gam[i] * (sxw[3 * (sl[i] - s0) + c] - W.xw0[3 * sl[i] + c]);
-    double u0 = T[0] * u3[0] + T[2] * u3[1] + T[4] * u3[2];
-    double u1 = T[1] * u3[0] + T[3] * u3[1] + T[5] * u3[2];
-    double hu[4];
-    acc += smooth_norm(u0, u1, mu * L.lam[q], eh, nullptr, hu);
-  }
-  for (int k = tid; k < L.g_n[e]; k += blockDim.x) {
-    int q = W.env_slot[e] + k;
-    int s = L.g_slot[q];
-    double u0 = sxw[3 * (s - s0)] - W.xw0[3 * s], u1 = sxw[3 * (s - s0) + 2] - W.xw0[3 * s + 2];
-    double hu[4];
-    acc += smooth_norm(u0, u1, mu * L.g_lam[q], eh, nullptr, hu);
-  }
-  double tot = block_sum(acc, sh);
+    double eh = W.env_epsv[e] * h, mu = W.env_mu[e];
+    for (int k = tid; k < L.n[e]; k += RED_THREADS) {
+      long long q = L.off[e] + k;
+      int4 s4 = L.slots[q];
+      int sl[4] = {s4.x, s4.y, s4.z, s4.w};
+      const double* gam = L.gamma + 4 * q;
+      const double* T = L.tangent + 6 * q;
+      double u3[3] = {0, 0, 0};
+      for (int i = 0; i < 4; ++i)
+        for (int c = 0; c < 3; ++c) u3[c] += gam[i] * (sxw[3 * (sl[i] - s0) + c] - W.xw0[3 * sl[i] + c]);
+      double u0 = T[0] * u3[0] + T[2] * u3[1] + T[4] * u3[2];
+      double u1 = T[1] * u3[0] + T[3] * u3[1] + T[5] * u3[2];
+      double hu[4];
+      acc += smooth_norm(u0, u1, mu * L.lam[q], eh, nullptr, hu);
+    }
+    for (int k = tid; k < L.g_n[e]; k += RED_THREADS) {
+      int q = W.env_slot[e] + k;
+      int s = L.g_slot[q];
+      double u0 = sxw[3 * (s - s0)] - W.xw0[3 * s], u1 = sxw[3 * (s - s0) + 2] - W.xw0[3 * s + 2];
+      double hu[4];
+      acc += smooth_norm(u0, u1, mu * L.g_lam[q], eh, nullptr, hu);
+    }
+    return acc;
+  };
+  double tot = block_sum_virtual(sweep, sh);
   __syncthreads();  // sxw is reused by the caller
   return tot;
 }
 
-IPC_GLOBAL void __launch_bounds__(RED_THREADS) k_ls_value(World W, EnvState S, Cands C, Lags L,
+constexpr int LS_THREADS = 128;  // launch width of k_ls_value (the sums are RED_THREADS-lane sums)
+IPC_GLOBAL void __launch_bounds__(LS_THREADS) k_ls_value(World W, EnvState S, Cands C, Lags L,
                                                            const double* __restrict__ x,
                                                            const double* __restrict__ p,
                                                            const double* __restrict__ xhat, double h2, double h,
