@@ -9,6 +9,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/ipc_b200.h"
@@ -127,16 +128,37 @@ static inline void prof_end(int kid, cudaStream_t s) {
   else p->pending.push_back(p->cur);
   p->cur.kid = -1;
 }
-#define IPC_LAUNCH(kid, stream, kern, grid, block, smem, ...) \
-  do {                                                        \
-    prof_begin((kid), (stream));                              \
-    kern<<<grid, block, smem, stream>>>(__VA_ARGS__);         \
-    CK(cudaPeekAtLastError());                                \
-    prof_end((kid), (stream));                                \
+// Kernel launches go through cudaLaunchKernelEx with programmatic stream
+// serialization (IPC_PDL=0: plain launches): a kernel is scheduled while its
+// predecessor on the stream drains and waits in ipc_pdl_wait() before its
+// first memory access, so the ≈25 dependent launches of a Newton iteration
+// overlap their launch latency with the previous kernel's tail.
+static bool g_pdl = getenv("IPC_PDL") == nullptr || getenv("IPC_PDL")[0] != '0';
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+#define IPC_LAUNCH(kid, stream, kern, grid, block, smem, ...)  \
+  do {                                                         \
+    prof_begin((kid), (stream));                               \
+    CK(launch_pdl(kern, dim3(grid), dim3(block), (size_t)(smem), stream, __VA_ARGS__)); \
+    prof_end((kid), (stream));                                 \
   } while (0)
 
 namespace ipc {
 __global__ void k_mark_unconverged(int n_env, EnvState S) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n_env && S.newton_active[e]) {
     S.converged[e] = 0;
@@ -144,6 +166,7 @@ __global__ void k_mark_unconverged(int n_env, EnvState S) {
   }
 }
 __global__ void k_step_begin(int n_env, EnvState S) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_env) return;
   S.newton_iters[e] = 0; S.ccd_calls[e] = 0; S.al_outer[e] = 0; S.ls_failed[e] = 0;
@@ -152,6 +175,7 @@ __global__ void k_step_begin(int n_env, EnvState S) {
 // intersection check of the incoming state: any candidate value is inf
 __global__ void k_start_check(World W, EnvState S, Cands C, const double* ptv, const double* eev,
                               const double* gv, int* ok) {
+  ipc_pdl_wait();
   int e = blockIdx.x;
   if (!ok[e]) {
     if (threadIdx.x == 0) S.err[e] = 0;
@@ -168,6 +192,7 @@ __global__ void k_start_check(World W, EnvState S, Cands C, const double* ptv, c
   }
 }
 __global__ void k_status(int n_env, const int* newton, const int* ls, const int* ov1, const int* ov2, int* out) {
+  ipc_pdl_wait();
   __shared__ int a, b;
   if (threadIdx.x == 0) a = b = 0;
   __syncthreads();
@@ -198,6 +223,7 @@ __global__ void k_status(int n_env, const int* newton, const int* ls, const int*
 __global__ void k_loop_ctl(int n_env, const int* newton, const int* ls, const int* ov1, const int* ov2, int* ctl,
                            int max_iters, int max_halvings, int ls_m, int tail, cudaGraphConditionalHandle h_loop,
                            cudaGraphConditionalHandle h_mode) {
+  ipc_pdl_wait();
   __shared__ int a, b;
   if (threadIdx.x == 0) a = b = 0;
   __syncthreads();
@@ -235,6 +261,7 @@ __global__ void k_loop_ctl(int n_env, const int* newton, const int* ls, const in
 }
 // dxw = xw(x + p) - xw(x); sweep boxes over [xw, xw + dxw] (ref broadphase.py:206)
 __global__ void k_sweep_box2(int n, const double* xwt, const double* xw, double* dxw, double* lo, double* hi) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 3 * n) return;
   double d = __dsub_rn(xwt[i], xw[i]);
@@ -244,10 +271,12 @@ __global__ void k_sweep_box2(int n, const double* xwt, const double* xw, double*
   hi[i] = fmax(a, b);
 }
 __global__ void k_copy_int(int n, const int* a, int* b) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) b[i] = a[i];
 }
-__global__ void k_and_not(int n, int* a, const int* b) {  // a &= !b
+__global__ void k_and_not(int n, int* a, const int* b) {
+  ipc_pdl_wait();  // a &= !b
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && b[i]) a[i] = 0;
 }
@@ -256,6 +285,7 @@ __global__ void k_and_not(int n, int* a, const int* b) {  // a &= !b
 __global__ void k_slot_forces(World W, Cands C, const double* pt_g, const unsigned char* pt_act,
                               const double* ee_g, const unsigned char* ee_act, const double* gnd_gy,
                               double h, double* out) {
+  ipc_pdl_wait();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= W.n_slot) return;
   int e = W.slot_env[s];
@@ -289,6 +319,7 @@ __global__ void k_slot_forces(World W, Cands C, const double* pt_g, const unsign
 }
 __global__ void k_group_forces(World W, const double* slot_f, const unsigned long long* groups, int ng,
                                double* out) {
+  ipc_pdl_wait();
   int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= W.n_env * ng) return;
   int e = q / ng;
@@ -302,6 +333,7 @@ __global__ void k_group_forces(World W, const double* slot_f, const unsigned lon
 }
 __global__ void k_group_distance(World W, Cands C, const double* xw, const unsigned long long* ga,
                                  const unsigned long long* gb, double* out) {
+  ipc_pdl_wait();
   int e = blockIdx.x;
   __shared__ double sh[8];
   int cb0 = W.env_cbody[e];
@@ -336,6 +368,7 @@ __global__ void k_group_distance(World W, Cands C, const double* xw, const unsig
   }
 }
 __global__ void k_ground_distance(World W, const double* xw, const unsigned long long* g, double* out) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= W.n_env) return;
   if (!W.env_has_ground[e]) {
@@ -2187,6 +2220,7 @@ int ipc_world_ground_distance(ipc_world* w, const uint64_t* g, double* out) {
 // ---------------------------------------------------------------------------
 namespace {
 __global__ void k_t_dist(int kind, long long n, const double* st, int* region, double* s, double* g, double* h) {
+  ipc_pdl_wait();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   V3 X[4];
@@ -2203,6 +2237,7 @@ __global__ void k_t_dist(int kind, long long n, const double* st, int* region, d
   for (int k = 0; k < 144; ++k) h[144 * i + k] = H[k];
 }
 __global__ void k_t_ccd(int kind, long long n, const double* px, const double* pdx, double cons, double* a) {
+  ipc_pdl_wait();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   V3 X[4], D[4];
@@ -2214,11 +2249,13 @@ __global__ void k_t_ccd(int kind, long long n, const double* px, const double* p
 }
 template <int N>
 __global__ void k_t_psd(long long n, double* m) {
+  ipc_pdl_wait();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) psd_project<N>(m + (long long)N * N * i, N);
 }
 __global__ void k_t_elastic(int model, long long n, const double* F, double mu, double lam, double* psi, double* P,
                             double* H9) {
+  ipc_pdl_wait();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   M3 f;

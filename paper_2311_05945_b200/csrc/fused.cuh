@@ -400,6 +400,7 @@ static __device__ bool env_candidates(const FusedArgs& A, const double* lo, cons
 IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_broad_sm(World W, const double* __restrict__ lo,
                                                           const double* __restrict__ hi, Cands C,
                                                           const int* env_mask, int cap_d) {
+  ipc_pdl_wait();
   extern __shared__ double bsm[];
   int e = blockIdx.x;
   if (env_mask && !env_mask[e]) return;
@@ -692,6 +693,7 @@ static __device__ bool env_step(const FusedArgs& A, int e, double* sm) {
 // continues its Newton loop from iteration it0 in its own CTA (same state in
 // EnvState / World, same item functions), without per-iteration launches.
 __global__ void __launch_bounds__(256, 1) k_env_newton_rest(FusedArgs A, int it0) {
+  ipc_pdl_wait();
   extern __shared__ double sm[];
   __shared__ int s_e;
   for (;;) {
@@ -716,6 +718,7 @@ __global__ void __launch_bounds__(256, 1) k_env_newton_rest(FusedArgs A, int it0
 // interact, so only the per-env step order matters); a contact-onset solve
 // in one env overlaps with the other envs' later steps.
 __global__ void __launch_bounds__(256, 1) k_env_steps(FusedArgs A, const double* sched, int n_cons, int k0, int k1) {
+  ipc_pdl_wait();
   extern __shared__ double sm[];
   __shared__ int s_e;
   for (;;) {
@@ -736,6 +739,7 @@ __global__ void __launch_bounds__(256, 1) k_env_steps(FusedArgs A, const double*
 }
 
 __global__ void __launch_bounds__(256, 1) k_env_step(FusedArgs A) {
+  ipc_pdl_wait();
   extern __shared__ double sm[];
   __shared__ int s_e;
   for (;;) {

@@ -42,6 +42,7 @@ __device__ __forceinline__ void world_slot(const World& W, const double* __restr
 }
 
 IPC_GLOBAL void k_world(World W, const double* __restrict__ x, double* __restrict__ xw) {
+  ipc_pdl_wait();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < W.n_slot) world_slot(W, x, xw, s);
 }
@@ -51,6 +52,7 @@ IPC_GLOBAL void k_world(World W, const double* __restrict__ x, double* __restric
 // scale is a power of two, so scale * alpha equals repeated halving exactly
 IPC_GLOBAL void k_axpy_env(World W, const double* a, const double* b, const double* alpha, double scale,
                            const int* flag, double* out) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= W.n_dof) return;
   int e = W.dof_env[i];
@@ -58,6 +60,7 @@ IPC_GLOBAL void k_axpy_env(World W, const double* a, const double* b, const doub
 }
 
 IPC_GLOBAL void k_sub(int n, const double* a, const double* b, double* out) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = __dsub_rn(a[i], b[i]);
 }
@@ -213,6 +216,7 @@ __device__ __forceinline__ void chunk_box(const World& W, const double* __restri
 }
 
 IPC_GLOBAL void k_chunk_boxes(World W, const double* __restrict__ lo, const double* __restrict__ hi) {
+  ipc_pdl_wait();
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < W.n_tchunk + W.n_echunk) chunk_box(W, lo, hi, c);
 }
@@ -422,6 +426,7 @@ IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_broad(World W, const double* __r
                                                        const double* __restrict__ hi, Cands C,
                                                        int kind, const int* env_mask, int pass,
                                                        int* blk_cnt) {
+  ipc_pdl_wait();
   if (kind < 0) kind = blockIdx.y;  // all three kinds in one launch
   int e = blockIdx.x;
   if (env_mask && !env_mask[e]) return;
@@ -513,6 +518,7 @@ static __device__ bool ss_filter_env(const World& W, const Cands& S, const doubl
 // and flag the env for a superset rebuild.
 IPC_GLOBAL void k_ss_check(World W, const double* __restrict__ lo, const double* __restrict__ hi, double* bb_lo,
                            double* bb_hi, double pad, const int* env_mask, int* valid, int* rebuild) {
+  ipc_pdl_wait();
   int e = blockIdx.x;
   if (env_mask && !env_mask[e]) {
     if (threadIdx.x == 0) rebuild[e] = 0;
@@ -539,6 +545,7 @@ IPC_GLOBAL void k_ss_check(World W, const double* __restrict__ lo, const double*
 IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_ss_filter(World W, const double* __restrict__ lo,
                                                           const double* __restrict__ hi, Cands S, Cands C,
                                                           const int* env_mask) {
+  ipc_pdl_wait();
   int e = blockIdx.x;
   if (env_mask && !env_mask[e]) return;
   ss_filter_env(W, S, lo, hi, C, e);
@@ -547,6 +554,7 @@ IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_ss_filter(World W, const double*
 // per-env exclusive prefix of candidate counts over flagged envs (one CTA);
 // pre has n_env + 1 entries, pre[n_env] = total
 IPC_GLOBAL void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
+  ipc_pdl_wait();
   __shared__ int part[1024];
   int tid = threadIdx.x, nt = blockDim.x;
   int per = (n_env + nt - 1) / nt;
@@ -571,6 +579,7 @@ IPC_GLOBAL void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
 
 // the three candidate-count prefixes (PT, EE, ground) in one launch
 IPC_GLOBAL void k_prefix3(int n_env, Cands C, const int* flag) {
+  ipc_pdl_wait();
   const int* cnt = blockIdx.x == 0 ? C.n_pt : (blockIdx.x == 1 ? C.n_ee : C.n_gnd);
   int* pre = blockIdx.x == 0 ? C.pre_pt : (blockIdx.x == 1 ? C.pre_ee : C.pre_gnd);
   __shared__ int part[1024];
@@ -680,6 +689,7 @@ __device__ __forceinline__ void body_item(const World& W, const double* __restri
 IPC_GLOBAL void k_body(World W, const double* __restrict__ x, const double* __restrict__ xhat,
                        double h2, int deriv, const int* env_flag, double* val, double* g12,
                        double* h144) {
+  ipc_pdl_wait();
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= W.n_aff) return;
   if (env_flag && !env_flag[W.aff_env[b]]) return;
@@ -744,6 +754,7 @@ __device__ __forceinline__ void tet_item(const World& W, const double* __restric
 
 IPC_GLOBAL void k_tet(World W, const double* __restrict__ x, double h2, int deriv,
                       const int* env_flag, double* val, double* g12, double* hp) {
+  ipc_pdl_wait();
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= W.n_tet) return;
   if (env_flag && !env_flag[W.tet_env[t]]) return;
@@ -815,6 +826,7 @@ __device__ __forceinline__ bool pair_value_item(const World& W, const double* __
 
 IPC_GLOBAL void k_pair_dist(World W, const double* __restrict__ xw, Cands C, int deriv, PairIO io,
                             double* env_min_s) {
+  ipc_pdl_wait();
   const int kind = blockIdx.y;
   const int* pre = kind == 0 ? C.pre_pt : C.pre_ee;
   int total = pre[W.n_env];
@@ -1039,6 +1051,7 @@ __device__ __forceinline__ void pair_hess_item(const World& W, const double* __r
 
 template <int kind>
 __global__ void __launch_bounds__(64) k_pair_hess(World W, const double* __restrict__ xw, Cands C, PairIO io) {
+  ipc_pdl_wait();
   int total = io.work_n[kind];
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < total; w += gridDim.x * blockDim.x)
     pair_hess_item<kind>(W, xw, C, io.work[kind][w], io.work_env[kind][w], io.g[kind], io.h[kind], io.act[kind]);
@@ -1077,6 +1090,7 @@ __device__ __forceinline__ void ground_item(const World& W, const double* __rest
 IPC_GLOBAL void k_ground(World W, const double* __restrict__ xw, Cands C, int deriv,
                          const int* env_flag, double* val, double* gy, double* hyy,
                          double* env_min_s) {
+  ipc_pdl_wait();
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   int e = blockIdx.y;
   if (k >= C.n_gnd[e]) return;
@@ -1211,6 +1225,7 @@ static __device__ void lags_env(const World& W, const double* __restrict__ xw, c
 }
 
 IPC_GLOBAL void k_lags(World W, const double* __restrict__ xw, Cands C, Lags L, const int* env_flag) {
+  ipc_pdl_wait();
   int e = blockIdx.x;
   if (env_flag && !env_flag[e]) return;
   lags_env(W, xw, C, L, e);
@@ -1274,6 +1289,7 @@ __device__ __forceinline__ void friction_item(const World& W, const double* __re
 IPC_GLOBAL void k_friction(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
                            Lags L, double h, int deriv, const int* env_flag, double* val,
                            double* g12, double* hp) {
+  ipc_pdl_wait();
   int total = L.pre[W.n_env];
   for (int gi = blockIdx.x * blockDim.x + threadIdx.x; gi < total; gi += gridDim.x * blockDim.x) {
     int e = find_env(L.pre, W.n_env, gi);
@@ -1302,6 +1318,7 @@ __device__ __forceinline__ void friction_gnd_item(const World& W, const double* 
 IPC_GLOBAL void k_friction_gnd(World W, const double* __restrict__ xw, const double* __restrict__ xw0,
                                Lags L, double h, int deriv, const int* env_flag, double* val,
                                double* g3, double* h3) {
+  ipc_pdl_wait();
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   int e = blockIdx.y;
   if (k >= L.g_n[e]) return;
@@ -1375,6 +1392,7 @@ __device__ __forceinline__ double ccd_ground_item(const World& W, const double* 
 
 IPC_GLOBAL void k_ccd_pairs(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
                             Cands C, double conservative, const int* env_flag, double* env_alpha) {
+  ipc_pdl_wait();
   const int kind = blockIdx.y;
   const int* pre = kind == 0 ? C.pre_pt : C.pre_ee;
   int total = pre[W.n_env];
@@ -1389,6 +1407,7 @@ IPC_GLOBAL void k_ccd_pairs(World W, const double* __restrict__ xw, const double
 
 IPC_GLOBAL void k_ccd_ground(World W, const double* __restrict__ xw, const double* __restrict__ dxw,
                              Cands C, double conservative, const int* env_flag, double* env_alpha) {
+  ipc_pdl_wait();
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   int e = blockIdx.y;
   if (k >= C.n_gnd[e]) return;

@@ -86,6 +86,7 @@ __device__ __forceinline__ int lbvh_delta(const unsigned* code, int n, int i, in
 // leaf l (sorted position) holds primitive bvh_prim[leaf0 + l].
 IPC_GLOBAL void __launch_bounds__(LBVH_THREADS) k_lbvh_build(World W, const double* __restrict__ lo,
                                                              const double* __restrict__ hi) {
+  ipc_pdl_wait();
   const int k = blockIdx.x;
   const int kind = W.tree_kind[k], p0 = W.tree_p0[k], n = W.tree_n[k];
   const int node0 = W.tree_node0[k], leaf0 = W.tree_leaf0[k];

@@ -91,6 +91,7 @@ IPC_GLOBAL void __launch_bounds__(RED_THREADS) k_env_energy(World W, const doubl
                                                              const double* __restrict__ xhat, Terms T,
                                                              Cands C, Lags L, const int* env_flag,
                                                              double* out) {
+  ipc_pdl_wait();
   int e = blockIdx.x;
   if (env_flag && !env_flag[e]) return;
   double s = env_energy_block(W, x, xhat, T, C, L, e);
@@ -283,6 +284,7 @@ IPC_GLOBAL void __launch_bounds__(LS_THREADS) k_ls_value(World W, EnvState S, Ca
                                                            const double* __restrict__ p,
                                                            const double* __restrict__ xhat, double h2, double h,
                                                            double* e_multi) {
+  ipc_pdl_wait();
   extern __shared__ double sxw[];
   int e = blockIdx.x, m = blockIdx.y;
   if (!S.ls_active[e]) return;
@@ -912,6 +914,7 @@ IPC_GLOBAL void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState
                                                                 Lags L, const double* __restrict__ x,
                                                                 const double* __restrict__ xhat,
                                                                 double* p_out, double* g_out, long long* dtm) {
+  ipc_pdl_wait();
   extern __shared__ double sm[];
   int e = blockIdx.x;
   if (!S.newton_active[e]) return;
@@ -930,6 +933,7 @@ __device__ __forceinline__ void newton_begin_env(const EnvState& S, const int* f
   }
 }
 IPC_GLOBAL void k_newton_begin(int n_env, EnvState S, const int* flag) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n_env) newton_begin_env(S, flag, e);
 }
@@ -956,6 +960,7 @@ __device__ __forceinline__ void newton_check_env(const EnvState& S, double h, do
   S.alpha_max[e] = 1.0;
 }
 IPC_GLOBAL void k_newton_check(int n_env, EnvState S, double h, double tol) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n_env) newton_check_env(S, h, tol, e);
 }
@@ -973,6 +978,7 @@ __device__ __forceinline__ void ls_begin_env(const EnvState& S, int* ls_count, i
   }
 }
 IPC_GLOBAL void k_ls_begin(int n_env, EnvState S, int* ls_count) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n_env) ls_begin_env(S, ls_count, e);
 }
@@ -999,6 +1005,7 @@ __device__ __forceinline__ void ls_check_env(const EnvState& S, int* ls_count, i
   }
 }
 IPC_GLOBAL void k_ls_check(World W, EnvState S, int* ls_count, int max_halvings, int* accepted) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < W.n_env) ls_check_env(S, ls_count, max_halvings, accepted, e);
 }
@@ -1008,6 +1015,7 @@ IPC_GLOBAL void k_ls_check(World W, EnvState S, int* ls_count, int max_halvings,
 // have accepted (same floor / halving-count rules, ref solver.py:257-272)
 IPC_GLOBAL void k_ls_check_multi(World W, EnvState S, int* ls_count, int max_halvings, int M,
                                  const double* e_multi, int* accepted) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= W.n_env) return;
   accepted[e] = 0;
@@ -1042,6 +1050,7 @@ IPC_GLOBAL void k_ls_check_multi(World W, EnvState S, int* ls_count, int max_hal
 }
 
 IPC_GLOBAL void k_copy_env(World W, const double* src, double* dst, const int* flag) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= W.n_dof) return;
   if (flag[W.dof_env[i]]) dst[i] = src[i];
@@ -1072,11 +1081,13 @@ __device__ __forceinline__ void al_update_env(const World& W, const EnvState& S,
   if (!has || res <= 1e-6 || S.ls_failed[e]) S.al_active[e] = 0;
 }
 IPC_GLOBAL void k_al_update(World W, EnvState S, int outer) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < W.n_env) al_update_env(W, S, outer, e);
 }
 
 IPC_GLOBAL void k_cons_reset(World W, const double* targets) {
+  ipc_pdl_wait();
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= W.n_cons) return;
   for (int i = 0; i < 12; ++i) {
@@ -1089,10 +1100,12 @@ IPC_GLOBAL void k_cons_reset(World W, const double* targets) {
 
 // x̂ = x + h v + h² a_g (ref bodies.py:292)
 IPC_GLOBAL void k_predictor(World W, double h) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < W.n_dof) W.xhat[i] = W.x[i] + h * W.v[i];
 }
 IPC_GLOBAL void k_predictor_forces(World W, double h) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double hh = h * h;
   if (i < W.n_vert) {
@@ -1107,6 +1120,7 @@ IPC_GLOBAL void k_predictor_forces(World W, double h) {
 }
 
 IPC_GLOBAL void k_finalize(World W, double h, const int* ok) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= W.n_dof) return;
   int e = W.dof_env[i];
@@ -1125,23 +1139,28 @@ __device__ __forceinline__ void kappa_adapt_env(const World& W, const EnvState& 
   if (md < 1e-4 * dhat && k < 1e8 * k0) W.env_kappa[e] = fmin(2.0 * k, 1e8 * k0);
 }
 IPC_GLOBAL void k_kappa_adapt(World W, EnvState S, const int* ok) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < W.n_env && ok[e]) kappa_adapt_env(W, S, e);
 }
 
 IPC_GLOBAL void k_fill(int n, double* a, double v) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
 }
 IPC_GLOBAL void k_fill_flag(int n, double* a, double v, const int* flag) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && flag[i]) a[i] = v;
 }
 IPC_GLOBAL void k_fill_int(int n, int* a, int v) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
 }
 IPC_GLOBAL void k_count(int n, const int* flag, int* out) {
+  ipc_pdl_wait();
   __shared__ int s;
   if (threadIdx.x == 0) s = 0;
   __syncthreads();
@@ -1151,6 +1170,7 @@ IPC_GLOBAL void k_count(int n, const int* flag, int* out) {
   if (threadIdx.x == 0) *out = s;
 }
 IPC_GLOBAL void k_sweep_box(int n, const double* xw, const double* dxw, double* lo, double* hi) {
+  ipc_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 3 * n) return;
   double a = xw[i], b = __dadd_rn(xw[i], dxw[i]);

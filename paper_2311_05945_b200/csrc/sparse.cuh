@@ -205,6 +205,7 @@ static __device__ void visit_element(const AsmIn& A, long long q, Emit emit) {
 }
 
 IPC_GLOBAL void k_asm_count(AsmIn A, int* counts) {
+  ipc_pdl_wait();
   long long n = A.sp.total();
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
     int c = 0;
@@ -214,6 +215,7 @@ IPC_GLOBAL void k_asm_count(AsmIn A, int* counts) {
 }
 
 IPC_GLOBAL void k_asm_emit(AsmIn A, const long long* offs, unsigned long long* keys, double* vals, int* idx) {
+  ipc_pdl_wait();
   long long n = A.sp.total();
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
     long long o = offs[q];
@@ -228,12 +230,14 @@ IPC_GLOBAL void k_asm_emit(AsmIn A, const long long* offs, unsigned long long* k
 
 // head flags of sorted keys (1 at the first item of every run)
 IPC_GLOBAL void k_asm_heads(long long n, const unsigned long long* keys, int* heads) {
+  ipc_pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     heads[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
 }
 
 // run starts: seg_start[u] = first sorted position of unique key u
 IPC_GLOBAL void k_asm_starts(long long n, const int* heads, const long long* uidx, long long* seg_start) {
+  ipc_pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     if (heads[i]) seg_start[uidx[i]] = i;
 }
@@ -243,6 +247,7 @@ IPC_GLOBAL void k_asm_starts(long long n, const int* heads, const long long* uid
 IPC_GLOBAL void k_asm_reduce(long long n_items, long long n_unique, const unsigned long long* keys,
                              const long long* seg_start, const int* perm, const double* vals, double* g,
                              unsigned* bcol, double* bval, int* row_cnt, int* bpos) {
+  ipc_pdl_wait();
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n_unique; u += (long long)gridDim.x * blockDim.x) {
     long long a = seg_start[u], b = (u + 1 < n_unique) ? seg_start[u + 1] : n_items;
     unsigned long long key = keys[a];
@@ -271,6 +276,7 @@ IPC_GLOBAL void k_asm_reduce(long long n_items, long long n_unique, const unsign
 // entries sit at the end of each row's run: col GRAD_COL sorts last)
 IPC_GLOBAL void k_bsr_rowfirst(long long n_unique, const unsigned long long* keys, const long long* seg_start,
                                int* row_first) {
+  ipc_pdl_wait();
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n_unique; u += (long long)gridDim.x * blockDim.x) {
     unsigned row = (unsigned)(keys[seg_start[u]] >> 32);
     if (u == 0 || (unsigned)(keys[seg_start[u - 1]] >> 32) != row) row_first[row] = (int)u;
@@ -356,6 +362,7 @@ __device__ __forceinline__ bool row_live(const Pcg& P, int node) { return P.env_
 // M⁻¹ = inverse of each node's diagonal 3x3 block, and of each affine body's
 // 12x12 diagonal block (aff_blocks); x = 0, r = b = -g, z = p = M⁻¹ r
 IPC_GLOBAL void k_pcg_setup(Pcg P, const double* g) {
+  ipc_pdl_wait();
   for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < P.n_node; nd += gridDim.x * blockDim.x) {
     int e = P.node_env[nd];
     if (!P.env_on[e]) continue;
@@ -400,6 +407,7 @@ IPC_GLOBAL void k_pcg_setup(Pcg P, const double* g) {
 // z = p = M⁻¹ r after k_pcg_setup (a separate pass: affine rows need the
 // whole body's r and Minv12)
 IPC_GLOBAL void k_pcg_setup_z(Pcg P) {
+  ipc_pdl_wait();
   for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < P.n_node; nd += gridDim.x * blockDim.x) {
     if (!P.env_on[P.node_env[nd]]) continue;
     double z[3];
@@ -413,6 +421,7 @@ IPC_GLOBAL void k_pcg_setup_z(Pcg P) {
 
 // chunk partial dots: which 0 -> (r·z, b·b) ; 1 -> p·Ap ; 2 -> (r·z, r·r)
 IPC_GLOBAL void k_pcg_partial(Pcg P, int which) {
+  ipc_pdl_wait();
   __shared__ double sh[2][8];
   int c = blockIdx.x;
   if (c >= P.n_chunk) return;
@@ -451,6 +460,7 @@ IPC_GLOBAL void k_pcg_partial(Pcg P, int which) {
 
 // per-env scalar step. stage 0: init rz, bb; 1: pAp; 2: new rz / rr, β, convergence
 IPC_GLOBAL void k_pcg_env(Pcg P, int n_env, int stage, double rtol2) {
+  ipc_pdl_wait();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_env || !P.env_on[e]) return;
   if (stage != 0 && !P.env_live[e]) return;
@@ -475,6 +485,7 @@ IPC_GLOBAL void k_pcg_env(Pcg P, int n_env, int stage, double rtol2) {
 // direction, fallback and norms per env (ref solver.py:241): p = x unless the
 // solve produced non-finite values or an ascent direction, then p = -g
 IPC_GLOBAL void k_pcg_finish(World W, EnvState S, Pcg P, const double* g, double* p_out, double* g_out) {
+  ipc_pdl_wait();
   __shared__ double sh[3][8];
   int e = blockIdx.x;
   if (!S.newton_active[e]) return;
@@ -632,6 +643,7 @@ __device__ __forceinline__ void block_env_sums(const Pcg& P, int e, const double
 // needed. cnt[0..1]: live-env counters (alternating), cnt[2]: cumulative
 // iteration count (stats).
 IPC_GLOBAL void k_pcg_coop(Pcg P, int n_env, double rtol2, int max_iters, int* cnt, double* part1, double* part2) {
+  ipc_pdl_wait();
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[64];
   __shared__ double es[6];  // env sums: cur (rz, rr), part1 (pAp, -), nxt (rz, rr)

@@ -27,6 +27,12 @@
 #endif
 #include <stdint.h>
 
+// Programmatic dependent launch: the engine launches its kernels with
+// programmatic stream serialization, so a kernel may be scheduled while its
+// predecessor drains; every kernel waits here before touching memory (a no-op
+// when launched without the attribute).
+__device__ __forceinline__ void ipc_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 namespace ipc {
 
 struct Cands {
