@@ -133,7 +133,7 @@ static inline void prof_end(int kid, cudaStream_t s) {
 // predecessor on the stream drains and waits in ipc_pdl_wait() before its
 // first memory access, so the ≈25 dependent launches of a Newton iteration
 // overlap their launch latency with the previous kernel's tail.
-static bool g_pdl = getenv("IPC_PDL") == nullptr || getenv("IPC_PDL")[0] != '0';
+static bool g_pdl = true;  // read at every world creation (IPC_PDL)
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                                      Args&&... args) {
@@ -1703,6 +1703,7 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     for (int i = 0; i < 3; ++i) CK(cudaStreamCreateWithFlags(&w->side[i], cudaStreamNonBlocking));
     for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&w->fj[i], cudaEventDisableTiming));
     if (w->fused_timers_on && !w->sparse) w->fused_setup();  // timer block for the batched solve too
+    g_pdl = getenv("IPC_PDL") == nullptr || getenv("IPC_PDL")[0] != '0';
     CK(cudaDeviceSynchronize());
     *out = w;
     return 0;
