@@ -87,6 +87,76 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+class RetractBatch:
+    """Persistent retraction batch: E grasps of one gripper model on fixed
+    objects. The object meshes and the hand topology (triangles, per-link
+    ranges) are packed once; run(poses, opened) evaluates the batched FK,
+    the hand's world vertices and the palm normals and launches the probe
+    search (ipc_repair_retract, every array uploaded per call). Same arrays,
+    bit for bit, as retract_batch packs for a shared-model batch."""
+
+    def __init__(self, gripper, obj_meshes):
+        self.g0 = gripper
+        self.E = E = len(obj_meshes)
+        self.sched, self.end = retraction_schedule()
+        g0 = gripper
+        self.names = names = sorted(g0.links)  # == Gripper.bodies() order
+        nv = [len(g0.links[ln].mesh.vertices) for ln in names]
+        nt = [len(g0.links[ln].mesh.triangles) for ln in names]
+        vo = np.concatenate([[0], np.cumsum(nv)[:-1]])
+        tri_one = np.concatenate([np.asarray(g0.links[ln].mesh.triangles, dtype=np.int32) + o
+                                  for ln, o in zip(names, vo)]).astype(np.int32)
+        per_env = int(np.sum(nv))
+        L = len(names)
+        self.lo = np.array([jt.lower for jt in g0.joints])
+        self.hi = np.array([jt.upper for jt in g0.joints])
+        self.rest = [g0.links[ln].mesh.vertices[None] for ln in names]
+        self.arrs = dict(
+            env_link=_i32(np.arange(E + 1) * L),
+            link_vert=_i32(np.concatenate([[0], np.cumsum(np.tile(nv, E))])),
+            link_tri=_i32(np.concatenate([[0], np.cumsum(np.tile(nt, E))])),
+            hand_t=_i32((tri_one[None] + (per_env * np.arange(E, dtype=np.int32))[:, None, None]).reshape(-1, 3)),
+            obj_v=_f64(np.concatenate([m[0] for m in obj_meshes])) if E else _f64(np.zeros((0, 3))),
+            obj_t=_i32(np.concatenate([m[1] for m in obj_meshes]).reshape(-1, 3)) if E else _i32(np.zeros((0, 3))),
+            env_ov=_i32(np.concatenate([[0], np.cumsum([len(m[0]) for m in obj_meshes])])),
+            env_ot=_i32(np.concatenate([[0], np.cumsum([np.size(m[1]) // 3 for m in obj_meshes])])),
+            retr=_f64(self.sched))
+
+    def hand_world(self, poses, opened):
+        """World vertices of every link of every env, (E * per_env, 3)."""
+        from .batch import batch_fk
+
+        fk = batch_fk(self.g0, np.asarray(poses, dtype=np.float64),
+                      np.clip(np.asarray(opened, dtype=np.float64), self.lo, self.hi))
+        per = []
+        for ln, x0 in zip(self.names, self.rest):
+            t = fk[ln]
+            a = t[:, :3, :3].reshape(-1, 9).reshape(-1, 3, 3)
+            per.append(x0 @ np.transpose(a, (0, 2, 1)) + t[:, None, :3, 3])
+        return np.concatenate(per, axis=1).reshape(-1, 3)
+
+    def run(self, poses, opened):
+        """(cleared bool[E], retraction_m float[E], probe_index int[E])"""
+        lib = N.load()
+        E = self.E
+        if E == 0:
+            return np.zeros(0, bool), np.zeros(0), np.zeros(0, np.int32)
+        a = self.arrs
+        hv = _f64(self.hand_world(poses, opened))
+        normal = _f64(np.asarray(poses, dtype=np.float64)[:, :3, :3] @ self.g0.palm_normal_local)
+        d = N.RepairDesc(E, N.ptr(a["env_link"], N._i32p), N.ptr(a["link_vert"], N._i32p),
+                         N.ptr(a["link_tri"], N._i32p), N.ptr(hv, N._f64p),
+                         N.ptr(a["hand_t"], N._i32p), N.ptr(a["env_ov"], N._i32p),
+                         N.ptr(a["env_ot"], N._i32p), N.ptr(a["obj_v"], N._f64p),
+                         N.ptr(a["obj_t"], N._i32p), N.ptr(normal, N._f64p),
+                         len(self.sched), N.ptr(a["retr"], N._f64p))
+        idx = np.zeros(E, np.int32)
+        N.check(lib.ipc_repair_retract(N.C.byref(d), N.ptr(idx, N._i32p)))
+        cleared = idx < len(self.sched)
+        retraction = np.where(cleared, self.sched[np.minimum(idx, len(self.sched) - 1)], self.end)
+        return cleared, retraction, idx
+
+
 def retract_batch(grippers, poses, opened, obj_meshes):
     """The probe loop of ref repair.py:98-113 for E envs in one launch.
 

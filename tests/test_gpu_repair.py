@@ -247,3 +247,16 @@ def test_dexterous_hand_repair_matches_reference(golden):
         pts.append(_hand_points(g))
     got = max_penetration_batch(pts, meshes)
     np.testing.assert_allclose(got, z["pen_before"], rtol=1e-12, atol=1e-15)
+
+
+def test_retract_batch_persistent_equals_one_shot():
+    """RetractBatch (objects and hand topology packed once) gives the same
+    probe indices as retract_batch on the dexterous hand."""
+    import bench
+    from paper_2311_05945_b200.robot.repair import RetractBatch, retract_batch
+
+    model, objs, poses, joints, grippers, opened, meshes = bench._repair_inputs(48, 7, "dex")
+    a = retract_batch(grippers, poses, opened, meshes)
+    b = RetractBatch(grippers[0], meshes).run(poses, opened)
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
