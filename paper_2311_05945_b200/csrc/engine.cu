@@ -449,6 +449,7 @@ struct ipc_world {
   double *xlo = nullptr, *xhi = nullptr, *xwt = nullptr;
   double *env_alpha = nullptr;
   int *enable = nullptr, *ok = nullptr, *al_flag = nullptr, *accepted = nullptr, *ls_count = nullptr, *d_count = nullptr;
+  int* env_order = nullptr;  // start order of the per-env dense-solve CTAs (k_env_order)
   int* h_count = nullptr;  // pinned
   double* slot_force = nullptr;
   double* d_targets = nullptr;
@@ -607,7 +608,7 @@ struct ipc_world {
     if (ss_pad > 0.0 && &cs != &ss) {
       IPC_LAUNCH(kid, st, k_ss_check, n_env, 256, 0, W, lo, hi, bb_lo, bb_hi, ss_pad, env_mask, ss_valid, ss_rebuild);
       launch_broad_raw(ss, bb_lo, bb_hi, ss_rebuild, kid);
-      IPC_LAUNCH(kid, st, k_ss_filter, n_env, BP_THREADS, 0, W, lo, hi, ss.c, cs.c, env_mask);
+      IPC_LAUNCH(kid, st, k_ss_filter, n_env, BP_THREADS, 0, W, lo, hi, ss.c, cs.c, env_mask, env_order);
       return;
     }
     launch_broad_raw(cs, lo, hi, env_mask, kid);
@@ -615,7 +616,7 @@ struct ipc_world {
   void launch_broad_raw(CandStore& cs, const double* lo, const double* hi, const int* env_mask, int kid) {
     if (broad_smem && bp_z == 1) {
       IPC_LAUNCH(kid, st, k_broad_sm, n_env, BP_THREADS, broad_smem, W, lo, hi, cs.c, env_mask,
-                 (int)(broad_smem / sizeof(double)));
+                 (int)(broad_smem / sizeof(double)), env_order);
       return;
     }
     IPC_LAUNCH(kid, st, k_chunk_boxes, nblk(W.n_tchunk + W.n_echunk, 128), 128, 0, W, lo, hi);
@@ -724,7 +725,7 @@ struct ipc_world {
 
   void energy(const double* x, CandStore& cs, PairBufs& pb, const int* flag, double* out) {
     Terms T{body_val, tet_val, pb.pt_val, pb.ee_val, pb.gnd_val, fr_val, frg_val, nullptr};
-    IPC_LAUNCH(K_ENERGY, st, k_env_energy, n_env, RED_THREADS, 0, W, x, W.xhat, T, cs.c, L, flag, out);
+    IPC_LAUNCH(K_ENERGY, st, k_env_energy, n_env, RED_THREADS, 0, W, x, W.xhat, T, cs.c, L, flag, out, env_order);
   }
 
   // ---- one Newton iteration = three fixed launch sequences ----------------
@@ -741,9 +742,10 @@ struct ipc_world {
       fork_to(side[0], fj[0]);
       Terms T{body_val, tet_val, pb_dcd.pt_val, pb_dcd.ee_val, pb_dcd.gnd_val, fr_val, frg_val, nullptr};
       IPC_LAUNCH(K_ENERGY, side[0], k_env_energy, n_env, RED_THREADS, 0, W, W.x, W.xhat, T, dcd.c, L, S.newton_active,
-                 S.e0);
+                 S.e0, env_order);
+      IPC_LAUNCH(K_MISC, st, k_env_order, 1, 1024, 0, n_env, S.newton_active, dcd.c, L, env_order);
       IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, dense_smem, W, S, D_with(pb_dcd), dcd.c, L, W.x,
-                 W.xhat, W.p, W.grad, dense_timers());
+                 W.xhat, W.p, W.grad, dense_timers(), env_order);
       join_from(side[0], fj[1]);
     }
     IPC_LAUNCH(K_MISC, st, k_newton_check, nblk(n_env, 128), 128, 0, n_env, S, cfg.h, cfg.newton_tol);
@@ -768,7 +770,7 @@ struct ipc_world {
   void seq_ls_round(const ipc_step_config& cfg, int M) {
     if (!sparse) {
       IPC_LAUNCH(K_ENERGY, st, k_ls_value, dim3(n_env, M), LS_THREADS, (size_t)3 * max_slots * sizeof(double), W, S,
-                 sweep.c, L, W.x, W.p, W.xhat, cfg.h * cfg.h, cfg.h, e_multi);
+                 sweep.c, L, W.x, W.p, W.xhat, cfg.h * cfg.h, cfg.h, e_multi, env_order);
     } else {
       double scale = 1.0;
       for (int m = 0; m < M; ++m, scale *= 0.5) {
@@ -1667,6 +1669,12 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     w->enable = P.alloc<int>(ne);
     w->ok = P.alloc<int>(ne); w->al_flag = S.al_active; w->accepted = P.alloc<int>(ne);
     w->ls_count = P.alloc<int>(ne); w->d_count = P.alloc<int>(1);
+    w->env_order = P.alloc<int>(ne);
+    {
+      std::vector<int> iota(ne);
+      for (int e = 0; e < ne; ++e) iota[e] = e;
+      CK(cudaMemcpy(w->env_order, iota.data(), sizeof(int) * ne, cudaMemcpyHostToDevice));
+    }
     w->env_alpha = P.alloc<double>(ne);
     CK(cudaMallocHost(&w->h_count, sizeof(int)));
     // capacities: exhaustive for small envs, bounded for large ones

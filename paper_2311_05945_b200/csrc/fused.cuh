@@ -399,10 +399,10 @@ static __device__ bool env_candidates(const FusedArgs& A, const double* lo, cons
 // (all three kinds; chunk boxes built in shared memory).
 IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_broad_sm(World W, const double* __restrict__ lo,
                                                           const double* __restrict__ hi, Cands C,
-                                                          const int* env_mask, int cap_d) {
+                                                          const int* env_mask, int cap_d, const int* order) {
   ipc_pdl_wait();
   extern __shared__ double bsm[];
-  int e = blockIdx.x;
+  int e = order ? order[blockIdx.x] : blockIdx.x;
   if (env_mask && !env_mask[e]) return;
   env_broad_sm(W, lo, hi, C, e, bsm, cap_d);
 }

@@ -544,9 +544,9 @@ IPC_GLOBAL void k_ss_check(World W, const double* __restrict__ lo, const double*
 
 IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_ss_filter(World W, const double* __restrict__ lo,
                                                           const double* __restrict__ hi, Cands S, Cands C,
-                                                          const int* env_mask) {
+                                                          const int* env_mask, const int* order) {
   ipc_pdl_wait();
-  int e = blockIdx.x;
+  int e = order ? order[blockIdx.x] : blockIdx.x;
   if (env_mask && !env_mask[e]) return;
   ss_filter_env(W, S, lo, hi, C, e);
 }

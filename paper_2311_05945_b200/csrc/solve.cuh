@@ -90,9 +90,9 @@ static __device__ double env_energy_block(const World& W, const double* __restri
 IPC_GLOBAL void __launch_bounds__(RED_THREADS) k_env_energy(World W, const double* __restrict__ x,
                                                              const double* __restrict__ xhat, Terms T,
                                                              Cands C, Lags L, const int* env_flag,
-                                                             double* out) {
+                                                             double* out, const int* order) {
   ipc_pdl_wait();
-  int e = blockIdx.x;
+  int e = order ? order[blockIdx.x] : blockIdx.x;
   if (env_flag && !env_flag[e]) return;
   double s = env_energy_block(W, x, xhat, T, C, L, e);
   if (threadIdx.x == 0) out[e] = s;
@@ -283,10 +283,10 @@ IPC_GLOBAL void __launch_bounds__(LS_THREADS) k_ls_value(World W, EnvState S, Ca
                                                            const double* __restrict__ x,
                                                            const double* __restrict__ p,
                                                            const double* __restrict__ xhat, double h2, double h,
-                                                           double* e_multi) {
+                                                           double* e_multi, const int* order) {
   ipc_pdl_wait();
   extern __shared__ double sxw[];
-  int e = blockIdx.x, m = blockIdx.y;
+  int e = order ? order[blockIdx.x] : blockIdx.x, m = blockIdx.y;
   if (!S.ls_active[e]) return;
   double a = S.alpha[e] * ldexp(1.0, -m);
   double tot = ls_value_block(W, C, L, x, p, xhat, h2, h, a, e, sxw);
@@ -910,13 +910,56 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
   dmark(5);
 }
 
+// Order in which the per-env CTAs of the dense solve start: most records
+// first (a heavy env starting in the last wave is the kernel's tail), active
+// before converged envs, ties by env index. One CTA, bitonic sort of
+// (records << 12 | (4095 - env)) in shared memory; identity beyond 4096 envs.
+constexpr int ORDER_MAX = 4096;
+IPC_GLOBAL void __launch_bounds__(1024) k_env_order(int n_env, const int* active, Cands C, Lags L, int* order) {
+  ipc_pdl_wait();
+  __shared__ long long key[ORDER_MAX];
+  int tid = threadIdx.x;
+  if (n_env > ORDER_MAX) {
+    for (int e = tid; e < n_env; e += blockDim.x) order[e] = e;
+    return;
+  }
+  int n2 = 1;
+  while (n2 < n_env) n2 <<= 1;
+  for (int i = tid; i < n2; i += blockDim.x) {
+    long long k = -1;  // padding sorts last
+    if (i < n_env) {
+      long long w = active[i] ? 1 + (long long)C.n_pt[i] + C.n_ee[i] + L.n[i] : 0;
+      k = (w << 12) | (ORDER_MAX - 1 - i);
+    }
+    key[i] = k;
+  }
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < n2; i += blockDim.x) {
+        int j = i ^ stride;
+        if (j > i) {
+          bool desc = (i & size) == 0;  // descending overall
+          long long a = key[i], b = key[j];
+          if (desc ? a < b : a > b) {
+            key[i] = b;
+            key[j] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = tid; i < n_env; i += blockDim.x) order[i] = ORDER_MAX - 1 - (int)(key[i] & (ORDER_MAX - 1));
+}
+
 IPC_GLOBAL void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState S, Derivs D, Cands C,
                                                                 Lags L, const double* __restrict__ x,
                                                                 const double* __restrict__ xhat,
-                                                                double* p_out, double* g_out, long long* dtm) {
+                                                                double* p_out, double* g_out, long long* dtm,
+                                                                const int* order) {
   ipc_pdl_wait();
   extern __shared__ double sm[];
-  int e = blockIdx.x;
+  int e = order ? order[blockIdx.x] : blockIdx.x;
   if (!S.newton_active[e]) return;
   dense_solve_block(W, S, D, C, L, x, xhat, p_out, g_out, e, sm, dtm);
 }
