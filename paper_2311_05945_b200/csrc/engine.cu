@@ -1078,7 +1078,7 @@ struct ipc_world {
   // ---------------- fused per-env step (dense worlds) ----------------
   bool fused_on = false;    // IPC_FUSED=1: whole step in the fused per-env kernel
   bool fused_timers_on = false;  // IPC_FUSED_TIMERS=1: per-phase SM cycles of the fused kernels
-  int tail_envs = 148;      // batched schedule: hand off to per-env CTAs at <= this many active envs
+  int tail_envs = 444;      // batched schedule: hand off to per-env CTAs at <= this many active envs (3 x SMs)
   int fused_max_dof = 128;  // dense LDLᵀ in shared memory: n² doubles
   int* fq = nullptr;
   long long* d_fstat = nullptr;
@@ -1607,7 +1607,10 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
       if (fz) w->fused_on = fz[0] == '1';
       const char* ftz = getenv("IPC_FUSED_TIMERS");
       w->fused_timers_on = ftz && ftz[0] == '1';
-      w->tail_envs = w->n_sm;
+      // hand-off at three waves of the per-env kernel (one CTA per SM): a
+      // batched iteration costs about three per-env iterations here
+      // (measured: 148 / 296 / 444 / 518 envs -> 2.58 / 2.53 / 2.47 / 2.75 ms per step)
+      w->tail_envs = 3 * w->n_sm;
       const char* tz = getenv("IPC_TAIL");
       if (tz) w->tail_envs = atoi(tz);
       const char* ez = getenv("IPC_BROAD_ITEMS");

@@ -304,7 +304,7 @@ struct Derivs {
   double *frg_g, *frg_h;             // 3, 9 per ground lag
 };
 
-constexpr int DENSE_THREADS = 256;
+constexpr int DENSE_THREADS = 256;  // launch width of k_dense_solve and the fused kernels
 constexpr int DENSE_MAX_N = 160;  // largest env system on the dense path (engine.cu DENSE_MAX)
 constexpr int DENSE_REG_N = 64;   // warp-register substitution up to this size
 constexpr int LDL_NB = 12;        // panel width of the blocked LDLᵀ
@@ -406,7 +406,8 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
     s_pkrc[tid] = (unsigned char)(r << 4 | (r + rem));
   }
   int ntile = 3 * (n / 3) * (n / 3 + 1) / 2;
-  for (int v0 = 0; v0 < total; v0 += DENSE_THREADS) {
+  const int nthr = blockDim.x, nwarp = nthr >> 5;
+  for (int v0 = 0; v0 < total; v0 += nthr) {
     // ordered compaction of the contributing records of this window
     int v = v0 + tid, t = 0, j = v;
     bool on = false;
@@ -422,7 +423,7 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
     __syncthreads();
     if (tid == 0) {
       int acc = 0;
-      for (int w = 0; w < DENSE_THREADS / 32; ++w) {
+      for (int w = 0; w < nwarp; ++w) {
         int c = wtot[w];
         wtot[w] = acc;
         acc += c;
@@ -477,7 +478,7 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
         for (int a = 0; a < 4; ++a) R.grp[4 * tid + a] = hgrp[4 * (k0 + tid) + a];
       }
       // stage Hessians (unpacked), gradients and lever arms (all threads)
-      for (int i = tid; i < nr * 102; i += DENSE_THREADS) {
+      for (int i = tid; i < nr * 102; i += nthr) {
         int k = i / 102, q = i - 102 * k;
         int src = hsrc[k0 + k], t = src >> 28, j = src & ((1 << 28) - 1);
         double val = 0.0;
@@ -513,7 +514,7 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
       }
       __syncthreads();
       // records of the chunk touching each group pair (A ≥ B)
-      for (int P = wid; P < npairs; P += DENSE_THREADS / 32) {
+      for (int P = wid; P < npairs; P += nwarp) {
         int A = (int)((sqrtf(8.0f * (float)P + 1.0f) - 1.0f) * 0.5f);
         while ((A + 1) * (A + 2) / 2 <= P) ++A;
         while (A * (A + 1) / 2 > P) --A;
@@ -528,7 +529,7 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
       }
       __syncthreads();
       // tile owners: H[r][c0..c0+2] += Σ_a w_a(r) Σ_b w_b(c) Hs[ia][ib] per record
-      for (int T = tid; T < ntile; T += DENSE_THREADS) {
+      for (int T = tid; T < ntile; T += nthr) {
         int r, c0;
         tile_rc(T, &r, &c0);
         int gr = gi[r], gc = gi[c0];
@@ -577,7 +578,7 @@ static __device__ void assemble_records(const World& W, const Derivs& D, const C
         if (ncol > 2) H[r * n + c0 + 2] = h2;
       }
       // owners of the gradient: records touching the DoF's group
-      for (int r = tid; r < n; r += DENSE_THREADS) {
+      for (int r = tid; r < n; r += nthr) {
         int gr = gi[r], iR, jR;
         lift_ij(r - dkey[r], &iR, &jR);
         unsigned bm = pm[gr * (gr + 1) / 2 + gr];
@@ -698,7 +699,7 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
   {
     __shared__ unsigned sb[DENSE_MAX_N / 32 + 1];
     int nw = (n + 31) / 32;
-    for (int w0 = 0; w0 < nw; w0 += DENSE_THREADS / 32) {
+    for (int w0 = 0; w0 < nw; w0 += (int)(blockDim.x >> 5)) {
       int d = 32 * (w0 + (tid >> 5)) + (tid & 31);
       unsigned b = __ballot_sync(0xffffffffu, d < n && dkey[d] == d);
       if ((tid & 31) == 0 && w0 + (tid >> 5) < nw) sb[w0 + (tid >> 5)] = b;
