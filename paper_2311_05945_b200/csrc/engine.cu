@@ -1133,6 +1133,7 @@ struct ipc_world {
 
   FusedArgs fused_args(const ipc_step_config& cfg) {
     FusedArgs A{};
+    A.order = env_order;
     A.W = W;
     A.S = S;
     A.dc = dcd.c;

@@ -67,6 +67,7 @@ struct FusedArgs {
   int *ok, *accepted, *ls_count;
   const double* targets;
   int* queue;        // [0]: next env
+  const int* order;  // queue position -> env (nullptr: identity)
   long long* stat;   // [0] Newton iterations, [1] line-search trials
   long long* timers; // [FT_N] phase cycles, or nullptr (timers off)
   double h, newton_tol, ccd_cons;
@@ -701,8 +702,9 @@ __global__ void __launch_bounds__(256, 1) k_env_newton_rest(FusedArgs A, int it0
     if (threadIdx.x == 0) {
       int e = A.W.n_env;
       if (!*(volatile int*)A.dc.overflow && !*(volatile int*)A.sw.overflow)
-        do {
+        do {  // heaviest envs first (k_env_order of the last batched iteration)
           e = atomicAdd(A.queue, 1);
+          if (e < A.W.n_env && A.order) e = A.order[e];
         } while (e < A.W.n_env && !A.S.newton_active[e]);
       s_e = e;
     }
