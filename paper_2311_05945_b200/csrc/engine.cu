@@ -743,7 +743,6 @@ struct ipc_world {
       Terms T{body_val, tet_val, pb_dcd.pt_val, pb_dcd.ee_val, pb_dcd.gnd_val, fr_val, frg_val, nullptr};
       IPC_LAUNCH(K_ENERGY, side[0], k_env_energy, n_env, RED_THREADS, 0, W, W.x, W.xhat, T, dcd.c, L, S.newton_active,
                  S.e0, env_order);
-      IPC_LAUNCH(K_MISC, st, k_env_order, 1, 1024, 0, n_env, S.newton_active, dcd.c, L, env_order);
       IPC_LAUNCH(K_DENSE, st, k_dense_solve, n_env, DENSE_THREADS, dense_smem, W, S, D_with(pb_dcd), dcd.c, L, W.x,
                  W.xhat, W.p, W.grad, dense_timers(), env_order);
       join_from(side[0], fj[1]);
@@ -1011,6 +1010,9 @@ struct ipc_world {
 
   void newton_solve(const ipc_step_config& cfg) {
     IPC_LAUNCH(K_MISC, st, k_newton_begin, nblk(n_env, 128), 128, 0, n_env, S, al_flag);
+    // start order of the per-env CTAs for this solve, from the latest
+    // candidate and lag counts (only scheduling: any order gives the same bits)
+    if (!sparse) IPC_LAUNCH(K_MISC, st, k_env_order, 1, 1024, 0, n_env, S.newton_active, dcd.c, L, env_order);
     bool graphs = use_graphs && !sparse;
     if (graphs) ensure_graphs(cfg);
     int tail = 0;
