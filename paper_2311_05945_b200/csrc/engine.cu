@@ -212,7 +212,8 @@ __global__ void k_status(int n_env, const int* newton, const int* ls, const int*
 }
 // Device-driven Newton loop control (the body of the loop graph's WHILE
 // node, after the SWITCH that ran one Newton iteration (mode 0) or one
-// line-search round (mode 1)). Mirrors the host loop of newton_solve: line
+// line-search round of LS_M (mode 1) or, from the second round of an
+// iteration, LS_M2 speculative trials (mode 2)). Mirrors the host loop of newton_solve: line
 // search rounds while any env is still backtracking and fewer than
 // max_halvings+1 trials were made, then the next iteration unless no env is
 // active, the iteration cap is reached, the active count fits the per-env
@@ -221,8 +222,8 @@ __global__ void k_status(int n_env, const int* newton, const int* ls, const int*
 // [2] line-search rounds (stats), [3] active envs at exit, [4] overflow,
 // [5] mode of the body that just ran (set here for the next one; 0 at launch)
 __global__ void k_loop_ctl(int n_env, const int* newton, const int* ls, const int* ov1, const int* ov2, int* ctl,
-                           int max_iters, int max_halvings, int ls_m, int tail, cudaGraphConditionalHandle h_loop,
-                           cudaGraphConditionalHandle h_mode) {
+                           int max_iters, int max_halvings, int ls_m, int ls_m2, int tail,
+                           cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_mode) {
   ipc_pdl_wait();
   __shared__ int a, b;
   if (threadIdx.x == 0) a = b = 0;
@@ -242,7 +243,7 @@ __global__ void k_loop_ctl(int n_env, const int* newton, const int* ls, const in
     ctl[0] += 1;
     ctl[1] = 1;
   } else {
-    ctl[1] += ls_m;
+    ctl[1] += ctl[5] == 1 ? ls_m : ls_m2;
   }
   ctl[2] += 1;
   ctl[3] = a;
@@ -251,7 +252,7 @@ __global__ void k_loop_ctl(int n_env, const int* newton, const int* ls, const in
   if (ov) {
     loop = 0;
   } else if (b && ctl[1] < max_halvings + 1) {
-    mode = 1;
+    mode = ctl[5] == 0 ? 1 : 2;  // first follow-up round: LS_M trials, then LS_M2
   } else if (a == 0 || ctl[0] >= max_iters || (tail > 0 && a <= tail)) {
     loop = 0;
   }
@@ -786,9 +787,11 @@ struct ipc_world {
   void seq_ls(const ipc_step_config& cfg) { seq_ls_round(cfg, 1); }
 
   // M speculative halvings in one round (follow-up rounds only)
-  static constexpr int LS_M = 8;
+  static constexpr int LS_M = 8;    // trials of an iteration's first follow-up round
+  static constexpr int LS_M2 = 32;  // trials of later rounds (few envs still backtracking)
   double* e_multi = nullptr;
   void seq_ls_multi(const ipc_step_config& cfg) { seq_ls_round(cfg, LS_M); }
+  void seq_ls_multi2(const ipc_step_config& cfg) { seq_ls_round(cfg, LS_M2); }
 
   // ---- CUDA graphs of the sequences (dense worlds) ------------------------
   struct Graph {
@@ -796,7 +799,7 @@ struct ipc_world {
     long long kernels = 0;
     std::vector<Prof::Rec> timed;  // event pairs recorded inside the graph
   };
-  Graph g_iter, g_ls;
+  Graph g_iter, g_ls, g_ls2;
   bool graphs_valid = false;
   bool use_graphs = true;
   ipc_step_config graph_cfg{};
@@ -853,7 +856,7 @@ struct ipc_world {
   void drop_graphs() {
     if (loop_exec) cudaGraphExecDestroy(loop_exec);
     loop_exec = nullptr;
-    for (Graph* g : {&g_iter, &g_ls}) {
+    for (Graph* g : {&g_iter, &g_ls, &g_ls2}) {
       if (g->exec) cudaGraphExecDestroy(g->exec);
       g->exec = nullptr;
       for (auto& r : g->timed) { prof.pool.push_back(r.a); prof.pool.push_back(r.b); }
@@ -895,6 +898,7 @@ struct ipc_world {
       seq_ls(cfg);
     });
     capture(g_ls, [&] { seq_ls_multi(cfg); });
+    capture(g_ls2, [&] { seq_ls_multi2(cfg); });
     graph_cfg = cfg;
     graph_prof_on = prof.on;
     graph_prof_mask = prof.mask;
@@ -964,10 +968,11 @@ struct ipc_world {
     sp.type = cudaGraphNodeTypeConditional;
     sp.conditional.handle = h_mode;
     sp.conditional.type = cudaGraphCondTypeSwitch;
-    sp.conditional.size = 2;
+    sp.conditional.size = 3;
     cudaGraphNode_t snode;
     CK(cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
-    cudaGraph_t b_iter = sp.conditional.phGraph_out[0], b_ls = sp.conditional.phGraph_out[1];
+    cudaGraph_t b_iter = sp.conditional.phGraph_out[0], b_ls = sp.conditional.phGraph_out[1],
+                b_ls2 = sp.conditional.phGraph_out[2];
     const bool prof_on = prof.on;
     prof.on = false;  // conditional bodies take no event nodes
     auto capture_into = [&](cudaGraph_t target, const cudaGraphNode_t* deps, size_t ndep, auto fn) {
@@ -986,11 +991,12 @@ struct ipc_world {
       seq_ls(cfg);
     });
     capture_into(b_ls, nullptr, 0, [&] { seq_ls_multi(cfg); });
+    capture_into(b_ls2, nullptr, 0, [&] { seq_ls_multi2(cfg); });
     // the control kernel follows the SWITCH in the body
     capture_into(body, &snode, 1, [&] {
       k_loop_ctl<<<1, 1024, 0, st>>>(n_env, S.newton_active, S.ls_active, dcd.c.overflow, sweep.c.overflow,
-                                     d_loopctl, cfg.max_newton_iters, cfg.max_line_search_halvings, LS_M, tail,
-                                     h_loop, h_mode);
+                                     d_loopctl, cfg.max_newton_iters, cfg.max_line_search_halvings, LS_M, LS_M2,
+                                     tail, h_loop, h_mode);
       CK(cudaPeekAtLastError());
     });
     CK(cudaGraphInstantiate(&loop_exec, g, 0));
@@ -1058,8 +1064,12 @@ struct ipc_world {
       ++stat_iters;
       ++stat_ls_rounds;
       Status s = status();
-      for (int ls = 1; s.ls && ls < cfg.max_line_search_halvings + 1; ls += LS_M) {
-        if (graphs) run(g_ls); else seq_ls_multi(cfg);
+      for (int ls = 1, r = 0; s.ls && ls < cfg.max_line_search_halvings + 1; ls += r++ == 0 ? LS_M : LS_M2) {
+        if (r == 0) {
+          if (graphs) run(g_ls); else seq_ls_multi(cfg);
+        } else {
+          if (graphs) run(g_ls2); else seq_ls_multi2(cfg);
+        }
         ++stat_ls_rounds;
         s = status();
       }
@@ -1589,7 +1599,7 @@ int ipc_world_create(const ipc_world_desc* d, ipc_world** out) {
     w->xhi = P.alloc<double>(3 * (size_t)d->n_slot);
     w->slot_force = P.alloc<double>(3 * (size_t)d->n_slot);
     w->d_status = P.alloc<int>(4);
-    w->e_multi = P.alloc<double>((size_t)ipc_world::LS_M * ne);
+    w->e_multi = P.alloc<double>((size_t)ipc_world::LS_M2 * ne);
     CK(cudaMallocHost(&w->h_status, 8 * sizeof(int)));
     w->d_targets = P.alloc<double>(12 * (size_t)d->n_cons);
     w->h_env_slot.assign(d->env_slot, d->env_slot + ne + 1);
