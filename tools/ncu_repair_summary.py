@@ -1,7 +1,9 @@
 """Summarise an ncu --set full capture of k_repair_retract into the JSON
 bench.py reads for the config-4 roofline (profiles/r1e_repair_ncu.json).
 
-    python tools/ncu_repair_summary.py gpurun_out/repair_retract.ncu-rep ENVS SEED OUT.json
+    python tools/ncu_repair_summary.py gpurun_out/repair_retract.ncu-rep ENVS SEED OUT.json [HAND]
+
+REPORT may also be the raw-page CSV exported on the GPU box (`ncu -i … --page raw --csv`).
 """
 import csv
 import io
@@ -10,8 +12,12 @@ import subprocess
 import sys
 
 rep, envs, seed, out = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                     text=True, check=True).stdout
+hand = sys.argv[5] if len(sys.argv) > 5 else "pj"
+if rep.endswith(".csv"):
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, units, v = rows[0], rows[1], rows[2]
 m = {n: (u, x) for n, u, x in zip(h, units, v)}
@@ -29,7 +35,7 @@ dadd = num("sm__sass_thread_inst_executed_op_dadd_pred_on.sum")
 dmul = num("sm__sass_thread_inst_executed_op_dmul_pred_on.sum")
 dfma = num("sm__sass_thread_inst_executed_op_dfma_pred_on.sum")
 summary = {
-    "kernel": "k_repair_retract", "envs": envs, "seed": seed,
+    "kernel": "k_repair_retract", "envs": envs, "seed": seed, "hand": hand,
     "source": f"ncu --set full --clock-control none, one launch ({rep})",
     "duration_s_under_ncu": num("gpu__time_duration.sum"),
     "fp64_flops": dadd + dmul + 2 * dfma, "dadd": dadd, "dmul": dmul, "dfma": dfma,
