@@ -1828,13 +1828,13 @@ static void step_core(ipc_world* w, const ipc_step_config* cfg, const double* ta
         w->lags_stale = false;
       }
       if (fp == 0) {
-        IPC_LAUNCH(K_LAGS, st, k_lags, ne, BP_THREADS, 0, W, W.xw0, w->dcd.c, w->L, w->ok);
+        IPC_LAUNCH(K_LAGS, st, k_lags, ne, BP_THREADS, 0, W, W.xw0, w->dcd.c, w->L, w->ok, w->env_order);
         IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, ne, w->L.n, w->ok, w->L.pre);
         IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, ne, w->L.g_n, w->ok, w->L.g_pre);
       } else {
         w->world_pos(W.x, W.xw);
         w->broad(w->dcd, w->pb_dcd, true, W.xw, W.xw, w->ok);
-        IPC_LAUNCH(K_LAGS, st, k_lags, ne, BP_THREADS, 0, W, W.xw, w->dcd.c, w->L, w->ok);
+        IPC_LAUNCH(K_LAGS, st, k_lags, ne, BP_THREADS, 0, W, W.xw, w->dcd.c, w->L, w->ok, w->env_order);
         IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, ne, w->L.n, w->ok, w->L.pre);
         IPC_LAUNCH(K_MISC, st, k_prefix, 1, 1024, 0, ne, w->L.g_n, w->ok, w->L.g_pre);
       }

@@ -1224,9 +1224,10 @@ static __device__ void lags_env(const World& W, const double* __restrict__ xw, c
   if (threadIdx.x == 0) L.g_n[e] = gbase;
 }
 
-IPC_GLOBAL void k_lags(World W, const double* __restrict__ xw, Cands C, Lags L, const int* env_flag) {
+IPC_GLOBAL void k_lags(World W, const double* __restrict__ xw, Cands C, Lags L, const int* env_flag,
+                       const int* order) {
   ipc_pdl_wait();
-  int e = blockIdx.x;
+  int e = order ? order[blockIdx.x] : blockIdx.x;
   if (env_flag && !env_flag[e]) return;
   lags_env(W, xw, C, L, e);
 }
