@@ -256,11 +256,15 @@ def parity_block(traj, xs_gpu, its_gpu, dof_pre, free_flags):
     largest |DoF|, Newton-count mismatches over (env, step), and whether every
     env of the batch ended every step intersection-free."""
     max_rel, mism, n, where, lst, noise = 0.0, 0, 0, None, [], 0
+    over, rels = [], []
     for e, (xc, ic) in enumerate(zip(traj["x"], traj["newton"])):
         lo, hi = int(dof_pre[e]), int(dof_pre[e + 1])
         for k in range(len(xc)):
             xg = xs_gpu[k][lo:hi]
             rel = float(np.abs(xg - xc[k]).max() / np.abs(xc[k]).max())
+            rels.append(rel)
+            if rel > 1e-6:
+                over.append([e, k, rel])
             if rel > max_rel:
                 max_rel, where = rel, [e, k]
             if its_gpu[k][e] != ic[k]:
@@ -273,7 +277,10 @@ def parity_block(traj, xs_gpu, its_gpu, dof_pre, free_flags):
                     lst.append([e, k, int(its_gpu[k][e]), int(ic[k]), lp])
             n += 1
     return {"envs": len(traj["x"]), "steps": len(traj["x"][0]) if traj["x"] else 0,
-            "max_rel_dof": max_rel, "max_rel_at_env_step": where, "newton_mismatches": mism,
+            "max_rel_dof": max_rel, "max_rel_at_env_step": where,
+            "median_rel_dof": float(np.median(rels)) if rels else None,
+            "env_steps_over_tolerance": len(over), "over_tolerance_env_step_rel": over[:12],
+            "newton_mismatches": mism,
             "newton_mismatches_at_noise_level_p": noise,
             "mismatch_list_env_step_gpu_cpu_cpu_last_p_over_h": lst, "compared_env_steps": n,
             "tolerance_rel_dof": 1e-6,
