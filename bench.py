@@ -279,7 +279,8 @@ def parity_block(traj, xs_gpu, its_gpu, dof_pre, free_flags):
     return {"envs": len(traj["x"]), "steps": len(traj["x"][0]) if traj["x"] else 0,
             "max_rel_dof": max_rel, "max_rel_at_env_step": where,
             "median_rel_dof": float(np.median(rels)) if rels else None,
-            "env_steps_over_tolerance": len(over), "over_tolerance_env_step_rel": over[:12],
+            "env_steps_over_tolerance": len(over), "envs_over_tolerance": sorted({o[0] for o in over}),
+            "over_tolerance_env_step_rel": over[:12],
             "newton_mismatches": mism,
             "newton_mismatches_at_noise_level_p": noise,
             "mismatch_list_env_step_gpu_cpu_cpu_last_p_over_h": lst, "compared_env_steps": n,
