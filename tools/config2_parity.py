@@ -7,6 +7,7 @@ by block (soft vertices, each affine body). GPU only.
 import json
 import os
 import sys
+import time
 
 import numpy as np
 
@@ -37,13 +38,15 @@ def main():
     for k in range(len(z["x"])):
         g.set_targets(joint_values=np.minimum(g.joint_values + 1e-3, 0.0262))
         st0 = engine_of(sc).stats() if k else None
+        t0 = time.perf_counter()
         _, rep = step(sc, cfg)
+        wall_ms = 1e3 * (time.perf_counter() - t0)
         st1 = engine_of(sc).stats()
         x = sc.state.gather()
         scale = np.abs(z["x"][k]).max()
         err = {name: float(np.abs(x[o:o + n] - z["x"][k][o:o + n]).max() / scale)
                for name, o, n in blocks}
-        out = {"step": k, "newton": [rep.newton_iters, int(z["newton_iters"][k])],
+        out = {"step": k, "wall_ms": wall_ms, "newton": [rep.newton_iters, int(z["newton_iters"][k])],
                "al": [rep.al_outer, int(z["al_outer"][k])],
                "pcg_iters": st1["pcg_iters"] - (st0["pcg_iters"] if st0 else 0),
                "max_rel": max(err.values()), "by_block": err,
