@@ -451,6 +451,7 @@ struct ipc_world {
   double *env_alpha = nullptr;
   int *enable = nullptr, *ok = nullptr, *al_flag = nullptr, *accepted = nullptr, *ls_count = nullptr, *d_count = nullptr;
   int* env_order = nullptr;  // start order of the per-env dense-solve CTAs (k_env_order)
+  bool use_env_order = getenv("IPC_ENV_ORDER") == nullptr || getenv("IPC_ENV_ORDER")[0] != '0';  // 0: identity
   int* h_count = nullptr;  // pinned
   double* slot_force = nullptr;
   double* d_targets = nullptr;
@@ -1018,7 +1019,8 @@ struct ipc_world {
     IPC_LAUNCH(K_MISC, st, k_newton_begin, nblk(n_env, 128), 128, 0, n_env, S, al_flag);
     // start order of the per-env CTAs for this solve, from the latest
     // candidate and lag counts (only scheduling: any order gives the same bits)
-    if (!sparse) IPC_LAUNCH(K_MISC, st, k_env_order, 1, 1024, 0, n_env, S.newton_active, dcd.c, L, env_order);
+    if (!sparse && use_env_order)
+      IPC_LAUNCH(K_MISC, st, k_env_order, 1, 1024, 0, n_env, S.newton_active, dcd.c, L, env_order);
     bool graphs = use_graphs && !sparse;
     if (graphs) ensure_graphs(cfg);
     int tail = 0;

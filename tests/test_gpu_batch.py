@@ -191,3 +191,24 @@ def test_programmatic_launch_is_bit_identical(monkeypatch):
         del w
     assert out["1"][1] == out["0"][1]
     assert np.array_equal(out["1"][0], out["0"][0])
+
+
+def test_env_start_order_is_scheduling_only(monkeypatch):
+    """The heaviest-first start order of the per-env CTAs (k_env_order) only
+    reorders scheduling: identity order gives the same bits."""
+    from paper_2311_05945_b200 import workloads as WL
+    from paper_2311_05945_b200.solver import SolverConfig
+    from paper_2311_05945_b200.world import GpuWorld
+
+    E, K = 48, 10
+    out = {}
+    for order in ("1", "0"):
+        monkeypatch.setenv("IPC_ENV_ORDER", order)
+        scenes, grippers, half, poses = WL.grasp_batch(E, seed=11)
+        w = GpuWorld(scenes)
+        w.upload_schedule(WL.schedule(grippers, half, poses, K))
+        its = [[r.newton_iters for r in w.step_scheduled(SolverConfig(), k)] for k in range(K)]
+        out[order] = (w.get_state()[0].copy(), its)
+        del w
+    assert out["1"][1] == out["0"][1]
+    assert np.array_equal(out["1"][0], out["0"][0])
