@@ -1020,7 +1020,8 @@ struct ipc_world {
     // start order of the per-env CTAs for this solve, from the latest
     // candidate and lag counts (only scheduling: any order gives the same bits)
     if (!sparse && use_env_order)
-      IPC_LAUNCH(K_MISC, st, k_env_order, 1, 1024, 0, n_env, S.newton_active, dcd.c, L, env_order);
+      IPC_LAUNCH(K_MISC, st, k_env_order, n_env <= ORDER_MAX ? (n_env + ORDER_ENVS - 1) / ORDER_ENVS : 148,
+                 ORDER_ENVS * 32, 0, n_env, S.newton_active, dcd.c, L, env_order);
     bool graphs = use_graphs && !sparse;
     if (graphs) ensure_graphs(cfg);
     int tail = 0;

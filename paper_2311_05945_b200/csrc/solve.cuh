@@ -913,44 +913,34 @@ static __device__ void dense_solve_block(const World& W, const EnvState& S, cons
 
 // Order in which the per-env CTAs of the dense solve start: most records
 // first (a heavy env starting in the last wave is the kernel's tail), active
-// before converged envs, ties by env index. One CTA, bitonic sort of
-// (records << 12 | (4095 - env)) in shared memory; identity beyond 4096 envs.
+// before converged envs, ties by env index. Keys (records << 12 | (4095 -
+// env)) are unique, so an env's slot is its rank = the number of larger keys:
+// ORDER_ENVS envs per CTA, one warp per env counting over the keys staged in
+// shared memory (no sorting network, no serial stages; grid = n_env / 32).
+// Identity beyond 4096 envs.
 constexpr int ORDER_MAX = 4096;
-IPC_GLOBAL void __launch_bounds__(1024) k_env_order(int n_env, const int* active, Cands C, Lags L, int* order) {
+constexpr int ORDER_ENVS = 32;  // envs ranked per CTA (one warp each)
+IPC_GLOBAL void __launch_bounds__(ORDER_ENVS * 32) k_env_order(int n_env, const int* active, Cands C, Lags L,
+                                                               int* order) {
   ipc_pdl_wait();
   __shared__ long long key[ORDER_MAX];
   int tid = threadIdx.x;
   if (n_env > ORDER_MAX) {
-    for (int e = tid; e < n_env; e += blockDim.x) order[e] = e;
+    for (int e = blockIdx.x * blockDim.x + tid; e < n_env; e += gridDim.x * blockDim.x) order[e] = e;
     return;
   }
-  int n2 = 1;
-  while (n2 < n_env) n2 <<= 1;
-  for (int i = tid; i < n2; i += blockDim.x) {
-    long long k = -1;  // padding sorts last
-    if (i < n_env) {
-      long long w = active[i] ? 1 + (long long)C.n_pt[i] + C.n_ee[i] + L.n[i] : 0;
-      k = (w << 12) | (ORDER_MAX - 1 - i);
-    }
-    key[i] = k;
+  for (int i = tid; i < n_env; i += blockDim.x) {
+    long long w = active[i] ? 1 + (long long)C.n_pt[i] + C.n_ee[i] + L.n[i] : 0;
+    key[i] = (w << 12) | (ORDER_MAX - 1 - i);
   }
   __syncthreads();
-  for (int size = 2; size <= n2; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < n2; i += blockDim.x) {
-        int j = i ^ stride;
-        if (j > i) {
-          bool desc = (i & size) == 0;  // descending overall
-          long long a = key[i], b = key[j];
-          if (desc ? a < b : a > b) {
-            key[i] = b;
-            key[j] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  for (int i = tid; i < n_env; i += blockDim.x) order[i] = ORDER_MAX - 1 - (int)(key[i] & (ORDER_MAX - 1));
+  int lane = tid & 31, e = blockIdx.x * ORDER_ENVS + (tid >> 5);
+  if (e >= n_env) return;
+  long long k = key[e];
+  unsigned cnt = 0;
+  for (int j = lane; j < n_env; j += 32) cnt += key[j] > k;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (lane == 0) order[cnt] = e;
 }
 
 IPC_GLOBAL void __launch_bounds__(DENSE_THREADS) k_dense_solve(World W, EnvState S, Derivs D, Cands C,
