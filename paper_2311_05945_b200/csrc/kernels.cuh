@@ -551,30 +551,46 @@ IPC_GLOBAL void __launch_bounds__(BP_THREADS) k_ss_filter(World W, const double*
   ss_filter_env(W, S, lo, hi, C, e);
 }
 
-// per-env exclusive prefix of candidate counts over flagged envs (one CTA);
-// pre has n_env + 1 entries, pre[n_env] = total
-IPC_GLOBAL void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
-  ipc_pdl_wait();
-  __shared__ int part[1024];
-  int tid = threadIdx.x, nt = blockDim.x;
+// per-env exclusive prefix of counts over flagged envs, one CTA: each thread
+// sums a contiguous run of envs, the run totals are scanned with warp
+// shuffles (two barriers), then each thread writes its run. pre has n_env + 1
+// entries, pre[n_env] = total.
+__device__ __forceinline__ void block_prefix_envs(int n_env, const int* __restrict__ cnt, const int* flag,
+                                                  int* pre) {
+  __shared__ int wsum[32];
+  int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   int per = (n_env + nt - 1) / nt;
   int a = tid * per, b = min(n_env, a + per);
   int s = 0;
   for (int e = a; e < b; ++e) s += (flag == nullptr || flag[e]) ? cnt[e] : 0;
-  part[tid] = s;
-  __syncthreads();
-  for (int o = 1; o < nt; o <<= 1) {
-    int v = tid >= o ? part[tid - o] : 0;
-    __syncthreads();
-    part[tid] += v;
-    __syncthreads();
+  int inc = s;  // inclusive scan within the warp
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
   }
-  int run = part[tid] - s;
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int nw = (nt + 31) >> 5;
+    int w = lane < nw ? wsum[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    wsum[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  int run = inc - s + (wid ? wsum[wid - 1] : 0);
   for (int e = a; e < b; ++e) {
     pre[e] = run;
     run += (flag == nullptr || flag[e]) ? cnt[e] : 0;
   }
-  if (tid == nt - 1) pre[n_env] = part[nt - 1];
+  if (tid == nt - 1) pre[n_env] = run;
+}
+
+IPC_GLOBAL void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
+  ipc_pdl_wait();
+  block_prefix_envs(n_env, cnt, flag, pre);
 }
 
 // the three candidate-count prefixes (PT, EE, ground) in one launch
@@ -582,26 +598,7 @@ IPC_GLOBAL void k_prefix3(int n_env, Cands C, const int* flag) {
   ipc_pdl_wait();
   const int* cnt = blockIdx.x == 0 ? C.n_pt : (blockIdx.x == 1 ? C.n_ee : C.n_gnd);
   int* pre = blockIdx.x == 0 ? C.pre_pt : (blockIdx.x == 1 ? C.pre_ee : C.pre_gnd);
-  __shared__ int part[1024];
-  int tid = threadIdx.x, nt = blockDim.x;
-  int per = (n_env + nt - 1) / nt;
-  int a = tid * per, b = min(n_env, a + per);
-  int s = 0;
-  for (int e = a; e < b; ++e) s += (flag == nullptr || flag[e]) ? cnt[e] : 0;
-  part[tid] = s;
-  __syncthreads();
-  for (int o = 1; o < nt; o <<= 1) {
-    int v = tid >= o ? part[tid - o] : 0;
-    __syncthreads();
-    part[tid] += v;
-    __syncthreads();
-  }
-  int run = part[tid] - s;
-  for (int e = a; e < b; ++e) {
-    pre[e] = run;
-    run += (flag == nullptr || flag[e]) ? cnt[e] : 0;
-  }
-  if (tid == nt - 1) pre[n_env] = part[nt - 1];
+  block_prefix_envs(n_env, cnt, flag, pre);
 }
 
 // env owning flattened item g: pre[e] <= g < pre[e+1] (last such e)
