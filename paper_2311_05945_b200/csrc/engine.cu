@@ -260,16 +260,39 @@ __global__ void k_loop_ctl(int n_env, const int* newton, const int* ls, const in
   cudaGraphSetConditional(h_mode, mode);
   cudaGraphSetConditional(h_loop, loop);
 }
-// dxw = xw(x + p) - xw(x); sweep boxes over [xw, xw + dxw] (ref broadphase.py:206)
-__global__ void k_sweep_box2(int n, const double* xwt, const double* xw, double* dxw, double* lo, double* hi) {
+// sweep boxes along p, one pass per slot: x_t = x + p on flagged envs (as
+// k_axpy_env), xw(x_t) (as world_slot), dxw = xw(x_t) - xw(x) and the boxes
+// over [xw, xw + dxw] (ref broadphase.py:206); x_t and xw(x_t) stay in
+// registers (the batched path has no other reader of them)
+__global__ void k_sweep_slots(World W, const double* __restrict__ x, const double* __restrict__ p,
+                              const int* flag, const double* __restrict__ xw, double* dxw, double* lo,
+                              double* hi) {
   ipc_pdl_wait();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 3 * n) return;
-  double d = __dsub_rn(xwt[i], xw[i]);
-  dxw[i] = d;
-  double a = xw[i], b = __dadd_rn(xw[i], d);
-  lo[i] = fmin(a, b);
-  hi[i] = fmax(a, b);
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= W.n_slot) return;
+  int d = W.slot_dof[s];
+  bool on = flag == nullptr || flag[W.dof_env[d]];
+  auto xt = [&](int j) { return on ? __dadd_rn(x[j], __dmul_rn(1.0, p[j])) : x[j]; };
+  double t[3];
+  if (!W.slot_aff[s]) {
+    for (int i = 0; i < 3; ++i) t[i] = xt(d + i);
+  } else {
+    const double* r = W.slot_rest + 3 * s;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      int a = d + 3 + 3 * i;
+      double m = __dadd_rn(__dadd_rn(__dmul_rn(xt(a), r[0]), __dmul_rn(xt(a + 1), r[1])), __dmul_rn(xt(a + 2), r[2]));
+      t[i] = __dadd_rn(xt(d + i), m);
+    }
+  }
+  for (int i = 0; i < 3; ++i) {
+    int k = 3 * s + i;
+    double w = xw[k], dd = __dsub_rn(t[i], w);
+    dxw[k] = dd;
+    double b = __dadd_rn(w, dd);
+    lo[k] = fmin(w, b);
+    hi[k] = fmax(w, b);
+  }
 }
 __global__ void k_copy_int(int n, const int* a, int* b) {
   ipc_pdl_wait();
@@ -753,9 +776,8 @@ struct ipc_world {
   }
   // CCD bound along p (ref solver.py:333-343)
   void seq_ccd(const ipc_step_config& cfg) {
-    IPC_LAUNCH(K_MISC, st, k_axpy_env, nblk(W.n_dof, 256), 256, 0, W, W.x, W.p, nullptr, 1.0, S.ls_active, W.xt);
-    world_pos(W.xt, xwt);
-    IPC_LAUNCH(K_MISC, st, k_sweep_box2, nblk(3 * W.n_slot, 256), 256, 0, W.n_slot, xwt, W.xw, W.dxw, xlo, xhi);
+    IPC_LAUNCH(K_MISC, st, k_sweep_slots, nblk(W.n_slot, 128), 128, 0, W, W.x, W.p, S.ls_active, W.xw, W.dxw, xlo,
+               xhi);
     broad_nosync(sweep, xlo, xhi, S.ls_active);
     IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.alpha_max, 1.0, S.ls_active);
     fork_to(side[0], fj[0]);  // ground crossings as a parallel branch
