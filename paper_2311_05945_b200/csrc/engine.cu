@@ -654,9 +654,12 @@ struct ipc_world {
       IPC_LAUNCH(kid, st, k_broad, dim3(n_env, 2, bp_z), BP_THREADS, 0, W, lo, hi, cs.c, -1, env_mask, 1, bp_cnt);
     }
   }
-  void broad_nosync(CandStore& cs, const double* lo, const double* hi, const int* env_mask) {
+  // fill: optional per-env array set to v on the masked envs in the same launch
+  void broad_nosync(CandStore& cs, const double* lo, const double* hi, const int* env_mask, double* fill = nullptr,
+                    double v = 0.0) {
     launch_broad(cs, lo, hi, env_mask);
-    IPC_LAUNCH(K_MISC, st, k_prefix3, 3, 1024, 0, n_env, cs.c, env_mask);
+    IPC_LAUNCH(K_MISC, st, k_prefix3, fill && env_mask ? 4 : 3, 1024, 0, n_env, cs.c, env_mask, fill, v);
+    if (fill && !env_mask) IPC_LAUNCH(K_MISC, st, k_fill, nblk(n_env, 128), 128, 0, n_env, fill, v);
   }
 
   // run broad phase; grow capacities and retry on overflow
@@ -674,7 +677,7 @@ struct ipc_world {
       CK(cudaMemcpyAsync(h_status, sweep.c.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       if (!*h_count && !*h_status) {
-        IPC_LAUNCH(K_MISC, st, k_prefix3, 3, 1024, 0, n_env, cs.c, env_mask);
+        IPC_LAUNCH(K_MISC, st, k_prefix3, 3, 1024, 0, n_env, cs.c, env_mask, nullptr, 0.0);
         return;
       }
       // grow the overflowed stores to 1.5x their unclipped counts (at least 4x)
@@ -757,8 +760,7 @@ struct ipc_world {
   // head: DCD broad phase, derivative pass of every term, E0, solve, check
   void seq_head(const ipc_step_config& cfg) {
     world_pos(W.x, W.xw);
-    broad_nosync(dcd, W.xw, W.xw, S.newton_active);
-    IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.min_s, INFINITY, S.newton_active);
+    broad_nosync(dcd, W.xw, W.xw, S.newton_active, S.min_s, INFINITY);
     terms(W.x, W.xw, dcd, pb_dcd, true, cfg.h, S.newton_active, S.min_s);
     if (sparse) {
       energy(W.x, dcd, pb_dcd, S.newton_active, S.e0);
@@ -778,8 +780,7 @@ struct ipc_world {
   void seq_ccd(const ipc_step_config& cfg) {
     IPC_LAUNCH(K_MISC, st, k_sweep_slots, nblk(W.n_slot, 128), 128, 0, W, W.x, W.p, S.ls_active, W.xw, W.dxw, xlo,
                xhi);
-    broad_nosync(sweep, xlo, xhi, S.ls_active);
-    IPC_LAUNCH(K_MISC, st, k_fill_flag, nblk(n_env, 128), 128, 0, n_env, S.alpha_max, 1.0, S.ls_active);
+    broad_nosync(sweep, xlo, xhi, S.ls_active, S.alpha_max, 1.0);
     fork_to(side[0], fj[0]);  // ground crossings as a parallel branch
     IPC_LAUNCH(K_CCD, side[0], k_ccd_ground, dim3(nblk(max_slots, 128), n_env), 128, 0, W, W.xw, W.dxw, sweep.c,
                cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
@@ -803,9 +804,8 @@ struct ipc_world {
         energy(W.xt, sweep, pb_sweep, S.ls_active, e_multi + (size_t)m * n_env);
       }
     }
-    IPC_LAUNCH(K_MISC, st, k_ls_check_multi, nblk(n_env, 128), 128, 0, W, S, ls_count,
-               cfg.max_line_search_halvings, M, e_multi, accepted);
-    IPC_LAUNCH(K_MISC, st, k_axpy_env, nblk(W.n_dof, 256), 256, 0, W, W.x, W.p, S.alpha, 1.0, accepted, W.x);
+    IPC_LAUNCH(K_MISC, st, k_ls_check_apply, n_env, 64, 0, W, S, ls_count, cfg.max_line_search_halvings, M, e_multi,
+               accepted, W.x, W.p);
   }
   void seq_ls(const ipc_step_config& cfg) { seq_ls_round(cfg, 1); }
 

@@ -593,9 +593,16 @@ IPC_GLOBAL void k_prefix(int n_env, const int* cnt, const int* flag, int* pre) {
   block_prefix_envs(n_env, cnt, flag, pre);
 }
 
-// the three candidate-count prefixes (PT, EE, ground) in one launch
-IPC_GLOBAL void k_prefix3(int n_env, Cands C, const int* flag) {
+// the three candidate-count prefixes (PT, EE, ground) in one launch; a
+// fourth CTA (when fill is given) sets fill[e] = v on the flagged envs (the
+// per-iteration reset of min_s / alpha_max that follows every broad phase)
+IPC_GLOBAL void k_prefix3(int n_env, Cands C, const int* flag, double* fill, double v) {
   ipc_pdl_wait();
+  if (blockIdx.x == 3) {
+    for (int e = threadIdx.x; e < n_env; e += blockDim.x)
+      if (flag[e]) fill[e] = v;
+    return;
+  }
   const int* cnt = blockIdx.x == 0 ? C.n_pt : (blockIdx.x == 1 ? C.n_ee : C.n_gnd);
   int* pre = blockIdx.x == 0 ? C.pre_pt : (blockIdx.x == 1 ? C.pre_ee : C.pre_gnd);
   block_prefix_envs(n_env, cnt, flag, pre);

@@ -1047,11 +1047,9 @@ IPC_GLOBAL void k_ls_check(World W, EnvState S, int* ls_count, int max_halvings,
 // speculative backtracking: trials m = 0..M-1 evaluated E(x + α 2^-m p) into
 // e_multi[m * n_env + e]; take the first trial the sequential search would
 // have accepted (same floor / halving-count rules, ref solver.py:257-272)
-IPC_GLOBAL void k_ls_check_multi(World W, EnvState S, int* ls_count, int max_halvings, int M,
-                                 const double* e_multi, int* accepted) {
-  ipc_pdl_wait();
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= W.n_env) return;
+__device__ __forceinline__ void ls_check_multi_env(const World& W, const EnvState& S, int* ls_count,
+                                                   int max_halvings, int M, const double* e_multi, int* accepted,
+                                                   int e) {
   accepted[e] = 0;
   if (!S.ls_active[e]) return;
   double a = S.alpha[e];
@@ -1081,6 +1079,24 @@ IPC_GLOBAL void k_ls_check_multi(World W, EnvState S, int* ls_count, int max_hal
     S.converged[e] = 0;
     S.newton_active[e] = 0;
   }
+}
+// the round's Armijo check and, for an accepted env, x += alpha p over its
+// DoFs (the per-env check and k_axpy_env in one launch, one CTA per env;
+// same operations, same bits)
+IPC_GLOBAL void k_ls_check_apply(World W, EnvState S, int* ls_count, int max_halvings, int M,
+                                 const double* e_multi, int* accepted, double* x, const double* __restrict__ p) {
+  ipc_pdl_wait();
+  __shared__ int acc;
+  int e = blockIdx.x;
+  if (threadIdx.x == 0) {
+    ls_check_multi_env(W, S, ls_count, max_halvings, M, e_multi, accepted, e);
+    acc = accepted[e];
+  }
+  __syncthreads();
+  if (!acc) return;
+  double a = S.alpha[e] * 1.0;
+  for (int i = W.env_dof[e] + threadIdx.x; i < W.env_dof[e + 1]; i += blockDim.x)
+    x[i] = __dadd_rn(x[i], __dmul_rn(a, p[i]));
 }
 
 IPC_GLOBAL void k_copy_env(World W, const double* src, double* dst, const int* flag) {
