@@ -788,13 +788,14 @@ struct ipc_world {
       IPC_LAUNCH(K_CCD, st, k_ccd_pairs, dim3(n_sm * 8, 2), 64, 0, W, W.xw, W.dxw, sweep.c,
                  cfg.ccd_conservative_factor, S.ls_active, S.alpha_max);
     join_from(side[0], fj[1]);
-    IPC_LAUNCH(K_MISC, st, k_ls_begin, nblk(n_env, 128), 128, 0, n_env, S, ls_count);
+    if (sparse)  // dense worlds: folded into the first k_ls_value round
+      IPC_LAUNCH(K_MISC, st, k_ls_begin, nblk(n_env, 128), 128, 0, n_env, S, ls_count);
   }
   // one backtracking round (ref solver.py:257): M speculative halvings
-  void seq_ls_round(const ipc_step_config& cfg, int M) {
+  void seq_ls_round(const ipc_step_config& cfg, int M, bool begin = false) {
     if (!sparse) {
       IPC_LAUNCH(K_ENERGY, st, k_ls_value, dim3(n_env, M), LS_THREADS, (size_t)3 * max_slots * sizeof(double), W, S,
-                 sweep.c, L, W.x, W.p, W.xhat, cfg.h * cfg.h, cfg.h, e_multi, env_order);
+                 sweep.c, L, W.x, W.p, W.xhat, cfg.h * cfg.h, cfg.h, e_multi, env_order, begin ? ls_count : nullptr);
     } else {
       double scale = 1.0;
       for (int m = 0; m < M; ++m, scale *= 0.5) {
@@ -807,7 +808,7 @@ struct ipc_world {
     IPC_LAUNCH(K_MISC, st, k_ls_check_apply, n_env, 64, 0, W, S, ls_count, cfg.max_line_search_halvings, M, e_multi,
                accepted, W.x, W.p);
   }
-  void seq_ls(const ipc_step_config& cfg) { seq_ls_round(cfg, 1); }
+  void seq_ls(const ipc_step_config& cfg) { seq_ls_round(cfg, 1, true); }
 
   // M speculative halvings in one round (follow-up rounds only)
   static constexpr int LS_M = 8;    // trials of an iteration's first follow-up round

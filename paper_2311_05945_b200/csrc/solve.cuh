@@ -283,12 +283,30 @@ IPC_GLOBAL void __launch_bounds__(LS_THREADS) k_ls_value(World W, EnvState S, Ca
                                                            const double* __restrict__ x,
                                                            const double* __restrict__ p,
                                                            const double* __restrict__ xhat, double h2, double h,
-                                                           double* e_multi, const int* order) {
+                                                           double* e_multi, const int* order, int* ls_count) {
   ipc_pdl_wait();
   extern __shared__ double sxw[];
   int e = order ? order[blockIdx.x] : blockIdx.x, m = blockIdx.y;
   if (!S.ls_active[e]) return;
-  double a = S.alpha[e] * ldexp(1.0, -m);
+  double a0;
+  if (ls_count) {  // first round of an iteration: the line-search start (k_ls_begin) folded in
+    a0 = S.alpha_max[e];
+    if (threadIdx.x == 0 && m == 0) {
+      S.ccd_calls[e] += 1;
+      S.alpha[e] = a0;
+      ls_count[e] = 0;
+      if (a0 < 1e-12) {  // ALPHA_FLOOR before any evaluation
+        S.ls_active[e] = 0;
+        S.ls_failed[e] = 1;
+        S.converged[e] = 0;
+        S.newton_active[e] = 0;
+      }
+    }
+    if (a0 < 1e-12) return;
+  } else {
+    a0 = S.alpha[e];
+  }
+  double a = a0 * ldexp(1.0, -m);
   double tot = ls_value_block(W, C, L, x, p, xhat, h2, h, a, e, sxw);
   if (threadIdx.x == 0) e_multi[(long long)m * W.n_env + e] = tot;
 }
