@@ -628,14 +628,18 @@ struct ipc_world {
   // extracts the exact lists; fused.cuh env_candidates), or directly
   int* ss_valid = nullptr;    // [n_env] superset holds the broad phase of the current build boxes
   int* ss_rebuild = nullptr;  // [n_env] scratch: envs to rebuild in this call
-  void launch_broad(CandStore& cs, const double* lo, const double* hi, const int* env_mask) {
+  // world_x: compute the world positions xw(world_x) into lo (== hi) first
+  void launch_broad(CandStore& cs, const double* lo, const double* hi, const int* env_mask,
+                    const double* world_x = nullptr) {
     int kid = &cs == &sweep ? K_BROAD_SWEEP : K_BROAD_DCD;
     if (ss_pad > 0.0 && &cs != &ss) {
-      IPC_LAUNCH(kid, st, k_ss_check, n_env, 256, 0, W, lo, hi, bb_lo, bb_hi, ss_pad, env_mask, ss_valid, ss_rebuild);
+      IPC_LAUNCH(kid, st, k_ss_check, n_env, 256, 0, W, lo, hi, bb_lo, bb_hi, ss_pad, env_mask, ss_valid, ss_rebuild,
+                 world_x, const_cast<double*>(lo));
       launch_broad_raw(ss, bb_lo, bb_hi, ss_rebuild, kid);
       IPC_LAUNCH(kid, st, k_ss_filter, n_env, BP_THREADS, 0, W, lo, hi, ss.c, cs.c, env_mask, env_order);
       return;
     }
+    if (world_x) world_pos(world_x, const_cast<double*>(lo));
     launch_broad_raw(cs, lo, hi, env_mask, kid);
   }
   void launch_broad_raw(CandStore& cs, const double* lo, const double* hi, const int* env_mask, int kid) {
@@ -656,8 +660,8 @@ struct ipc_world {
   }
   // fill: optional per-env array set to v on the masked envs in the same launch
   void broad_nosync(CandStore& cs, const double* lo, const double* hi, const int* env_mask, double* fill = nullptr,
-                    double v = 0.0) {
-    launch_broad(cs, lo, hi, env_mask);
+                    double v = 0.0, const double* world_x = nullptr) {
+    launch_broad(cs, lo, hi, env_mask, world_x);
     IPC_LAUNCH(K_MISC, st, k_prefix3, fill && env_mask ? 4 : 3, 1024, 0, n_env, cs.c, env_mask, fill, v);
     if (fill && !env_mask) IPC_LAUNCH(K_MISC, st, k_fill, nblk(n_env, 128), 128, 0, n_env, fill, v);
   }
@@ -759,8 +763,7 @@ struct ipc_world {
   // ---- one Newton iteration = three fixed launch sequences ----------------
   // head: DCD broad phase, derivative pass of every term, E0, solve, check
   void seq_head(const ipc_step_config& cfg) {
-    world_pos(W.x, W.xw);
-    broad_nosync(dcd, W.xw, W.xw, S.newton_active, S.min_s, INFINITY);
+    broad_nosync(dcd, W.xw, W.xw, S.newton_active, S.min_s, INFINITY, W.x);  // xw = world(x) first
     terms(W.x, W.xw, dcd, pb_dcd, true, cfg.h, S.newton_active, S.min_s);
     if (sparse) {
       energy(W.x, dcd, pb_dcd, S.newton_active, S.e0);

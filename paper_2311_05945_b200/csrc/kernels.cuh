@@ -516,10 +516,18 @@ static __device__ bool ss_filter_env(const World& W, const Cands& S, const doubl
 // Batched superset check (one CTA per env): does every slot's query box lie
 // inside its build box? If not, write fresh build boxes (query box ± pad·d̂)
 // and flag the env for a superset rebuild.
-IPC_GLOBAL void k_ss_check(World W, const double* __restrict__ lo, const double* __restrict__ hi, double* bb_lo,
-                           double* bb_hi, double pad, const int* env_mask, int* valid, int* rebuild) {
+// With wx given, the CTA first writes its env's world positions xw(wx) into
+// xw_out (k_world folded in, every env; lo / hi may alias xw_out, hence no
+// __restrict__ / read-only loads on them).
+IPC_GLOBAL void k_ss_check(World W, const double* lo, const double* hi, double* bb_lo, double* bb_hi, double pad,
+                           const int* env_mask, int* valid, int* rebuild, const double* __restrict__ wx,
+                           double* xw_out) {
   ipc_pdl_wait();
   int e = blockIdx.x;
+  if (wx) {
+    for (int s = W.env_slot[e] + threadIdx.x; s < W.env_slot[e + 1]; s += blockDim.x) world_slot(W, wx, xw_out, s);
+    __syncthreads();
+  }
   if (env_mask && !env_mask[e]) {
     if (threadIdx.x == 0) rebuild[e] = 0;
     return;
