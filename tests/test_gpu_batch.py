@@ -212,3 +212,29 @@ def test_env_start_order_is_scheduling_only(monkeypatch):
         del w
     assert out["1"][1] == out["0"][1]
     assert np.array_equal(out["1"][0], out["0"][0])
+
+
+@pytest.mark.parametrize("knob,value", [("IPC_SS_PAD", "0"), ("IPC_LOOP_GRAPH", "0")])
+def test_bit_identical_knobs(monkeypatch, knob, value):
+    """Knobs that only change how the step is scheduled or searched give the
+    same bits: no candidate superset (plain broad phase, separate world-position
+    launch) and the host-driven Newton loop instead of the conditional graph."""
+    from paper_2311_05945_b200 import workloads as WL
+    from paper_2311_05945_b200.solver import SolverConfig
+    from paper_2311_05945_b200.world import GpuWorld
+
+    E, K = 48, 10
+    out = {}
+    for v in (None, value):
+        if v is None:
+            monkeypatch.delenv(knob, raising=False)
+        else:
+            monkeypatch.setenv(knob, v)
+        scenes, grippers, half, poses = WL.grasp_batch(E, seed=5)
+        w = GpuWorld(scenes)
+        w.upload_schedule(WL.schedule(grippers, half, poses, K))
+        its = [[r.newton_iters for r in w.step_scheduled(SolverConfig(), k)] for k in range(K)]
+        out[v] = (w.get_state()[0].copy(), its)
+        del w
+    assert out[None][1] == out[value][1]
+    assert np.array_equal(out[None][0], out[value][0])
